@@ -1,0 +1,184 @@
+/*
+ * jt.h — C-ABI of libjt, the B200 device boundary of paper_2211_07260_b200.
+ *
+ * The reference package (jouletune) has no FFI: its device boundary is the
+ * duck-typed SimulatedDevice (pkg/src/jouletune/device.py:246-382). libjt is
+ * what a maintainer binds to replace that simulator with a real GPU; each
+ * entry point below names the reference interface it stands in for.
+ * Plain C types only (no torch, no CUDA types in signatures); every call
+ * returns a jt_status and leaves a message retrievable with jt_last_error().
+ *
+ * Threading: one jt_ctx per (process, GPU). Calls on one ctx are serialised
+ * by the caller (the reference benchmark loop is single threaded,
+ * SPEC.md:465). jt_compile() is context free and thread safe, so configs can
+ * be compiled on a host thread pool while the GPU is busy. The only thread
+ * libjt creates is the NVML sampler inside jt_bench()/jt_sampler_*.
+ */
+#ifndef JT_H
+#define JT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define JT_ABI_VERSION 1
+
+/* Status codes and the Python exception each maps to (native.py):         */
+typedef enum {
+    JT_OK = 0,
+    JT_EINVAL = 1,     /* malformed argument            -> ConfigurationError */
+    JT_ENOGPU = 2,     /* no driver / device             -> CapabilityError   */
+    JT_ECUDA = 3,      /* CUDA driver error              -> DomainError       */
+    JT_ECOMPILE = 4,   /* NVRTC rejected the config      -> DomainError       */
+    JT_ELAUNCH = 5,    /* launch shape / smem rejected   -> DomainError       */
+    JT_ENVML = 6,      /* NVML missing or failed         -> CapabilityError   */
+    JT_ENOPERM = 7,    /* NVML refused (clock lock etc.) -> recorded, no raise */
+    JT_ENOTSUP = 8     /* not supported on this device   -> CapabilityError   */
+} jt_status;
+
+typedef struct jt_ctx jt_ctx;
+typedef struct jt_module jt_module;
+typedef struct jt_kernel jt_kernel;
+
+/* Static device description; replaces DeviceSpec's inputs
+ * (reference device.py:44-78: supported_core_clocks, base/peak clock,
+ * power_limit_range, tdp). All clocks in MHz, power in mW. */
+typedef struct {
+    int ordinal;
+    int cc_major, cc_minor;
+    int sm_count;
+    int max_smem_optin;          /* bytes per block with opt-in            */
+    int l2_bytes;
+    unsigned long long total_mem;
+    char name[128];
+    char pci_bus_id[32];
+    int nvml_ok;                 /* NVML handle resolved by PCI bus id      */
+    int energy_counter_ok;
+    int instant_power_ok;
+    unsigned n_clocks;           /* supported SM clocks at the top memory clock, ascending */
+    unsigned clocks_mhz[512];
+    unsigned mem_clock_mhz;
+    unsigned max_sm_clock_mhz;
+    unsigned default_sm_clock_mhz; /* default applications clock (base)    */
+    unsigned power_limit_min_mw, power_limit_max_mw;
+    unsigned power_limit_default_mw, power_limit_mw;
+    unsigned tdp_mw;             /* enforced default limit                   */
+} jt_device_info;
+
+/* One NVML sample. Times are seconds on the jt_now() clock.
+ * Replaces the simulator's PowerSample trace (device.py:124-127, 366-378). */
+typedef struct {
+    double t_s;
+    double power_w;              /* NVML_FI_DEV_POWER_INSTANT (NaN if n/a)  */
+    double power_avg_w;          /* nvmlDeviceGetPowerUsage (1 s average)   */
+    double energy_j;             /* total energy counter (NaN if n/a)       */
+    double energy_stamp_s;       /* driver timestamp of the energy field, jt_now() clock */
+    unsigned sm_mhz, mem_mhz, temp_c, pad;
+    unsigned long long reasons;  /* clocks-event reason bitmask             */
+} jt_sample;
+
+/* Kernel argument; replaces nothing in the reference (kernels were simulated
+ * by PerformanceSurface, device.py:148-243). */
+typedef enum { JT_ARG_PTR = 0, JT_ARG_I32 = 1, JT_ARG_F32 = 2, JT_ARG_F64 = 3, JT_ARG_I64 = 4 } jt_arg_kind;
+typedef struct {
+    int kind;
+    int pad;
+    union { unsigned long long ptr; long long i64; double f64; float f32; int i32; } v;
+} jt_arg;
+
+typedef struct {
+    unsigned grid[3];
+    unsigned block[3];
+    unsigned smem_bytes;         /* dynamic shared memory                   */
+    unsigned cluster_x;          /* 0/1 = no cluster                        */
+} jt_launch_shape;
+
+/* Result of a device-timed back-to-back loop; replaces the runtime /
+ * repetitions / total_duration of Execution (device.py:130-138, 349-382). */
+typedef struct {
+    double first_launch_s;       /* event time of the untimed probe launch  */
+    double per_launch_s;         /* loop time / reps                        */
+    double total_s;              /* CUDA-event loop time                    */
+    int reps;
+    int n_samples;               /* samples written                          */
+    double host_t_enqueue;       /* jt_now() before the first timed launch  */
+    double host_t_done;          /* jt_now() after the stop event completed */
+    double loop_t0;              /* estimated device start = done - total   */
+} jt_bench_result;
+
+/* --- context ------------------------------------------------------------ */
+int jt_abi_version(void);
+double jt_now(void);                           /* CLOCK_MONOTONIC seconds   */
+const char *jt_last_error(void);               /* thread-local message      */
+int jt_device_count(int *count);
+int jt_open(int ordinal, jt_ctx **out);        /* retains the primary context, resolves NVML by PCI id */
+int jt_close(jt_ctx *ctx);                     /* resets clocks/limits this ctx changed */
+int jt_device_info_get(jt_ctx *ctx, jt_device_info *out);
+
+/* --- memory (Execution inputs; the simulator had none) -------------------- */
+int jt_alloc(jt_ctx *ctx, size_t bytes, unsigned long long *dptr);
+int jt_free(jt_ctx *ctx, unsigned long long dptr);
+int jt_host_alloc(jt_ctx *ctx, size_t bytes, void **hptr);   /* pinned */
+int jt_host_free(jt_ctx *ctx, void *hptr);
+int jt_h2d(jt_ctx *ctx, unsigned long long dst, const void *src, size_t bytes);
+int jt_d2h(jt_ctx *ctx, void *dst, unsigned long long src, size_t bytes);
+int jt_memset_d8(jt_ctx *ctx, unsigned long long dst, unsigned char value, size_t bytes);
+int jt_synchronize(jt_ctx *ctx);
+
+/* --- kernels: per-config compile + load (Kernel Tuner's compile step) ---- */
+int jt_compile(const char *source, const char *program_name, const char *const *options, int n_options,
+               void **image, size_t *image_bytes, char *log, size_t log_capacity);
+void jt_free_image(void *image);
+int jt_module_load(jt_ctx *ctx, const void *image, size_t image_bytes, jt_module **out);
+int jt_module_unload(jt_ctx *ctx, jt_module *module);
+int jt_kernel_get(jt_ctx *ctx, jt_module *module, const char *name, jt_kernel **out);
+int jt_kernel_attributes(jt_ctx *ctx, jt_kernel *kernel, int *regs, int *static_smem, int *local_bytes,
+                         int *max_threads);
+
+/* --- execution (SimulatedDevice.execute, device.py:349-382) ------------------ */
+int jt_launch(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args);
+/* Event-timed loop of exactly `reps` launches; *seconds = total device time. */
+int jt_time(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args,
+            int reps, double *seconds);
+/* The benchmark primitive: one probe launch, then reps = clamp(ceil(min_seconds
+ * / probe), min_reps, max_reps) back-to-back launches between two CUDA events
+ * while the NVML sampler records every `sample_period_us` into `samples`
+ * (capacity `cap`; may be NULL to skip sampling). */
+int jt_bench(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args,
+             double min_seconds, int min_reps, int max_reps, int sample_period_us, jt_bench_result *out,
+             jt_sample *samples, int cap);
+/* Overwrite a scratch buffer larger than L2 (126 MB on B200). */
+int jt_l2_flush(jt_ctx *ctx);
+
+/* --- NVML sensors (observers.py:81-124 sensor semantics, real sources) --- */
+int jt_sample_now(jt_ctx *ctx, jt_sample *out);
+int jt_sampler_start(jt_ctx *ctx, int period_us, int cap);
+int jt_sampler_stop(jt_ctx *ctx, jt_sample *out, int cap, int *n);
+
+/* --- clock / power controller (set_core_clock / set_power_limit,
+ *     device.py:277-293). JT_ENOPERM is returned, not fatal, when NVML
+ *     refuses; callers then record the observed clock. ------------------- */
+int jt_clock_lock(jt_ctx *ctx, unsigned min_mhz, unsigned max_mhz);
+int jt_clock_reset(jt_ctx *ctx);
+/* Fallback knob when locked clocks are refused: NVML applications clocks. */
+int jt_app_clocks_set(jt_ctx *ctx, unsigned mem_mhz, unsigned sm_mhz);
+int jt_app_clocks_reset(jt_ctx *ctx);
+int jt_power_limit_set(jt_ctx *ctx, unsigned milliwatts);
+int jt_power_limit_reset(jt_ctx *ctx);
+
+/* --- kernel-suite helpers ------------------------------------------------ */
+/* PnPoly edge table for the chosen crossing METHOD (see
+ * csrc/kernels/pnpoly.cu): edges[4k..4k+3] = {vy_k, a, b, c},
+ * ybounds[2k..2k+1] = {min, max} of the edge's y range. Computed in IEEE
+ * float32 with explicit fmaf so the device and the oracle see the same bits. */
+int jt_pnpoly_edges(const float *vx, const float *vy, int n, int method, float *edges, float *ybounds);
+/* Copy host bytes into a __constant__ / __device__ symbol of a loaded module. */
+int jt_module_set_global(jt_ctx *ctx, jt_module *module, const char *name, const void *src, size_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JT_H */

@@ -1,0 +1,335 @@
+"""The real device: a B200 behind libjt, drop-in for ``SimulatedDevice``.
+
+``B200Device`` implements the duck-typed device interface the tuner,
+observers and CLI call (reference ``device.py:246-382``) for
+one bound :class:`~.kernels.KernelProblem` — the way Kernel Tuner's
+``tune_kernel`` binds one kernel source to a device:
+
+* ``set_core_clock(MHz)`` — ``DomainError`` if not an NVML-supported clock;
+  otherwise locks the SM clock with ``nvmlDeviceSetGpuLockedClocks`` (no-op if
+  unchanged, settle wait only on a real change). If NVML refuses
+  (NO_PERMISSION) nothing is raised: ``clock_locked`` turns False, the
+  observed clock becomes the truth and results carry ``nvml_clock_locked=0``.
+* ``set_power_limit(W)`` — range-checked ``nvmlDeviceSetPowerManagementLimit``.
+* ``execute(config, duration_hint)`` — compile (NVRTC, cached) and load the
+  config's module, run one probe launch and then a CUDA-event-timed
+  back-to-back loop of >= max(duration_hint, min_window) seconds while the
+  NVML sampler thread in libjt records instant power, the energy counter, SM
+  clock, temperature and clock-event reasons. The returned
+  :class:`~.device.Execution` has ``runtime`` = loop time / reps, a power
+  trace re-based to the loop start, ``window`` = the steady part of the loop,
+  ``counter_power`` = energy-counter slope over that window and
+  ``effective_clock`` = median observed SM clock.
+* ``read_voltage`` — ``CapabilityError`` (B200 exposes no core voltage).
+
+All controller changes are undone by :meth:`close` (and by libjt at exit).
+"""
+
+from __future__ import annotations
+
+import math
+import statistics
+import time
+from dataclasses import replace
+from typing import Any, Callable, Mapping
+
+import numpy as np
+
+from .device import EXECUTION_PARAMS, DeviceSpec, DeviceState, Execution, PowerSample
+from .errors import CapabilityError, ConfigurationError, DomainError
+from .gpu import ENERGY, E_STAMP, GPU, MEM_MHZ, P_INST, REASONS, SM_MHZ, SW_POWER_CAP, TEMP, T
+from .kernels import KernelProblem, make_problem
+from .searchspace import KernelConfig, normalize_value
+
+__all__ = ["B200Device", "counter_slope", "steady_window"]
+
+
+def steady_window(total: float, settle: float) -> tuple[float, float]:
+    """Skip the first ``settle`` s (power ramp), but keep >= half the loop."""
+    skip = min(settle, 0.5 * total)
+    return (skip, total)
+
+
+def counter_slope(samples, t0: float, t1: float) -> float | None:
+    """Energy-counter power (W) over [t0, t1] from (time, energy) samples.
+
+    The counter updates in steps (cadence is device specific), so the slope
+    is taken between the first and last *change points* inside the window,
+    stamped with the driver's own field timestamp when available. Returns
+    None when fewer than two distinct readings fall in the window.
+    """
+    pts = []
+    last_e = None
+    for s in samples:
+        e = s[ENERGY]
+        if not math.isfinite(e):
+            continue
+        t = s[E_STAMP] if math.isfinite(s[E_STAMP]) else s[T]
+        if e != last_e:
+            pts.append((t, e))
+            last_e = e
+    inside = [(t, e) for t, e in pts if t0 <= t <= t1]
+    if len(inside) < 2:
+        return None
+    (ta, ea), (tb, eb) = inside[0], inside[-1]
+    if tb - ta <= 0:
+        return None
+    return (eb - ea) / (tb - ta)
+
+
+class B200Device:
+    """One CUDA ordinal + one bound kernel problem (see module docstring)."""
+
+    def __init__(
+        self,
+        problem: KernelProblem | str = "conv2d",
+        ordinal: int = 0,
+        *,
+        gpu: GPU | None = None,
+        min_window: float = 0.05,
+        settle: float = 0.02,
+        clock_settle: float = 0.05,
+        sample_period_us: int = 1000,
+        answer: np.ndarray | None = None,
+        verify: Callable[[np.ndarray, np.ndarray, Mapping[str, Any]], bool] | None = None,
+        problem_kwargs: Mapping[str, Any] | None = None,
+    ):
+        self.problem = make_problem(problem, **(problem_kwargs or {})) if isinstance(problem, str) else problem
+        self.gpu = gpu if gpu is not None else GPU(ordinal)
+        self._owns_gpu = gpu is None
+        self.min_window = float(min_window)
+        self.settle = float(settle)
+        self.clock_settle = float(clock_settle)
+        self.sample_period_us = int(sample_period_us)
+        self.sample_rate_hz = 1e6 / self.sample_period_us
+        self.answer = answer
+        self.verify = verify
+        self.execution_count = 0
+        self.clock_locked: bool | None = None  # None = never requested
+        #: "locked" (nvmlDeviceSetGpuLockedClocks), "application" (applications
+        #: clocks), "refused" (observed clocks recorded instead) or None (untried)
+        self.clock_mode: str | None = None
+        self.last_observed_clock: float | None = None
+        self.spec = self._probe_spec()
+        self.state = DeviceState(self.spec.base_clock, self.spec.power_limit_range[1])
+        self._requested_clock: float | None = None
+        self._requested_limit: float | None = None
+        if self.problem.gpu is not self.gpu:
+            self.problem.prepare(self.gpu)
+
+    # -- construction helpers ---------------------------------------------
+    def _probe_spec(self) -> DeviceSpec:
+        info = self.gpu.info
+        clocks = self.gpu.supported_clocks()
+        if len(clocks) < 2:
+            raise CapabilityError(f"NVML reports no supported SM clocks for {self.gpu.name}")
+        peak = max(clocks)
+        base_req = info.default_sm_clock_mhz or peak
+        base = min(clocks, key=lambda c: (abs(c - base_req), -c))
+        lo = info.power_limit_min_mw / 1000.0 or 100.0
+        hi = info.power_limit_max_mw / 1000.0 or 1000.0
+        tdp = max(info.power_limit_default_mw / 1000.0, hi)
+        if not 0 < lo < hi:
+            lo, hi = 0.5 * hi, hi
+        return DeviceSpec(
+            name=f"{self.gpu.name} (cuda:{self.gpu.ordinal}, {info.pci_bus_id.decode()})",
+            supported_core_clocks=tuple(float(c) for c in clocks),
+            base_clock=float(base),
+            peak_clock=float(peak),
+            power_limit_range=(lo, hi),
+            tdp=tdp,
+            voltage_readable=False,
+        )
+
+    @classmethod
+    def from_document(cls, data: Mapping[str, Any]) -> "B200Device":
+        """``{"kind": "b200", "kernel": "conv2d", "ordinal": 0, ...}`` device files."""
+        extra = {k: data[k] for k in ("min_window", "settle", "clock_settle", "sample_period_us") if k in data}
+        return cls(data.get("kernel", "conv2d"), int(data.get("ordinal", 0)),
+                   problem_kwargs=data.get("problem", {}), **extra)
+
+    def close(self) -> None:
+        try:
+            if self._requested_clock is not None:
+                self._reset_clock()
+            if self._requested_limit is not None:
+                self.gpu.reset_power_limit()
+        finally:
+            self._requested_clock = None
+            self._requested_limit = None
+            if self._owns_gpu:
+                self.gpu.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- controller -----------------------------------------------------------
+    def set_core_clock(self, clock: float) -> DeviceState:
+        if clock not in self.spec.supported_core_clocks:
+            raise DomainError(
+                f"{clock} MHz is not supported on {self.spec.name}; supported: {list(self.spec.supported_core_clocks)}"
+            )
+        if self._requested_clock != float(clock):
+            self.clock_locked = self._apply_clock(int(clock))
+            self._requested_clock = float(clock)
+            time.sleep(self.clock_settle)
+        self.state = replace(self.state, core_clock=float(clock))
+        return self.state
+
+    def _apply_clock(self, mhz: int) -> bool:
+        """Locked clocks, else applications clocks; False if NVML refuses both."""
+        if self.clock_mode in (None, "locked"):
+            if self.gpu.lock_clocks(mhz, mhz):
+                self.clock_mode = "locked"
+                return True
+        if self.clock_mode in (None, "application"):
+            if self.gpu.set_app_clocks(int(self.gpu.info.mem_clock_mhz), mhz):
+                self.clock_mode = "application"
+                return True
+        self.clock_mode = "refused"
+        return False
+
+    def release_clock(self) -> None:
+        """Back to driver-managed clocks (e.g. before an untuned measurement)."""
+        if self._requested_clock is not None:
+            self._reset_clock()
+            self._requested_clock = None
+            self.clock_locked = None
+            time.sleep(self.clock_settle)
+
+    def _reset_clock(self) -> None:
+        if self.clock_mode == "locked":
+            self.gpu.reset_clocks()
+        elif self.clock_mode == "application":
+            self.gpu.reset_app_clocks()
+
+    def set_power_limit(self, watts: float) -> DeviceState:
+        lo, hi = self.spec.power_limit_range
+        if not lo <= watts <= hi:
+            raise DomainError(f"power limit {watts} W outside [{lo}, {hi}] W on {self.spec.name}")
+        if self._requested_limit != float(watts):
+            self.gpu.set_power_limit(float(watts))
+            self._requested_limit = float(watts)
+            time.sleep(self.clock_settle)
+        self.state = replace(self.state, power_limit=float(watts))
+        return self.state
+
+    def effective_clock(self, requested: float | None = None, *, utilization: float = 1.0) -> float:
+        if self.last_observed_clock is not None:
+            return self.last_observed_clock
+        return self.state.core_clock if requested is None else requested
+
+    def read_voltage(self, clock: float) -> float:
+        raise CapabilityError(f"{self.spec.name} does not expose core voltage through NVML")
+
+    # -- execution ----------------------------------------------------------------
+    def kernel_view(self, config: KernelConfig) -> KernelConfig:
+        return config.drop(*EXECUTION_PARAMS)
+
+    def _compiled(self, config: KernelConfig):
+        kernel_cfg = self.kernel_view(config).normalized().as_dict()
+        defaults = self.problem.default_config()
+        merged = {**defaults, **kernel_cfg} if kernel_cfg.keys() <= defaults.keys() else kernel_cfg
+        kernel = self.problem.kernel(merged)
+        launch = self.problem.launch(merged)
+        if launch.threads > 1024:
+            raise DomainError(f"{launch.threads} threads per block exceed the 1024 limit")
+        return merged, kernel, launch
+
+    def probe_runtime(self, config: KernelConfig) -> float:
+        merged, kernel, launch = self._compiled(config)
+        self.problem.bind(kernel, merged)
+        args = self.problem.args(merged)
+        self.gpu.time(kernel, launch, args, reps=1)  # warm-up
+        return self.gpu.time(kernel, launch, args, reps=1)
+
+    def execute(self, config: KernelConfig, duration_hint: float = 0.0) -> Execution:
+        merged, kernel, launch = self._compiled(config)
+        self.problem.bind(kernel, merged)
+        args = self.problem.args(merged)
+        if self.answer is not None:
+            self.problem.reset_output()
+        run = self.gpu.bench(
+            kernel,
+            launch,
+            args,
+            min_seconds=max(float(duration_hint), self.min_window),
+            sample_period_us=self.sample_period_us,
+        )
+        self.execution_count += 1
+        if self.answer is not None:
+            self._check_answer(merged)
+        return self._execution(run)
+
+    def _check_answer(self, config) -> None:
+        got = self.problem.fetch_output()
+        if self.verify is not None:
+            ok = self.verify(got, self.answer, config)
+        else:
+            ok = np.array_equal(got, self.answer)
+        if not ok:
+            raise DomainError(f"output of {self.problem.name} config {config} does not match the answer")
+
+    def _execution(self, run) -> Execution:
+        total = run.total_s
+        t0 = run.loop_t0
+        trace: list[PowerSample] = []
+        before = [s for s in run.samples if s[T] < t0]
+        during = [s for s in run.samples if t0 <= s[T] <= t0 + total]
+        after = [s for s in run.samples if s[T] > t0 + total]
+        if before and math.isfinite(before[-1][P_INST]):
+            trace.append(PowerSample(0.0, before[-1][P_INST]))
+        for s in during:
+            if math.isfinite(s[P_INST]):
+                trace.append(PowerSample(s[T] - t0, s[P_INST]))
+        if after and math.isfinite(after[0][P_INST]):
+            trace.append(PowerSample(total, after[0][P_INST]))
+        window = steady_window(total, self.settle)
+        steady = [s for s in during if window[0] <= s[T] - t0 <= window[1]] or during or run.samples
+        slope = counter_slope(run.samples, t0 + window[0], t0 + window[1])
+        if slope is None:
+            # counter cadence longer than the window: fall back to the whole loop
+            slope = counter_slope(run.samples, t0 - 0.05, t0 + total + 0.05)
+        clocks = [s[SM_MHZ] for s in steady if s[SM_MHZ]]
+        observed = float(statistics.median(clocks)) if clocks else float(self.state.core_clock)
+        self.last_observed_clock = observed
+        reasons = 0
+        for s in steady:
+            reasons |= int(s[REASONS])
+        telemetry = {
+            "sm_clock": observed,
+            "mem_clock": float(statistics.median([s[MEM_MHZ] for s in steady])) if steady else math.nan,
+            "temperature": float(statistics.median([s[TEMP] for s in steady])) if steady else math.nan,
+            "clock_locked": 1.0 if self.clock_locked else 0.0,
+            "throttle_reasons": float(reasons),
+            "power_capped": 1.0 if reasons & SW_POWER_CAP else 0.0,
+            "reps": float(run.reps),
+        }
+        return Execution(
+            runtime=run.per_launch_s,
+            samples=tuple(trace),
+            effective_clock=observed,
+            repetitions=run.reps,
+            total_duration=total,
+            window=window,
+            counter_energy=None if slope is None else slope * total,
+            counter_power=slope,
+            telemetry=telemetry,
+        )
+
+    # -- helpers for workflows ---------------------------------------------------
+    def clock_grid(self, step_mhz: float | None = None, lo: float | None = None) -> list[int]:
+        """Supported clocks, optionally thinned to >= step_mhz apart and >= lo."""
+        grid = [int(normalize_value(c)) for c in self.spec.supported_core_clocks]
+        if lo is not None:
+            grid = [c for c in grid if c >= lo]
+        if step_mhz:
+            thinned = [grid[-1]]
+            for c in reversed(grid[:-1]):
+                if thinned[-1] - c >= step_mhz:
+                    thinned.append(c)
+            grid = sorted(thinned)
+        return grid

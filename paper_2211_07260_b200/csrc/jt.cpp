@@ -1,0 +1,942 @@
+// libjt — the B200 device boundary (see include/jt.h for the contract).
+//
+// Host-side runtime only: CUDA driver API (primary context, one
+// non-blocking stream per ctx, CUDA events), NVRTC for per-config kernel
+// compilation to sm_100a cubins, and NVML (dlopen'ed, so the library loads on
+// machines without a driver) for the sampler thread and the clock / power
+// controller. The kernels themselves live in csrc/kernels/*.cu and reach the
+// GPU through jt_compile + jt_module_load.
+#include "jt.h"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvml.h>
+#include <nvrtc.h>
+#include <time.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_error = buf;
+    return code;
+}
+
+double mono_now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
+double real_now() {
+    timespec ts;
+    clock_gettime(CLOCK_REALTIME, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
+
+// ---------------------------------------------------------------------------
+// CUDA driver, resolved at runtime through cuGetProcAddress so that libjt
+// loads (and its symbols can be inspected) on a machine without a driver.
+#define JT_DRIVER_FNS(X) \
+    X(cuCtxSetCurrent) \
+    X(cuDeviceGet) \
+    X(cuDeviceGetAttribute) \
+    X(cuDeviceGetCount) \
+    X(cuDeviceGetName) \
+    X(cuDeviceGetPCIBusId) \
+    X(cuDevicePrimaryCtxRelease) \
+    X(cuDevicePrimaryCtxRetain) \
+    X(cuDeviceTotalMem) \
+    X(cuEventCreate) \
+    X(cuEventDestroy) \
+    X(cuEventElapsedTime) \
+    X(cuEventRecord) \
+    X(cuEventSynchronize) \
+    X(cuFuncGetAttribute) \
+    X(cuFuncSetAttribute) \
+    X(cuGetErrorName) \
+    X(cuGetErrorString) \
+    X(cuInit) \
+    X(cuLaunchKernel) \
+    X(cuLaunchKernelEx) \
+    X(cuMemAlloc) \
+    X(cuMemFree) \
+    X(cuMemFreeHost) \
+    X(cuMemHostAlloc) \
+    X(cuMemcpyDtoHAsync) \
+    X(cuMemcpyHtoDAsync) \
+    X(cuMemsetD8Async) \
+    X(cuModuleGetFunction) \
+    X(cuModuleGetGlobal) \
+    X(cuModuleLoadData) \
+    X(cuModuleUnload) \
+    X(cuStreamCreate) \
+    X(cuStreamDestroy) \
+    X(cuStreamSynchronize)
+
+struct Driver {
+    bool ok = false;
+#define JT_DECL(fn) decltype(&::fn) p_##fn = nullptr;
+    JT_DRIVER_FNS(JT_DECL)
+#undef JT_DECL
+};
+
+Driver D;
+std::once_flag g_driver_once;
+std::string g_driver_why;
+
+void driver_load() {
+    void *lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_LOCAL);
+    if (!lib) lib = dlopen("libcuda.so", RTLD_NOW | RTLD_LOCAL);
+    if (!lib) {
+        g_driver_why = "libcuda.so.1 not found (no NVIDIA driver)";
+        return;
+    }
+    using getproc_t = CUresult (*)(const char *, void **, int, cuuint64_t, CUdriverProcAddressQueryResult *);
+    auto getproc = reinterpret_cast<getproc_t>(dlsym(lib, "cuGetProcAddress_v2"));
+    if (!getproc) {
+        g_driver_why = "driver lacks cuGetProcAddress_v2 (needs a CUDA 12 driver)";
+        return;
+    }
+    bool all = true;
+#define JT_LOAD(fn)                                                                          \
+    {                                                                                        \
+        CUdriverProcAddressQueryResult st;                                                   \
+        if (getproc(#fn, reinterpret_cast<void **>(&D.p_##fn), CUDA_VERSION, 0, &st) != CUDA_SUCCESS || !D.p_##fn) { \
+            all = false;                                                                     \
+            g_driver_why = "driver symbol missing: " #fn;                                    \
+        }                                                                                    \
+    }
+    JT_DRIVER_FNS(JT_LOAD)
+#undef JT_LOAD
+    D.ok = all;
+}
+
+bool driver_ready() {
+    std::call_once(g_driver_once, driver_load);
+    return D.ok;
+}
+
+const char *cu_name(CUresult r) {
+    const char *s = nullptr;
+    if (D.p_cuGetErrorName) D.p_cuGetErrorName(r, &s);
+    return s ? s : "CUDA_ERROR_?";
+}
+
+int cu_fail(CUresult r, const char *what) {
+    const char *desc = nullptr;
+    if (D.p_cuGetErrorString) D.p_cuGetErrorString(r, &desc);
+    int code = JT_ECUDA;
+    switch (r) {
+        case CUDA_ERROR_NO_DEVICE:
+        case CUDA_ERROR_NOT_INITIALIZED:
+        case CUDA_ERROR_INVALID_DEVICE:
+        case CUDA_ERROR_STUB_LIBRARY:
+            code = JT_ENOGPU;
+            break;
+        case CUDA_ERROR_INVALID_VALUE:
+        case CUDA_ERROR_LAUNCH_OUT_OF_RESOURCES:
+        case CUDA_ERROR_INVALID_CLUSTER_SIZE:
+        case CUDA_ERROR_NOT_SUPPORTED:
+            code = JT_ELAUNCH;
+            break;
+        default:
+            break;
+    }
+    return fail(code, "%s: %s (%s)", what, cu_name(r), desc ? desc : "");
+}
+
+#define CU_TRY(call, what)                          \
+    do {                                            \
+        CUresult r_ = (call);                       \
+        if (r_ != CUDA_SUCCESS) return cu_fail(r_, what); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// NVML, resolved at runtime.
+struct Nvml {
+    void *lib = nullptr;
+    bool ok = false;
+    nvmlReturn_t (*Init)() = nullptr;
+    const char *(*ErrorString)(nvmlReturn_t) = nullptr;
+    nvmlReturn_t (*HandleByPci)(const char *, nvmlDevice_t *) = nullptr;
+    nvmlReturn_t (*FieldValues)(nvmlDevice_t, int, nvmlFieldValue_t *) = nullptr;
+    nvmlReturn_t (*PowerUsage)(nvmlDevice_t, unsigned *) = nullptr;
+    nvmlReturn_t (*TotalEnergy)(nvmlDevice_t, unsigned long long *) = nullptr;
+    nvmlReturn_t (*ClockInfo)(nvmlDevice_t, nvmlClockType_t, unsigned *) = nullptr;
+    nvmlReturn_t (*MaxClockInfo)(nvmlDevice_t, nvmlClockType_t, unsigned *) = nullptr;
+    nvmlReturn_t (*DefaultAppClock)(nvmlDevice_t, nvmlClockType_t, unsigned *) = nullptr;
+    nvmlReturn_t (*Temperature)(nvmlDevice_t, nvmlTemperatureSensors_t, unsigned *) = nullptr;
+    nvmlReturn_t (*Reasons)(nvmlDevice_t, unsigned long long *) = nullptr;
+    nvmlReturn_t (*MemClocks)(nvmlDevice_t, unsigned *, unsigned *) = nullptr;
+    nvmlReturn_t (*GrClocks)(nvmlDevice_t, unsigned, unsigned *, unsigned *) = nullptr;
+    nvmlReturn_t (*LimitRange)(nvmlDevice_t, unsigned *, unsigned *) = nullptr;
+    nvmlReturn_t (*Limit)(nvmlDevice_t, unsigned *) = nullptr;
+    nvmlReturn_t (*DefaultLimit)(nvmlDevice_t, unsigned *) = nullptr;
+    nvmlReturn_t (*EnforcedLimit)(nvmlDevice_t, unsigned *) = nullptr;
+    nvmlReturn_t (*SetLocked)(nvmlDevice_t, unsigned, unsigned) = nullptr;
+    nvmlReturn_t (*ResetLocked)(nvmlDevice_t) = nullptr;
+    nvmlReturn_t (*SetLimit)(nvmlDevice_t, unsigned) = nullptr;
+    nvmlReturn_t (*SetAppClocks)(nvmlDevice_t, unsigned, unsigned) = nullptr;
+    nvmlReturn_t (*ResetAppClocks)(nvmlDevice_t) = nullptr;
+};
+
+Nvml g_nvml;
+std::once_flag g_nvml_once;
+
+template <class F>
+void sym(void *lib, F &fn, const char *name) {
+    fn = reinterpret_cast<F>(dlsym(lib, name));
+}
+
+void nvml_load() {
+    const char *names[] = {"libnvidia-ml.so.1", "libnvidia-ml.so"};
+    for (const char *n : names) {
+        g_nvml.lib = dlopen(n, RTLD_NOW | RTLD_LOCAL);
+        if (g_nvml.lib) break;
+    }
+    if (!g_nvml.lib) return;
+    void *l = g_nvml.lib;
+    sym(l, g_nvml.Init, "nvmlInit_v2");
+    sym(l, g_nvml.ErrorString, "nvmlErrorString");
+    sym(l, g_nvml.HandleByPci, "nvmlDeviceGetHandleByPciBusId_v2");
+    sym(l, g_nvml.FieldValues, "nvmlDeviceGetFieldValues");
+    sym(l, g_nvml.PowerUsage, "nvmlDeviceGetPowerUsage");
+    sym(l, g_nvml.TotalEnergy, "nvmlDeviceGetTotalEnergyConsumption");
+    sym(l, g_nvml.ClockInfo, "nvmlDeviceGetClockInfo");
+    sym(l, g_nvml.MaxClockInfo, "nvmlDeviceGetMaxClockInfo");
+    sym(l, g_nvml.DefaultAppClock, "nvmlDeviceGetDefaultApplicationsClock");
+    sym(l, g_nvml.Temperature, "nvmlDeviceGetTemperature");
+    sym(l, g_nvml.Reasons, "nvmlDeviceGetCurrentClocksEventReasons");
+    if (!g_nvml.Reasons) sym(l, g_nvml.Reasons, "nvmlDeviceGetCurrentClocksThrottleReasons");
+    sym(l, g_nvml.MemClocks, "nvmlDeviceGetSupportedMemoryClocks");
+    sym(l, g_nvml.GrClocks, "nvmlDeviceGetSupportedGraphicsClocks");
+    sym(l, g_nvml.LimitRange, "nvmlDeviceGetPowerManagementLimitConstraints");
+    sym(l, g_nvml.Limit, "nvmlDeviceGetPowerManagementLimit");
+    sym(l, g_nvml.DefaultLimit, "nvmlDeviceGetPowerManagementDefaultLimit");
+    sym(l, g_nvml.EnforcedLimit, "nvmlDeviceGetEnforcedPowerLimit");
+    sym(l, g_nvml.SetLocked, "nvmlDeviceSetGpuLockedClocks");
+    sym(l, g_nvml.ResetLocked, "nvmlDeviceResetGpuLockedClocks");
+    sym(l, g_nvml.SetLimit, "nvmlDeviceSetPowerManagementLimit");
+    sym(l, g_nvml.SetAppClocks, "nvmlDeviceSetApplicationsClocks");
+    sym(l, g_nvml.ResetAppClocks, "nvmlDeviceResetApplicationsClocks");
+    g_nvml.ok = g_nvml.Init && g_nvml.HandleByPci && g_nvml.Init() == NVML_SUCCESS;
+}
+
+const char *nvml_err(nvmlReturn_t r) {
+    return g_nvml.ErrorString ? g_nvml.ErrorString(r) : "nvml error";
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct jt_module {
+    CUmodule mod;
+};
+
+struct jt_kernel {
+    CUfunction fn;
+    unsigned smem_attr = 0;  // dynamic smem limit already raised to this value
+};
+
+struct jt_ctx {
+    int ordinal = 0;
+    CUdevice dev = 0;
+    CUcontext cu = nullptr;
+    CUstream stream = nullptr;
+    CUevent ev_a = nullptr, ev_b = nullptr;
+    CUdeviceptr flush_buf = 0;
+    size_t flush_bytes = 0;
+    jt_device_info info{};
+    nvmlDevice_t nvdev = nullptr;
+    bool have_nvml = false;
+    double realtime_offset = 0.0;  // real_now() - mono_now() at open
+    bool clocks_locked = false;
+    bool app_clocks_set = false;
+    bool limit_changed = false;
+    // sampler
+    std::thread sampler;
+    std::atomic<bool> sampling{false};
+    std::mutex sample_mu;
+    std::vector<jt_sample> samples;
+    size_t sample_cap = 0;
+    int period_us = 1000;
+    std::vector<jt_module *> modules;
+    std::vector<jt_kernel *> kernels;
+};
+
+namespace {
+
+std::mutex g_open_mu;
+std::set<jt_ctx *> g_open;
+std::once_flag g_atexit_once;
+
+void reset_controls(jt_ctx *c) {
+    if (!c->have_nvml) return;
+    if (c->clocks_locked && g_nvml.ResetLocked) {
+        g_nvml.ResetLocked(c->nvdev);
+        c->clocks_locked = false;
+    }
+    if (c->app_clocks_set && g_nvml.ResetAppClocks) {
+        g_nvml.ResetAppClocks(c->nvdev);
+        c->app_clocks_set = false;
+    }
+    if (c->limit_changed && g_nvml.SetLimit && c->info.power_limit_default_mw) {
+        g_nvml.SetLimit(c->nvdev, c->info.power_limit_default_mw);
+        c->limit_changed = false;
+    }
+}
+
+void reset_all_at_exit() {
+    std::lock_guard<std::mutex> g(g_open_mu);
+    for (jt_ctx *c : g_open) reset_controls(c);
+}
+
+int bind(jt_ctx *c) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    CU_TRY(D.p_cuCtxSetCurrent(c->cu), "cuCtxSetCurrent");
+    return JT_OK;
+}
+
+void read_sample(jt_ctx *c, jt_sample *s) {
+    std::memset(s, 0, sizeof *s);
+    s->t_s = mono_now();
+    s->power_w = NAN;
+    s->power_avg_w = NAN;
+    s->energy_j = NAN;
+    s->energy_stamp_s = NAN;
+    if (!c->have_nvml) return;
+    nvmlFieldValue_t fv[2];
+    std::memset(fv, 0, sizeof fv);
+    fv[0].fieldId = NVML_FI_DEV_POWER_INSTANT;
+    fv[1].fieldId = NVML_FI_DEV_TOTAL_ENERGY_CONSUMPTION;
+    if (g_nvml.FieldValues && g_nvml.FieldValues(c->nvdev, 2, fv) == NVML_SUCCESS) {
+        if (fv[0].nvmlReturn == NVML_SUCCESS) {
+            double mw = fv[0].valueType == NVML_VALUE_TYPE_UNSIGNED_LONG_LONG ? (double)fv[0].value.ullVal
+                                                                               : (double)fv[0].value.uiVal;
+            s->power_w = mw * 1e-3;
+        }
+        if (fv[1].nvmlReturn == NVML_SUCCESS) {
+            s->energy_j = (double)fv[1].value.ullVal * 1e-3;
+            s->energy_stamp_s = (double)fv[1].timestamp * 1e-6 - c->realtime_offset;
+        }
+    }
+    if (std::isnan(s->energy_j) && g_nvml.TotalEnergy) {
+        unsigned long long mj = 0;
+        if (g_nvml.TotalEnergy(c->nvdev, &mj) == NVML_SUCCESS) s->energy_j = mj * 1e-3;
+    }
+    unsigned v = 0;
+    if (g_nvml.PowerUsage && g_nvml.PowerUsage(c->nvdev, &v) == NVML_SUCCESS) s->power_avg_w = v * 1e-3;
+    if (g_nvml.ClockInfo && g_nvml.ClockInfo(c->nvdev, NVML_CLOCK_SM, &v) == NVML_SUCCESS) s->sm_mhz = v;
+    if (g_nvml.ClockInfo && g_nvml.ClockInfo(c->nvdev, NVML_CLOCK_MEM, &v) == NVML_SUCCESS) s->mem_mhz = v;
+    if (g_nvml.Temperature && g_nvml.Temperature(c->nvdev, NVML_TEMPERATURE_GPU, &v) == NVML_SUCCESS)
+        s->temp_c = v;
+    unsigned long long reasons = 0;
+    if (g_nvml.Reasons && g_nvml.Reasons(c->nvdev, &reasons) == NVML_SUCCESS) s->reasons = reasons;
+}
+
+void sampler_loop(jt_ctx *c) {
+    using clk = std::chrono::steady_clock;
+    auto next = clk::now();
+    const auto period = std::chrono::microseconds(c->period_us);
+    while (c->sampling.load(std::memory_order_relaxed)) {
+        jt_sample s;
+        read_sample(c, &s);
+        {
+            std::lock_guard<std::mutex> g(c->sample_mu);
+            if (c->samples.size() < c->sample_cap) c->samples.push_back(s);
+        }
+        next += period;
+        auto now = clk::now();
+        if (next < now) next = now;  // fell behind: do not burst
+        std::this_thread::sleep_until(next);
+    }
+}
+
+int start_sampler(jt_ctx *c, int period_us, int cap) {
+    if (c->sampling.load()) return fail(JT_EINVAL, "sampler already running");
+    c->period_us = std::max(period_us, 100);
+    c->sample_cap = (size_t)std::max(cap, 1);
+    c->samples.clear();
+    c->samples.reserve(c->sample_cap);
+    c->sampling.store(true);
+    c->sampler = std::thread(sampler_loop, c);
+    return JT_OK;
+}
+
+int stop_sampler(jt_ctx *c, jt_sample *out, int cap, int *n) {
+    if (!c->sampling.load()) {
+        if (n) *n = 0;
+        return JT_OK;
+    }
+    c->sampling.store(false);
+    if (c->sampler.joinable()) c->sampler.join();
+    // one closing sample so the trace covers the end of the measured region
+    jt_sample last;
+    read_sample(c, &last);
+    std::lock_guard<std::mutex> g(c->sample_mu);
+    if (c->samples.size() < c->sample_cap) c->samples.push_back(last);
+    int k = (int)std::min<size_t>(c->samples.size(), (size_t)std::max(cap, 0));
+    if (out && k) std::memcpy(out, c->samples.data(), k * sizeof(jt_sample));
+    if (n) *n = k;
+    return JT_OK;
+}
+
+int launch_on(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, void **params) {
+    if (s->smem_bytes > 48 * 1024 && s->smem_bytes != k->smem_attr) {
+        CUresult r = D.p_cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)s->smem_bytes);
+        if (r != CUDA_SUCCESS) return cu_fail(r, "raise dynamic shared memory limit");
+        k->smem_attr = s->smem_bytes;
+    }
+    if (s->cluster_x > 1) {
+        CUlaunchConfig cfg;
+        std::memset(&cfg, 0, sizeof cfg);
+        cfg.gridDimX = s->grid[0];
+        cfg.gridDimY = s->grid[1];
+        cfg.gridDimZ = s->grid[2];
+        cfg.blockDimX = s->block[0];
+        cfg.blockDimY = s->block[1];
+        cfg.blockDimZ = s->block[2];
+        cfg.sharedMemBytes = s->smem_bytes;
+        cfg.hStream = c->stream;
+        CUlaunchAttribute attr;
+        std::memset(&attr, 0, sizeof attr);
+        attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+        attr.value.clusterDim.x = s->cluster_x;
+        attr.value.clusterDim.y = 1;
+        attr.value.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        CU_TRY(D.p_cuLaunchKernelEx(&cfg, k->fn, params, nullptr), "cuLaunchKernelEx");
+        return JT_OK;
+    }
+    CU_TRY(D.p_cuLaunchKernel(k->fn, s->grid[0], s->grid[1], s->grid[2], s->block[0], s->block[1], s->block[2],
+                          s->smem_bytes, c->stream, params, nullptr),
+           "cuLaunchKernel");
+    return JT_OK;
+}
+
+int pack_args(const jt_arg *args, int n, std::vector<void *> &params) {
+    if (n < 0 || (n > 0 && !args)) return fail(JT_EINVAL, "bad argument list");
+    params.resize(n);
+    for (int i = 0; i < n; ++i) {
+        const jt_arg &a = args[i];
+        switch (a.kind) {
+            case JT_ARG_PTR: params[i] = (void *)&a.v.ptr; break;
+            case JT_ARG_I32: params[i] = (void *)&a.v.i32; break;
+            case JT_ARG_F32: params[i] = (void *)&a.v.f32; break;
+            case JT_ARG_F64: params[i] = (void *)&a.v.f64; break;
+            case JT_ARG_I64: params[i] = (void *)&a.v.i64; break;
+            default: return fail(JT_EINVAL, "argument %d has unknown kind %d", i, a.kind);
+        }
+    }
+    return JT_OK;
+}
+
+int check_shape(const jt_launch_shape *s) {
+    if (!s) return fail(JT_EINVAL, "null launch shape");
+    for (int i = 0; i < 3; ++i)
+        if (s->grid[i] == 0 || s->block[i] == 0) return fail(JT_ELAUNCH, "zero grid/block dimension");
+    return JT_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int jt_abi_version(void) { return JT_ABI_VERSION; }
+
+double jt_now(void) { return mono_now(); }
+
+const char *jt_last_error(void) { return g_error.c_str(); }
+
+int jt_device_count(int *count) {
+    if (!count) return fail(JT_EINVAL, "null count");
+    *count = 0;
+    if (!driver_ready()) return fail(JT_ENOGPU, "%s", g_driver_why.c_str());
+    CUresult r = D.p_cuInit(0);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuInit");
+    CU_TRY(D.p_cuDeviceGetCount(count), "cuDeviceGetCount");
+    return JT_OK;
+}
+
+int jt_open(int ordinal, jt_ctx **out) {
+    if (!out) return fail(JT_EINVAL, "null out");
+    *out = nullptr;
+    if (!driver_ready()) return fail(JT_ENOGPU, "%s", g_driver_why.c_str());
+    CUresult r = D.p_cuInit(0);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuInit (no usable CUDA driver/GPU)");
+    int n = 0;
+    CU_TRY(D.p_cuDeviceGetCount(&n), "cuDeviceGetCount");
+    if (ordinal < 0 || ordinal >= n) return fail(JT_ENOGPU, "CUDA ordinal %d not present (%d devices)", ordinal, n);
+    auto *c = new jt_ctx();
+    c->ordinal = ordinal;
+    c->realtime_offset = real_now() - mono_now();
+    auto bail = [&](int code) {
+        delete c;
+        return code;
+    };
+    if ((r = D.p_cuDeviceGet(&c->dev, ordinal)) != CUDA_SUCCESS) return bail(cu_fail(r, "cuDeviceGet"));
+    if ((r = D.p_cuDevicePrimaryCtxRetain(&c->cu, c->dev)) != CUDA_SUCCESS) return bail(cu_fail(r, "retain primary ctx"));
+    if ((r = D.p_cuCtxSetCurrent(c->cu)) != CUDA_SUCCESS) return bail(cu_fail(r, "cuCtxSetCurrent"));
+    if ((r = D.p_cuStreamCreate(&c->stream, CU_STREAM_NON_BLOCKING)) != CUDA_SUCCESS) return bail(cu_fail(r, "stream"));
+    if ((r = D.p_cuEventCreate(&c->ev_a, CU_EVENT_DEFAULT)) != CUDA_SUCCESS) return bail(cu_fail(r, "event"));
+    if ((r = D.p_cuEventCreate(&c->ev_b, CU_EVENT_DEFAULT)) != CUDA_SUCCESS) return bail(cu_fail(r, "event"));
+
+    jt_device_info &d = c->info;
+    d.ordinal = ordinal;
+    D.p_cuDeviceGetName(d.name, sizeof d.name, c->dev);
+    D.p_cuDeviceGetAttribute(&d.cc_major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, c->dev);
+    D.p_cuDeviceGetAttribute(&d.cc_minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, c->dev);
+    D.p_cuDeviceGetAttribute(&d.sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, c->dev);
+    D.p_cuDeviceGetAttribute(&d.max_smem_optin, CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_BLOCK_OPTIN, c->dev);
+    D.p_cuDeviceGetAttribute(&d.l2_bytes, CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE, c->dev);
+    size_t mem = 0;
+    D.p_cuDeviceTotalMem(&mem, c->dev);
+    d.total_mem = mem;
+    D.p_cuDeviceGetPCIBusId(d.pci_bus_id, sizeof d.pci_bus_id, c->dev);
+
+    std::call_once(g_nvml_once, nvml_load);
+    if (g_nvml.ok && g_nvml.HandleByPci(d.pci_bus_id, &c->nvdev) == NVML_SUCCESS) {
+        c->have_nvml = true;
+        d.nvml_ok = 1;
+        jt_sample probe;
+        read_sample(c, &probe);
+        d.energy_counter_ok = !std::isnan(probe.energy_j);
+        d.instant_power_ok = !std::isnan(probe.power_w);
+        unsigned mems[64];
+        unsigned nm = 64;
+        if (g_nvml.MemClocks && g_nvml.MemClocks(c->nvdev, &nm, mems) == NVML_SUCCESS && nm > 0) {
+            d.mem_clock_mhz = *std::max_element(mems, mems + nm);
+            unsigned ng = 512;
+            unsigned grs[512];
+            if (g_nvml.GrClocks && g_nvml.GrClocks(c->nvdev, d.mem_clock_mhz, &ng, grs) == NVML_SUCCESS) {
+                std::sort(grs, grs + ng);
+                ng = (unsigned)(std::unique(grs, grs + ng) - grs);
+                d.n_clocks = ng;
+                std::memcpy(d.clocks_mhz, grs, ng * sizeof(unsigned));
+            }
+        }
+        unsigned v = 0;
+        if (g_nvml.MaxClockInfo && g_nvml.MaxClockInfo(c->nvdev, NVML_CLOCK_SM, &v) == NVML_SUCCESS)
+            d.max_sm_clock_mhz = v;
+        if (g_nvml.DefaultAppClock && g_nvml.DefaultAppClock(c->nvdev, NVML_CLOCK_SM, &v) == NVML_SUCCESS)
+            d.default_sm_clock_mhz = v;
+        unsigned lo = 0, hi = 0;
+        if (g_nvml.LimitRange && g_nvml.LimitRange(c->nvdev, &lo, &hi) == NVML_SUCCESS) {
+            d.power_limit_min_mw = lo;
+            d.power_limit_max_mw = hi;
+        }
+        if (g_nvml.DefaultLimit && g_nvml.DefaultLimit(c->nvdev, &v) == NVML_SUCCESS) d.power_limit_default_mw = v;
+        if (g_nvml.Limit && g_nvml.Limit(c->nvdev, &v) == NVML_SUCCESS) d.power_limit_mw = v;
+        if (g_nvml.EnforcedLimit && g_nvml.EnforcedLimit(c->nvdev, &v) == NVML_SUCCESS) d.tdp_mw = v;
+    }
+    {
+        std::lock_guard<std::mutex> g(g_open_mu);
+        g_open.insert(c);
+    }
+    std::call_once(g_atexit_once, [] { std::atexit(reset_all_at_exit); });
+    *out = c;
+    return JT_OK;
+}
+
+int jt_close(jt_ctx *c) {
+    if (!c) return JT_OK;
+    {
+        std::lock_guard<std::mutex> g(g_open_mu);
+        g_open.erase(c);
+    }
+    if (c->sampling.load()) stop_sampler(c, nullptr, 0, nullptr);
+    reset_controls(c);
+    D.p_cuCtxSetCurrent(c->cu);
+    D.p_cuStreamSynchronize(c->stream);
+    for (jt_kernel *k : c->kernels) delete k;
+    for (jt_module *m : c->modules) {
+        D.p_cuModuleUnload(m->mod);
+        delete m;
+    }
+    if (c->flush_buf) D.p_cuMemFree(c->flush_buf);
+    D.p_cuEventDestroy(c->ev_a);
+    D.p_cuEventDestroy(c->ev_b);
+    D.p_cuStreamDestroy(c->stream);
+    D.p_cuDevicePrimaryCtxRelease(c->dev);
+    delete c;
+    return JT_OK;
+}
+
+int jt_device_info_get(jt_ctx *c, jt_device_info *out) {
+    if (!c || !out) return fail(JT_EINVAL, "null argument");
+    if (c->have_nvml) {
+        unsigned v = 0;
+        if (g_nvml.Limit && g_nvml.Limit(c->nvdev, &v) == NVML_SUCCESS) c->info.power_limit_mw = v;
+    }
+    *out = c->info;
+    return JT_OK;
+}
+
+// --- memory ------------------------------------------------------------------
+int jt_alloc(jt_ctx *c, size_t bytes, unsigned long long *dptr) {
+    if (int e = bind(c)) return e;
+    if (!dptr || bytes == 0) return fail(JT_EINVAL, "bad allocation request");
+    CUdeviceptr p = 0;
+    CU_TRY(D.p_cuMemAlloc(&p, bytes), "cuMemAlloc");
+    *dptr = (unsigned long long)p;
+    return JT_OK;
+}
+
+int jt_free(jt_ctx *c, unsigned long long dptr) {
+    if (int e = bind(c)) return e;
+    CU_TRY(D.p_cuMemFree((CUdeviceptr)dptr), "cuMemFree");
+    return JT_OK;
+}
+
+int jt_host_alloc(jt_ctx *c, size_t bytes, void **hptr) {
+    if (int e = bind(c)) return e;
+    if (!hptr || bytes == 0) return fail(JT_EINVAL, "bad host allocation request");
+    CU_TRY(D.p_cuMemHostAlloc(hptr, bytes, CU_MEMHOSTALLOC_PORTABLE), "cuMemHostAlloc");
+    return JT_OK;
+}
+
+int jt_host_free(jt_ctx *c, void *hptr) {
+    if (int e = bind(c)) return e;
+    CU_TRY(D.p_cuMemFreeHost(hptr), "cuMemFreeHost");
+    return JT_OK;
+}
+
+int jt_h2d(jt_ctx *c, unsigned long long dst, const void *src, size_t bytes) {
+    if (int e = bind(c)) return e;
+    CU_TRY(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, c->stream), "cuMemcpyHtoDAsync");
+    CU_TRY(D.p_cuStreamSynchronize(c->stream), "h2d sync");
+    return JT_OK;
+}
+
+int jt_d2h(jt_ctx *c, void *dst, unsigned long long src, size_t bytes) {
+    if (int e = bind(c)) return e;
+    CU_TRY(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, c->stream), "cuMemcpyDtoHAsync");
+    CU_TRY(D.p_cuStreamSynchronize(c->stream), "d2h sync");
+    return JT_OK;
+}
+
+int jt_memset_d8(jt_ctx *c, unsigned long long dst, unsigned char value, size_t bytes) {
+    if (int e = bind(c)) return e;
+    CU_TRY(D.p_cuMemsetD8Async((CUdeviceptr)dst, value, bytes, c->stream), "cuMemsetD8Async");
+    return JT_OK;
+}
+
+int jt_synchronize(jt_ctx *c) {
+    if (int e = bind(c)) return e;
+    CU_TRY(D.p_cuStreamSynchronize(c->stream), "cuStreamSynchronize");
+    return JT_OK;
+}
+
+// --- compile / load ------------------------------------------------------------
+int jt_compile(const char *source, const char *program_name, const char *const *options, int n_options,
+               void **image, size_t *image_bytes, char *log, size_t log_capacity) {
+    if (!source || !image || !image_bytes) return fail(JT_EINVAL, "null compile argument");
+    *image = nullptr;
+    *image_bytes = 0;
+    if (log && log_capacity) log[0] = 0;
+    nvrtcProgram prog;
+    nvrtcResult r = nvrtcCreateProgram(&prog, source, program_name ? program_name : "kernel.cu", 0, nullptr, nullptr);
+    if (r != NVRTC_SUCCESS) return fail(JT_ECOMPILE, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+    r = nvrtcCompileProgram(prog, n_options, options);
+    size_t log_size = 0;
+    nvrtcGetProgramLogSize(prog, &log_size);
+    if (log && log_capacity && log_size > 1) {
+        std::vector<char> buf(log_size + 1);
+        nvrtcGetProgramLog(prog, buf.data());
+        size_t k = std::min(log_capacity - 1, log_size);
+        std::memcpy(log, buf.data(), k);
+        log[k] = 0;
+    }
+    if (r != NVRTC_SUCCESS) {
+        nvrtcDestroyProgram(&prog);
+        return fail(JT_ECOMPILE, "nvrtcCompileProgram: %s", nvrtcGetErrorString(r));
+    }
+    size_t n = 0;
+    r = nvrtcGetCUBINSize(prog, &n);
+    if (r != NVRTC_SUCCESS || n == 0) {
+        nvrtcDestroyProgram(&prog);
+        return fail(JT_ECOMPILE, "no cubin produced (use --gpu-architecture=sm_100a): %s", nvrtcGetErrorString(r));
+    }
+    void *buf = std::malloc(n);
+    nvrtcGetCUBIN(prog, (char *)buf);
+    nvrtcDestroyProgram(&prog);
+    *image = buf;
+    *image_bytes = n;
+    return JT_OK;
+}
+
+void jt_free_image(void *image) { std::free(image); }
+
+int jt_module_load(jt_ctx *c, const void *image, size_t image_bytes, jt_module **out) {
+    if (int e = bind(c)) return e;
+    if (!image || !image_bytes || !out) return fail(JT_EINVAL, "null module image");
+    CUmodule m;
+    CUresult r = D.p_cuModuleLoadData(&m, image);
+    if (r != CUDA_SUCCESS) {
+        int code = cu_fail(r, "cuModuleLoadData");
+        return code == JT_ECUDA ? JT_ECOMPILE : code;
+    }
+    auto *jm = new jt_module{m};
+    c->modules.push_back(jm);
+    *out = jm;
+    return JT_OK;
+}
+
+int jt_module_unload(jt_ctx *c, jt_module *m) {
+    if (int e = bind(c)) return e;
+    if (!m) return JT_OK;
+    auto it = std::find(c->modules.begin(), c->modules.end(), m);
+    if (it == c->modules.end()) return fail(JT_EINVAL, "module not owned by this context");
+    D.p_cuModuleUnload(m->mod);
+    c->modules.erase(it);
+    delete m;
+    return JT_OK;
+}
+
+int jt_kernel_get(jt_ctx *c, jt_module *m, const char *name, jt_kernel **out) {
+    if (int e = bind(c)) return e;
+    if (!m || !name || !out) return fail(JT_EINVAL, "null kernel lookup argument");
+    CUfunction f;
+    CUresult r = D.p_cuModuleGetFunction(&f, m->mod, name);
+    if (r != CUDA_SUCCESS) return fail(JT_EINVAL, "kernel %s not in module: %s", name, cu_name(r));
+    auto *k = new jt_kernel();
+    k->fn = f;
+    c->kernels.push_back(k);
+    *out = k;
+    return JT_OK;
+}
+
+int jt_kernel_attributes(jt_ctx *c, jt_kernel *k, int *regs, int *static_smem, int *local_bytes, int *max_threads) {
+    if (int e = bind(c)) return e;
+    if (!k) return fail(JT_EINVAL, "null kernel");
+    if (regs) D.p_cuFuncGetAttribute(regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k->fn);
+    if (static_smem) D.p_cuFuncGetAttribute(static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, k->fn);
+    if (local_bytes) D.p_cuFuncGetAttribute(local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, k->fn);
+    if (max_threads) D.p_cuFuncGetAttribute(max_threads, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, k->fn);
+    return JT_OK;
+}
+
+// --- execution -----------------------------------------------------------------
+int jt_launch(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *args, int n_args) {
+    if (int e = bind(c)) return e;
+    if (!k) return fail(JT_EINVAL, "null kernel");
+    if (int e = check_shape(s)) return e;
+    std::vector<void *> params;
+    if (int e = pack_args(args, n_args, params)) return e;
+    return launch_on(c, k, s, params.data());
+}
+
+int jt_time(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *args, int n_args, int reps,
+            double *seconds) {
+    if (int e = bind(c)) return e;
+    if (!k || !seconds || reps < 1) return fail(JT_EINVAL, "bad jt_time arguments");
+    if (int e = check_shape(s)) return e;
+    std::vector<void *> params;
+    if (int e = pack_args(args, n_args, params)) return e;
+    CU_TRY(D.p_cuEventRecord(c->ev_a, c->stream), "cuEventRecord");
+    for (int i = 0; i < reps; ++i)
+        if (int e = launch_on(c, k, s, params.data())) return e;
+    CU_TRY(D.p_cuEventRecord(c->ev_b, c->stream), "cuEventRecord");
+    CU_TRY(D.p_cuEventSynchronize(c->ev_b), "kernel execution");
+    float ms = 0.f;
+    CU_TRY(D.p_cuEventElapsedTime(&ms, c->ev_a, c->ev_b), "cuEventElapsedTime");
+    *seconds = ms * 1e-3;
+    return JT_OK;
+}
+
+int jt_bench(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *args, int n_args, double min_seconds,
+             int min_reps, int max_reps, int sample_period_us, jt_bench_result *out, jt_sample *samples, int cap) {
+    if (int e = bind(c)) return e;
+    if (!k || !out) return fail(JT_EINVAL, "bad jt_bench arguments");
+    if (int e = check_shape(s)) return e;
+    std::memset(out, 0, sizeof *out);
+    std::vector<void *> params;
+    if (int e = pack_args(args, n_args, params)) return e;
+    min_reps = std::max(min_reps, 1);
+    max_reps = std::max(max_reps, min_reps);
+    const bool sampling = samples && cap > 0;
+    if (sampling)
+        if (int e = start_sampler(c, sample_period_us, cap)) return e;
+    auto finish = [&](int code) {
+        if (sampling) {
+            int n = 0;
+            stop_sampler(c, samples, cap, &n);
+            out->n_samples = n;
+        }
+        return code;
+    };
+    // probe launch (also the warm-up): untimed by the loop, timed by events
+    CUresult r;
+    if ((r = D.p_cuEventRecord(c->ev_a, c->stream)) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
+    if (int e = launch_on(c, k, s, params.data())) return finish(e);
+    if ((r = D.p_cuEventRecord(c->ev_b, c->stream)) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
+    if ((r = D.p_cuEventSynchronize(c->ev_b)) != CUDA_SUCCESS) return finish(cu_fail(r, "kernel execution"));
+    float ms = 0.f;
+    D.p_cuEventElapsedTime(&ms, c->ev_a, c->ev_b);
+    out->first_launch_s = ms * 1e-3;
+    double probe = std::max(out->first_launch_s, 1e-7);
+    long want = (long)std::ceil(min_seconds / probe);
+    int reps = (int)std::min<long>(std::max<long>(want, min_reps), max_reps);
+
+    out->host_t_enqueue = mono_now();
+    if ((r = D.p_cuEventRecord(c->ev_a, c->stream)) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
+    for (int i = 0; i < reps; ++i)
+        if (int e = launch_on(c, k, s, params.data())) return finish(e);
+    if ((r = D.p_cuEventRecord(c->ev_b, c->stream)) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
+    if ((r = D.p_cuEventSynchronize(c->ev_b)) != CUDA_SUCCESS) return finish(cu_fail(r, "kernel execution"));
+    out->host_t_done = mono_now();
+    D.p_cuEventElapsedTime(&ms, c->ev_a, c->ev_b);
+    out->total_s = ms * 1e-3;
+    out->reps = reps;
+    out->per_launch_s = out->total_s / reps;
+    out->loop_t0 = out->host_t_done - out->total_s;
+    return finish(JT_OK);
+}
+
+int jt_l2_flush(jt_ctx *c) {
+    if (int e = bind(c)) return e;
+    if (!c->flush_buf) {
+        c->flush_bytes = std::max<size_t>((size_t)c->info.l2_bytes * 2, (size_t)256 << 20);
+        CU_TRY(D.p_cuMemAlloc(&c->flush_buf, c->flush_bytes), "alloc L2 flush buffer");
+    }
+    CU_TRY(D.p_cuMemsetD8Async(c->flush_buf, 0x5a, c->flush_bytes, c->stream), "L2 flush");
+    return JT_OK;
+}
+
+// --- sensors ---------------------------------------------------------------------
+int jt_sample_now(jt_ctx *c, jt_sample *out) {
+    if (!c || !out) return fail(JT_EINVAL, "null argument");
+    read_sample(c, out);
+    return c->have_nvml ? JT_OK : fail(JT_ENVML, "NVML not available for this device");
+}
+
+int jt_sampler_start(jt_ctx *c, int period_us, int cap) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    return start_sampler(c, period_us, cap);
+}
+
+int jt_sampler_stop(jt_ctx *c, jt_sample *out, int cap, int *n) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    return stop_sampler(c, out, cap, n);
+}
+
+// --- controller ------------------------------------------------------------------
+static int nvml_status(nvmlReturn_t r, const char *what) {
+    if (r == NVML_SUCCESS) return JT_OK;
+    if (r == NVML_ERROR_NO_PERMISSION) return fail(JT_ENOPERM, "%s: %s", what, nvml_err(r));
+    if (r == NVML_ERROR_NOT_SUPPORTED) return fail(JT_ENOTSUP, "%s: %s", what, nvml_err(r));
+    if (r == NVML_ERROR_INVALID_ARGUMENT) return fail(JT_EINVAL, "%s: %s", what, nvml_err(r));
+    return fail(JT_ENVML, "%s: %s", what, nvml_err(r));
+}
+
+int jt_clock_lock(jt_ctx *c, unsigned min_mhz, unsigned max_mhz) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    if (!c->have_nvml || !g_nvml.SetLocked) return fail(JT_ENVML, "NVML clock control unavailable");
+    if (min_mhz > max_mhz) return fail(JT_EINVAL, "min clock above max clock");
+    int e = nvml_status(g_nvml.SetLocked(c->nvdev, min_mhz, max_mhz), "nvmlDeviceSetGpuLockedClocks");
+    if (e == JT_OK) c->clocks_locked = true;
+    return e;
+}
+
+int jt_clock_reset(jt_ctx *c) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    if (!c->have_nvml || !g_nvml.ResetLocked) return fail(JT_ENVML, "NVML clock control unavailable");
+    int e = nvml_status(g_nvml.ResetLocked(c->nvdev), "nvmlDeviceResetGpuLockedClocks");
+    if (e == JT_OK) c->clocks_locked = false;
+    return e;
+}
+
+int jt_app_clocks_set(jt_ctx *c, unsigned mem_mhz, unsigned sm_mhz) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    if (!c->have_nvml || !g_nvml.SetAppClocks) return fail(JT_ENVML, "NVML applications clocks unavailable");
+    int e = nvml_status(g_nvml.SetAppClocks(c->nvdev, mem_mhz, sm_mhz), "nvmlDeviceSetApplicationsClocks");
+    if (e == JT_OK) c->app_clocks_set = true;
+    return e;
+}
+
+int jt_app_clocks_reset(jt_ctx *c) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    if (!c->have_nvml || !g_nvml.ResetAppClocks) return fail(JT_ENVML, "NVML applications clocks unavailable");
+    int e = nvml_status(g_nvml.ResetAppClocks(c->nvdev), "nvmlDeviceResetApplicationsClocks");
+    if (e == JT_OK) c->app_clocks_set = false;
+    return e;
+}
+
+int jt_power_limit_set(jt_ctx *c, unsigned mw) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    if (!c->have_nvml || !g_nvml.SetLimit) return fail(JT_ENVML, "NVML power control unavailable");
+    int e = nvml_status(g_nvml.SetLimit(c->nvdev, mw), "nvmlDeviceSetPowerManagementLimit");
+    if (e == JT_OK) c->limit_changed = (mw != c->info.power_limit_default_mw);
+    return e;
+}
+
+int jt_power_limit_reset(jt_ctx *c) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    if (!c->info.power_limit_default_mw) return fail(JT_ENOTSUP, "default power limit unknown");
+    return jt_power_limit_set(c, c->info.power_limit_default_mw);
+}
+
+// --- kernel-suite helpers ---------------------------------------------------------
+int jt_pnpoly_edges(const float *vx, const float *vy, int n, int method, float *edges, float *ybounds) {
+    if (!vx || !vy || !edges || !ybounds || n < 3) return fail(JT_EINVAL, "polygon needs >= 3 vertices");
+    if (method < 0 || method > 2) return fail(JT_EINVAL, "unknown PnPoly method %d", method);
+    for (int k = 0; k < n; ++k) {
+        const int p = (k + n - 1) % n;
+        const float dx = vx[p] - vx[k];
+        const float dy = vy[p] - vy[k];
+        float *e = edges + 4 * k;
+        e[0] = vy[k];
+        if (method == 0) {
+            e[1] = vx[k];
+            e[2] = dx;
+            e[3] = dy;
+        } else {
+            volatile float slope = dx / dy;  // IEEE division, never contracted
+            e[1] = method == 1 ? vx[k] : std::fmaf(-slope, vy[k], vx[k]);
+            e[2] = slope;
+            e[3] = 0.f;
+        }
+        ybounds[2 * k] = std::min(vy[k], vy[p]);
+        ybounds[2 * k + 1] = std::max(vy[k], vy[p]);
+    }
+    return JT_OK;
+}
+
+int jt_module_set_global(jt_ctx *c, jt_module *m, const char *name, const void *src, size_t bytes) {
+    if (int e = bind(c)) return e;
+    if (!m || !name || !src) return fail(JT_EINVAL, "null argument");
+    CUdeviceptr p = 0;
+    size_t size = 0;
+    CUresult r = D.p_cuModuleGetGlobal(&p, &size, m->mod, name);
+    if (r != CUDA_SUCCESS) return fail(JT_EINVAL, "module has no global %s (%s)", name, cu_name(r));
+    if (bytes > size) return fail(JT_EINVAL, "global %s holds %zu bytes, got %zu", name, size, bytes);
+    CU_TRY(D.p_cuMemcpyHtoDAsync(p, src, bytes, c->stream), "copy to module global");
+    CU_TRY(D.p_cuStreamSynchronize(c->stream), "copy to module global");
+    return JT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,497 @@
+// PnPoly point-in-polygon (crossing number), sm_100a, compiled per config by NVRTC.
+//
+// No reference code exists for this kernel: it is the paper's
+// Kernel-Tuner PnPoly benchmark rebuilt for B200. Output bitmap[i] = 1 when
+// point i is inside the polygon (odd number of edge crossings of the ray
+// y = py, x > px).
+//
+// Tunables (-D):
+//   BLOCK_SIZE_X  threads per block
+//   TILE          points per thread (edge data is loaded once per TILE points)
+//   VEC           1: float2 point loads; 2: float4 loads (two points per load)
+//   METHOD        edge crossing formula, each bit-exact against its own
+//                 float32 oracle (oracle/pnpoly_oracle.c):
+//                   0  x = (dx * (py - vy)) / dy + vx      (IEEE div, no FMA)
+//                   1  x = fma(slope, py - vy, vx)         (slope = dx / dy)
+//                   2  x = fma(slope, py, icpt)            (icpt = fma(-slope, vy, vx))
+//   BETWEEN       0: (vy_k > py) != (vy_prev > py)   1: ymin <= py < ymax
+//                 (identical booleans; different instruction shapes)
+//   POLY_SMEM     0: edge table in __constant__ memory; 1: staged in shared memory
+//   VERTICES      polygon size (compile-time so the edge loop is counted)
+//   ASM           1: hand-written PTX edge loop (needs BETWEEN=1, POLY_SMEM=1,
+//                 METHOD 2, TILE in {1,2,4,6}): per edge one LDS.128 of the
+//                 packed record {ymin, ymax, slope, icpt}, then per point
+//                   setp.ge  s, py, ymin; setp.lt.and s, py, ymax, s;
+//                   fma.rn x, slope, py, icpt;
+//                   @s setp.lt.xor in, px, x, in      (toggle fused in the compare)
+//                 with the inside flags living in predicate registers for the
+//                 whole loop (TILE inside flags + 1 scratch <= 7 predicates).
+//                 2: same, but two edges' crossings (s & left) are folded into
+//                 the flag with one 3-input predicate XOR (PLOP3) per point.
+//                 3: sign-bit formulation on the FMA pipe (needs POLY_SMEM=1,
+//                 METHOD=2, TILE in {2,4,6,8}): per edge-point
+//                   FADD d = py - vy_k; FFMA x; FADD e = px - x;
+//                   LOP3 t = (d ^ d_prev) & e; (1/2) LOP3 acc ^= t1 ^ t2
+//                 inside = sign bit of acc. Bit-exact against the oracle's
+//                 formulation 3 (same as formula 2 unless a coordinate is -0.0).
+//
+// Edge table (built on the host in float32, see kernels.py): per edge k from
+// vertex k-1 (cyclic) to vertex k, a float4 {vy_k, a, b, c} and a float2
+// {ymin, ymax}:
+//   METHOD 0: a = vx_k, b = dx = vx_{k-1} - vx_k, c = dy = vy_{k-1} - vy_k
+//   METHOD 1: a = vx_k, b = slope = dx / dy, c = unused
+//   METHOD 2: a = icpt, b = slope,           c = unused
+#ifndef BLOCK_SIZE_X
+#define BLOCK_SIZE_X 256
+#endif
+#ifndef TILE
+#define TILE 4
+#endif
+#ifndef VEC
+#define VEC 1
+#endif
+#ifndef METHOD
+#define METHOD 2
+#endif
+#ifndef BETWEEN
+#define BETWEEN 0
+#endif
+#ifndef POLY_SMEM
+#define POLY_SMEM 0
+#endif
+#ifndef VERTICES
+#define VERTICES 600
+#endif
+#ifndef ASM
+#define ASM 0
+#endif
+#if VEC == 2 && (TILE % 2) != 0
+#error "VEC=2 needs an even TILE"
+#endif
+#if (ASM == 1 || ASM == 2) && !(BETWEEN == 1 && POLY_SMEM == 1 && METHOD == 2 && \
+             (TILE == 1 || TILE == 2 || TILE == 4 || TILE == 6))
+#error "ASM=1|2 needs BETWEEN=1, POLY_SMEM=1, METHOD=2 and TILE in {1,2,4,6}"
+#endif
+#if ASM == 3 && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
+#error "ASM=3 needs POLY_SMEM=1, METHOD=2 and TILE in {2,4,6,8}"
+#endif
+// packed records {ymin, ymax, slope, icpt} (METHOD 2) padded
+// to a multiple of 4 with never-spanning dummies {+inf, -inf, 0, 0}
+#define NPACK (((VERTICES) + 3) / 4 * 4)
+
+#if ASM == 1 || ASM == 2
+#define PT_X(PY) "fma.rn.f32 x, sl, %" PY ", ic;\n"
+#define PT(PIN, PX, PY)                         \
+    "setp.ge.f32 s, %" PY ", ylo;\n"            \
+    "setp.lt.and.f32 s, %" PY ", yhi, s;\n"     \
+    PT_X(PY)                                    \
+    "@s setp.lt.xor.f32 " PIN ", %" PX ", x, " PIN ";\n"
+#define LD_EDGE(OFF) "ld.shared.v4.f32 {ylo, yhi, sl, ic}, [ptr+" OFF "];\n"
+#if TILE == 1
+#define PTS PT("p0", "1", "2")
+#define BASE_OP "3"
+#define END_OP "5"
+#define OUT_SELP "selp.u32 %0, 1, 0, p0;\n"
+#define PREDS ".reg .pred p0, s;\n"
+#define INIT "setp.ne.u32 p0, %4, 0;\n"
+#elif TILE == 2
+#define PTS PT("p0", "2", "4") PT("p1", "3", "5")
+#define BASE_OP "6"
+#define END_OP "8"
+#define OUT_SELP "selp.u32 %0, 1, 0, p0;\n" "selp.u32 %1, 1, 0, p1;\n"
+#define PREDS ".reg .pred p0, p1, s;\n"
+#define INIT "setp.ne.u32 p0, %7, 0;\n" "mov.pred p1, p0;\n"
+#elif TILE == 4
+#define PTS PT("p0", "4", "8") PT("p1", "5", "9") PT("p2", "6", "10") PT("p3", "7", "11")
+#define BASE_OP "12"
+#define END_OP "14"
+#define OUT_SELP "selp.u32 %0, 1, 0, p0;\n" "selp.u32 %1, 1, 0, p1;\n" \
+                 "selp.u32 %2, 1, 0, p2;\n" "selp.u32 %3, 1, 0, p3;\n"
+#define PREDS ".reg .pred p0, p1, p2, p3, s;\n"
+#define INIT "setp.ne.u32 p0, %13, 0;\n" "mov.pred p1, p0;\n" "mov.pred p2, p0;\n" "mov.pred p3, p0;\n"
+#else
+#define PTS PT("p0", "6", "12") PT("p1", "7", "13") PT("p2", "8", "14") \
+            PT("p3", "9", "15") PT("p4", "10", "16") PT("p5", "11", "17")
+#define BASE_OP "18"
+#define END_OP "20"
+#define OUT_SELP "selp.u32 %0, 1, 0, p0;\n" "selp.u32 %1, 1, 0, p1;\n" "selp.u32 %2, 1, 0, p2;\n" \
+                 "selp.u32 %3, 1, 0, p3;\n" "selp.u32 %4, 1, 0, p4;\n" "selp.u32 %5, 1, 0, p5;\n"
+#define PREDS ".reg .pred p0, p1, p2, p3, p4, p5, s;\n"
+#define INIT "setp.ne.u32 p0, %19, 0;\n" "mov.pred p1, p0;\n" "mov.pred p2, p0;\n" \
+             "mov.pred p3, p0;\n" "mov.pred p4, p0;\n" "mov.pred p5, p0;\n"
+#endif
+#if ASM == 2
+// pair mode: two edges per point feed one 3-input predicate XOR (PLOP3)
+#define PT2(PIN, PX, PY)                                 \
+    "setp.ge.f32 s, %" PY ", ylo;\n"                     \
+    "setp.lt.and.f32 s, %" PY ", yhi, s;\n"              \
+    "fma.rn.f32 x, sl, %" PY ", ic;\n"                   \
+    "setp.lt.and.f32 q, %" PX ", x, s;\n"                \
+    "setp.ge.f32 s, %" PY ", ylo2;\n"                    \
+    "setp.lt.and.f32 s, %" PY ", yhi2, s;\n"             \
+    "fma.rn.f32 x, sl2, %" PY ", ic2;\n"                 \
+    "setp.lt.and.f32 s, %" PX ", x, s;\n"                \
+    "xor.pred " PIN ", " PIN ", q;\n"                    \
+    "xor.pred " PIN ", " PIN ", s;\n"
+#define LD_EDGE2(OFF, OFF2) "ld.shared.v4.f32 {ylo, yhi, sl, ic}, [ptr+" OFF "];\n" \
+                            "ld.shared.v4.f32 {ylo2, yhi2, sl2, ic2}, [ptr+" OFF2 "];\n"
+#if TILE == 1
+#define PTS2 PT2("p0", "1", "2")
+#elif TILE == 2
+#define PTS2 PT2("p0", "2", "4") PT2("p1", "3", "5")
+#elif TILE == 4
+#define PTS2 PT2("p0", "4", "8") PT2("p1", "5", "9") PT2("p2", "6", "10") PT2("p3", "7", "11")
+#else
+#define PTS2 PT2("p0", "6", "12") PT2("p1", "7", "13") PT2("p2", "8", "14") \
+             PT2("p3", "9", "15") PT2("p4", "10", "16") PT2("p5", "11", "17")
+#endif
+#define EDGE(OFF) ""
+#define BODY LD_EDGE2("0", "16") PTS2 LD_EDGE2("32", "48") PTS2
+#define EXTRA_REGS ".reg .pred q;\n.reg .f32 ylo2, yhi2, sl2, ic2;\n"
+#else
+#define EDGE(OFF) LD_EDGE(OFF) PTS
+#define BODY EDGE("0") EDGE("16") EDGE("32") EDGE("48")
+#define EXTRA_REGS ""
+#endif
+#endif
+#if ASM == 3
+// sign-bit variant: every comparison becomes the sign of an exactly rounded
+// float32 difference (FADD on the FMA pipe); the crossing bit of edge k for a
+// point is  sign((py - vy_k) ^ (py - vy_{k-1})) & sign(px - x_k)  (one LOP3),
+// and two edges' bits fold into the parity word with one 3-input XOR LOP3.
+#if TILE == 2
+#define S3_POINTS \
+    "sub.rn.f32 da, %4, vy0;\n" "fma.rn.f32 x, sl0, %4, ic0;\n" "sub.rn.f32 e, %2, x;\n" "lop3.b32 t1, da, dp0, e, 0x28;\n" \
+    "sub.rn.f32 db, %4, vy1;\n" "fma.rn.f32 x, sl1, %4, ic1;\n" "sub.rn.f32 e, %2, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %0, %0, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %4, vy2;\n" "fma.rn.f32 x, sl2, %4, ic2;\n" "sub.rn.f32 e, %2, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp0, %4, vy3;\n" "fma.rn.f32 x, sl3, %4, ic3;\n" "sub.rn.f32 e, %2, x;\n" "lop3.b32 t2, dp0, da, e, 0x28;\n" \
+    "lop3.b32 %0, %0, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %5, vy0;\n" "fma.rn.f32 x, sl0, %5, ic0;\n" "sub.rn.f32 e, %3, x;\n" "lop3.b32 t1, da, dp1, e, 0x28;\n" \
+    "sub.rn.f32 db, %5, vy1;\n" "fma.rn.f32 x, sl1, %5, ic1;\n" "sub.rn.f32 e, %3, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %1, %1, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %5, vy2;\n" "fma.rn.f32 x, sl2, %5, ic2;\n" "sub.rn.f32 e, %3, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp1, %5, vy3;\n" "fma.rn.f32 x, sl3, %5, ic3;\n" "sub.rn.f32 e, %3, x;\n" "lop3.b32 t2, dp1, da, e, 0x28;\n" \
+    "lop3.b32 %1, %1, t1, t2, 0x96;\n"
+#define S3_INIT "sub.rn.f32 dp0, %4, %8;\n" "sub.rn.f32 dp1, %5, %8;\n"
+#define S3_REGS ".reg .b32 dp0, dp1, da, db, e, t1, t2;\n"
+#define S3_BASE "6"
+#define S3_SPAN "7"
+#elif TILE == 4
+#define S3_POINTS \
+    "sub.rn.f32 da, %8, vy0;\n" "fma.rn.f32 x, sl0, %8, ic0;\n" "sub.rn.f32 e, %4, x;\n" "lop3.b32 t1, da, dp0, e, 0x28;\n" \
+    "sub.rn.f32 db, %8, vy1;\n" "fma.rn.f32 x, sl1, %8, ic1;\n" "sub.rn.f32 e, %4, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %0, %0, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %8, vy2;\n" "fma.rn.f32 x, sl2, %8, ic2;\n" "sub.rn.f32 e, %4, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp0, %8, vy3;\n" "fma.rn.f32 x, sl3, %8, ic3;\n" "sub.rn.f32 e, %4, x;\n" "lop3.b32 t2, dp0, da, e, 0x28;\n" \
+    "lop3.b32 %0, %0, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %9, vy0;\n" "fma.rn.f32 x, sl0, %9, ic0;\n" "sub.rn.f32 e, %5, x;\n" "lop3.b32 t1, da, dp1, e, 0x28;\n" \
+    "sub.rn.f32 db, %9, vy1;\n" "fma.rn.f32 x, sl1, %9, ic1;\n" "sub.rn.f32 e, %5, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %1, %1, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %9, vy2;\n" "fma.rn.f32 x, sl2, %9, ic2;\n" "sub.rn.f32 e, %5, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp1, %9, vy3;\n" "fma.rn.f32 x, sl3, %9, ic3;\n" "sub.rn.f32 e, %5, x;\n" "lop3.b32 t2, dp1, da, e, 0x28;\n" \
+    "lop3.b32 %1, %1, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %10, vy0;\n" "fma.rn.f32 x, sl0, %10, ic0;\n" "sub.rn.f32 e, %6, x;\n" "lop3.b32 t1, da, dp2, e, 0x28;\n" \
+    "sub.rn.f32 db, %10, vy1;\n" "fma.rn.f32 x, sl1, %10, ic1;\n" "sub.rn.f32 e, %6, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %2, %2, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %10, vy2;\n" "fma.rn.f32 x, sl2, %10, ic2;\n" "sub.rn.f32 e, %6, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp2, %10, vy3;\n" "fma.rn.f32 x, sl3, %10, ic3;\n" "sub.rn.f32 e, %6, x;\n" "lop3.b32 t2, dp2, da, e, 0x28;\n" \
+    "lop3.b32 %2, %2, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %11, vy0;\n" "fma.rn.f32 x, sl0, %11, ic0;\n" "sub.rn.f32 e, %7, x;\n" "lop3.b32 t1, da, dp3, e, 0x28;\n" \
+    "sub.rn.f32 db, %11, vy1;\n" "fma.rn.f32 x, sl1, %11, ic1;\n" "sub.rn.f32 e, %7, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %3, %3, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %11, vy2;\n" "fma.rn.f32 x, sl2, %11, ic2;\n" "sub.rn.f32 e, %7, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp3, %11, vy3;\n" "fma.rn.f32 x, sl3, %11, ic3;\n" "sub.rn.f32 e, %7, x;\n" "lop3.b32 t2, dp3, da, e, 0x28;\n" \
+    "lop3.b32 %3, %3, t1, t2, 0x96;\n"
+#define S3_INIT "sub.rn.f32 dp0, %8, %14;\n" "sub.rn.f32 dp1, %9, %14;\n" "sub.rn.f32 dp2, %10, %14;\n" "sub.rn.f32 dp3, %11, %14;\n"
+#define S3_REGS ".reg .b32 dp0, dp1, dp2, dp3, da, db, e, t1, t2;\n"
+#define S3_BASE "12"
+#define S3_SPAN "13"
+#elif TILE == 6
+#define S3_POINTS \
+    "sub.rn.f32 da, %12, vy0;\n" "fma.rn.f32 x, sl0, %12, ic0;\n" "sub.rn.f32 e, %6, x;\n" "lop3.b32 t1, da, dp0, e, 0x28;\n" \
+    "sub.rn.f32 db, %12, vy1;\n" "fma.rn.f32 x, sl1, %12, ic1;\n" "sub.rn.f32 e, %6, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %0, %0, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %12, vy2;\n" "fma.rn.f32 x, sl2, %12, ic2;\n" "sub.rn.f32 e, %6, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp0, %12, vy3;\n" "fma.rn.f32 x, sl3, %12, ic3;\n" "sub.rn.f32 e, %6, x;\n" "lop3.b32 t2, dp0, da, e, 0x28;\n" \
+    "lop3.b32 %0, %0, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %13, vy0;\n" "fma.rn.f32 x, sl0, %13, ic0;\n" "sub.rn.f32 e, %7, x;\n" "lop3.b32 t1, da, dp1, e, 0x28;\n" \
+    "sub.rn.f32 db, %13, vy1;\n" "fma.rn.f32 x, sl1, %13, ic1;\n" "sub.rn.f32 e, %7, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %1, %1, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %13, vy2;\n" "fma.rn.f32 x, sl2, %13, ic2;\n" "sub.rn.f32 e, %7, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp1, %13, vy3;\n" "fma.rn.f32 x, sl3, %13, ic3;\n" "sub.rn.f32 e, %7, x;\n" "lop3.b32 t2, dp1, da, e, 0x28;\n" \
+    "lop3.b32 %1, %1, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %14, vy0;\n" "fma.rn.f32 x, sl0, %14, ic0;\n" "sub.rn.f32 e, %8, x;\n" "lop3.b32 t1, da, dp2, e, 0x28;\n" \
+    "sub.rn.f32 db, %14, vy1;\n" "fma.rn.f32 x, sl1, %14, ic1;\n" "sub.rn.f32 e, %8, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %2, %2, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %14, vy2;\n" "fma.rn.f32 x, sl2, %14, ic2;\n" "sub.rn.f32 e, %8, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp2, %14, vy3;\n" "fma.rn.f32 x, sl3, %14, ic3;\n" "sub.rn.f32 e, %8, x;\n" "lop3.b32 t2, dp2, da, e, 0x28;\n" \
+    "lop3.b32 %2, %2, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %15, vy0;\n" "fma.rn.f32 x, sl0, %15, ic0;\n" "sub.rn.f32 e, %9, x;\n" "lop3.b32 t1, da, dp3, e, 0x28;\n" \
+    "sub.rn.f32 db, %15, vy1;\n" "fma.rn.f32 x, sl1, %15, ic1;\n" "sub.rn.f32 e, %9, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %3, %3, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %15, vy2;\n" "fma.rn.f32 x, sl2, %15, ic2;\n" "sub.rn.f32 e, %9, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp3, %15, vy3;\n" "fma.rn.f32 x, sl3, %15, ic3;\n" "sub.rn.f32 e, %9, x;\n" "lop3.b32 t2, dp3, da, e, 0x28;\n" \
+    "lop3.b32 %3, %3, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %16, vy0;\n" "fma.rn.f32 x, sl0, %16, ic0;\n" "sub.rn.f32 e, %10, x;\n" "lop3.b32 t1, da, dp4, e, 0x28;\n" \
+    "sub.rn.f32 db, %16, vy1;\n" "fma.rn.f32 x, sl1, %16, ic1;\n" "sub.rn.f32 e, %10, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %4, %4, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %16, vy2;\n" "fma.rn.f32 x, sl2, %16, ic2;\n" "sub.rn.f32 e, %10, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp4, %16, vy3;\n" "fma.rn.f32 x, sl3, %16, ic3;\n" "sub.rn.f32 e, %10, x;\n" "lop3.b32 t2, dp4, da, e, 0x28;\n" \
+    "lop3.b32 %4, %4, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %17, vy0;\n" "fma.rn.f32 x, sl0, %17, ic0;\n" "sub.rn.f32 e, %11, x;\n" "lop3.b32 t1, da, dp5, e, 0x28;\n" \
+    "sub.rn.f32 db, %17, vy1;\n" "fma.rn.f32 x, sl1, %17, ic1;\n" "sub.rn.f32 e, %11, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %5, %5, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %17, vy2;\n" "fma.rn.f32 x, sl2, %17, ic2;\n" "sub.rn.f32 e, %11, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp5, %17, vy3;\n" "fma.rn.f32 x, sl3, %17, ic3;\n" "sub.rn.f32 e, %11, x;\n" "lop3.b32 t2, dp5, da, e, 0x28;\n" \
+    "lop3.b32 %5, %5, t1, t2, 0x96;\n"
+#define S3_INIT "sub.rn.f32 dp0, %12, %20;\n" "sub.rn.f32 dp1, %13, %20;\n" "sub.rn.f32 dp2, %14, %20;\n" "sub.rn.f32 dp3, %15, %20;\n" "sub.rn.f32 dp4, %16, %20;\n" "sub.rn.f32 dp5, %17, %20;\n"
+#define S3_REGS ".reg .b32 dp0, dp1, dp2, dp3, dp4, dp5, da, db, e, t1, t2;\n"
+#define S3_BASE "18"
+#define S3_SPAN "19"
+#elif TILE == 8
+#define S3_POINTS \
+    "sub.rn.f32 da, %16, vy0;\n" "fma.rn.f32 x, sl0, %16, ic0;\n" "sub.rn.f32 e, %8, x;\n" "lop3.b32 t1, da, dp0, e, 0x28;\n" \
+    "sub.rn.f32 db, %16, vy1;\n" "fma.rn.f32 x, sl1, %16, ic1;\n" "sub.rn.f32 e, %8, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %0, %0, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %16, vy2;\n" "fma.rn.f32 x, sl2, %16, ic2;\n" "sub.rn.f32 e, %8, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp0, %16, vy3;\n" "fma.rn.f32 x, sl3, %16, ic3;\n" "sub.rn.f32 e, %8, x;\n" "lop3.b32 t2, dp0, da, e, 0x28;\n" \
+    "lop3.b32 %0, %0, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %17, vy0;\n" "fma.rn.f32 x, sl0, %17, ic0;\n" "sub.rn.f32 e, %9, x;\n" "lop3.b32 t1, da, dp1, e, 0x28;\n" \
+    "sub.rn.f32 db, %17, vy1;\n" "fma.rn.f32 x, sl1, %17, ic1;\n" "sub.rn.f32 e, %9, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %1, %1, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %17, vy2;\n" "fma.rn.f32 x, sl2, %17, ic2;\n" "sub.rn.f32 e, %9, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp1, %17, vy3;\n" "fma.rn.f32 x, sl3, %17, ic3;\n" "sub.rn.f32 e, %9, x;\n" "lop3.b32 t2, dp1, da, e, 0x28;\n" \
+    "lop3.b32 %1, %1, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %18, vy0;\n" "fma.rn.f32 x, sl0, %18, ic0;\n" "sub.rn.f32 e, %10, x;\n" "lop3.b32 t1, da, dp2, e, 0x28;\n" \
+    "sub.rn.f32 db, %18, vy1;\n" "fma.rn.f32 x, sl1, %18, ic1;\n" "sub.rn.f32 e, %10, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %2, %2, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %18, vy2;\n" "fma.rn.f32 x, sl2, %18, ic2;\n" "sub.rn.f32 e, %10, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp2, %18, vy3;\n" "fma.rn.f32 x, sl3, %18, ic3;\n" "sub.rn.f32 e, %10, x;\n" "lop3.b32 t2, dp2, da, e, 0x28;\n" \
+    "lop3.b32 %2, %2, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %19, vy0;\n" "fma.rn.f32 x, sl0, %19, ic0;\n" "sub.rn.f32 e, %11, x;\n" "lop3.b32 t1, da, dp3, e, 0x28;\n" \
+    "sub.rn.f32 db, %19, vy1;\n" "fma.rn.f32 x, sl1, %19, ic1;\n" "sub.rn.f32 e, %11, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %3, %3, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %19, vy2;\n" "fma.rn.f32 x, sl2, %19, ic2;\n" "sub.rn.f32 e, %11, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp3, %19, vy3;\n" "fma.rn.f32 x, sl3, %19, ic3;\n" "sub.rn.f32 e, %11, x;\n" "lop3.b32 t2, dp3, da, e, 0x28;\n" \
+    "lop3.b32 %3, %3, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %20, vy0;\n" "fma.rn.f32 x, sl0, %20, ic0;\n" "sub.rn.f32 e, %12, x;\n" "lop3.b32 t1, da, dp4, e, 0x28;\n" \
+    "sub.rn.f32 db, %20, vy1;\n" "fma.rn.f32 x, sl1, %20, ic1;\n" "sub.rn.f32 e, %12, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %4, %4, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %20, vy2;\n" "fma.rn.f32 x, sl2, %20, ic2;\n" "sub.rn.f32 e, %12, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp4, %20, vy3;\n" "fma.rn.f32 x, sl3, %20, ic3;\n" "sub.rn.f32 e, %12, x;\n" "lop3.b32 t2, dp4, da, e, 0x28;\n" \
+    "lop3.b32 %4, %4, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %21, vy0;\n" "fma.rn.f32 x, sl0, %21, ic0;\n" "sub.rn.f32 e, %13, x;\n" "lop3.b32 t1, da, dp5, e, 0x28;\n" \
+    "sub.rn.f32 db, %21, vy1;\n" "fma.rn.f32 x, sl1, %21, ic1;\n" "sub.rn.f32 e, %13, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %5, %5, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %21, vy2;\n" "fma.rn.f32 x, sl2, %21, ic2;\n" "sub.rn.f32 e, %13, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp5, %21, vy3;\n" "fma.rn.f32 x, sl3, %21, ic3;\n" "sub.rn.f32 e, %13, x;\n" "lop3.b32 t2, dp5, da, e, 0x28;\n" \
+    "lop3.b32 %5, %5, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %22, vy0;\n" "fma.rn.f32 x, sl0, %22, ic0;\n" "sub.rn.f32 e, %14, x;\n" "lop3.b32 t1, da, dp6, e, 0x28;\n" \
+    "sub.rn.f32 db, %22, vy1;\n" "fma.rn.f32 x, sl1, %22, ic1;\n" "sub.rn.f32 e, %14, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %6, %6, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %22, vy2;\n" "fma.rn.f32 x, sl2, %22, ic2;\n" "sub.rn.f32 e, %14, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp6, %22, vy3;\n" "fma.rn.f32 x, sl3, %22, ic3;\n" "sub.rn.f32 e, %14, x;\n" "lop3.b32 t2, dp6, da, e, 0x28;\n" \
+    "lop3.b32 %6, %6, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %23, vy0;\n" "fma.rn.f32 x, sl0, %23, ic0;\n" "sub.rn.f32 e, %15, x;\n" "lop3.b32 t1, da, dp7, e, 0x28;\n" \
+    "sub.rn.f32 db, %23, vy1;\n" "fma.rn.f32 x, sl1, %23, ic1;\n" "sub.rn.f32 e, %15, x;\n" "lop3.b32 t2, db, da, e, 0x28;\n" \
+    "lop3.b32 %7, %7, t1, t2, 0x96;\n" \
+    "sub.rn.f32 da, %23, vy2;\n" "fma.rn.f32 x, sl2, %23, ic2;\n" "sub.rn.f32 e, %15, x;\n" "lop3.b32 t1, da, db, e, 0x28;\n" \
+    "sub.rn.f32 dp7, %23, vy3;\n" "fma.rn.f32 x, sl3, %23, ic3;\n" "sub.rn.f32 e, %15, x;\n" "lop3.b32 t2, dp7, da, e, 0x28;\n" \
+    "lop3.b32 %7, %7, t1, t2, 0x96;\n"
+#define S3_INIT "sub.rn.f32 dp0, %16, %26;\n" "sub.rn.f32 dp1, %17, %26;\n" "sub.rn.f32 dp2, %18, %26;\n" "sub.rn.f32 dp3, %19, %26;\n" "sub.rn.f32 dp4, %20, %26;\n" "sub.rn.f32 dp5, %21, %26;\n" "sub.rn.f32 dp6, %22, %26;\n" "sub.rn.f32 dp7, %23, %26;\n"
+#define S3_REGS ".reg .b32 dp0, dp1, dp2, dp3, dp4, dp5, dp6, dp7, da, db, e, t1, t2;\n"
+#define S3_BASE "24"
+#define S3_SPAN "25"
+#endif
+#define S3_LD "ld.shared.v4.f32 {vy0, sl0, ic0, z}, [ptr+0];\n" "ld.shared.v4.f32 {vy1, sl1, ic1, z}, [ptr+16];\n" \
+              "ld.shared.v4.f32 {vy2, sl2, ic2, z}, [ptr+32];\n" "ld.shared.v4.f32 {vy3, sl3, ic3, z}, [ptr+48];\n"
+#define S3_ASM                                                                                     \
+    "{\n" S3_REGS ".reg .f32 vy0, vy1, vy2, vy3, sl0, sl1, sl2, sl3, ic0, ic1, ic2, ic3, x, z;\n"  \
+    ".reg .u32 ptr, end;\n.reg .pred s;\n" S3_INIT "mov.u32 ptr, %" S3_BASE ";\n"                  \
+    "add.u32 end, ptr, %" S3_SPAN ";\n" "PNPOLY_S3_LOOP:\n" S3_LD S3_POINTS                        \
+    "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_S3_LOOP;\n}\n"
+#endif
+
+
+__constant__ float4 c_edges[VERTICES];
+__constant__ float2 c_ybounds[VERTICES];
+
+__device__ __forceinline__ float crossing_x(float4 e, float py) {
+#if METHOD == 0
+    return __fadd_rn(__fdiv_rn(__fmul_rn(e.z, __fsub_rn(py, e.x)), e.w), e.y);
+#elif METHOD == 1
+    return __fmaf_rn(e.z, __fsub_rn(py, e.x), e.y);
+#else
+    return __fmaf_rn(e.z, py, e.y);
+#endif
+}
+
+extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X)
+pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
+       const float4 *__restrict__ g_edges, const float2 *__restrict__ g_ybounds,
+       const float4 *__restrict__ g_packed) {
+#if ASM
+    // packed records, NPACK entries (ASM 1/2: {ymin, ymax, slope, icpt};
+    // ASM 3: {vy_k, slope, icpt, 0})
+    __shared__ __align__(16) float4 s_packed[NPACK];
+    for (int k = threadIdx.x; k < NPACK; k += BLOCK_SIZE_X) s_packed[k] = g_packed[k];
+    __syncthreads();
+#elif POLY_SMEM
+    __shared__ float4 s_edges[VERTICES];
+#if BETWEEN == 1
+    __shared__ float2 s_ybounds[VERTICES];
+#endif
+    for (int k = threadIdx.x; k < VERTICES; k += BLOCK_SIZE_X) {
+        s_edges[k] = g_edges[k];
+#if BETWEEN == 1
+        s_ybounds[k] = g_ybounds[k];
+#endif
+    }
+    __syncthreads();
+    const float4 *edges = s_edges;
+#if BETWEEN == 1
+    const float2 *ybounds = s_ybounds;
+#endif
+#else
+    const float4 *edges = c_edges;
+#if BETWEEN == 1
+    const float2 *ybounds = c_ybounds;
+#endif
+#endif
+
+    // Coalesced: in step t, consecutive threads own consecutive points
+    // (VEC=1: float2) or point pairs (VEC=2: float4).
+    const long long block_base = (long long)blockIdx.x * (BLOCK_SIZE_X * TILE);
+    float px[TILE], py[TILE];
+    int idx[TILE];
+#pragma unroll
+    for (int t = 0; t < TILE / VEC; ++t) {
+        const long long first = block_base + (long long)VEC * ((long long)t * BLOCK_SIZE_X + threadIdx.x);
+#if VEC == 2
+        idx[2 * t] = (int)first;
+        idx[2 * t + 1] = (int)first + 1;
+        if (first + 1 < n) {
+            const float4 q = reinterpret_cast<const float4 *>(points)[first >> 1];
+            px[2 * t] = q.x;
+            py[2 * t] = q.y;
+            px[2 * t + 1] = q.z;
+            py[2 * t + 1] = q.w;
+        } else {
+            const float2 q = first < n ? points[first] : make_float2(0.f, 0.f);
+            px[2 * t] = q.x;
+            py[2 * t] = q.y;
+            px[2 * t + 1] = 0.f;
+            py[2 * t + 1] = 0.f;
+        }
+#else
+        idx[t] = (int)first;
+        const float2 q = first < n ? points[first] : make_float2(0.f, 0.f);
+        px[t] = q.x;
+        py[t] = q.y;
+#endif
+    }
+
+#if ASM == 3
+    unsigned inside[TILE];
+    {
+        unsigned acc[TILE];
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) acc[t] = 0u;
+        const unsigned sbase = (unsigned)__cvta_generic_to_shared(s_packed);
+        const unsigned span = NPACK * 16u;
+        const float vy_last = s_packed[VERTICES - 1].x;
+#if TILE == 2
+        asm volatile(S3_ASM : "+r"(acc[0]), "+r"(acc[1]) : "f"(px[0]), "f"(px[1]), "f"(py[0]), "f"(py[1]),
+                     "r"(sbase), "r"(span), "f"(vy_last));
+#elif TILE == 4
+        asm volatile(S3_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3])
+                     : "f"(px[0]), "f"(px[1]), "f"(px[2]), "f"(px[3]), "f"(py[0]), "f"(py[1]), "f"(py[2]), "f"(py[3]),
+                       "r"(sbase), "r"(span), "f"(vy_last));
+#elif TILE == 6
+        asm volatile(S3_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3]), "+r"(acc[4]), "+r"(acc[5])
+                     : "f"(px[0]), "f"(px[1]), "f"(px[2]), "f"(px[3]), "f"(px[4]), "f"(px[5]), "f"(py[0]), "f"(py[1]),
+                       "f"(py[2]), "f"(py[3]), "f"(py[4]), "f"(py[5]), "r"(sbase), "r"(span), "f"(vy_last));
+#else
+        asm volatile(S3_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3]), "+r"(acc[4]), "+r"(acc[5]),
+                     "+r"(acc[6]), "+r"(acc[7])
+                     : "f"(px[0]), "f"(px[1]), "f"(px[2]), "f"(px[3]), "f"(px[4]), "f"(px[5]), "f"(px[6]), "f"(px[7]),
+                       "f"(py[0]), "f"(py[1]), "f"(py[2]), "f"(py[3]), "f"(py[4]), "f"(py[5]), "f"(py[6]), "f"(py[7]),
+                       "r"(sbase), "r"(span), "f"(vy_last));
+#endif
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) inside[t] = acc[t] >> 31;
+    }
+#elif ASM
+    unsigned inside[TILE];
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(s_packed);
+    const unsigned zero = 0u;
+    const unsigned span = NPACK * 16u;
+#if TILE == 1
+    asm volatile("{\n" PREDS EXTRA_REGS ".reg .f32 ylo, yhi, sl, ic, x;\n.reg .u32 ptr, end;\n" INIT
+                 "mov.u32 ptr, %" BASE_OP ";\nadd.u32 end, ptr, %" END_OP ";\n"
+                 "PNPOLY_LOOP:\n" BODY
+                 "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_LOOP;\n" OUT_SELP "}\n"
+                 : "=r"(inside[0]) : "f"(px[0]), "f"(py[0]), "r"(sbase), "r"(zero), "r"(span));
+#elif TILE == 2
+    asm volatile("{\n" PREDS EXTRA_REGS ".reg .f32 ylo, yhi, sl, ic, x;\n.reg .u32 ptr, end;\n" INIT
+                 "mov.u32 ptr, %" BASE_OP ";\nadd.u32 end, ptr, %" END_OP ";\n"
+                 "PNPOLY_LOOP:\n" BODY
+                 "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_LOOP;\n" OUT_SELP "}\n"
+                 : "=r"(inside[0]), "=r"(inside[1])
+                 : "f"(px[0]), "f"(px[1]), "f"(py[0]), "f"(py[1]), "r"(sbase), "r"(zero), "r"(span));
+#elif TILE == 4
+    asm volatile("{\n" PREDS EXTRA_REGS ".reg .f32 ylo, yhi, sl, ic, x;\n.reg .u32 ptr, end;\n" INIT
+                 "mov.u32 ptr, %" BASE_OP ";\nadd.u32 end, ptr, %" END_OP ";\n"
+                 "PNPOLY_LOOP:\n" BODY
+                 "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_LOOP;\n" OUT_SELP "}\n"
+                 : "=r"(inside[0]), "=r"(inside[1]), "=r"(inside[2]), "=r"(inside[3])
+                 : "f"(px[0]), "f"(px[1]), "f"(px[2]), "f"(px[3]), "f"(py[0]), "f"(py[1]), "f"(py[2]), "f"(py[3]),
+                   "r"(sbase), "r"(zero), "r"(span));
+#else
+    asm volatile("{\n" PREDS EXTRA_REGS ".reg .f32 ylo, yhi, sl, ic, x;\n.reg .u32 ptr, end;\n" INIT
+                 "mov.u32 ptr, %" BASE_OP ";\nadd.u32 end, ptr, %" END_OP ";\n"
+                 "PNPOLY_LOOP:\n" BODY
+                 "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_LOOP;\n" OUT_SELP "}\n"
+                 : "=r"(inside[0]), "=r"(inside[1]), "=r"(inside[2]), "=r"(inside[3]), "=r"(inside[4]),
+                   "=r"(inside[5])
+                 : "f"(px[0]), "f"(px[1]), "f"(px[2]), "f"(px[3]), "f"(px[4]), "f"(px[5]), "f"(py[0]), "f"(py[1]),
+                   "f"(py[2]), "f"(py[3]), "f"(py[4]), "f"(py[5]), "r"(sbase), "r"(zero), "r"(span));
+#endif
+#else
+    bool inside[TILE];
+#if BETWEEN == 0
+    bool prev_above[TILE];
+    const float vy_last = edges[VERTICES - 1].x;
+#pragma unroll
+    for (int t = 0; t < TILE; ++t) prev_above[t] = vy_last > py[t];
+#endif
+#pragma unroll
+    for (int t = 0; t < TILE; ++t) inside[t] = false;
+
+#pragma unroll 4
+    for (int k = 0; k < VERTICES; ++k) {
+        const float4 e = edges[k];
+#if BETWEEN == 1
+        const float2 yb = ybounds[k];
+#endif
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) {
+#if BETWEEN == 0
+            const bool above = e.x > py[t];
+            const bool spans = above != prev_above[t];
+            prev_above[t] = above;
+#else
+            const bool spans = (yb.x <= py[t]) & (py[t] < yb.y);
+#endif
+            // predicated toggle: ptxas folds this into one @P FSETP.LT.XOR
+            const float xc = crossing_x(e, py[t]);
+            if (spans) inside[t] = inside[t] != (px[t] < xc);
+        }
+    }
+
+#endif
+#pragma unroll
+    for (int t = 0; t < TILE; ++t)
+        if (idx[t] < n) bitmap[idx[t]] = inside[t] ? 1 : 0;
+}

@@ -1,0 +1,238 @@
+// CLBlast-style FP32 SIMT SGEMM for sm_100a, compiled per config by NVRTC.
+//
+//   C[M][N] = alpha * sum_k A[m][k] * B[k][n] + beta * C[m][n]
+//
+// Storage (BLAS conventions): A column-major (M contiguous, i.e. a K x M
+// row-major buffer "AT"), B row-major (K x N, N contiguous), C row-major.
+// This is the layout CLBlast's xgemm kernel works in after its
+// pre-processing, so the tunables keep CLBlast's meaning (PAPER.md:309-316,
+// fixture analogue pkg/src/jouletune/fixtures/gemm_space.json):
+//
+//   MWG, NWG, KWG   CTA tile (M, N) and K step staged per iteration
+//   MDIMC, NDIMC    threads of the CTA along M / N (CTA = MDIMC*NDIMC)
+//   MDIMA, NDIMB    thread shape along M (for A) / N (for B) when loading tiles
+//   KWI             unroll factor of the inner k loop
+//   VWM, VWN        vector widths along M / N (fragment loads, A/B tile loads)
+//   STRM, STRN      0: a thread's MWI (NWI) outputs are contiguous in M (N);
+//                   1: strided by MDIMC*VWM (NDIMC*VWN) -> conflict-free smem
+//   SA, SB          1: stage the A (B) tile in shared memory (double buffered);
+//                   0: read fragments straight from global memory through L1
+//
+// Requirements (the tuning-space restrictions, kernels.py):
+//   MWG % (MDIMC*VWM) == 0, NWG % (NDIMC*VWN) == 0,
+//   MWG % (MDIMA*VWM) == 0, NWG % (NDIMB*VWN) == 0,
+//   KWG % (MDIMC*NDIMC/MDIMA) == 0, KWG % (MDIMC*NDIMC/NDIMB) == 0,
+//   KWG % KWI == 0, M % MWG == 0, N % NWG == 0, K % KWG == 0.
+#ifndef MWG
+#define MWG 128
+#endif
+#ifndef NWG
+#define NWG 128
+#endif
+#ifndef KWG
+#define KWG 16
+#endif
+#ifndef MDIMC
+#define MDIMC 16
+#endif
+#ifndef NDIMC
+#define NDIMC 16
+#endif
+#ifndef MDIMA
+#define MDIMA 32
+#endif
+#ifndef NDIMB
+#define NDIMB 32
+#endif
+#ifndef KWI
+#define KWI 2
+#endif
+#ifndef VWM
+#define VWM 4
+#endif
+#ifndef VWN
+#define VWN 4
+#endif
+#ifndef STRM
+#define STRM 1
+#endif
+#ifndef STRN
+#define STRN 1
+#endif
+#ifndef SA
+#define SA 1
+#endif
+#ifndef SB
+#define SB 1
+#endif
+
+#define THREADS (MDIMC * NDIMC)
+#define MWI (MWG / MDIMC)
+#define NWI (NWG / NDIMC)
+#define KDIMA (THREADS / MDIMA)
+#define KDIMB (THREADS / NDIMB)
+#define MWA (MWG / MDIMA)  // M elements per thread when loading A
+#define KWA (KWG / KDIMA)  // K rows per thread when loading A
+#define NWB (NWG / NDIMB)
+#define KWB (KWG / KDIMB)
+
+#if (MWG % (MDIMC * VWM)) || (NWG % (NDIMC * VWN)) || (MWG % (MDIMA * VWM)) || (NWG % (NDIMB * VWN)) || \
+    (KWG % KDIMA) || (KWG % KDIMB) || (KWG % KWI) || (THREADS % MDIMA) || (THREADS % NDIMB)
+#error "invalid CLBlast-style SGEMM configuration"
+#endif
+
+template <int W>
+struct vec;
+template <>
+struct vec<1> { typedef float t; };
+template <>
+struct vec<2> { typedef float2 t; };
+template <>
+struct vec<4> { typedef float4 t; };
+typedef typename vec<VWM>::t vm_t;
+typedef typename vec<VWN>::t vn_t;
+
+__device__ __forceinline__ float lane(const float &v, int) { return v; }
+__device__ __forceinline__ float lane(const float2 &v, int i) { return i == 0 ? v.x : v.y; }
+__device__ __forceinline__ float lane(const float4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
+// Offset (in vectors of VWM) of this thread's w-th A fragment vector inside the MWG tile.
+__device__ __forceinline__ int frag_m(int tm, int w) {
+#if STRM == 0
+    return tm * (MWI / VWM) + w;
+#else
+    return w * MDIMC + tm;
+#endif
+}
+__device__ __forceinline__ int frag_n(int tn, int w) {
+#if STRN == 0
+    return tn * (NWI / VWN) + w;
+#else
+    return w * NDIMC + tn;
+#endif
+}
+
+extern "C" __global__ void __launch_bounds__(THREADS)
+sgemm(const int M, const int N, const int K, const float alpha, const float beta,
+      const float *__restrict__ at, const float *__restrict__ b, float *__restrict__ c) {
+    const int tid = threadIdx.x;
+    const int tm = tid % MDIMC, tn = tid / MDIMC;
+    const int m0 = blockIdx.x * MWG, n0 = blockIdx.y * NWG;
+
+#if SA
+    __shared__ __align__(16) vm_t a_sm[2][KWG][MWG / VWM];
+    const int ma = tid % MDIMA, ka = tid / MDIMA;
+    vm_t a_reg[KWA][MWA / VWM];
+#endif
+#if SB
+    __shared__ __align__(16) vn_t b_sm[2][KWG][NWG / VWN];
+    const int nb = tid % NDIMB, kb = tid / NDIMB;
+    vn_t b_reg[KWB][NWB / VWN];
+#endif
+
+    float acc[MWI][NWI];
+#pragma unroll
+    for (int i = 0; i < MWI; ++i)
+#pragma unroll
+        for (int j = 0; j < NWI; ++j) acc[i][j] = 0.f;
+
+    const vm_t *at_v = reinterpret_cast<const vm_t *>(at);
+    const vn_t *b_v = reinterpret_cast<const vn_t *>(b);
+    const int lda_v = M / VWM, ldb_v = N / VWN;
+
+    auto fetch = [&](int k0) {
+#if SA
+#pragma unroll
+        for (int kk = 0; kk < KWA; ++kk)
+#pragma unroll
+            for (int mv = 0; mv < MWA / VWM; ++mv)
+                a_reg[kk][mv] = __ldg(at_v + (size_t)(k0 + ka + kk * KDIMA) * lda_v + m0 / VWM + ma + mv * MDIMA);
+#endif
+#if SB
+#pragma unroll
+        for (int kk = 0; kk < KWB; ++kk)
+#pragma unroll
+            for (int nv = 0; nv < NWB / VWN; ++nv)
+                b_reg[kk][nv] = __ldg(b_v + (size_t)(k0 + kb + kk * KDIMB) * ldb_v + n0 / VWN + nb + nv * NDIMB);
+#endif
+    };
+    auto stash = [&](int buf) {
+#if SA
+#pragma unroll
+        for (int kk = 0; kk < KWA; ++kk)
+#pragma unroll
+            for (int mv = 0; mv < MWA / VWM; ++mv) a_sm[buf][ka + kk * KDIMA][ma + mv * MDIMA] = a_reg[kk][mv];
+#endif
+#if SB
+#pragma unroll
+        for (int kk = 0; kk < KWB; ++kk)
+#pragma unroll
+            for (int nv = 0; nv < NWB / VWN; ++nv) b_sm[buf][kb + kk * KDIMB][nb + nv * NDIMB] = b_reg[kk][nv];
+#endif
+    };
+
+    const int tiles = K / KWG;
+#if SA || SB
+    fetch(0);
+    stash(0);
+    __syncthreads();
+#endif
+#pragma unroll 1
+    for (int t = 0; t < tiles; ++t) {
+        const int buf = t & 1;
+        const int k0 = t * KWG;
+#if SA || SB
+        if (t + 1 < tiles) fetch(k0 + KWG);
+#endif
+#pragma unroll 1
+        for (int kw = 0; kw < KWG; kw += KWI) {
+#pragma unroll
+            for (int ki = 0; ki < KWI; ++ki) {
+                const int k = kw + ki;
+                vm_t af[MWI / VWM];
+                vn_t bf[NWI / VWN];
+#pragma unroll
+                for (int w = 0; w < MWI / VWM; ++w) {
+#if SA
+                    af[w] = a_sm[buf][k][frag_m(tm, w)];
+#else
+                    af[w] = __ldg(at_v + (size_t)(k0 + k) * lda_v + m0 / VWM + frag_m(tm, w));
+#endif
+                }
+#pragma unroll
+                for (int w = 0; w < NWI / VWN; ++w) {
+#if SB
+                    bf[w] = b_sm[buf][k][frag_n(tn, w)];
+#else
+                    bf[w] = __ldg(b_v + (size_t)(k0 + k) * ldb_v + n0 / VWN + frag_n(tn, w));
+#endif
+                }
+#pragma unroll
+                for (int i = 0; i < MWI; ++i)
+#pragma unroll
+                    for (int j = 0; j < NWI; ++j)
+                        acc[i][j] = fmaf(lane(af[i / VWM], i % VWM), lane(bf[j / VWN], j % VWN), acc[i][j]);
+            }
+        }
+#if SA || SB
+        if (t + 1 < tiles) stash(buf ^ 1);
+        __syncthreads();
+#endif
+    }
+
+    // epilogue: C = alpha * acc + beta * C, VWN-wide row segments
+#pragma unroll
+    for (int i = 0; i < MWI; ++i) {
+        const int m = m0 + frag_m(tm, i / VWM) * VWM + i % VWM;
+#pragma unroll
+        for (int w = 0; w < NWI / VWN; ++w) {
+            const int n = n0 + frag_n(tn, w) * VWN;
+            vn_t *dst = reinterpret_cast<vn_t *>(c + (size_t)m * N + n);
+            vn_t old = beta != 0.f ? *dst : vn_t();
+            float *o = reinterpret_cast<float *>(&old);
+#pragma unroll
+            for (int v = 0; v < VWN; ++v) o[v] = fmaf(alpha, acc[i][w * VWN + v], beta * o[v]);
+            *dst = old;
+        }
+    }
+}

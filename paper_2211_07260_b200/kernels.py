@@ -1,0 +1,513 @@
+"""The tuned kernel suite: problem definitions, tunable spaces, launch geometry.
+
+Each :class:`KernelProblem` binds one sm_100a kernel source
+(``csrc/kernels/*.cu``) to a synthetic, seeded input of the size
+``BASELINE.json`` names, the Kernel-Tuner-style tunable-parameter dict
+(``{"parameters": {name: [values]}, "restrictions": [expr]}``, the format of
+the reference's ``SearchSpace.from_dict``, ``searchspace.py:253-264``), the
+per-config ``-D`` defines, the launch shape and the algorithmic work used for
+``gflops`` / ``gflops_per_w`` (``tuner.default_metrics``) and rooflines.
+
+Inputs, all float32 from ``np.random.default_rng(seed)``:
+
+* PnPoly: 20,000,000 points uniform in [-1,1]^2 (seed 4); a 600-vertex
+  star-shaped polygon (sorted angles, radius 0.5 + 0.3 U); int32 bitmap.
+* Conv2D: (4096+16)^2 input U[0,1) and a 17x17 filter U[0,1) (seed 3);
+  4096^2 valid-mode output.
+* SGEMM: A, B, C0 U[-1,1) 4096^2 (seeds 0/1/2), alpha 1, beta 0.5;
+  A column-major, B and C row-major.
+
+The kernels never see the oracle; verification against a user-provided
+``answer`` happens in :mod:`.b200` and in the tests.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Any, Mapping
+
+import numpy as np
+
+from . import native
+from .gpu import GPU, DeviceArray, Kernel, Launch, f32, i32
+from .searchspace import KernelConfig, SearchSpace
+
+__all__ = [
+    "KernelProblem",
+    "PnPolyProblem",
+    "Conv2DProblem",
+    "SgemmProblem",
+    "BurnerProblem",
+    "PROBLEMS",
+    "make_problem",
+]
+
+
+@dataclass
+class KernelProblem:
+    """Base class: subclasses fill the hooks below."""
+
+    name: str = ""
+    source: str = ""
+    symbol: str = ""
+    seed: int = 0
+    # filled by prepare()
+    gpu: GPU | None = field(default=None, repr=False)
+    buffers: dict = field(default_factory=dict, repr=False)
+
+    # -- description ------------------------------------------------------
+    @property
+    def total_flops(self) -> float:
+        raise NotImplementedError
+
+    @property
+    def algorithmic_bytes(self) -> float:
+        raise NotImplementedError
+
+    #: "fp32" (FFMA-pipe roofline) or "issue" (lane-instruction roofline)
+    roofline_kind = "fp32"
+
+    def tune_params(self) -> dict[str, list]:
+        raise NotImplementedError
+
+    def restrictions(self) -> list[str]:
+        return []
+
+    def space_document(self) -> dict[str, Any]:
+        return {"parameters": self.tune_params(), "restrictions": self.restrictions()}
+
+    def space(self) -> SearchSpace:
+        return SearchSpace.from_dict(self.space_document())
+
+    def default_config(self) -> dict[str, Any]:
+        raise NotImplementedError
+
+    def defines(self, config: Mapping[str, Any]) -> dict[str, Any]:
+        return {k.upper(): v for k, v in config.items()}
+
+    def launch(self, config: Mapping[str, Any]) -> Launch:
+        raise NotImplementedError
+
+    # -- device side ----------------------------------------------------------
+    def host_inputs(self) -> dict[str, np.ndarray]:
+        raise NotImplementedError
+
+    def prepare(self, gpu: GPU) -> None:
+        raise NotImplementedError
+
+    def args(self, config: Mapping[str, Any]) -> list:
+        raise NotImplementedError
+
+    def bind(self, kernel: Kernel, config: Mapping[str, Any]) -> None:
+        """Per-run constant-memory uploads (no-op by default)."""
+
+    def reset_output(self) -> None:
+        """Zero the output so a stale result can never pass verification."""
+        out = self.buffers.get("out")
+        if out is not None:
+            out.fill(0)
+
+    def fetch_output(self) -> np.ndarray:
+        return self.buffers["out"].download()
+
+    # -- compilation ------------------------------------------------------------
+    def options(self, config: Mapping[str, Any]) -> list[str]:
+        return native._nvrtc_options(self.defines(config))
+
+    def cubin(self, config: Mapping[str, Any]) -> bytes:
+        return native.compile_cubin(native.kernel_source(self.source), self.name, self.options(config))
+
+    def kernel(self, config: Mapping[str, Any]) -> Kernel:
+        if self.gpu is None:
+            raise RuntimeError(f"{self.name}: prepare(gpu) first")
+        return self.gpu.load(self.cubin(config), self.symbol)
+
+
+def _as_dict(config) -> dict[str, Any]:
+    return config.as_dict() if isinstance(config, KernelConfig) else dict(config)
+
+
+# -- PnPoly -----------------------------------------------------------------------------
+
+
+@dataclass
+class PnPolyProblem(KernelProblem):
+    name: str = "pnpoly"
+    source: str = "pnpoly.cu"
+    symbol: str = "pnpoly"
+    seed: int = 4
+    n_points: int = 20_000_000
+    n_vertices: int = 600
+
+    roofline_kind = "issue"
+    #: lane-instruction slots credited per edge test (SURVEY §8(d) convention)
+    ops_per_edge = 3
+
+    @property
+    def edge_tests(self) -> float:
+        return float(self.n_points) * self.n_vertices
+
+    @property
+    def total_flops(self) -> float:
+        return self.ops_per_edge * self.edge_tests
+
+    @property
+    def algorithmic_bytes(self) -> float:
+        return 8.0 * self.n_points + 4.0 * self.n_points + 8.0 * self.n_vertices
+
+    def tune_params(self):
+        return {
+            "block_size_x": [32 * i for i in range(1, 33)],
+            "tile": [1, 2, 4, 6, 8],
+            "vec": [1, 2],
+            "method": [0, 1, 2],
+            "between": [0, 1],
+            "poly_smem": [0, 1],
+            "asm": [0, 1, 2, 3],
+        }
+
+    def restrictions(self):
+        return [
+            "vec == 1 or tile % 2 == 0",
+            "asm == 0 or (poly_smem == 1 and method == 2)",
+            "asm == 0 or asm == 3 or (between == 1 and tile != 8)",
+            "asm != 3 or (between == 0 and tile != 1)",
+        ]
+
+    def default_config(self):
+        return {"block_size_x": 256, "tile": 4, "vec": 2, "method": 2, "between": 0, "poly_smem": 1, "asm": 3}
+
+    @staticmethod
+    def formula(config) -> int:
+        """Which exactly-specified crossing formulation a config computes:
+        0/1/2 = METHOD (IEEE compares), 3 = sign-bit form of METHOD 2 (ASM=3)."""
+        c = _as_dict(config)
+        return 3 if c.get("asm", 0) == 3 else c["method"]
+
+    def defines(self, config):
+        c = _as_dict(config)
+        return {
+            "BLOCK_SIZE_X": c["block_size_x"],
+            "TILE": c["tile"],
+            "VEC": c["vec"],
+            "METHOD": c["method"],
+            "BETWEEN": c["between"],
+            "POLY_SMEM": c["poly_smem"],
+            "ASM": c.get("asm", 0),
+            "VERTICES": self.n_vertices,
+        }
+
+    def launch(self, config):
+        c = _as_dict(config)
+        per_block = c["block_size_x"] * c["tile"]
+        return Launch((math.ceil(self.n_points / per_block), 1, 1), (c["block_size_x"], 1, 1))
+
+    def host_inputs(self):
+        rng = np.random.default_rng(self.seed)
+        theta = np.sort(rng.uniform(0.0, 2.0 * np.pi, self.n_vertices))
+        radius = 0.5 + 0.3 * rng.uniform(0.0, 1.0, self.n_vertices)
+        vx = (radius * np.cos(theta)).astype(np.float32)
+        vy = (radius * np.sin(theta)).astype(np.float32)
+        points = rng.uniform(-1.0, 1.0, (self.n_points, 2)).astype(np.float32)
+        return {"points": points, "vx": vx, "vy": vy}
+
+    def prepare(self, gpu, inputs=None):
+        self.gpu = gpu
+        inputs = inputs or self.host_inputs()
+        self.inputs = inputs
+        self._tables = {m: native.pnpoly_edges(inputs["vx"], inputs["vy"], m) for m in (0, 1, 2)}
+        self.buffers = {
+            "out": gpu.empty((self.n_points,), np.int32),
+            "points": gpu.array(inputs["points"], slack=16),
+        }
+        for m, (edges, yb) in self._tables.items():
+            self.buffers[f"edges{m}"] = gpu.array(edges)
+            self.buffers[f"ybounds{m}"] = gpu.array(yb)
+        self.buffers["packed"] = gpu.array(self.packed_table())
+        self.buffers["packed3"] = gpu.array(self.chain_table())
+
+    def chain_table(self) -> np.ndarray:
+        """{vy_k, slope, icpt, 0} per edge for the sign-bit chain (ASM=3),
+        padded to a multiple of 4 with copies of the last vertex's vy (a
+        zero-length continuation of the chain, which never toggles)."""
+        edges, _ = self._tables[2]
+        n = edges.shape[0]
+        npack = (n + 3) // 4 * 4
+        table = np.zeros((npack, 4), dtype=np.float32)
+        table[:, 0] = edges[n - 1, 0]
+        table[:n, 0] = edges[:, 0]
+        table[:n, 1] = edges[:, 2]
+        table[:n, 2] = edges[:, 1]
+        return table
+
+    def packed_table(self) -> np.ndarray:
+        """{ymin, ymax, slope, icpt} per edge (METHOD 2), padded to a multiple
+        of 4 with never-spanning dummies {+inf, -inf, 0, 0} (pure repacking of
+        the libjt edge table; no arithmetic)."""
+        edges, yb = self._tables[2]
+        n = edges.shape[0]
+        npack = (n + 3) // 4 * 4
+        packed = np.zeros((npack, 4), dtype=np.float32)
+        packed[:, 0] = np.inf
+        packed[:, 1] = -np.inf
+        packed[:n, 0] = yb[:, 0]
+        packed[:n, 1] = yb[:, 1]
+        packed[:n, 2] = edges[:, 2]
+        packed[:n, 3] = edges[:, 1]
+        return packed
+
+    def args(self, config):
+        m = _as_dict(config)["method"]
+        b = self.buffers
+        packed = b["packed3"] if _as_dict(config).get("asm", 0) == 3 else b["packed"]
+        return [b["out"], b["points"], i32(self.n_points), b[f"edges{m}"], b[f"ybounds{m}"], packed]
+
+    def bind(self, kernel, config):
+        c = _as_dict(config)
+        if not c["poly_smem"]:
+            edges, yb = self._tables[c["method"]]
+            kernel.set_global("c_edges", edges)
+            kernel.set_global("c_ybounds", yb)
+
+
+# -- Conv2D -------------------------------------------------------------------------------
+
+
+@dataclass
+class Conv2DProblem(KernelProblem):
+    name: str = "conv2d"
+    source: str = "conv2d.cu"
+    symbol: str = "conv2d"
+    seed: int = 3
+    width: int = 4096
+    height: int = 4096
+    fw: int = 17
+    fh: int = 17
+
+    @property
+    def total_flops(self) -> float:
+        return 2.0 * self.fw * self.fh * self.width * self.height
+
+    @property
+    def algorithmic_bytes(self) -> float:
+        return 4.0 * ((self.width + self.fw - 1) * (self.height + self.fh - 1) + self.width * self.height
+                      + self.fw * self.fh)
+
+    def tune_params(self):
+        return {
+            "block_size_x": [16, 32, 64],
+            "block_size_y": [1, 2, 4, 8, 16],
+            "tile_size_x": [1, 2, 4, 8],
+            "tile_size_y": [1, 2, 4, 8],
+            "use_shmem": [0, 1],
+            "use_padding": [0, 1],
+        }
+
+    def restrictions(self):
+        return [
+            "32 <= block_size_x * block_size_y <= 1024",
+            "tile_size_x * tile_size_y <= 32",
+            f"{self.width} % (block_size_x * tile_size_x) == 0",
+            f"{self.height} % (block_size_y * tile_size_y) == 0",
+            "use_shmem == 1 or use_padding == 0",
+            f"use_shmem == 0 or (block_size_y * tile_size_y + {self.fh - 1}) * "
+            f"(block_size_x * tile_size_x + {self.fw - 1} + 4 * use_padding) * 4 <= 48000",
+        ]
+
+    def default_config(self):
+        return {"block_size_x": 32, "block_size_y": 4, "tile_size_x": 4, "tile_size_y": 4, "use_shmem": 1,
+                "use_padding": 0}
+
+    def defines(self, config):
+        c = _as_dict(config)
+        return {
+            "BLOCK_X": c["block_size_x"],
+            "BLOCK_Y": c["block_size_y"],
+            "TILE_X": c["tile_size_x"],
+            "TILE_Y": c["tile_size_y"],
+            "USE_SMEM": c["use_shmem"],
+            "PAD": 4 * c["use_padding"],
+            "IMAGE_W": self.width,
+            "IMAGE_H": self.height,
+            "FW": self.fw,
+            "FH": self.fh,
+        }
+
+    def launch(self, config):
+        c = _as_dict(config)
+        gx = self.width // (c["block_size_x"] * c["tile_size_x"])
+        gy = self.height // (c["block_size_y"] * c["tile_size_y"])
+        return Launch((gx, gy, 1), (c["block_size_x"], c["block_size_y"], 1))
+
+    def host_inputs(self):
+        rng = np.random.default_rng(self.seed)
+        image = rng.uniform(0.0, 1.0, (self.height + self.fh - 1, self.width + self.fw - 1)).astype(np.float32)
+        filt = rng.uniform(0.0, 1.0, (self.fh, self.fw)).astype(np.float32)
+        return {"image": image, "filter": filt}
+
+    def prepare(self, gpu, inputs=None):
+        self.gpu = gpu
+        inputs = inputs or self.host_inputs()
+        self.inputs = inputs
+        self.buffers = {
+            "out": gpu.empty((self.height, self.width), np.float32),
+            "image": gpu.array(inputs["image"], slack=64),
+        }
+
+    def args(self, config):
+        return [self.buffers["out"], self.buffers["image"]]
+
+    def bind(self, kernel, config):
+        kernel.set_global("d_filter", self.inputs["filter"])
+
+
+# -- SGEMM --------------------------------------------------------------------------------
+
+
+@dataclass
+class SgemmProblem(KernelProblem):
+    name: str = "sgemm"
+    source: str = "sgemm.cu"
+    symbol: str = "sgemm"
+    seed: int = 0
+    m: int = 4096
+    n: int = 4096
+    k: int = 4096
+    alpha: float = 1.0
+    beta: float = 0.5
+    #: "paper": Kernel Tuner's CLBlast value lists; "b200": widened for 227 KB smem / 255 regs
+    value_set: str = "paper"
+
+    @property
+    def total_flops(self) -> float:
+        return 2.0 * self.m * self.n * self.k
+
+    @property
+    def algorithmic_bytes(self) -> float:
+        return 4.0 * (self.m * self.k + self.k * self.n + 2 * self.m * self.n)
+
+    def tune_params(self):
+        if self.value_set == "b200":
+            return {
+                "MWG": [64, 128, 256], "NWG": [64, 128, 256], "KWG": [8, 16, 32],
+                "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32, 64], "NDIMB": [8, 16, 32, 64],
+                "KWI": [1, 2, 4, 8], "VWM": [1, 2, 4], "VWN": [1, 2, 4], "STRM": [0, 1], "STRN": [0, 1],
+                "SA": [0, 1], "SB": [0, 1],
+            }
+        return {
+            "MWG": [16, 32, 64, 128], "NWG": [16, 32, 64, 128], "KWG": [16, 32],
+            "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32], "NDIMB": [8, 16, 32],
+            "KWI": [2, 8], "VWM": [1, 2, 4, 8], "VWN": [1, 2, 4, 8], "STRM": [0, 1], "STRN": [0, 1],
+            "SA": [0, 1], "SB": [0, 1],
+        }
+
+    def restrictions(self):
+        # CLBlast's xgemm constraints (KWG % KWI, tile divisibility, load shapes)
+        # plus the B200 static-smem budget (double buffered) and vector widths <= 4.
+        return [
+            "KWG % KWI == 0",
+            "MWG % (MDIMC * VWM) == 0",
+            "NWG % (NDIMC * VWN) == 0",
+            "MWG % (MDIMA * VWM) == 0",
+            "NWG % (NDIMB * VWN) == 0",
+            "KWG % ((MDIMC * NDIMC) / MDIMA) == 0",
+            "KWG % ((MDIMC * NDIMC) / NDIMB) == 0",
+            "(MDIMC * NDIMC) % MDIMA == 0",
+            "(MDIMC * NDIMC) % NDIMB == 0",
+            "VWM <= 4 and VWN <= 4",
+            "(SA * KWG * MWG + SB * KWG * NWG) * 2 * 4 <= 48 * 1024",
+            "(MWG / MDIMC) * (NWG / NDIMC) <= 128",
+            f"{self.m} % MWG == 0 and {self.n} % NWG == 0 and {self.k} % KWG == 0",
+        ]
+
+    def default_config(self):
+        return {"MWG": 128, "NWG": 128, "KWG": 16, "MDIMC": 16, "NDIMC": 16, "MDIMA": 32, "NDIMB": 32,
+                "KWI": 2, "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1}
+
+    def defines(self, config):
+        return dict(_as_dict(config))
+
+    def launch(self, config):
+        c = _as_dict(config)
+        return Launch((self.m // c["MWG"], self.n // c["NWG"], 1), (c["MDIMC"] * c["NDIMC"], 1, 1))
+
+    def host_inputs(self):
+        a = np.random.default_rng(self.seed).uniform(-1.0, 1.0, (self.m, self.k)).astype(np.float32)
+        b = np.random.default_rng(self.seed + 1).uniform(-1.0, 1.0, (self.k, self.n)).astype(np.float32)
+        c0 = np.random.default_rng(self.seed + 2).uniform(-1.0, 1.0, (self.m, self.n)).astype(np.float32)
+        return {"a": a, "b": b, "c0": c0}
+
+    def prepare(self, gpu, inputs=None):
+        self.gpu = gpu
+        inputs = inputs or self.host_inputs()
+        self.inputs = inputs
+        self.buffers = {
+            "at": gpu.array(np.ascontiguousarray(inputs["a"].T)),  # column-major A == row-major A^T
+            "b": gpu.array(inputs["b"]),
+            "out": gpu.array(inputs["c0"]),
+        }
+
+    def reset_output(self):
+        # C is read (beta != 0) and written: every run restarts from C0.
+        self.buffers["out"].upload(self.inputs["c0"])
+
+    def args(self, config):
+        b = self.buffers
+        return [i32(self.m), i32(self.n), i32(self.k), f32(self.alpha), f32(self.beta), b["at"], b["b"], b["out"]]
+
+
+# -- burner (P(f) sweep load) ---------------------------------------------------------------
+
+
+@dataclass
+class BurnerProblem(KernelProblem):
+    name: str = "burner"
+    source: str = "burner.cu"
+    symbol: str = "burner"
+    iters: int = 4096
+    blocks_per_sm: int = 8
+
+    @property
+    def total_flops(self) -> float:
+        sms = self.gpu.sm_count if self.gpu else 148
+        return 2.0 * 16 * 8 * self.iters * 256 * self.blocks_per_sm * sms
+
+    @property
+    def algorithmic_bytes(self) -> float:
+        return 0.0
+
+    def tune_params(self):
+        return {"chains": [8], "block": [256]}
+
+    def default_config(self):
+        return {"chains": 8, "block": 256}
+
+    def launch(self, config):
+        sms = self.gpu.sm_count if self.gpu else 148
+        return Launch((sms * self.blocks_per_sm, 1, 1), (256, 1, 1))
+
+    def host_inputs(self):
+        return {}
+
+    def prepare(self, gpu, inputs=None):
+        self.gpu = gpu
+        self.buffers = {"sink": gpu.empty((gpu.sm_count * self.blocks_per_sm * 256,), np.float32)}
+
+    def reset_output(self):
+        pass
+
+    def args(self, config):
+        return [self.buffers["sink"], i32(self.iters), f32(1.0)]
+
+
+PROBLEMS = {"pnpoly": PnPolyProblem, "conv2d": Conv2DProblem, "sgemm": SgemmProblem, "burner": BurnerProblem}
+
+
+def make_problem(name: str, **kwargs) -> KernelProblem:
+    try:
+        return PROBLEMS[name](**kwargs)
+    except KeyError:
+        from .errors import ConfigurationError
+
+        raise ConfigurationError(f"unknown kernel {name!r}; choose from {sorted(PROBLEMS)}") from None
