@@ -150,6 +150,14 @@ int jt_time(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const 
 int jt_bench(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args,
              double min_seconds, int min_reps, int max_reps, int sample_period_us, jt_bench_result *out,
              jt_sample *samples, int cap);
+/* CUDA events on the context's stream: an indexed pool of `n` events for
+ * timing arbitrary launch/copy sequences (bench.py). */
+int jt_events_reserve(jt_ctx *ctx, int n);
+int jt_event_record(jt_ctx *ctx, int index);
+int jt_event_elapsed(jt_ctx *ctx, int start, int stop, double *seconds);
+/* Async copies on the context stream (host memory should be pinned). */
+int jt_h2d_async(jt_ctx *ctx, unsigned long long dst, const void *src, size_t bytes);
+int jt_d2h_async(jt_ctx *ctx, void *dst, unsigned long long src, size_t bytes);
 /* Overwrite a scratch buffer larger than L2 (126 MB on B200). */
 int jt_l2_flush(jt_ctx *ctx);
 

@@ -282,6 +282,7 @@ struct jt_ctx {
     std::vector<jt_sample> samples;
     size_t sample_cap = 0;
     int period_us = 1000;
+    std::vector<CUevent> events;
     std::vector<jt_module *> modules;
     std::vector<jt_kernel *> kernels;
 };
@@ -578,6 +579,7 @@ int jt_close(jt_ctx *c) {
         delete m;
     }
     if (c->flush_buf) D.p_cuMemFree(c->flush_buf);
+    for (CUevent e : c->events) D.p_cuEventDestroy(e);
     D.p_cuEventDestroy(c->ev_a);
     D.p_cuEventDestroy(c->ev_b);
     D.p_cuStreamDestroy(c->stream);
@@ -815,6 +817,47 @@ int jt_bench(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *ar
     out->per_launch_s = out->total_s / reps;
     out->loop_t0 = out->host_t_done - out->total_s;
     return finish(JT_OK);
+}
+
+int jt_events_reserve(jt_ctx *c, int n) {
+    if (int e = bind(c)) return e;
+    if (n < 0 || n > (1 << 20)) return fail(JT_EINVAL, "bad event count %d", n);
+    while ((int)c->events.size() < n) {
+        CUevent ev;
+        CU_TRY(D.p_cuEventCreate(&ev, CU_EVENT_DEFAULT), "cuEventCreate");
+        c->events.push_back(ev);
+    }
+    return JT_OK;
+}
+
+int jt_event_record(jt_ctx *c, int index) {
+    if (int e = bind(c)) return e;
+    if (index < 0 || index >= (int)c->events.size()) return fail(JT_EINVAL, "event %d not reserved", index);
+    CU_TRY(D.p_cuEventRecord(c->events[index], c->stream), "cuEventRecord");
+    return JT_OK;
+}
+
+int jt_event_elapsed(jt_ctx *c, int start, int stop, double *seconds) {
+    if (int e = bind(c)) return e;
+    const int n = (int)c->events.size();
+    if (!seconds || start < 0 || stop < 0 || start >= n || stop >= n) return fail(JT_EINVAL, "bad event index");
+    CU_TRY(D.p_cuEventSynchronize(c->events[stop]), "cuEventSynchronize");
+    float ms = 0.f;
+    CU_TRY(D.p_cuEventElapsedTime(&ms, c->events[start], c->events[stop]), "cuEventElapsedTime");
+    *seconds = ms * 1e-3;
+    return JT_OK;
+}
+
+int jt_h2d_async(jt_ctx *c, unsigned long long dst, const void *src, size_t bytes) {
+    if (int e = bind(c)) return e;
+    CU_TRY(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, c->stream), "cuMemcpyHtoDAsync");
+    return JT_OK;
+}
+
+int jt_d2h_async(jt_ctx *c, void *dst, unsigned long long src, size_t bytes) {
+    if (int e = bind(c)) return e;
+    CU_TRY(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, c->stream), "cuMemcpyDtoHAsync");
+    return JT_OK;
 }
 
 int jt_l2_flush(jt_ctx *c) {

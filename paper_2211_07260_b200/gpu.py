@@ -171,10 +171,14 @@ class GPU:
         check(L.jt_device_info_get(self.handle, ctypes.byref(info)), "jt_device_info_get")
         self.info = info
         self._modules: dict[str, Kernel] = {}
+        self._pinned: list = []
 
     # -- lifecycle --------------------------------------------------------
     def close(self) -> None:
         if self.handle:
+            for ptr in self._pinned:
+                native.lib().jt_host_free(self.handle, ptr)
+            self._pinned = []
             native.lib().jt_close(self.handle)
             self.handle = None
 
@@ -214,6 +218,35 @@ class GPU:
 
     def synchronize(self) -> None:
         check(native.lib().jt_synchronize(self.handle), "jt_synchronize")
+
+    # -- events / async copies (bench.py) --------------------------------------
+    def reserve_events(self, n: int) -> None:
+        check(native.lib().jt_events_reserve(self.handle, int(n)), "jt_events_reserve")
+
+    def record(self, index: int) -> None:
+        check(native.lib().jt_event_record(self.handle, int(index)), "jt_event_record")
+
+    def elapsed(self, start: int, stop: int) -> float:
+        out = ctypes.c_double()
+        check(native.lib().jt_event_elapsed(self.handle, int(start), int(stop), ctypes.byref(out)), "jt_event_elapsed")
+        return out.value
+
+    def h2d_async(self, dst: "DeviceArray", host: np.ndarray) -> None:
+        check(native.lib().jt_h2d_async(self.handle, dst.ptr, host.ctypes.data, host.nbytes), "jt_h2d_async")
+
+    def d2h_async(self, host: np.ndarray, src: "DeviceArray") -> None:
+        check(native.lib().jt_d2h_async(self.handle, host.ctypes.data, src.ptr, host.nbytes), "jt_d2h_async")
+
+    def pinned(self, shape, dtype=np.float32) -> np.ndarray:
+        """A numpy array backed by page-locked host memory owned by this context."""
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        ptr = ctypes.c_void_p()
+        check(native.lib().jt_host_alloc(self.handle, nbytes, ctypes.byref(ptr)), "jt_host_alloc")
+        buf = (ctypes.c_byte * nbytes).from_address(ptr.value)
+        arr = np.frombuffer(buf, dtype=dtype).reshape(shape)
+        self._pinned.append(ptr)
+        return arr
 
     def l2_flush(self) -> None:
         check(native.lib().jt_l2_flush(self.handle), "jt_l2_flush")

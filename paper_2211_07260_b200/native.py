@@ -51,7 +51,8 @@ EXPORTS = (
     "jt_kernel_get", "jt_kernel_attributes", "jt_launch", "jt_time", "jt_bench", "jt_l2_flush",
     "jt_sample_now", "jt_sampler_start", "jt_sampler_stop", "jt_clock_lock", "jt_clock_reset",
     "jt_app_clocks_set", "jt_app_clocks_reset", "jt_power_limit_set", "jt_power_limit_reset",
-    "jt_pnpoly_edges", "jt_module_set_global",
+    "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
+    "jt_h2d_async", "jt_d2h_async",
 )
 
 
@@ -205,6 +206,11 @@ def _declare(lib) -> None:
              c.POINTER(JTBenchResult), c.POINTER(JTSample), c.c_int],
         ),
         "jt_l2_flush": (c.c_int, [P]),
+        "jt_events_reserve": (c.c_int, [P, c.c_int]),
+        "jt_event_record": (c.c_int, [P, c.c_int]),
+        "jt_event_elapsed": (c.c_int, [P, c.c_int, c.c_int, c.POINTER(c.c_double)]),
+        "jt_h2d_async": (c.c_int, [P, c.c_ulonglong, P, c.c_size_t]),
+        "jt_d2h_async": (c.c_int, [P, P, c.c_ulonglong, c.c_size_t]),
         "jt_sample_now": (c.c_int, [P, c.POINTER(JTSample)]),
         "jt_sampler_start": (c.c_int, [P, c.c_int, c.c_int]),
         "jt_sampler_stop": (c.c_int, [P, c.POINTER(JTSample), c.c_int, c.POINTER(c.c_int)]),

@@ -1,0 +1,118 @@
+"""Host-buffer entry points of the kernel suite (what a user calls).
+
+``conv2d(image, filt)``, ``pnpoly(points, vx, vy)`` and ``sgemm(a, b, c)``
+take numpy arrays, copy the inputs to the B200 (asynchronously, fast when
+the arrays are page-locked — see :func:`pinned`), launch the tuned sm_100a
+kernel through libjt and copy the result back. Runners are cached per
+(kernel, shape, config, device) so repeated calls reuse compiled modules and
+device buffers. Configs default to the B200-tuned time-optimal ones
+(:mod:`.tuned`), else the kernel's default.
+"""
+
+from __future__ import annotations
+
+import threading
+from typing import Any, Mapping
+
+import numpy as np
+
+from . import tuned
+from .gpu import GPU
+from .kernels import KernelProblem, make_problem
+
+__all__ = ["Runner", "conv2d", "pnpoly", "sgemm", "pinned", "device"]
+
+_lock = threading.Lock()
+_gpus: dict[int, GPU] = {}
+_runners: dict[tuple, "Runner"] = {}
+
+
+def device(ordinal: int = 0) -> GPU:
+    with _lock:
+        gpu = _gpus.get(ordinal)
+        if gpu is None:
+            gpu = _gpus[ordinal] = GPU(ordinal)
+        return gpu
+
+
+def pinned(shape, dtype=np.float32, ordinal: int = 0) -> np.ndarray:
+    """Page-locked host array (H2D/D2H at full PCIe speed, fully async)."""
+    return device(ordinal).pinned(shape, dtype)
+
+
+class Runner:
+    """One prepared (problem, config) on one GPU: inputs in, output out."""
+
+    def __init__(self, problem: KernelProblem, config: Mapping[str, Any], gpu: GPU, inputs: dict[str, np.ndarray]):
+        self.problem = problem
+        self.config = dict(config)
+        self.gpu = gpu
+        problem.prepare(gpu, inputs)
+        self.kernel = problem.kernel(self.config)
+        self.launch_shape = problem.launch(self.config)
+        self.args = problem.args(self.config)
+
+    def run(self, uploads: Mapping[str, np.ndarray], out: np.ndarray | None = None) -> np.ndarray:
+        """H2D each named input buffer, launch once, D2H the output (one stream)."""
+        gpu = self.gpu
+        for name, host in uploads.items():
+            gpu.h2d_async(self.problem.buffers[name], np.ascontiguousarray(host))
+        self.problem.bind(self.kernel, self.config)
+        gpu.launch(self.kernel, self.launch_shape, self.args)
+        dst = self.problem.buffers["out"]
+        if out is None:
+            out = np.empty(dst.shape, dtype=dst.dtype)
+        gpu.d2h_async(out, dst)
+        gpu.synchronize()
+        return out
+
+
+def _runner(name: str, key: tuple, config, problem_kwargs: dict, inputs: dict, ordinal: int) -> Runner:
+    problem = make_problem(name, **problem_kwargs)
+    cfg = dict(config or tuned.best_config(name) or problem.default_config())
+    cache_key = (name, key, tuple(sorted(cfg.items())), ordinal)
+    with _lock:
+        hit = _runners.get(cache_key)
+    if hit is None:
+        hit = Runner(problem, cfg, device(ordinal), inputs)
+        with _lock:
+            _runners[cache_key] = hit
+    return hit
+
+
+def conv2d(image: np.ndarray, filt: np.ndarray, *, config=None, out=None, ordinal: int = 0) -> np.ndarray:
+    """Valid-mode 2D correlation of a pre-padded float32 image with a 17x17-style filter."""
+    image = np.asarray(image, dtype=np.float32)
+    filt = np.asarray(filt, dtype=np.float32)
+    fh, fw = filt.shape
+    h, w = image.shape[0] - fh + 1, image.shape[1] - fw + 1
+    r = _runner("conv2d", (h, w, fh, fw), config, {"width": w, "height": h, "fw": fw, "fh": fh},
+                {"image": image, "filter": filt}, ordinal)
+    r.problem.inputs["filter"] = filt
+    return r.run({"image": image}, out)
+
+
+def pnpoly(points: np.ndarray, vx: np.ndarray, vy: np.ndarray, *, config=None, out=None, ordinal: int = 0):
+    """int32 inside/outside bitmap for float32 points (n, 2) against a polygon."""
+    points = np.asarray(points, dtype=np.float32)
+    vx = np.asarray(vx, dtype=np.float32)
+    vy = np.asarray(vy, dtype=np.float32)
+    key = (points.shape[0], vx.size, vx.tobytes(), vy.tobytes())
+    r = _runner("pnpoly", key, config, {"n_points": points.shape[0], "n_vertices": vx.size},
+                {"points": points, "vx": vx, "vy": vy}, ordinal)
+    return r.run({"points": points}, out)
+
+
+def sgemm(a: np.ndarray, b: np.ndarray, c: np.ndarray, alpha: float = 1.0, beta: float = 0.0, *, config=None,
+          ordinal: int = 0) -> np.ndarray:
+    """alpha * a @ b + beta * c in FP32 (a is staged column-major, as BLAS 'N')."""
+    a = np.asarray(a, dtype=np.float32)
+    b = np.asarray(b, dtype=np.float32)
+    c = np.asarray(c, dtype=np.float32)
+    m, k = a.shape
+    n = b.shape[1]
+    r = _runner("sgemm", (m, n, k, float(alpha), float(beta)), config,
+                {"m": m, "n": n, "k": k, "alpha": float(alpha), "beta": float(beta)}, {"a": a, "b": b, "c0": c},
+                ordinal)
+    at = a.T if a.flags.f_contiguous else np.ascontiguousarray(a.T)
+    return r.run({"at": at, "b": b, "out": c})

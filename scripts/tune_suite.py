@@ -1,0 +1,205 @@
+"""Energy/time tuning of the kernel suite on one B200 through the drop-in API.
+
+For each kernel: build the (curated) tunable space, precompile every config
+with NVRTC on a host thread pool, then ``run_strategy`` with a
+``B200Device`` and an ``NVMLObserver`` (energy = NVML energy-counter slope x
+runtime) and the ``gflops`` / ``gflops_per_w`` user metrics. The time-optimal
+and energy-optimal configs are re-verified against the CPU oracle and written
+to ``paper_2211_07260_b200/tuned_b200.json``; every measurement goes to a
+JSONL result cache under ``results/`` (reference ``ResultCache`` format).
+
+If the controller can lock SM clocks, ``nvml_gr_clock`` joins the space
+(the paper's config x clock search); on pools where NVML refuses clock
+control the clock axis is dropped and the observed clock is recorded.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle import kernels_oracle as O  # noqa: E402  (checker only)
+from paper_2211_07260_b200 import (  # noqa: E402
+    CLOCK_PARAM, NVMLObserver, Objective, ResultCache, SearchSpace, TunableParameter, TuningRun, default_metrics,
+    run_strategy,
+)
+from paper_2211_07260_b200.b200 import B200Device  # noqa: E402
+from paper_2211_07260_b200.gpu import GPU  # noqa: E402
+from paper_2211_07260_b200.kernels import make_problem  # noqa: E402
+from paper_2211_07260_b200.tuned import TUNED_PATH  # noqa: E402
+
+RESULTS = Path(os.environ.get("JT_RESULTS_DIR", "gpurun_out/results"))
+
+
+def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
+    """(space document, strategy, budget) per kernel."""
+    if name == "pnpoly":
+        doc = {
+            "parameters": {
+                "block_size_x": [64, 128, 192, 256, 384, 512, 768, 1024],
+                "tile": [2, 4, 6, 8],
+                "vec": [2],
+                "method": [2],
+                "between": [0],
+                "poly_smem": [1],
+                "asm": [3],
+            },
+            "restrictions": [],
+        }
+        return doc, "exhaustive", None
+    if name == "conv2d":
+        return problem.space_document(), "exhaustive", None
+    if name == "sgemm":
+        doc = {
+            "parameters": {
+                "MWG": [64, 128], "NWG": [64, 128], "KWG": [16, 32], "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32],
+                "MDIMA": [16, 32], "NDIMB": [16, 32], "KWI": [2, 8], "VWM": [2, 4], "VWN": [2, 4],
+                "STRM": [0, 1], "STRN": [0, 1], "SA": [1], "SB": [1],
+            },
+            "restrictions": problem.restrictions(),
+        }
+        return doc, "random", 160
+    raise ValueError(name)
+
+
+def oracle_check(problem, cfg) -> tuple[bool, float]:
+    out = problem.fetch_output()
+    inp = problem.inputs
+    if problem.name == "pnpoly":
+        want = O.pnpoly(inp["points"], inp["vx"], inp["vy"], problem.formula(cfg))
+        bad = int((out != want).sum())
+        return bad == 0, float(bad)
+    if problem.name == "conv2d":
+        err = O.conv2d_error(out, O.conv2d(inp["image"], inp["filter"]), inp["image"], inp["filter"])
+        return err <= O.CONV_TOL, err
+    err = O.sgemm_error(out, O.sgemm(inp["a"], inp["b"], inp["c0"], problem.alpha, problem.beta))
+    return err <= O.SGEMM_TOL, err
+
+
+def summarize(result) -> dict:
+    obs = result.observer_results
+    return {
+        "config": result.config.as_dict(),
+        "time_s": result.time,
+        "energy_j": result.energy,
+        "gflops": result.metrics.get("gflops"),
+        "gflops_per_w": result.metrics.get("gflops_per_w"),
+        "power_w": obs.get("nvml_power"),
+        "sm_clock_mhz": obs.get("nvml_sm_clock"),
+        "temperature_c": obs.get("nvml_temperature"),
+        "clock_locked": obs.get("nvml_clock_locked"),
+    }
+
+
+def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | None) -> dict:
+    problem = make_problem(name)
+    doc, strategy, budget = curated_space(name, problem)
+    space = SearchSpace.from_dict(doc)
+    if clocks:
+        space = space.augment(TunableParameter(CLOCK_PARAM, tuple(clocks)))
+    kernel_space = SearchSpace.from_dict(doc)
+    configs = [c.as_dict() for c in kernel_space.enumerate()]
+    if strategy == "random" and budget:
+        rng = np.random.default_rng(seed)
+        configs = [configs[i] for i in rng.choice(len(configs), size=min(len(configs), budget * 2), replace=False)]
+    t0 = time.time()
+    with ThreadPoolExecutor(min(32, os.cpu_count() or 8)) as pool:
+        list(pool.map(lambda c: _try_compile(problem, c), configs))
+    compile_s = time.time() - t0
+
+    dev = B200Device(problem, gpu=gpu, min_window=duration)
+    RESULTS.mkdir(exist_ok=True)
+    cache = ResultCache(RESULTS / f"cache_{name}.jsonl")
+    metrics = default_metrics(problem.total_flops)
+    t0 = time.time()
+    outcome = run_strategy(
+        TuningRun(space, strategy, Objective("energy"), budget=budget, seed=seed),
+        dev,
+        [NVMLObserver(duration)],
+        user_metrics=metrics,
+        constants={"total_flops": problem.total_flops},
+        cache=cache,
+    )
+    tune_s = time.time() - t0
+    ok = [r for r in outcome.history if not r.failed]
+    by_time = min(ok, key=lambda r: r.time)
+    by_energy = min(ok, key=lambda r: r.energy)
+    entry = {
+        "space_size": space.size(),
+        "strategy": strategy,
+        "evaluations": outcome.evaluations,
+        "device_executions": outcome.device_executions,
+        "failed": sum(r.failed for r in outcome.history),
+        "compile_s": round(compile_s, 1),
+        "tune_s": round(tune_s, 1),
+        "points_per_s": round(outcome.device_executions / tune_s, 3) if tune_s > 0 else None,
+        "clock_mode": dev.clock_mode or "not requested",
+        "time_optimal": summarize(by_time),
+        "energy_optimal": summarize(by_energy),
+    }
+    # correctness gate on the two winners
+    for key in ("time_optimal", "energy_optimal"):
+        cfg = {k: v for k, v in entry[key]["config"].items() if not k.startswith("nvml_")}
+        k = problem.kernel(cfg)
+        problem.bind(k, cfg)
+        problem.reset_output()
+        gpu.launch(k, problem.launch(cfg), problem.args(cfg))
+        gpu.synchronize()
+        good, metric = oracle_check(problem, cfg)
+        entry[key]["oracle_ok"] = good
+        entry[key]["oracle_metric"] = metric
+    dev.release_clock()
+    for b in problem.buffers.values():
+        b.free()
+    print(name, json.dumps({k: entry[k] for k in ("space_size", "evaluations", "tune_s", "points_per_s")}),
+          "\n  time-opt  ", entry["time_optimal"], "\n  energy-opt", entry["energy_optimal"], flush=True)
+    return entry
+
+
+def _try_compile(problem, cfg):
+    try:
+        problem.cubin({**problem.default_config(), **cfg})
+    except Exception:  # noqa: BLE001  (the tuner records the failure later)
+        pass
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kernels", default="conv2d,pnpoly,sgemm")
+    ap.add_argument("--duration", type=float, default=0.4)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--clocks", default="auto", help="'auto', 'none' or comma list of MHz")
+    args = ap.parse_args()
+    gpu = GPU(0)
+    clocks = None
+    if args.clocks not in ("none", "auto"):
+        clocks = [int(c) for c in args.clocks.split(",")]
+    elif args.clocks == "auto":
+        probe = B200Device("burner", gpu=gpu)
+        probe.set_core_clock(probe.spec.peak_clock)
+        if probe.clock_mode != "refused":
+            grid = probe.clock_grid(step_mhz=150, lo=600)
+            clocks = grid
+        probe.release_clock()
+        print("clock control:", probe.clock_mode, "->", clocks, flush=True)
+    data = json.loads(TUNED_PATH.read_text()) if TUNED_PATH.exists() else {}
+    for name in args.kernels.split(","):
+        data[name] = tune(gpu, name, args.duration, args.seed, clocks)
+        TUNED_PATH.write_text(json.dumps(data, indent=1) + "\n")
+    Path("gpurun_out").mkdir(exist_ok=True)
+    Path("gpurun_out/tuned_b200.json").write_text(json.dumps(data, indent=1) + "\n")
+    gpu.close()
+
+
+if __name__ == "__main__":
+    main()
