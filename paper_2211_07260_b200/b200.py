@@ -86,7 +86,7 @@ class B200Device:
         ordinal: int = 0,
         *,
         gpu: GPU | None = None,
-        min_window: float = 0.05,
+        min_window: float = 0.25,
         settle: float = 0.02,
         clock_settle: float = 0.05,
         sample_period_us: int = 1000,
@@ -290,9 +290,15 @@ class B200Device:
         window = steady_window(total, self.settle)
         steady = [s for s in during if window[0] <= s[T] - t0 <= window[1]] or during or run.samples
         slope = counter_slope(run.samples, t0 + window[0], t0 + window[1])
+        source = 1.0  # energy counter
         if slope is None:
-            # counter cadence longer than the window: fall back to the whole loop
+            # counter cadence (~100 ms on B200) longer than the window: widen to the loop
             slope = counter_slope(run.samples, t0 - 0.05, t0 + total + 0.05)
+        if slope is None:
+            # still < 2 counter updates: median instant power over the steady window
+            inst = [s[P_INST] for s in steady if math.isfinite(s[P_INST])]
+            slope = float(statistics.median(inst)) if inst else None
+            source = 0.0
         clocks = [s[SM_MHZ] for s in steady if s[SM_MHZ]]
         observed = float(statistics.median(clocks)) if clocks else float(self.state.core_clock)
         self.last_observed_clock = observed
@@ -307,6 +313,7 @@ class B200Device:
             "throttle_reasons": float(reasons),
             "power_capped": 1.0 if reasons & SW_POWER_CAP else 0.0,
             "reps": float(run.reps),
+            "energy_source": source,
         }
         return Execution(
             runtime=run.per_launch_s,

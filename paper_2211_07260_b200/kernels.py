@@ -83,6 +83,22 @@ class KernelProblem:
     def default_config(self) -> dict[str, Any]:
         raise NotImplementedError
 
+    def is_valid(self, config: Mapping[str, Any]) -> bool:
+        """Config satisfies this problem's value lists and restrictions."""
+        merged = {**self.default_config(), **_as_dict(config)}
+        space = self.space()
+        return space.is_valid(KernelConfig.from_dict({k: merged[k] for k in space.names}))
+
+    def fitting_config(self, preferred: list) -> dict[str, Any]:
+        """First valid config among ``preferred`` (None entries skipped), else the
+        valid config closest (Hamming) to the default."""
+        for cfg in preferred:
+            if cfg and self.is_valid(cfg):
+                return {**self.default_config(), **cfg}
+        default = self.default_config()
+        best = min(self.space().enumerate(), key=lambda c: sum(c[k] != default.get(k) for k in c))
+        return best.as_dict()
+
     def defines(self, config: Mapping[str, Any]) -> dict[str, Any]:
         return {k.upper(): v for k, v in config.items()}
 

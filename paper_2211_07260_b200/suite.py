@@ -69,7 +69,11 @@ class Runner:
 
 def _runner(name: str, key: tuple, config, problem_kwargs: dict, inputs: dict, ordinal: int) -> Runner:
     problem = make_problem(name, **problem_kwargs)
-    cfg = dict(config or tuned.best_config(name) or problem.default_config())
+    if config:
+        cfg = dict(config)
+    else:  # tuned configs were tuned at the BASELINE size; keep the first that fits this shape
+        cfg = problem.fitting_config([tuned.best_config(name), tuned.best_config(name, "energy_optimal"),
+                                      problem.default_config()])
     cache_key = (name, key, tuple(sorted(cfg.items())), ordinal)
     with _lock:
         hit = _runners.get(cache_key)

@@ -1,0 +1,217 @@
+"""Kernel parity on the B200 through libjt (the C-ABI) against the CPU oracles.
+
+Bars: PnPoly bit-exact against the oracle formulation the
+config computes; Conv2D max|out - ref| / (sum|f| max|x|) <= 1e-5; SGEMM
+max|C - C64| / max|C64| <= 1e-5 (FP32, fp64 oracle).
+"""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import kernels_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    from paper_2211_07260_b200.gpu import GPU
+
+    g = GPU(0)
+    yield g
+    g.close()
+
+
+def run_once(gpu, problem, cfg):
+    k = problem.kernel(cfg)
+    problem.bind(k, cfg)
+    problem.reset_output()
+    gpu.launch(k, problem.launch(cfg), problem.args(cfg))
+    gpu.synchronize()
+    return problem.fetch_output()
+
+
+# -- PnPoly ---------------------------------------------------------------------------
+
+PNPOLY_CONFIGS = (
+    [dict(block_size_x=b, tile=t, vec=2, method=2, between=0, poly_smem=1, asm=3)
+     for b, t in itertools.product((96, 256, 1024), (2, 4, 6, 8))]
+    + [dict(block_size_x=b, tile=t, vec=v, method=2, between=1, poly_smem=1, asm=a)
+       for a, b, t, v in itertools.product((1, 2), (128,), (1, 2, 4, 6), (1, 2)) if not (v == 2 and t % 2)]
+    + [dict(block_size_x=b, tile=t, vec=v, method=m, between=bt, poly_smem=s, asm=0)
+       for m, bt, s, (b, t, v) in itertools.product((0, 1, 2), (0, 1), (0, 1), ((64, 1, 1), (256, 4, 2)))]
+)
+
+
+@pytest.fixture(scope="module")
+def pnpoly_small(gpu):
+    from paper_2211_07260_b200.kernels import PnPolyProblem
+
+    p = PnPolyProblem(n_points=1_000_003)  # ragged: not a multiple of any block*tile
+    p.prepare(gpu)
+    inp = p.inputs
+    refs = {m: O.pnpoly(inp["points"], inp["vx"], inp["vy"], m) for m in range(4)}
+    return p, refs
+
+
+@pytest.mark.parametrize("cfg", PNPOLY_CONFIGS, ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
+def test_pnpoly_bit_exact_across_configs(gpu, pnpoly_small, cfg):
+    p, refs = pnpoly_small
+    got = run_once(gpu, p, cfg)
+    want = refs[p.formula(cfg)]
+    assert got.dtype == np.int32 and got.shape == want.shape
+    assert np.array_equal(got, want), f"{int((got != want).sum())} points differ"
+
+
+@pytest.mark.parametrize("n", [1, 7, 4097])
+def test_pnpoly_tiny_and_ragged_inputs(gpu, n):
+    from paper_2211_07260_b200.kernels import PnPolyProblem
+
+    p = PnPolyProblem(n_points=n)
+    p.prepare(gpu)
+    for cfg in (p.default_config(), dict(p.default_config(), asm=0, between=1, vec=1, tile=1)):
+        got = run_once(gpu, p, cfg)
+        np.testing.assert_array_equal(got, O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"],
+                                                    p.formula(cfg)))
+
+
+def test_pnpoly_degenerate_points_and_polygon(gpu):
+    """Points on vertices, on horizontal/vertical edges and at y = vertex y;
+    a polygon with horizontal edges and a repeated vertex."""
+    from paper_2211_07260_b200.kernels import PnPolyProblem
+
+    vx = np.array([0.0, 0.5, 0.5, 1.0, 1.0, 0.0, 0.0], np.float32)
+    vy = np.array([0.0, 0.0, 0.25, 0.25, 1.0, 1.0, 1.0], np.float32)  # last vertex repeated
+    xs = np.unique(np.concatenate([vx, vx + 1e-7, vx - 1e-7, [0.25, 0.75, -0.5, 1.5]])).astype(np.float32)
+    ys = np.unique(np.concatenate([vy, vy + 1e-7, vy - 1e-7, [0.1, 0.6, -0.5, 1.5]])).astype(np.float32)
+    pts = np.array([[x, y] for x in xs for y in ys], np.float32)
+    p = PnPolyProblem(n_points=len(pts), n_vertices=vx.size)
+    p.prepare(gpu, {"points": pts, "vx": vx, "vy": vy})
+    for cfg in PNPOLY_CONFIGS[::5]:
+        got = run_once(gpu, p, cfg)
+        np.testing.assert_array_equal(got, O.pnpoly(pts, vx, vy, p.formula(cfg)), err_msg=str(cfg))
+    # the four formulations must agree with the textbook answer on clear cases
+    inside = run_once(gpu, p, p.default_config())
+    lookup = {(float(x), float(y)): v for (x, y), v in zip(pts, inside)}
+    f = lambda x, y: lookup[(float(np.float32(x)), float(np.float32(y)))]  # noqa: E731
+    assert f(0.25, 0.1) == 1 and f(0.75, 0.6) == 1 and f(0.75, 0.1) == 0
+    assert f(-0.5, 0.6) == 0 and f(1.5, 0.6) == 0
+
+
+def test_pnpoly_full_size_tuned_bit_exact(gpu):
+    from paper_2211_07260_b200 import tuned
+    from paper_2211_07260_b200.kernels import PnPolyProblem
+
+    p = PnPolyProblem()  # 20,000,000 points x 600 vertices (BASELINE configs[0])
+    p.prepare(gpu)
+    for cfg in [tuned.best_config("pnpoly") or p.default_config(), tuned.best_config("pnpoly", "energy_optimal")]:
+        if cfg is None:
+            continue
+        got = run_once(gpu, p, cfg)
+        want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], p.formula(cfg))
+        assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ"
+        # formula 3 (sign-bit) and the IEEE-compare formula 2 agree on this input
+        assert np.array_equal(want, O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2))
+
+
+# -- Conv2D ------------------------------------------------------------------------------
+
+CONV_CONFIGS = [
+    dict(block_size_x=32, block_size_y=4, tile_size_x=4, tile_size_y=4, use_shmem=1, use_padding=0),
+    dict(block_size_x=32, block_size_y=4, tile_size_x=4, tile_size_y=4, use_shmem=1, use_padding=1),
+    dict(block_size_x=64, block_size_y=8, tile_size_x=8, tile_size_y=2, use_shmem=0, use_padding=0),
+    dict(block_size_x=16, block_size_y=16, tile_size_x=1, tile_size_y=1, use_shmem=1, use_padding=0),
+    dict(block_size_x=16, block_size_y=2, tile_size_x=2, tile_size_y=8, use_shmem=0, use_padding=0),
+    dict(block_size_x=64, block_size_y=1, tile_size_x=2, tile_size_y=4, use_shmem=1, use_padding=1),
+    dict(block_size_x=32, block_size_y=16, tile_size_x=1, tile_size_y=8, use_shmem=1, use_padding=0),
+]
+
+
+@pytest.mark.parametrize("cfg", CONV_CONFIGS, ids=lambda c: "-".join(str(v) for v in c.values()))
+@pytest.mark.parametrize("shape", [(512, 512), (512, 256)])
+def test_conv2d_within_fp32_tolerance(gpu, cfg, shape):
+    from paper_2211_07260_b200.kernels import Conv2DProblem
+
+    w, h = shape
+    p = Conv2DProblem(width=w, height=h)
+    p.prepare(gpu)
+    got = run_once(gpu, p, cfg)
+    err = O.conv2d_error(got, O.conv2d(p.inputs["image"], p.inputs["filter"]), p.inputs["image"],
+                         p.inputs["filter"])
+    assert err <= O.CONV_TOL
+
+
+def test_conv2d_full_size_tuned(gpu):
+    from paper_2211_07260_b200 import tuned
+    from paper_2211_07260_b200.kernels import Conv2DProblem
+
+    p = Conv2DProblem()
+    p.prepare(gpu)
+    ref = O.conv2d(p.inputs["image"], p.inputs["filter"])
+    for obj in ("time_optimal", "energy_optimal"):
+        cfg = tuned.best_config("conv2d", obj) or p.default_config()
+        got = run_once(gpu, p, cfg)
+        assert O.conv2d_error(got, ref, p.inputs["image"], p.inputs["filter"]) <= O.CONV_TOL
+
+
+# -- SGEMM ---------------------------------------------------------------------------------
+
+SGEMM_CONFIGS = [
+    {},
+    dict(MWG=64, NWG=128, KWG=32, MDIMC=8, NDIMC=16, MDIMA=16, NDIMB=32, KWI=8, VWM=2, VWN=4, STRM=1, STRN=0),
+    dict(MWG=64, NWG=64, KWG=16, MDIMC=16, NDIMC=16, MDIMA=16, NDIMB=16, KWI=2, VWM=1, VWN=1, STRM=0, STRN=0),
+    dict(MWG=128, NWG=64, KWG=16, MDIMC=16, NDIMC=8, MDIMA=32, NDIMB=8, KWI=2, VWM=2, VWN=2, SA=0, SB=1),
+    dict(MWG=32, NWG=32, KWG=16, MDIMC=8, NDIMC=8, MDIMA=8, NDIMB=8, KWI=8, VWM=4, VWN=4, SA=0, SB=0),
+    dict(MWG=128, NWG=128, KWG=16, MDIMC=32, NDIMC=8, MDIMA=32, NDIMB=32, KWI=2, VWM=4, VWN=4, STRM=0, STRN=1),
+]
+
+
+@pytest.mark.parametrize("overrides", SGEMM_CONFIGS, ids=range(len(SGEMM_CONFIGS)))
+@pytest.mark.parametrize("mnk,beta", [((512, 512, 512), 0.5), ((256, 384, 128), 0.0)])
+def test_sgemm_within_fp32_tolerance(gpu, overrides, mnk, beta):
+    from paper_2211_07260_b200.kernels import SgemmProblem
+
+    m, n, k = mnk
+    p = SgemmProblem(m=m, n=n, k=k, beta=beta)
+    p.prepare(gpu)
+    cfg = {**p.default_config(), **overrides}
+    got = run_once(gpu, p, cfg)
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    assert O.sgemm_error(got, ref) <= O.SGEMM_TOL
+
+
+def test_sgemm_full_size_tuned(gpu):
+    from paper_2211_07260_b200 import tuned
+    from paper_2211_07260_b200.kernels import SgemmProblem
+
+    p = SgemmProblem()
+    p.prepare(gpu)
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    for obj in ("time_optimal", "energy_optimal"):
+        cfg = tuned.best_config("sgemm", obj) or p.default_config()
+        assert O.sgemm_error(run_once(gpu, p, cfg), ref) <= O.SGEMM_TOL
+
+
+# -- host-buffer API (suite) ---------------------------------------------------------------
+
+
+def test_suite_host_api_matches_oracles():
+    from paper_2211_07260_b200 import suite
+    from paper_2211_07260_b200.kernels import Conv2DProblem, PnPolyProblem, SgemmProblem
+
+    ci = Conv2DProblem(width=256, height=256).host_inputs()
+    out = suite.conv2d(ci["image"], ci["filter"])
+    assert O.conv2d_error(out, O.conv2d(ci["image"], ci["filter"]), ci["image"], ci["filter"]) <= O.CONV_TOL
+    # second call with a different image reuses the runner and re-uploads
+    img2 = ci["image"][::-1].copy()
+    out2 = suite.conv2d(img2, ci["filter"])
+    assert O.conv2d_error(out2, O.conv2d(img2, ci["filter"]), img2, ci["filter"]) <= O.CONV_TOL
+    pi = PnPolyProblem(n_points=100_000).host_inputs()
+    got = suite.pnpoly(pi["points"], pi["vx"], pi["vy"])
+    np.testing.assert_array_equal(got, O.pnpoly(pi["points"], pi["vx"], pi["vy"], 3))
+    si = SgemmProblem(m=256, n=128, k=64).host_inputs()
+    c = suite.sgemm(si["a"], si["b"], si["c0"], 1.0, 0.5, config=SgemmProblem().default_config() | {
+        "MWG": 64, "NWG": 64, "MDIMC": 16, "NDIMC": 16, "MDIMA": 16, "NDIMB": 16})
+    assert O.sgemm_error(c, O.sgemm(si["a"], si["b"], si["c0"], 1.0, 0.5)) <= O.SGEMM_TOL
