@@ -18,6 +18,8 @@
 //                 (identical booleans; different instruction shapes)
 //   POLY_SMEM     0: edge table in __constant__ memory; 1: staged in shared memory
 //   VERTICES      polygon size (compile-time so the edge loop is counted)
+//   (launch)      persist=1 in the tuning space sizes the grid to the SMs'
+//                 residency and the kernel strides over point tiles
 //   ASM           1: hand-written PTX edge loop (needs BETWEEN=1, POLY_SMEM=1,
 //                 METHOD 2, TILE in {1,2,4,6}): per edge one LDS.128 of the
 //                 packed record {ymin, ymax, slope, icpt}, then per point
@@ -34,6 +36,12 @@
 //                   LOP3 t = (d ^ d_prev) & e; (1/2) LOP3 acc ^= t1 ^ t2
 //                 inside = sign bit of acc. Bit-exact against the oracle's
 //                 formulation 3 (same as formula 2 unless a coordinate is -0.0).
+//                 4: ASM 3 with point pairs in packed f32x2 registers
+//                 (FADD2/FFMA2): 1.5 FMA-pipe + 1.5 ALU instructions per
+//                 edge-point (VEC=2, TILE in {4,8}); same formulation 3.
+//                 5: ASM 3 with sign(d_k ^ d_{k-1}) taken from an FMUL (IEEE
+//                 product sign): 4 FMA-pipe + 1 LOP3 per edge-point.
+//                 6: ASM 5 on point pairs (FADD2/FMUL2/FFMA2). Same formulation 3.
 //
 // Edge table (built on the host in float32, see kernels.py): per edge k from
 // vertex k-1 (cyclic) to vertex k, a float4 {vy_k, a, b, c} and a float2
@@ -74,6 +82,12 @@
 #endif
 #if ASM == 3 && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
 #error "ASM=3 needs POLY_SMEM=1, METHOD=2 and TILE in {2,4,6,8}"
+#endif
+#if (ASM == 4 || ASM == 6) && !(POLY_SMEM == 1 && METHOD == 2 && VEC == 2 && (TILE == 4 || TILE == 8))
+#error "ASM=4|6 needs POLY_SMEM=1, METHOD=2, VEC=2 and TILE in {4,8}"
+#endif
+#if ASM == 5 && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
+#error "ASM=5 needs POLY_SMEM=1, METHOD=2 and TILE in {2,4,6,8}"
 #endif
 // packed records {ymin, ymax, slope, icpt} (METHOD 2) padded
 // to a multiple of 4 with never-spanning dummies {+inf, -inf, 0, 0}
@@ -312,6 +326,1014 @@
     "add.u32 end, ptr, %" S3_SPAN ";\n" "PNPOLY_S3_LOOP:\n" S3_LD S3_POINTS                        \
     "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_S3_LOOP;\n}\n"
 #endif
+#if ASM == 4
+// paired variant of ASM 3: two points share every FP32 instruction through
+// Blackwell's packed f32x2 ops (FADD2 / FFMA2, each lane IEEE .rn, no ftz),
+// halving FMA-pipe issue; the sign-bit LOP3s stay per point on the ALU pipe.
+#if TILE == 4
+#define S4_REGS ".reg .b64 vy2, sl2, ic2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1;\n" \
+    ".reg .b32 lo0, hi0, lo1, hi1, lo2, hi2, t0a, t0b, t1a, t1b, t2a, t2b, t3a, t3b;\n" \
+    ".reg .f32 vy, sl, ic, z, vyl;\n"
+#define S4_INIT "mov.b32 vyl, %10;\n" \
+    "mov.b64 vy2, {vyl, vyl};\n" \
+    "sub.rn.f32x2 dp0, %6, vy2;\n" \
+    "sub.rn.f32x2 dp1, %7, vy2;\n"
+#define S4_BODY \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2, {sl, sl};\n" \
+    "mov.b64 ic2, {ic, ic};\n" \
+    "sub.rn.f32x2 dA0, %6, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %6, ic2;\n" \
+    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA0;\n" \
+    "mov.b64 {lo1, hi1}, dp0;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t0a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t1a, hi0, hi1, hi2, 0x28;\n" \
+    "sub.rn.f32x2 dA1, %7, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %7, ic2;\n" \
+    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA1;\n" \
+    "mov.b64 {lo1, hi1}, dp1;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t2a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t3a, hi0, hi1, hi2, 0x28;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+16];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2, {sl, sl};\n" \
+    "mov.b64 ic2, {ic, ic};\n" \
+    "sub.rn.f32x2 dB0, %6, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %6, ic2;\n" \
+    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "mov.b64 {lo0, hi0}, dB0;\n" \
+    "mov.b64 {lo1, hi1}, dA0;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t0b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t1b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %0, %0, t0a, t0b, 0x96;\n" \
+    "lop3.b32 %1, %1, t1a, t1b, 0x96;\n" \
+    "sub.rn.f32x2 dB1, %7, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %7, ic2;\n" \
+    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "mov.b64 {lo0, hi0}, dB1;\n" \
+    "mov.b64 {lo1, hi1}, dA1;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t2b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t3b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %2, %2, t2a, t2b, 0x96;\n" \
+    "lop3.b32 %3, %3, t3a, t3b, 0x96;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+32];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2, {sl, sl};\n" \
+    "mov.b64 ic2, {ic, ic};\n" \
+    "sub.rn.f32x2 dA0, %6, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %6, ic2;\n" \
+    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA0;\n" \
+    "mov.b64 {lo1, hi1}, dB0;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t0a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t1a, hi0, hi1, hi2, 0x28;\n" \
+    "sub.rn.f32x2 dA1, %7, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %7, ic2;\n" \
+    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA1;\n" \
+    "mov.b64 {lo1, hi1}, dB1;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t2a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t3a, hi0, hi1, hi2, 0x28;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+48];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2, {sl, sl};\n" \
+    "mov.b64 ic2, {ic, ic};\n" \
+    "sub.rn.f32x2 dp0, %6, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %6, ic2;\n" \
+    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "mov.b64 {lo0, hi0}, dp0;\n" \
+    "mov.b64 {lo1, hi1}, dA0;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t0b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t1b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %0, %0, t0a, t0b, 0x96;\n" \
+    "lop3.b32 %1, %1, t1a, t1b, 0x96;\n" \
+    "sub.rn.f32x2 dp1, %7, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %7, ic2;\n" \
+    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "mov.b64 {lo0, hi0}, dp1;\n" \
+    "mov.b64 {lo1, hi1}, dA1;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t2b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t3b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %2, %2, t2a, t2b, 0x96;\n" \
+    "lop3.b32 %3, %3, t3a, t3b, 0x96;\n"
+#define S4_BASE "8"
+#define S4_SPAN "9"
+#elif TILE == 8
+#define S4_REGS ".reg .b64 vy2, sl2, ic2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3;\n" \
+    ".reg .b32 lo0, hi0, lo1, hi1, lo2, hi2, t0a, t0b, t1a, t1b, t2a, t2b, t3a, t3b, t4a, t4b, t5a, t5b, t6a, t6b, t7a, t7b;\n" \
+    ".reg .f32 vy, sl, ic, z, vyl;\n"
+#define S4_INIT "mov.b32 vyl, %18;\n" \
+    "mov.b64 vy2, {vyl, vyl};\n" \
+    "sub.rn.f32x2 dp0, %12, vy2;\n" \
+    "sub.rn.f32x2 dp1, %13, vy2;\n" \
+    "sub.rn.f32x2 dp2, %14, vy2;\n" \
+    "sub.rn.f32x2 dp3, %15, vy2;\n"
+#define S4_BODY \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2, {sl, sl};\n" \
+    "mov.b64 ic2, {ic, ic};\n" \
+    "sub.rn.f32x2 dA0, %12, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %12, ic2;\n" \
+    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA0;\n" \
+    "mov.b64 {lo1, hi1}, dp0;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t0a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t1a, hi0, hi1, hi2, 0x28;\n" \
+    "sub.rn.f32x2 dA1, %13, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %13, ic2;\n" \
+    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA1;\n" \
+    "mov.b64 {lo1, hi1}, dp1;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t2a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t3a, hi0, hi1, hi2, 0x28;\n" \
+    "sub.rn.f32x2 dA2, %14, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %14, ic2;\n" \
+    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA2;\n" \
+    "mov.b64 {lo1, hi1}, dp2;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t4a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t5a, hi0, hi1, hi2, 0x28;\n" \
+    "sub.rn.f32x2 dA3, %15, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %15, ic2;\n" \
+    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA3;\n" \
+    "mov.b64 {lo1, hi1}, dp3;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t6a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t7a, hi0, hi1, hi2, 0x28;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+16];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2, {sl, sl};\n" \
+    "mov.b64 ic2, {ic, ic};\n" \
+    "sub.rn.f32x2 dB0, %12, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %12, ic2;\n" \
+    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "mov.b64 {lo0, hi0}, dB0;\n" \
+    "mov.b64 {lo1, hi1}, dA0;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t0b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t1b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %0, %0, t0a, t0b, 0x96;\n" \
+    "lop3.b32 %1, %1, t1a, t1b, 0x96;\n" \
+    "sub.rn.f32x2 dB1, %13, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %13, ic2;\n" \
+    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "mov.b64 {lo0, hi0}, dB1;\n" \
+    "mov.b64 {lo1, hi1}, dA1;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t2b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t3b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %2, %2, t2a, t2b, 0x96;\n" \
+    "lop3.b32 %3, %3, t3a, t3b, 0x96;\n" \
+    "sub.rn.f32x2 dB2, %14, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %14, ic2;\n" \
+    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "mov.b64 {lo0, hi0}, dB2;\n" \
+    "mov.b64 {lo1, hi1}, dA2;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t4b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t5b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %4, %4, t4a, t4b, 0x96;\n" \
+    "lop3.b32 %5, %5, t5a, t5b, 0x96;\n" \
+    "sub.rn.f32x2 dB3, %15, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %15, ic2;\n" \
+    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "mov.b64 {lo0, hi0}, dB3;\n" \
+    "mov.b64 {lo1, hi1}, dA3;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t6b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t7b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %6, %6, t6a, t6b, 0x96;\n" \
+    "lop3.b32 %7, %7, t7a, t7b, 0x96;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+32];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2, {sl, sl};\n" \
+    "mov.b64 ic2, {ic, ic};\n" \
+    "sub.rn.f32x2 dA0, %12, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %12, ic2;\n" \
+    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA0;\n" \
+    "mov.b64 {lo1, hi1}, dB0;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t0a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t1a, hi0, hi1, hi2, 0x28;\n" \
+    "sub.rn.f32x2 dA1, %13, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %13, ic2;\n" \
+    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA1;\n" \
+    "mov.b64 {lo1, hi1}, dB1;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t2a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t3a, hi0, hi1, hi2, 0x28;\n" \
+    "sub.rn.f32x2 dA2, %14, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %14, ic2;\n" \
+    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA2;\n" \
+    "mov.b64 {lo1, hi1}, dB2;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t4a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t5a, hi0, hi1, hi2, 0x28;\n" \
+    "sub.rn.f32x2 dA3, %15, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %15, ic2;\n" \
+    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "mov.b64 {lo0, hi0}, dA3;\n" \
+    "mov.b64 {lo1, hi1}, dB3;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t6a, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t7a, hi0, hi1, hi2, 0x28;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+48];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2, {sl, sl};\n" \
+    "mov.b64 ic2, {ic, ic};\n" \
+    "sub.rn.f32x2 dp0, %12, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %12, ic2;\n" \
+    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "mov.b64 {lo0, hi0}, dp0;\n" \
+    "mov.b64 {lo1, hi1}, dA0;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t0b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t1b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %0, %0, t0a, t0b, 0x96;\n" \
+    "lop3.b32 %1, %1, t1a, t1b, 0x96;\n" \
+    "sub.rn.f32x2 dp1, %13, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %13, ic2;\n" \
+    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "mov.b64 {lo0, hi0}, dp1;\n" \
+    "mov.b64 {lo1, hi1}, dA1;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t2b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t3b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %2, %2, t2a, t2b, 0x96;\n" \
+    "lop3.b32 %3, %3, t3a, t3b, 0x96;\n" \
+    "sub.rn.f32x2 dp2, %14, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %14, ic2;\n" \
+    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "mov.b64 {lo0, hi0}, dp2;\n" \
+    "mov.b64 {lo1, hi1}, dA2;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t4b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t5b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %4, %4, t4a, t4b, 0x96;\n" \
+    "lop3.b32 %5, %5, t5a, t5b, 0x96;\n" \
+    "sub.rn.f32x2 dp3, %15, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, %15, ic2;\n" \
+    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "mov.b64 {lo0, hi0}, dp3;\n" \
+    "mov.b64 {lo1, hi1}, dA3;\n" \
+    "mov.b64 {lo2, hi2}, e2;\n" \
+    "lop3.b32 t6b, lo0, lo1, lo2, 0x28;\n" \
+    "lop3.b32 t7b, hi0, hi1, hi2, 0x28;\n" \
+    "lop3.b32 %6, %6, t6a, t6b, 0x96;\n" \
+    "lop3.b32 %7, %7, t7a, t7b, 0x96;\n"
+#define S4_BASE "16"
+#define S4_SPAN "17"
+#endif
+#define S4_ASM                                                                         \
+    "{\n" S4_REGS ".reg .u32 ptr, end;\n.reg .pred s;\n" S4_INIT                       \
+    "mov.u32 ptr, %" S4_BASE ";\nadd.u32 end, ptr, %" S4_SPAN ";\n" "PNPOLY_S4_LOOP:\n" \
+    S4_BODY "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_S4_LOOP;\n}\n"
+#endif
+#if ASM == 5
+// ASM 3 with the sign XOR of consecutive (py - vy) moved to the FMA pipe:
+// sign(d_k * d_{k-1}) == sign(d_k) ^ sign(d_{k-1}) exactly (IEEE product
+// sign), leaving one 3-input LOP3 per edge-point: acc ^= m & e.
+#if TILE == 2
+#define S5_REGS ".reg .b32 m, e, dp0, dA0, dB0, dp1, dA1, dB1;\n" \
+    ".reg .f32 vy, sl, ic, z, x;\n"
+#define S5_INIT "sub.rn.f32 dp0, %4, %8;\n" \
+    "sub.rn.f32 dp1, %5, %8;\n"
+#define S5_BODY \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
+    "sub.rn.f32 dA0, %4, vy;\n" \
+    "mul.rn.f32 m, dA0, dp0;\n" \
+    "fma.rn.f32 x, sl, %4, ic;\n" \
+    "sub.rn.f32 e, %2, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dA1, %5, vy;\n" \
+    "mul.rn.f32 m, dA1, dp1;\n" \
+    "fma.rn.f32 x, sl, %5, ic;\n" \
+    "sub.rn.f32 e, %3, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+16];\n" \
+    "sub.rn.f32 dB0, %4, vy;\n" \
+    "mul.rn.f32 m, dB0, dA0;\n" \
+    "fma.rn.f32 x, sl, %4, ic;\n" \
+    "sub.rn.f32 e, %2, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dB1, %5, vy;\n" \
+    "mul.rn.f32 m, dB1, dA1;\n" \
+    "fma.rn.f32 x, sl, %5, ic;\n" \
+    "sub.rn.f32 e, %3, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+32];\n" \
+    "sub.rn.f32 dA0, %4, vy;\n" \
+    "mul.rn.f32 m, dA0, dB0;\n" \
+    "fma.rn.f32 x, sl, %4, ic;\n" \
+    "sub.rn.f32 e, %2, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dA1, %5, vy;\n" \
+    "mul.rn.f32 m, dA1, dB1;\n" \
+    "fma.rn.f32 x, sl, %5, ic;\n" \
+    "sub.rn.f32 e, %3, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+48];\n" \
+    "sub.rn.f32 dp0, %4, vy;\n" \
+    "mul.rn.f32 m, dp0, dA0;\n" \
+    "fma.rn.f32 x, sl, %4, ic;\n" \
+    "sub.rn.f32 e, %2, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dp1, %5, vy;\n" \
+    "mul.rn.f32 m, dp1, dA1;\n" \
+    "fma.rn.f32 x, sl, %5, ic;\n" \
+    "sub.rn.f32 e, %3, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n"
+#define S5_BASE "6"
+#define S5_SPAN "7"
+#elif TILE == 4
+#define S5_REGS ".reg .b32 m, e, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3;\n" \
+    ".reg .f32 vy, sl, ic, z, x;\n"
+#define S5_INIT "sub.rn.f32 dp0, %8, %14;\n" \
+    "sub.rn.f32 dp1, %9, %14;\n" \
+    "sub.rn.f32 dp2, %10, %14;\n" \
+    "sub.rn.f32 dp3, %11, %14;\n"
+#define S5_BODY \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
+    "sub.rn.f32 dA0, %8, vy;\n" \
+    "mul.rn.f32 m, dA0, dp0;\n" \
+    "fma.rn.f32 x, sl, %8, ic;\n" \
+    "sub.rn.f32 e, %4, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dA1, %9, vy;\n" \
+    "mul.rn.f32 m, dA1, dp1;\n" \
+    "fma.rn.f32 x, sl, %9, ic;\n" \
+    "sub.rn.f32 e, %5, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dA2, %10, vy;\n" \
+    "mul.rn.f32 m, dA2, dp2;\n" \
+    "fma.rn.f32 x, sl, %10, ic;\n" \
+    "sub.rn.f32 e, %6, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dA3, %11, vy;\n" \
+    "mul.rn.f32 m, dA3, dp3;\n" \
+    "fma.rn.f32 x, sl, %11, ic;\n" \
+    "sub.rn.f32 e, %7, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+16];\n" \
+    "sub.rn.f32 dB0, %8, vy;\n" \
+    "mul.rn.f32 m, dB0, dA0;\n" \
+    "fma.rn.f32 x, sl, %8, ic;\n" \
+    "sub.rn.f32 e, %4, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dB1, %9, vy;\n" \
+    "mul.rn.f32 m, dB1, dA1;\n" \
+    "fma.rn.f32 x, sl, %9, ic;\n" \
+    "sub.rn.f32 e, %5, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dB2, %10, vy;\n" \
+    "mul.rn.f32 m, dB2, dA2;\n" \
+    "fma.rn.f32 x, sl, %10, ic;\n" \
+    "sub.rn.f32 e, %6, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dB3, %11, vy;\n" \
+    "mul.rn.f32 m, dB3, dA3;\n" \
+    "fma.rn.f32 x, sl, %11, ic;\n" \
+    "sub.rn.f32 e, %7, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+32];\n" \
+    "sub.rn.f32 dA0, %8, vy;\n" \
+    "mul.rn.f32 m, dA0, dB0;\n" \
+    "fma.rn.f32 x, sl, %8, ic;\n" \
+    "sub.rn.f32 e, %4, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dA1, %9, vy;\n" \
+    "mul.rn.f32 m, dA1, dB1;\n" \
+    "fma.rn.f32 x, sl, %9, ic;\n" \
+    "sub.rn.f32 e, %5, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dA2, %10, vy;\n" \
+    "mul.rn.f32 m, dA2, dB2;\n" \
+    "fma.rn.f32 x, sl, %10, ic;\n" \
+    "sub.rn.f32 e, %6, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dA3, %11, vy;\n" \
+    "mul.rn.f32 m, dA3, dB3;\n" \
+    "fma.rn.f32 x, sl, %11, ic;\n" \
+    "sub.rn.f32 e, %7, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+48];\n" \
+    "sub.rn.f32 dp0, %8, vy;\n" \
+    "mul.rn.f32 m, dp0, dA0;\n" \
+    "fma.rn.f32 x, sl, %8, ic;\n" \
+    "sub.rn.f32 e, %4, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dp1, %9, vy;\n" \
+    "mul.rn.f32 m, dp1, dA1;\n" \
+    "fma.rn.f32 x, sl, %9, ic;\n" \
+    "sub.rn.f32 e, %5, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dp2, %10, vy;\n" \
+    "mul.rn.f32 m, dp2, dA2;\n" \
+    "fma.rn.f32 x, sl, %10, ic;\n" \
+    "sub.rn.f32 e, %6, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dp3, %11, vy;\n" \
+    "mul.rn.f32 m, dp3, dA3;\n" \
+    "fma.rn.f32 x, sl, %11, ic;\n" \
+    "sub.rn.f32 e, %7, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n"
+#define S5_BASE "12"
+#define S5_SPAN "13"
+#elif TILE == 6
+#define S5_REGS ".reg .b32 m, e, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3, dp4, dA4, dB4, dp5, dA5, dB5;\n" \
+    ".reg .f32 vy, sl, ic, z, x;\n"
+#define S5_INIT "sub.rn.f32 dp0, %12, %20;\n" \
+    "sub.rn.f32 dp1, %13, %20;\n" \
+    "sub.rn.f32 dp2, %14, %20;\n" \
+    "sub.rn.f32 dp3, %15, %20;\n" \
+    "sub.rn.f32 dp4, %16, %20;\n" \
+    "sub.rn.f32 dp5, %17, %20;\n"
+#define S5_BODY \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
+    "sub.rn.f32 dA0, %12, vy;\n" \
+    "mul.rn.f32 m, dA0, dp0;\n" \
+    "fma.rn.f32 x, sl, %12, ic;\n" \
+    "sub.rn.f32 e, %6, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dA1, %13, vy;\n" \
+    "mul.rn.f32 m, dA1, dp1;\n" \
+    "fma.rn.f32 x, sl, %13, ic;\n" \
+    "sub.rn.f32 e, %7, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dA2, %14, vy;\n" \
+    "mul.rn.f32 m, dA2, dp2;\n" \
+    "fma.rn.f32 x, sl, %14, ic;\n" \
+    "sub.rn.f32 e, %8, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dA3, %15, vy;\n" \
+    "mul.rn.f32 m, dA3, dp3;\n" \
+    "fma.rn.f32 x, sl, %15, ic;\n" \
+    "sub.rn.f32 e, %9, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "sub.rn.f32 dA4, %16, vy;\n" \
+    "mul.rn.f32 m, dA4, dp4;\n" \
+    "fma.rn.f32 x, sl, %16, ic;\n" \
+    "sub.rn.f32 e, %10, x;\n" \
+    "lop3.b32 %4, %4, m, e, 0x78;\n" \
+    "sub.rn.f32 dA5, %17, vy;\n" \
+    "mul.rn.f32 m, dA5, dp5;\n" \
+    "fma.rn.f32 x, sl, %17, ic;\n" \
+    "sub.rn.f32 e, %11, x;\n" \
+    "lop3.b32 %5, %5, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+16];\n" \
+    "sub.rn.f32 dB0, %12, vy;\n" \
+    "mul.rn.f32 m, dB0, dA0;\n" \
+    "fma.rn.f32 x, sl, %12, ic;\n" \
+    "sub.rn.f32 e, %6, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dB1, %13, vy;\n" \
+    "mul.rn.f32 m, dB1, dA1;\n" \
+    "fma.rn.f32 x, sl, %13, ic;\n" \
+    "sub.rn.f32 e, %7, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dB2, %14, vy;\n" \
+    "mul.rn.f32 m, dB2, dA2;\n" \
+    "fma.rn.f32 x, sl, %14, ic;\n" \
+    "sub.rn.f32 e, %8, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dB3, %15, vy;\n" \
+    "mul.rn.f32 m, dB3, dA3;\n" \
+    "fma.rn.f32 x, sl, %15, ic;\n" \
+    "sub.rn.f32 e, %9, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "sub.rn.f32 dB4, %16, vy;\n" \
+    "mul.rn.f32 m, dB4, dA4;\n" \
+    "fma.rn.f32 x, sl, %16, ic;\n" \
+    "sub.rn.f32 e, %10, x;\n" \
+    "lop3.b32 %4, %4, m, e, 0x78;\n" \
+    "sub.rn.f32 dB5, %17, vy;\n" \
+    "mul.rn.f32 m, dB5, dA5;\n" \
+    "fma.rn.f32 x, sl, %17, ic;\n" \
+    "sub.rn.f32 e, %11, x;\n" \
+    "lop3.b32 %5, %5, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+32];\n" \
+    "sub.rn.f32 dA0, %12, vy;\n" \
+    "mul.rn.f32 m, dA0, dB0;\n" \
+    "fma.rn.f32 x, sl, %12, ic;\n" \
+    "sub.rn.f32 e, %6, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dA1, %13, vy;\n" \
+    "mul.rn.f32 m, dA1, dB1;\n" \
+    "fma.rn.f32 x, sl, %13, ic;\n" \
+    "sub.rn.f32 e, %7, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dA2, %14, vy;\n" \
+    "mul.rn.f32 m, dA2, dB2;\n" \
+    "fma.rn.f32 x, sl, %14, ic;\n" \
+    "sub.rn.f32 e, %8, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dA3, %15, vy;\n" \
+    "mul.rn.f32 m, dA3, dB3;\n" \
+    "fma.rn.f32 x, sl, %15, ic;\n" \
+    "sub.rn.f32 e, %9, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "sub.rn.f32 dA4, %16, vy;\n" \
+    "mul.rn.f32 m, dA4, dB4;\n" \
+    "fma.rn.f32 x, sl, %16, ic;\n" \
+    "sub.rn.f32 e, %10, x;\n" \
+    "lop3.b32 %4, %4, m, e, 0x78;\n" \
+    "sub.rn.f32 dA5, %17, vy;\n" \
+    "mul.rn.f32 m, dA5, dB5;\n" \
+    "fma.rn.f32 x, sl, %17, ic;\n" \
+    "sub.rn.f32 e, %11, x;\n" \
+    "lop3.b32 %5, %5, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+48];\n" \
+    "sub.rn.f32 dp0, %12, vy;\n" \
+    "mul.rn.f32 m, dp0, dA0;\n" \
+    "fma.rn.f32 x, sl, %12, ic;\n" \
+    "sub.rn.f32 e, %6, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dp1, %13, vy;\n" \
+    "mul.rn.f32 m, dp1, dA1;\n" \
+    "fma.rn.f32 x, sl, %13, ic;\n" \
+    "sub.rn.f32 e, %7, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dp2, %14, vy;\n" \
+    "mul.rn.f32 m, dp2, dA2;\n" \
+    "fma.rn.f32 x, sl, %14, ic;\n" \
+    "sub.rn.f32 e, %8, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dp3, %15, vy;\n" \
+    "mul.rn.f32 m, dp3, dA3;\n" \
+    "fma.rn.f32 x, sl, %15, ic;\n" \
+    "sub.rn.f32 e, %9, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "sub.rn.f32 dp4, %16, vy;\n" \
+    "mul.rn.f32 m, dp4, dA4;\n" \
+    "fma.rn.f32 x, sl, %16, ic;\n" \
+    "sub.rn.f32 e, %10, x;\n" \
+    "lop3.b32 %4, %4, m, e, 0x78;\n" \
+    "sub.rn.f32 dp5, %17, vy;\n" \
+    "mul.rn.f32 m, dp5, dA5;\n" \
+    "fma.rn.f32 x, sl, %17, ic;\n" \
+    "sub.rn.f32 e, %11, x;\n" \
+    "lop3.b32 %5, %5, m, e, 0x78;\n"
+#define S5_BASE "18"
+#define S5_SPAN "19"
+#elif TILE == 8
+#define S5_REGS ".reg .b32 m, e, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3, dp4, dA4, dB4, dp5, dA5, dB5, dp6, dA6, dB6, dp7, dA7, dB7;\n" \
+    ".reg .f32 vy, sl, ic, z, x;\n"
+#define S5_INIT "sub.rn.f32 dp0, %16, %26;\n" \
+    "sub.rn.f32 dp1, %17, %26;\n" \
+    "sub.rn.f32 dp2, %18, %26;\n" \
+    "sub.rn.f32 dp3, %19, %26;\n" \
+    "sub.rn.f32 dp4, %20, %26;\n" \
+    "sub.rn.f32 dp5, %21, %26;\n" \
+    "sub.rn.f32 dp6, %22, %26;\n" \
+    "sub.rn.f32 dp7, %23, %26;\n"
+#define S5_BODY \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
+    "sub.rn.f32 dA0, %16, vy;\n" \
+    "mul.rn.f32 m, dA0, dp0;\n" \
+    "fma.rn.f32 x, sl, %16, ic;\n" \
+    "sub.rn.f32 e, %8, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dA1, %17, vy;\n" \
+    "mul.rn.f32 m, dA1, dp1;\n" \
+    "fma.rn.f32 x, sl, %17, ic;\n" \
+    "sub.rn.f32 e, %9, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dA2, %18, vy;\n" \
+    "mul.rn.f32 m, dA2, dp2;\n" \
+    "fma.rn.f32 x, sl, %18, ic;\n" \
+    "sub.rn.f32 e, %10, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dA3, %19, vy;\n" \
+    "mul.rn.f32 m, dA3, dp3;\n" \
+    "fma.rn.f32 x, sl, %19, ic;\n" \
+    "sub.rn.f32 e, %11, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "sub.rn.f32 dA4, %20, vy;\n" \
+    "mul.rn.f32 m, dA4, dp4;\n" \
+    "fma.rn.f32 x, sl, %20, ic;\n" \
+    "sub.rn.f32 e, %12, x;\n" \
+    "lop3.b32 %4, %4, m, e, 0x78;\n" \
+    "sub.rn.f32 dA5, %21, vy;\n" \
+    "mul.rn.f32 m, dA5, dp5;\n" \
+    "fma.rn.f32 x, sl, %21, ic;\n" \
+    "sub.rn.f32 e, %13, x;\n" \
+    "lop3.b32 %5, %5, m, e, 0x78;\n" \
+    "sub.rn.f32 dA6, %22, vy;\n" \
+    "mul.rn.f32 m, dA6, dp6;\n" \
+    "fma.rn.f32 x, sl, %22, ic;\n" \
+    "sub.rn.f32 e, %14, x;\n" \
+    "lop3.b32 %6, %6, m, e, 0x78;\n" \
+    "sub.rn.f32 dA7, %23, vy;\n" \
+    "mul.rn.f32 m, dA7, dp7;\n" \
+    "fma.rn.f32 x, sl, %23, ic;\n" \
+    "sub.rn.f32 e, %15, x;\n" \
+    "lop3.b32 %7, %7, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+16];\n" \
+    "sub.rn.f32 dB0, %16, vy;\n" \
+    "mul.rn.f32 m, dB0, dA0;\n" \
+    "fma.rn.f32 x, sl, %16, ic;\n" \
+    "sub.rn.f32 e, %8, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dB1, %17, vy;\n" \
+    "mul.rn.f32 m, dB1, dA1;\n" \
+    "fma.rn.f32 x, sl, %17, ic;\n" \
+    "sub.rn.f32 e, %9, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dB2, %18, vy;\n" \
+    "mul.rn.f32 m, dB2, dA2;\n" \
+    "fma.rn.f32 x, sl, %18, ic;\n" \
+    "sub.rn.f32 e, %10, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dB3, %19, vy;\n" \
+    "mul.rn.f32 m, dB3, dA3;\n" \
+    "fma.rn.f32 x, sl, %19, ic;\n" \
+    "sub.rn.f32 e, %11, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "sub.rn.f32 dB4, %20, vy;\n" \
+    "mul.rn.f32 m, dB4, dA4;\n" \
+    "fma.rn.f32 x, sl, %20, ic;\n" \
+    "sub.rn.f32 e, %12, x;\n" \
+    "lop3.b32 %4, %4, m, e, 0x78;\n" \
+    "sub.rn.f32 dB5, %21, vy;\n" \
+    "mul.rn.f32 m, dB5, dA5;\n" \
+    "fma.rn.f32 x, sl, %21, ic;\n" \
+    "sub.rn.f32 e, %13, x;\n" \
+    "lop3.b32 %5, %5, m, e, 0x78;\n" \
+    "sub.rn.f32 dB6, %22, vy;\n" \
+    "mul.rn.f32 m, dB6, dA6;\n" \
+    "fma.rn.f32 x, sl, %22, ic;\n" \
+    "sub.rn.f32 e, %14, x;\n" \
+    "lop3.b32 %6, %6, m, e, 0x78;\n" \
+    "sub.rn.f32 dB7, %23, vy;\n" \
+    "mul.rn.f32 m, dB7, dA7;\n" \
+    "fma.rn.f32 x, sl, %23, ic;\n" \
+    "sub.rn.f32 e, %15, x;\n" \
+    "lop3.b32 %7, %7, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+32];\n" \
+    "sub.rn.f32 dA0, %16, vy;\n" \
+    "mul.rn.f32 m, dA0, dB0;\n" \
+    "fma.rn.f32 x, sl, %16, ic;\n" \
+    "sub.rn.f32 e, %8, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dA1, %17, vy;\n" \
+    "mul.rn.f32 m, dA1, dB1;\n" \
+    "fma.rn.f32 x, sl, %17, ic;\n" \
+    "sub.rn.f32 e, %9, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dA2, %18, vy;\n" \
+    "mul.rn.f32 m, dA2, dB2;\n" \
+    "fma.rn.f32 x, sl, %18, ic;\n" \
+    "sub.rn.f32 e, %10, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dA3, %19, vy;\n" \
+    "mul.rn.f32 m, dA3, dB3;\n" \
+    "fma.rn.f32 x, sl, %19, ic;\n" \
+    "sub.rn.f32 e, %11, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "sub.rn.f32 dA4, %20, vy;\n" \
+    "mul.rn.f32 m, dA4, dB4;\n" \
+    "fma.rn.f32 x, sl, %20, ic;\n" \
+    "sub.rn.f32 e, %12, x;\n" \
+    "lop3.b32 %4, %4, m, e, 0x78;\n" \
+    "sub.rn.f32 dA5, %21, vy;\n" \
+    "mul.rn.f32 m, dA5, dB5;\n" \
+    "fma.rn.f32 x, sl, %21, ic;\n" \
+    "sub.rn.f32 e, %13, x;\n" \
+    "lop3.b32 %5, %5, m, e, 0x78;\n" \
+    "sub.rn.f32 dA6, %22, vy;\n" \
+    "mul.rn.f32 m, dA6, dB6;\n" \
+    "fma.rn.f32 x, sl, %22, ic;\n" \
+    "sub.rn.f32 e, %14, x;\n" \
+    "lop3.b32 %6, %6, m, e, 0x78;\n" \
+    "sub.rn.f32 dA7, %23, vy;\n" \
+    "mul.rn.f32 m, dA7, dB7;\n" \
+    "fma.rn.f32 x, sl, %23, ic;\n" \
+    "sub.rn.f32 e, %15, x;\n" \
+    "lop3.b32 %7, %7, m, e, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+48];\n" \
+    "sub.rn.f32 dp0, %16, vy;\n" \
+    "mul.rn.f32 m, dp0, dA0;\n" \
+    "fma.rn.f32 x, sl, %16, ic;\n" \
+    "sub.rn.f32 e, %8, x;\n" \
+    "lop3.b32 %0, %0, m, e, 0x78;\n" \
+    "sub.rn.f32 dp1, %17, vy;\n" \
+    "mul.rn.f32 m, dp1, dA1;\n" \
+    "fma.rn.f32 x, sl, %17, ic;\n" \
+    "sub.rn.f32 e, %9, x;\n" \
+    "lop3.b32 %1, %1, m, e, 0x78;\n" \
+    "sub.rn.f32 dp2, %18, vy;\n" \
+    "mul.rn.f32 m, dp2, dA2;\n" \
+    "fma.rn.f32 x, sl, %18, ic;\n" \
+    "sub.rn.f32 e, %10, x;\n" \
+    "lop3.b32 %2, %2, m, e, 0x78;\n" \
+    "sub.rn.f32 dp3, %19, vy;\n" \
+    "mul.rn.f32 m, dp3, dA3;\n" \
+    "fma.rn.f32 x, sl, %19, ic;\n" \
+    "sub.rn.f32 e, %11, x;\n" \
+    "lop3.b32 %3, %3, m, e, 0x78;\n" \
+    "sub.rn.f32 dp4, %20, vy;\n" \
+    "mul.rn.f32 m, dp4, dA4;\n" \
+    "fma.rn.f32 x, sl, %20, ic;\n" \
+    "sub.rn.f32 e, %12, x;\n" \
+    "lop3.b32 %4, %4, m, e, 0x78;\n" \
+    "sub.rn.f32 dp5, %21, vy;\n" \
+    "mul.rn.f32 m, dp5, dA5;\n" \
+    "fma.rn.f32 x, sl, %21, ic;\n" \
+    "sub.rn.f32 e, %13, x;\n" \
+    "lop3.b32 %5, %5, m, e, 0x78;\n" \
+    "sub.rn.f32 dp6, %22, vy;\n" \
+    "mul.rn.f32 m, dp6, dA6;\n" \
+    "fma.rn.f32 x, sl, %22, ic;\n" \
+    "sub.rn.f32 e, %14, x;\n" \
+    "lop3.b32 %6, %6, m, e, 0x78;\n" \
+    "sub.rn.f32 dp7, %23, vy;\n" \
+    "mul.rn.f32 m, dp7, dA7;\n" \
+    "fma.rn.f32 x, sl, %23, ic;\n" \
+    "sub.rn.f32 e, %15, x;\n" \
+    "lop3.b32 %7, %7, m, e, 0x78;\n"
+#define S5_BASE "24"
+#define S5_SPAN "25"
+#endif
+#define S5_ASM                                                                              \
+    "{\n" S5_REGS ".reg .u32 ptr, end;\n.reg .pred s;\n" S5_INIT "mov.u32 ptr, %" S5_BASE ";\n" \
+    "add.u32 end, ptr, %" S5_SPAN ";\n" "PNPOLY_S5_LOOP:\n" S5_BODY                              \
+    "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_S5_LOOP;\n}\n"
+#endif
+#if ASM == 6
+// ASM 5 on point pairs with packed f32x2 (FADD2 / FMUL2 / FFMA2).
+#if TILE == 4
+#define S6_REGS ".reg .b64 sl2b, ic2b, vy2, m2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1;\n" \
+    ".reg .b32 mlo, mhi, elo, ehi;\n" \
+    ".reg .f32 vy, sl, ic, z, vyl;\n"
+#define S6_INIT "mov.b32 vyl, %10;\n" \
+    "mov.b64 vy2, {vyl, vyl};\n" \
+    "sub.rn.f32x2 dp0, %6, vy2;\n" \
+    "sub.rn.f32x2 dp1, %7, vy2;\n"
+#define S6_BODY \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2b, {sl, sl};\n" \
+    "mov.b64 ic2b, {ic, ic};\n" \
+    "sub.rn.f32x2 dA0, %6, vy2;\n" \
+    "mul.rn.f32x2 m2, dA0, dp0;\n" \
+    "fma.rn.f32x2 x2, sl2b, %6, ic2b;\n" \
+    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
+    "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dA1, %7, vy2;\n" \
+    "mul.rn.f32x2 m2, dA1, dp1;\n" \
+    "fma.rn.f32x2 x2, sl2b, %7, ic2b;\n" \
+    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
+    "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+16];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2b, {sl, sl};\n" \
+    "mov.b64 ic2b, {ic, ic};\n" \
+    "sub.rn.f32x2 dB0, %6, vy2;\n" \
+    "mul.rn.f32x2 m2, dB0, dA0;\n" \
+    "fma.rn.f32x2 x2, sl2b, %6, ic2b;\n" \
+    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
+    "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dB1, %7, vy2;\n" \
+    "mul.rn.f32x2 m2, dB1, dA1;\n" \
+    "fma.rn.f32x2 x2, sl2b, %7, ic2b;\n" \
+    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
+    "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+32];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2b, {sl, sl};\n" \
+    "mov.b64 ic2b, {ic, ic};\n" \
+    "sub.rn.f32x2 dA0, %6, vy2;\n" \
+    "mul.rn.f32x2 m2, dA0, dB0;\n" \
+    "fma.rn.f32x2 x2, sl2b, %6, ic2b;\n" \
+    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
+    "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dA1, %7, vy2;\n" \
+    "mul.rn.f32x2 m2, dA1, dB1;\n" \
+    "fma.rn.f32x2 x2, sl2b, %7, ic2b;\n" \
+    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
+    "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+48];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2b, {sl, sl};\n" \
+    "mov.b64 ic2b, {ic, ic};\n" \
+    "sub.rn.f32x2 dp0, %6, vy2;\n" \
+    "mul.rn.f32x2 m2, dp0, dA0;\n" \
+    "fma.rn.f32x2 x2, sl2b, %6, ic2b;\n" \
+    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
+    "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dp1, %7, vy2;\n" \
+    "mul.rn.f32x2 m2, dp1, dA1;\n" \
+    "fma.rn.f32x2 x2, sl2b, %7, ic2b;\n" \
+    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
+    "lop3.b32 %3, %3, mhi, ehi, 0x78;\n"
+#define S6_BASE "8"
+#define S6_SPAN "9"
+#elif TILE == 8
+#define S6_REGS ".reg .b64 sl2b, ic2b, vy2, m2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3;\n" \
+    ".reg .b32 mlo, mhi, elo, ehi;\n" \
+    ".reg .f32 vy, sl, ic, z, vyl;\n"
+#define S6_INIT "mov.b32 vyl, %18;\n" \
+    "mov.b64 vy2, {vyl, vyl};\n" \
+    "sub.rn.f32x2 dp0, %12, vy2;\n" \
+    "sub.rn.f32x2 dp1, %13, vy2;\n" \
+    "sub.rn.f32x2 dp2, %14, vy2;\n" \
+    "sub.rn.f32x2 dp3, %15, vy2;\n"
+#define S6_BODY \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2b, {sl, sl};\n" \
+    "mov.b64 ic2b, {ic, ic};\n" \
+    "sub.rn.f32x2 dA0, %12, vy2;\n" \
+    "mul.rn.f32x2 m2, dA0, dp0;\n" \
+    "fma.rn.f32x2 x2, sl2b, %12, ic2b;\n" \
+    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
+    "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dA1, %13, vy2;\n" \
+    "mul.rn.f32x2 m2, dA1, dp1;\n" \
+    "fma.rn.f32x2 x2, sl2b, %13, ic2b;\n" \
+    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
+    "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dA2, %14, vy2;\n" \
+    "mul.rn.f32x2 m2, dA2, dp2;\n" \
+    "fma.rn.f32x2 x2, sl2b, %14, ic2b;\n" \
+    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %4, %4, mlo, elo, 0x78;\n" \
+    "lop3.b32 %5, %5, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dA3, %15, vy2;\n" \
+    "mul.rn.f32x2 m2, dA3, dp3;\n" \
+    "fma.rn.f32x2 x2, sl2b, %15, ic2b;\n" \
+    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %6, %6, mlo, elo, 0x78;\n" \
+    "lop3.b32 %7, %7, mhi, ehi, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+16];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2b, {sl, sl};\n" \
+    "mov.b64 ic2b, {ic, ic};\n" \
+    "sub.rn.f32x2 dB0, %12, vy2;\n" \
+    "mul.rn.f32x2 m2, dB0, dA0;\n" \
+    "fma.rn.f32x2 x2, sl2b, %12, ic2b;\n" \
+    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
+    "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dB1, %13, vy2;\n" \
+    "mul.rn.f32x2 m2, dB1, dA1;\n" \
+    "fma.rn.f32x2 x2, sl2b, %13, ic2b;\n" \
+    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
+    "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dB2, %14, vy2;\n" \
+    "mul.rn.f32x2 m2, dB2, dA2;\n" \
+    "fma.rn.f32x2 x2, sl2b, %14, ic2b;\n" \
+    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %4, %4, mlo, elo, 0x78;\n" \
+    "lop3.b32 %5, %5, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dB3, %15, vy2;\n" \
+    "mul.rn.f32x2 m2, dB3, dA3;\n" \
+    "fma.rn.f32x2 x2, sl2b, %15, ic2b;\n" \
+    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %6, %6, mlo, elo, 0x78;\n" \
+    "lop3.b32 %7, %7, mhi, ehi, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+32];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2b, {sl, sl};\n" \
+    "mov.b64 ic2b, {ic, ic};\n" \
+    "sub.rn.f32x2 dA0, %12, vy2;\n" \
+    "mul.rn.f32x2 m2, dA0, dB0;\n" \
+    "fma.rn.f32x2 x2, sl2b, %12, ic2b;\n" \
+    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
+    "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dA1, %13, vy2;\n" \
+    "mul.rn.f32x2 m2, dA1, dB1;\n" \
+    "fma.rn.f32x2 x2, sl2b, %13, ic2b;\n" \
+    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
+    "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dA2, %14, vy2;\n" \
+    "mul.rn.f32x2 m2, dA2, dB2;\n" \
+    "fma.rn.f32x2 x2, sl2b, %14, ic2b;\n" \
+    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %4, %4, mlo, elo, 0x78;\n" \
+    "lop3.b32 %5, %5, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dA3, %15, vy2;\n" \
+    "mul.rn.f32x2 m2, dA3, dB3;\n" \
+    "fma.rn.f32x2 x2, sl2b, %15, ic2b;\n" \
+    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %6, %6, mlo, elo, 0x78;\n" \
+    "lop3.b32 %7, %7, mhi, ehi, 0x78;\n" \
+    "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+48];\n" \
+    "mov.b64 vy2, {vy, vy};\n" \
+    "mov.b64 sl2b, {sl, sl};\n" \
+    "mov.b64 ic2b, {ic, ic};\n" \
+    "sub.rn.f32x2 dp0, %12, vy2;\n" \
+    "mul.rn.f32x2 m2, dp0, dA0;\n" \
+    "fma.rn.f32x2 x2, sl2b, %12, ic2b;\n" \
+    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
+    "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dp1, %13, vy2;\n" \
+    "mul.rn.f32x2 m2, dp1, dA1;\n" \
+    "fma.rn.f32x2 x2, sl2b, %13, ic2b;\n" \
+    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
+    "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dp2, %14, vy2;\n" \
+    "mul.rn.f32x2 m2, dp2, dA2;\n" \
+    "fma.rn.f32x2 x2, sl2b, %14, ic2b;\n" \
+    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %4, %4, mlo, elo, 0x78;\n" \
+    "lop3.b32 %5, %5, mhi, ehi, 0x78;\n" \
+    "sub.rn.f32x2 dp3, %15, vy2;\n" \
+    "mul.rn.f32x2 m2, dp3, dA3;\n" \
+    "fma.rn.f32x2 x2, sl2b, %15, ic2b;\n" \
+    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "mov.b64 {mlo, mhi}, m2;\n" \
+    "mov.b64 {elo, ehi}, e2;\n" \
+    "lop3.b32 %6, %6, mlo, elo, 0x78;\n" \
+    "lop3.b32 %7, %7, mhi, ehi, 0x78;\n"
+#define S6_BASE "16"
+#define S6_SPAN "17"
+#endif
+#define S6_ASM                                                                              \
+    "{\n" S6_REGS ".reg .u32 ptr, end;\n.reg .pred s;\n" S6_INIT "mov.u32 ptr, %" S6_BASE ";\n" \
+    "add.u32 end, ptr, %" S6_SPAN ";\n" "PNPOLY_S6_LOOP:\n" S6_BODY                              \
+    "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_S6_LOOP;\n}\n"
+#endif
 
 
 __constant__ float4 c_edges[VERTICES];
@@ -362,7 +1384,11 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 
     // Coalesced: in step t, consecutive threads own consecutive points
     // (VEC=1: float2) or point pairs (VEC=2: float4).
-    const long long block_base = (long long)blockIdx.x * (BLOCK_SIZE_X * TILE);
+    // PERSIST=1: a grid of ~SMs x resident blocks strides over point tiles, so
+    // each block stages the polygon once (no per-tile barrier / table reload)
+    const long long n_tiles = ((long long)n + BLOCK_SIZE_X * TILE - 1) / (BLOCK_SIZE_X * TILE);
+    for (long long tile_id = blockIdx.x; tile_id < n_tiles; tile_id += gridDim.x) {
+    const long long block_base = tile_id * (BLOCK_SIZE_X * TILE);
     float px[TILE], py[TILE];
     int idx[TILE];
 #pragma unroll
@@ -392,7 +1418,45 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #endif
     }
 
+#if ASM == 4 || ASM == 6
+#if ASM == 4
+#define SP_ASM S4_ASM
+#else
+#define SP_ASM S6_ASM
+#endif
+    unsigned inside[TILE];
+    {
+        unsigned acc[TILE];
+        unsigned long long pxp[TILE / 2], pyp[TILE / 2];
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) acc[t] = 0u;
+#pragma unroll
+        for (int q = 0; q < TILE / 2; ++q) {
+            // pair (2q, 2q+1) came from one float4 {x0, y0, x1, y1}
+            pxp[q] = ((unsigned long long)__float_as_uint(px[2 * q + 1]) << 32) | __float_as_uint(px[2 * q]);
+            pyp[q] = ((unsigned long long)__float_as_uint(py[2 * q + 1]) << 32) | __float_as_uint(py[2 * q]);
+        }
+        const unsigned sbase = (unsigned)__cvta_generic_to_shared(s_packed);
+        const unsigned span = NPACK * 16u;
+        const float vy_last = s_packed[VERTICES - 1].x;
+#if TILE == 4
+        asm volatile(SP_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3])
+                     : "l"(pxp[0]), "l"(pxp[1]), "l"(pyp[0]), "l"(pyp[1]), "r"(sbase), "r"(span), "f"(vy_last));
+#else
+        asm volatile(SP_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3]), "+r"(acc[4]), "+r"(acc[5]),
+                     "+r"(acc[6]), "+r"(acc[7])
+                     : "l"(pxp[0]), "l"(pxp[1]), "l"(pxp[2]), "l"(pxp[3]), "l"(pyp[0]), "l"(pyp[1]), "l"(pyp[2]),
+                       "l"(pyp[3]), "r"(sbase), "r"(span), "f"(vy_last));
+#endif
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) inside[t] = acc[t] >> 31;
+    }
+#elif ASM == 3 || ASM == 5
 #if ASM == 3
+#define SS_ASM S3_ASM
+#else
+#define SS_ASM S5_ASM
+#endif
     unsigned inside[TILE];
     {
         unsigned acc[TILE];
@@ -402,18 +1466,18 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
         const unsigned span = NPACK * 16u;
         const float vy_last = s_packed[VERTICES - 1].x;
 #if TILE == 2
-        asm volatile(S3_ASM : "+r"(acc[0]), "+r"(acc[1]) : "f"(px[0]), "f"(px[1]), "f"(py[0]), "f"(py[1]),
+        asm volatile(SS_ASM : "+r"(acc[0]), "+r"(acc[1]) : "f"(px[0]), "f"(px[1]), "f"(py[0]), "f"(py[1]),
                      "r"(sbase), "r"(span), "f"(vy_last));
 #elif TILE == 4
-        asm volatile(S3_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3])
+        asm volatile(SS_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3])
                      : "f"(px[0]), "f"(px[1]), "f"(px[2]), "f"(px[3]), "f"(py[0]), "f"(py[1]), "f"(py[2]), "f"(py[3]),
                        "r"(sbase), "r"(span), "f"(vy_last));
 #elif TILE == 6
-        asm volatile(S3_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3]), "+r"(acc[4]), "+r"(acc[5])
+        asm volatile(SS_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3]), "+r"(acc[4]), "+r"(acc[5])
                      : "f"(px[0]), "f"(px[1]), "f"(px[2]), "f"(px[3]), "f"(px[4]), "f"(px[5]), "f"(py[0]), "f"(py[1]),
                        "f"(py[2]), "f"(py[3]), "f"(py[4]), "f"(py[5]), "r"(sbase), "r"(span), "f"(vy_last));
 #else
-        asm volatile(S3_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3]), "+r"(acc[4]), "+r"(acc[5]),
+        asm volatile(SS_ASM : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3]), "+r"(acc[4]), "+r"(acc[5]),
                      "+r"(acc[6]), "+r"(acc[7])
                      : "f"(px[0]), "f"(px[1]), "f"(px[2]), "f"(px[3]), "f"(px[4]), "f"(px[5]), "f"(px[6]), "f"(px[7]),
                        "f"(py[0]), "f"(py[1]), "f"(py[2]), "f"(py[3]), "f"(py[4]), "f"(py[5]), "f"(py[6]), "f"(py[7]),
@@ -494,4 +1558,5 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
     for (int t = 0; t < TILE; ++t)
         if (idx[t] < n) bitmap[idx[t]] = inside[t] ? 1 : 0;
+    }  // tile loop
 }

@@ -180,7 +180,8 @@ class PnPolyProblem(KernelProblem):
             "method": [0, 1, 2],
             "between": [0, 1],
             "poly_smem": [0, 1],
-            "asm": [0, 1, 2, 3],
+            "asm": [0, 1, 2, 3, 4, 5, 6],
+            "persist": [0, 1],
         }
 
     def restrictions(self):
@@ -188,18 +189,20 @@ class PnPolyProblem(KernelProblem):
             "vec == 1 or tile % 2 == 0",
             "asm == 0 or (poly_smem == 1 and method == 2)",
             "asm == 0 or asm == 3 or (between == 1 and tile != 8)",
-            "asm != 3 or (between == 0 and tile != 1)",
+            "asm < 3 or (between == 0 and tile != 1)",
+            "(asm != 4 and asm != 6) or (vec == 2 and (tile == 4 or tile == 8))",
         ]
 
     def default_config(self):
-        return {"block_size_x": 256, "tile": 4, "vec": 2, "method": 2, "between": 0, "poly_smem": 1, "asm": 3}
+        return {"block_size_x": 256, "tile": 8, "vec": 2, "method": 2, "between": 0, "poly_smem": 1, "asm": 4,
+                "persist": 1}
 
     @staticmethod
     def formula(config) -> int:
         """Which exactly-specified crossing formulation a config computes:
         0/1/2 = METHOD (IEEE compares), 3 = sign-bit form of METHOD 2 (ASM=3)."""
         c = _as_dict(config)
-        return 3 if c.get("asm", 0) == 3 else c["method"]
+        return 3 if c.get("asm", 0) >= 3 else c["method"]
 
     def defines(self, config):
         c = _as_dict(config)
@@ -217,7 +220,12 @@ class PnPolyProblem(KernelProblem):
     def launch(self, config):
         c = _as_dict(config)
         per_block = c["block_size_x"] * c["tile"]
-        return Launch((math.ceil(self.n_points / per_block), 1, 1), (c["block_size_x"], 1, 1))
+        tiles = max(1, math.ceil(self.n_points / per_block))
+        if c.get("persist", 0):
+            sms = self.gpu.sm_count if self.gpu is not None else 148
+            resident = max(1, 2048 // c["block_size_x"])  # thread-limited residency per SM
+            tiles = min(tiles, sms * resident)
+        return Launch((tiles, 1, 1), (c["block_size_x"], 1, 1))
 
     def host_inputs(self):
         rng = np.random.default_rng(self.seed)
@@ -276,7 +284,7 @@ class PnPolyProblem(KernelProblem):
     def args(self, config):
         m = _as_dict(config)["method"]
         b = self.buffers
-        packed = b["packed3"] if _as_dict(config).get("asm", 0) == 3 else b["packed"]
+        packed = b["packed3"] if _as_dict(config).get("asm", 0) >= 3 else b["packed"]
         return [b["out"], b["points"], i32(self.n_points), b[f"edges{m}"], b[f"ybounds{m}"], packed]
 
     def bind(self, kernel, config):

@@ -52,9 +52,10 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
                 "method": [2],
                 "between": [0],
                 "poly_smem": [1],
-                "asm": [3],
+                "asm": [3, 4],
+                "persist": [0, 1],
             },
-            "restrictions": [],
+            "restrictions": ["asm != 4 or tile == 4 or tile == 8"],
         }
         return doc, "exhaustive", None
     if name == "conv2d":

@@ -265,3 +265,12 @@ def test_steered_power_capped_fit_recovers_optimum():
         f_opt = B.optimal_frequency(model, list(grid))
         hits += abs(f_opt - 1200.0) <= 0.1 * 1200.0
     assert hits >= 9
+
+
+def test_callable_metric_uses_milliseconds():
+    from paper_2211_07260_b200.facade import CallableMetric
+
+    m = CallableMetric("gflops", "0", fn=lambda p: 2e9 / 1e9 / (p["time"] / 1e3))
+    assert m.evaluate({"time": 0.5, "energy": 1.0}) == pytest.approx(4.0)
+    with pytest.raises(ConfigurationError):
+        CallableMetric("not an id", "0", fn=lambda p: 0)

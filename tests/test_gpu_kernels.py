@@ -36,8 +36,10 @@ def run_once(gpu, problem, cfg):
 # -- PnPoly ---------------------------------------------------------------------------
 
 PNPOLY_CONFIGS = (
-    [dict(block_size_x=b, tile=t, vec=2, method=2, between=0, poly_smem=1, asm=3)
-     for b, t in itertools.product((96, 256, 1024), (2, 4, 6, 8))]
+    [dict(block_size_x=b, tile=t, vec=2, method=2, between=0, poly_smem=1, asm=a, persist=ps)
+     for a, b, t, ps in itertools.product((3, 5), (96, 256, 1024), (2, 4, 6, 8), (0, 1))]
+    + [dict(block_size_x=b, tile=t, vec=2, method=2, between=0, poly_smem=1, asm=a, persist=ps)
+       for a, b, t, ps in itertools.product((4, 6), (128, 512), (4, 8), (0, 1))]
     + [dict(block_size_x=b, tile=t, vec=v, method=2, between=1, poly_smem=1, asm=a)
        for a, b, t, v in itertools.product((1, 2), (128,), (1, 2, 4, 6), (1, 2)) if not (v == 2 and t % 2)]
     + [dict(block_size_x=b, tile=t, vec=v, method=m, between=bt, poly_smem=s, asm=0)
