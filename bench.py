@@ -206,6 +206,12 @@ def kernel_profile(name: str, config: dict):
     return entry.get("dram_bytes_per_launch")
 
 
+def tf32_peak_gflops() -> float:
+    peaks = ROOT / "MEASURED_PEAKS.json"
+    bf16 = json.loads(peaks.read_text()).get("bf16_tflops", 1590.0) if peaks.exists() else 1590.0
+    return bf16 / 2.0 * 1e3
+
+
 def measure_tuned(gpu, name: str, objective: str, seconds: float = 0.6):
     from paper_2211_07260_b200 import tuned
     from paper_2211_07260_b200.gpu import fp32_peak_tflops
@@ -228,7 +234,13 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 0.6):
         "power_w": round(summ["counter_w"], 1) if summ["counter_w"] else None,
         "sm_mhz": summ["sm_mhz"],
     }
-    if summ["sm_mhz"]:
+    if prob.roofline_kind == "tensor":
+        # dense TF32 = half the measured dense bf16 rate (same tcgen05 cycles, K=8 vs K=16 per MMA)
+        peak = tf32_peak_gflops()
+        out["roofline_frac"] = round(rate / peak, 4)
+        out["roofline_peak_gflops"] = peak
+        out["roofline_basis"] = "MEASURED_PEAKS bf16_tflops / 2 (tcgen05 kind::tf32 issues K=8 per MMA vs K=16)"
+    elif summ["sm_mhz"]:
         peak = fp32_peak_tflops(gpu.sm_count, summ["sm_mhz"]) * 1e3
         if prob.roofline_kind == "issue":
             peak /= 2.0  # 1 lane-instruction slot per lane per clock, not 2 flop/FFMA
@@ -309,7 +321,7 @@ def run_ours(args, dist: Dist) -> int:
     # per-kernel tuned summaries (time- and energy-optimal) on this rank's GPU
     per_kernel = {}
     if dist.rank == 0 and not args.quick:
-        for name in ("conv2d", "pnpoly", "sgemm"):
+        for name in ("conv2d", "pnpoly", "sgemm", "sgemm_tf32"):
             per_kernel[name] = {obj: measure_tuned(gpu, name, obj) for obj in ("time_optimal", "energy_optimal")}
 
     cpu = None

@@ -82,7 +82,9 @@ typedef struct {
 
 /* Kernel argument; replaces nothing in the reference (kernels were simulated
  * by PerformanceSurface, device.py:148-243). */
-typedef enum { JT_ARG_PTR = 0, JT_ARG_I32 = 1, JT_ARG_F32 = 2, JT_ARG_F64 = 3, JT_ARG_I64 = 4 } jt_arg_kind;
+/* JT_ARG_BLOB: v.ptr is a host pointer to a by-value parameter (e.g. a
+ * 128-byte CUtensorMap from jt_tensor_map_2d) passed as __grid_constant__. */
+typedef enum { JT_ARG_PTR = 0, JT_ARG_I32 = 1, JT_ARG_F32 = 2, JT_ARG_F64 = 3, JT_ARG_I64 = 4, JT_ARG_BLOB = 5 } jt_arg_kind;
 typedef struct {
     int kind;
     int pad;
@@ -183,6 +185,13 @@ int jt_power_limit_reset(jt_ctx *ctx);
  * ybounds[2k..2k+1] = {min, max} of the edge's y range. Computed in IEEE
  * float32 with explicit fmaf so the device and the oracle see the same bits. */
 int jt_pnpoly_edges(const float *vx, const float *vy, int n, int method, float *edges, float *ybounds);
+/* TMA descriptor (CUtensorMap, 128 bytes written to out128) for a row-major
+ * fp32 matrix [rows][cols] at dptr, tiles of box_rows x box_cols elements.
+ * `swizzle` is a CUtensorMapSwizzle value: 0 none, 1 32B, 2 64B, 3 128B,
+ * 4 128B with 32-byte atoms (the MN-major TF32 UMMA layout), 6 128B/64B atoms
+ * (box_cols * 4 must be <= the swizzle span). */
+int jt_tensor_map_2d(jt_ctx *ctx, unsigned long long dptr, unsigned long long rows, unsigned long long cols,
+                     unsigned box_rows, unsigned box_cols, int swizzle, void *out128);
 /* Copy host bytes into a __constant__ / __device__ symbol of a loaded module. */
 int jt_module_set_global(jt_ctx *ctx, jt_module *module, const char *name, const void *src, size_t bytes);
 

@@ -93,7 +93,8 @@ double real_now() {
     X(cuModuleUnload) \
     X(cuStreamCreate) \
     X(cuStreamDestroy) \
-    X(cuStreamSynchronize)
+    X(cuStreamSynchronize) \
+    X(cuTensorMapEncodeTiled)
 
 struct Driver {
     bool ok = false;
@@ -449,6 +450,10 @@ int pack_args(const jt_arg *args, int n, std::vector<void *> &params) {
             case JT_ARG_F32: params[i] = (void *)&a.v.f32; break;
             case JT_ARG_F64: params[i] = (void *)&a.v.f64; break;
             case JT_ARG_I64: params[i] = (void *)&a.v.i64; break;
+            case JT_ARG_BLOB:
+                if (!a.v.ptr) return fail(JT_EINVAL, "argument %d: null blob", i);
+                params[i] = (void *)a.v.ptr;
+                break;
             default: return fail(JT_EINVAL, "argument %d has unknown kind %d", i, a.kind);
         }
     }
@@ -966,6 +971,28 @@ int jt_pnpoly_edges(const float *vx, const float *vy, int n, int method, float *
         ybounds[2 * k] = std::min(vy[k], vy[p]);
         ybounds[2 * k + 1] = std::max(vy[k], vy[p]);
     }
+    return JT_OK;
+}
+
+int jt_tensor_map_2d(jt_ctx *c, unsigned long long dptr, unsigned long long rows, unsigned long long cols,
+                     unsigned box_rows, unsigned box_cols, int swizzle, void *out128) {
+    if (int e = bind(c)) return e;
+    if (!out128 || !dptr || !rows || !cols || !box_rows || !box_cols) return fail(JT_EINVAL, "bad tensor map request");
+    if (swizzle < 0 || swizzle > 6) return fail(JT_EINVAL, "unknown swizzle mode %d", swizzle);
+    const unsigned span = swizzle == 1 ? 32 : swizzle == 2 ? 64 : 128;
+    if (swizzle && box_cols * 4 > span) return fail(JT_EINVAL, "box inner extent exceeds the swizzle span");
+    if ((cols * 4) % 16) return fail(JT_EINVAL, "row pitch must be a multiple of 16 bytes");
+    CUtensorMap map;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 4};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = D.p_cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)dptr, dims, strides, box,
+                                            estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            (CUtensorMapSwizzle)swizzle,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled");
+    std::memcpy(out128, &map, sizeof map);
     return JT_OK;
 }
 

@@ -16,7 +16,7 @@ from typing import Sequence
 import numpy as np
 
 from . import native
-from .native import ARG_F32, ARG_F64, ARG_I32, ARG_I64, ARG_PTR, JTArg, JTBenchResult, JTLaunchShape, JTSample, check
+from .native import ARG_BLOB, ARG_F32, ARG_F64, ARG_I32, ARG_I64, ARG_PTR, JTArg, JTBenchResult, JTLaunchShape, JTSample, check
 
 __all__ = ["GPU", "DeviceArray", "Kernel", "Launch", "BenchRun", "i32", "f32", "f64", "i64"]
 
@@ -42,6 +42,17 @@ def f32(v) -> _Scalar:
 
 def f64(v) -> _Scalar:
     return _Scalar(ARG_F64, float(v))
+
+
+class Blob:
+    """A by-value kernel parameter (e.g. a 128-byte CUtensorMap), 64-byte aligned."""
+
+    def __init__(self, data: bytes):
+        self._raw = ctypes.create_string_buffer(len(data) + 64)
+        base = ctypes.addressof(self._raw)
+        self.address = (base + 63) & ~63
+        ctypes.memmove(self.address, data, len(data))
+        self.nbytes = len(data)
 
 
 class DeviceArray:
@@ -110,6 +121,9 @@ def _pack(args: Sequence) -> ctypes.Array:
         if isinstance(a, DeviceArray):
             arr[i].kind = ARG_PTR
             arr[i].v.ptr = a.ptr
+        elif isinstance(a, Blob):
+            arr[i].kind = ARG_BLOB
+            arr[i].v.ptr = a.address
         elif isinstance(a, _Scalar):
             arr[i].kind = a.kind
             if a.kind == ARG_I32:
@@ -236,6 +250,17 @@ class GPU:
 
     def d2h_async(self, host: np.ndarray, src: "DeviceArray") -> None:
         check(native.lib().jt_d2h_async(self.handle, host.ctypes.data, src.ptr, host.nbytes), "jt_d2h_async")
+
+    SWIZZLE_128B = 3
+    SWIZZLE_128B_ATOM_32B = 4
+
+    def tensor_map_2d(self, array: "DeviceArray", rows: int, cols: int, box_rows: int, box_cols: int,
+                      swizzle: int = SWIZZLE_128B) -> Blob:
+        """TMA descriptor for a row-major fp32 [rows][cols] device matrix."""
+        out = ctypes.create_string_buffer(128)
+        check(native.lib().jt_tensor_map_2d(self.handle, array.ptr, int(rows), int(cols), int(box_rows),
+                                             int(box_cols), int(swizzle), out), "jt_tensor_map_2d")
+        return Blob(out.raw)
 
     def pinned(self, shape, dtype=np.float32) -> np.ndarray:
         """A numpy array backed by page-locked host memory owned by this context."""

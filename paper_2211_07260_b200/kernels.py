@@ -38,6 +38,7 @@ __all__ = [
     "PnPolyProblem",
     "Conv2DProblem",
     "SgemmProblem",
+    "SgemmTF32Problem",
     "BurnerProblem",
     "PROBLEMS",
     "make_problem",
@@ -481,6 +482,55 @@ class SgemmProblem(KernelProblem):
         return [i32(self.m), i32(self.n), i32(self.k), f32(self.alpha), f32(self.beta), b["at"], b["b"], b["out"]]
 
 
+@dataclass
+class SgemmTF32Problem(SgemmProblem):
+    """SGEMM on the 5th-gen tensor cores (tcgen05 kind::tf32, TMA, TMEM).
+
+    Same inputs, storage and oracle as :class:`SgemmProblem`; TF32 inputs
+    (10-bit mantissa) with FP32 accumulation, so it is held to its own
+    tolerance (oracle SGEMM_TF32_TOL) and reported separately (K1').
+    """
+
+    name: str = "sgemm_tf32"
+    source: str = "sgemm_tf32.cu"
+    symbol: str = "sgemm_tf32"
+    roofline_kind = "tensor"
+
+    def tune_params(self):
+        return {"BN": [64, 128, 256], "STAGES": [2, 3, 4, 5, 6]}
+
+    def restrictions(self):
+        return [
+            "STAGES * (16384 + BN * 128) + 2048 <= 232448",
+            f"{self.m} % 128 == 0 and {self.n} % BN == 0 and {self.k} % 32 == 0",
+        ]
+
+    def default_config(self):
+        return {"BN": 256, "STAGES": 4}
+
+    def smem_bytes(self, config) -> int:
+        c = _as_dict(config)
+        return c["STAGES"] * (128 * 32 * 4 + c["BN"] * 32 * 4) + 1024 + 256
+
+    def launch(self, config):
+        c = _as_dict(config)
+        return Launch((self.n // c["BN"], self.m // 128, 1), (128, 1, 1), smem=self.smem_bytes(c))
+
+    def prepare(self, gpu, inputs=None):
+        super().prepare(gpu, inputs)
+        # TMA descriptors: A^T is K x M row-major, B is K x N row-major; 32 x 32 fp32 boxes in the
+        # 128B-span / 32B-atom swizzle, the only smem layout UMMA accepts for MN-major TF32
+        sw = gpu.SWIZZLE_128B_ATOM_32B
+        self._maps = {
+            "a": gpu.tensor_map_2d(self.buffers["at"], self.k, self.m, 32, 32, sw),
+            "b": gpu.tensor_map_2d(self.buffers["b"], self.k, self.n, 32, 32, sw),
+        }
+
+    def args(self, config):
+        return [self._maps["a"], self._maps["b"], self.buffers["out"], i32(self.m), i32(self.n), i32(self.k),
+                f32(self.alpha), f32(self.beta)]
+
+
 # -- burner (P(f) sweep load) ---------------------------------------------------------------
 
 
@@ -525,7 +575,8 @@ class BurnerProblem(KernelProblem):
         return [self.buffers["sink"], i32(self.iters), f32(1.0)]
 
 
-PROBLEMS = {"pnpoly": PnPolyProblem, "conv2d": Conv2DProblem, "sgemm": SgemmProblem, "burner": BurnerProblem}
+PROBLEMS = {"pnpoly": PnPolyProblem, "conv2d": Conv2DProblem, "sgemm": SgemmProblem, "sgemm_tf32": SgemmTF32Problem,
+            "burner": BurnerProblem}
 
 
 def make_problem(name: str, **kwargs) -> KernelProblem:

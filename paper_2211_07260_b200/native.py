@@ -41,7 +41,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = "sm_100a"
 
 JT_OK, JT_EINVAL, JT_ENOGPU, JT_ECUDA, JT_ECOMPILE, JT_ELAUNCH, JT_ENVML, JT_ENOPERM, JT_ENOTSUP = range(9)
-ARG_PTR, ARG_I32, ARG_F32, ARG_F64, ARG_I64 = range(5)
+ARG_PTR, ARG_I32, ARG_F32, ARG_F64, ARG_I64, ARG_BLOB = range(6)
 
 # every function include/jt.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
@@ -52,7 +52,7 @@ EXPORTS = (
     "jt_sample_now", "jt_sampler_start", "jt_sampler_stop", "jt_clock_lock", "jt_clock_reset",
     "jt_app_clocks_set", "jt_app_clocks_reset", "jt_power_limit_set", "jt_power_limit_reset",
     "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
-    "jt_h2d_async", "jt_d2h_async",
+    "jt_h2d_async", "jt_d2h_async", "jt_tensor_map_2d",
 )
 
 
@@ -210,6 +210,7 @@ def _declare(lib) -> None:
         "jt_event_record": (c.c_int, [P, c.c_int]),
         "jt_event_elapsed": (c.c_int, [P, c.c_int, c.c_int, c.POINTER(c.c_double)]),
         "jt_h2d_async": (c.c_int, [P, c.c_ulonglong, P, c.c_size_t]),
+        "jt_tensor_map_2d": (c.c_int, [P, c.c_ulonglong, c.c_ulonglong, c.c_ulonglong, c.c_uint, c.c_uint, c.c_int, P]),
         "jt_d2h_async": (c.c_int, [P, P, c.c_ulonglong, c.c_size_t]),
         "jt_sample_now": (c.c_int, [P, c.POINTER(JTSample)]),
         "jt_sampler_start": (c.c_int, [P, c.c_int, c.c_int]),

@@ -37,7 +37,7 @@ def reference(problem):
         return {m: O.pnpoly(inp["points"], inp["vx"], inp["vy"], m) for m in (0, 1, 2, 3)}
     if problem.name == "conv2d":
         return O.conv2d(inp["image"], inp["filter"])
-    if problem.name == "sgemm":
+    if problem.name in ("sgemm", "sgemm_tf32"):
         return O.sgemm(inp["a"], inp["b"], inp["c0"], problem.alpha, problem.beta)
     return None
 
@@ -50,9 +50,9 @@ def check(problem, ref, cfg):
     if problem.name == "conv2d":
         err = O.conv2d_error(out, ref, problem.inputs["image"], problem.inputs["filter"])
         return err <= O.CONV_TOL, err
-    if problem.name == "sgemm":
+    if problem.name in ("sgemm", "sgemm_tf32"):
         err = O.sgemm_error(out, ref)
-        return err <= O.SGEMM_TOL, err
+        return err <= (O.SGEMM_TF32_TOL if problem.name == "sgemm_tf32" else O.SGEMM_TOL), err
     return True, 0.0
 
 

@@ -58,7 +58,7 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
             "restrictions": ["asm != 4 or tile == 4 or tile == 8"],
         }
         return doc, "exhaustive", None
-    if name == "conv2d":
+    if name in ("conv2d", "sgemm_tf32"):
         return problem.space_document(), "exhaustive", None
     if name == "sgemm":
         doc = {
@@ -84,7 +84,7 @@ def oracle_check(problem, cfg) -> tuple[bool, float]:
         err = O.conv2d_error(out, O.conv2d(inp["image"], inp["filter"]), inp["image"], inp["filter"])
         return err <= O.CONV_TOL, err
     err = O.sgemm_error(out, O.sgemm(inp["a"], inp["b"], inp["c0"], problem.alpha, problem.beta))
-    return err <= O.SGEMM_TOL, err
+    return err <= (O.SGEMM_TF32_TOL if problem.name == "sgemm_tf32" else O.SGEMM_TOL), err
 
 
 def summarize(result) -> dict:

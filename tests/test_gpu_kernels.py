@@ -217,3 +217,35 @@ def test_suite_host_api_matches_oracles():
     c = suite.sgemm(si["a"], si["b"], si["c0"], 1.0, 0.5, config=SgemmProblem().default_config() | {
         "MWG": 64, "NWG": 64, "MDIMC": 16, "NDIMC": 16, "MDIMA": 16, "NDIMB": 16})
     assert O.sgemm_error(c, O.sgemm(si["a"], si["b"], si["c0"], 1.0, 0.5)) <= O.SGEMM_TOL
+
+
+# -- SGEMM on tcgen05 (TF32, its own tolerance) -------------------------------------------------
+
+
+@pytest.mark.parametrize("cfg", [{"BN": 64, "STAGES": 3}, {"BN": 128, "STAGES": 6}, {"BN": 256, "STAGES": 2},
+                                 {"BN": 256, "STAGES": 4}], ids=str)
+@pytest.mark.parametrize("mnk,beta", [((256, 256, 256), 0.5), ((384, 512, 96), 0.0)])
+def test_sgemm_tf32_tcgen05_within_tf32_tolerance(gpu, cfg, mnk, beta):
+    from paper_2211_07260_b200.kernels import SgemmTF32Problem
+
+    m, n, k = mnk
+    if n % cfg["BN"]:
+        pytest.skip("N not a multiple of BN")
+    p = SgemmTF32Problem(m=m, n=n, k=k, beta=beta)
+    p.prepare(gpu)
+    got = run_once(gpu, p, cfg)
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    err = O.sgemm_error(got, ref)
+    assert err <= O.SGEMM_TF32_TOL
+    assert err > 1e-6  # really TF32 inputs, not an FP32 path
+
+
+def test_sgemm_tf32_full_size(gpu):
+    from paper_2211_07260_b200 import tuned
+    from paper_2211_07260_b200.kernels import SgemmTF32Problem
+
+    p = SgemmTF32Problem()
+    p.prepare(gpu)
+    cfg = tuned.best_config("sgemm_tf32") or p.default_config()
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    assert O.sgemm_error(run_once(gpu, p, cfg), ref) <= O.SGEMM_TF32_TOL
