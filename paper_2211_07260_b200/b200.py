@@ -35,11 +35,11 @@ from typing import Any, Callable, Mapping
 
 import numpy as np
 
-from .device import EXECUTION_PARAMS, DeviceSpec, DeviceState, Execution, PowerSample
+from .hardware import EXECUTION_PARAMS, DeviceSpec, DeviceState, Execution, PowerSample
 from .errors import CapabilityError, ConfigurationError, DomainError
 from .gpu import ENERGY, E_STAMP, GPU, MEM_MHZ, P_INST, REASONS, SM_MHZ, SW_POWER_CAP, TEMP, T
 from .kernels import KernelProblem, make_problem
-from .searchspace import KernelConfig, normalize_value
+from .spaces import KernelConfig, normalize_value
 
 __all__ = ["B200Device", "counter_slope", "steady_window"]
 

@@ -37,9 +37,10 @@ from . import native
 from .b200 import B200Device
 from .gpu import DeviceArray, Launch, f32, f64, i32, i64
 from .kernels import KernelProblem, make_problem
-from .observers import BenchmarkObserver, NVMLObserver
-from .searchspace import SearchSpace
-from .tuner import Objective, ResultCache, StrategyOutcome, TuningRun, UserMetric, run_strategy
+from .observer_hooks import BenchmarkObserver, NVMLObserver
+from .spaces import SearchSpace
+from .records import Objective, ResultCache, UserMetric
+from .search import StrategyOutcome, TuningRun, run_strategy
 
 __all__ = ["tune_kernel", "SourceProblem", "CallableMetric"]
 

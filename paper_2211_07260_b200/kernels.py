@@ -31,7 +31,7 @@ import numpy as np
 
 from . import native
 from .gpu import GPU, DeviceArray, Kernel, Launch, f32, i32
-from .searchspace import KernelConfig, SearchSpace
+from .spaces import KernelConfig, SearchSpace
 
 __all__ = [
     "KernelProblem",

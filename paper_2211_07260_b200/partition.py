@@ -30,11 +30,14 @@ from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Callable, Mapping, Sequence
 
-from .device import CLOCK_PARAM
+from .hardware import CLOCK_PARAM
 from .errors import ConfigurationError, TuningError
-from .observers import AveragedSensorConfig, BenchmarkObserver
-from .searchspace import KernelConfig, SearchSpace, normalize_value
-from .tuner import BenchmarkResult, MeasurementSetup, Objective, ResultCache, UserMetric, _Evaluator
+from .observer_hooks import BenchmarkObserver
+from .sensors import AveragedSensorConfig
+from .spaces import KernelConfig, SearchSpace, normalize_value
+from .measure import MeasurementSetup
+from .records import BenchmarkResult, Objective, ResultCache, UserMetric
+from .search import _Evaluator
 
 __all__ = ["Shard", "plan", "run_shard", "merge", "MergedRun", "run_distributed"]
 

@@ -47,15 +47,15 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
         doc = {
             "parameters": {
                 "block_size_x": [64, 128, 192, 256, 384, 512, 768, 1024],
-                "tile": [2, 4, 6, 8],
+                "tile": [4, 6, 8],
                 "vec": [2],
                 "method": [2],
                 "between": [0],
                 "poly_smem": [1],
-                "asm": [3, 4],
+                "asm": [3, 5],
                 "persist": [0, 1],
             },
-            "restrictions": ["asm != 4 or tile == 4 or tile == 8"],
+            "restrictions": [],
         }
         return doc, "exhaustive", None
     if name in ("conv2d", "sgemm_tf32"):
@@ -176,7 +176,7 @@ def _try_compile(problem, cfg):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--kernels", default="conv2d,pnpoly,sgemm")
+    ap.add_argument("--kernels", default="conv2d,pnpoly,sgemm,sgemm_tf32")
     ap.add_argument("--duration", type=float, default=0.4)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--clocks", default="auto", help="'auto', 'none' or comma list of MHz")
