@@ -1,14 +1,16 @@
 """Device-facing value types shared by the simulated and the real device.
 
-Reference: ``pkg/src/jouletune/device.py:38-138``. The execution parameters
-(``nvml_gr_clock``, ``nvml_mem_clock``, ``nvml_pwr_limit``) are ordinary
-tunables that the benchmark applies to the device instead of passing to the
-kernel. The duck-typed device interface the tuner, observers and CLI call is
-listed in SURVEY §8(b): ``spec``, ``state``, ``sample_rate_hz``,
-``execution_count``, ``set_core_clock``, ``set_power_limit``,
-``effective_clock``, ``read_voltage``, ``kernel_view``, ``execute`` and (new
-here) ``probe_runtime``. Implementations: :class:`.simulator.SimulatedDevice`
-(deterministic test backend) and :class:`.b200.B200Device` (the GPU).
+Execution parameters (``nvml_gr_clock``, ``nvml_mem_clock``,
+``nvml_pwr_limit``) are ordinary tunables that the benchmark applies to the
+device instead of passing to the kernel (reference
+``pkg/src/jouletune/device.py:38-41``).
+
+The duck-typed device interface the engine, observers and CLI call
+(SURVEY §8(b)): ``spec``, ``state``, ``sample_rate_hz``, ``execution_count``,
+``set_core_clock``, ``set_power_limit``, ``effective_clock``,
+``read_voltage``, ``kernel_view``, ``execute`` and (new) ``probe_runtime``.
+Implementations: :class:`.simulator.SimulatedDevice` (deterministic test
+backend) and :class:`.b200.B200Device` (the GPU).
 """
 
 from __future__ import annotations
@@ -29,7 +31,7 @@ __all__ = ["CLOCK_PARAM", "MEM_CLOCK_PARAM", "POWER_LIMIT_PARAM", "EXECUTION_PAR
 
 @dataclass(frozen=True)
 class DeviceSpec:
-    """What a device can do: clock grid, clock anchors, power-limit range."""
+    """Capabilities: clock grid (MHz, ascending, floats), anchors, power-limit range (W)."""
 
     name: str
     supported_core_clocks: tuple[float, ...]
@@ -43,17 +45,17 @@ class DeviceSpec:
         grid = tuple(float(c) for c in self.supported_core_clocks)
         object.__setattr__(self, "supported_core_clocks", grid)
         object.__setattr__(self, "power_limit_range", tuple(self.power_limit_range))
-        if len(grid) < 2 or list(grid) != sorted(set(grid)):
-            raise ConfigurationError(f"{self.name}: supported clocks must be a sorted set of >= 2 values")
-        if self.base_clock not in grid or self.peak_clock not in grid:
-            raise ConfigurationError(f"{self.name}: base and peak clock must be supported clocks")
-        if self.base_clock > self.peak_clock:
-            raise ConfigurationError(f"{self.name}: base clock above peak clock")
         lo, hi = self.power_limit_range
-        if not 0 < lo < hi:
-            raise ConfigurationError(f"{self.name}: bad power limit range {lo}..{hi}")
-        if hi > self.tdp:
-            raise ConfigurationError(f"{self.name}: power limit range exceeds TDP {self.tdp}")
+        checks = (
+            (len(grid) >= 2 and list(grid) == sorted(set(grid)), "supported clocks must be a sorted set of >= 2 values"),
+            (self.base_clock in grid and self.peak_clock in grid, "base and peak clock must be supported clocks"),
+            (self.base_clock <= self.peak_clock, "base clock above peak clock"),
+            (0 < lo < hi, f"bad power limit range {lo}..{hi}"),
+            (hi <= self.tdp, f"power limit range exceeds TDP {self.tdp}"),
+        )
+        for ok, problem in checks:
+            if not ok:
+                raise ConfigurationError(f"{self.name}: {problem}")
 
 
 @dataclass(frozen=True)
@@ -64,23 +66,26 @@ class DeviceState:
 
 @dataclass(frozen=True)
 class PowerSample:
-    timestamp: float
-    power: float
+    timestamp: float  # s since the start of the execution
+    power: float  # W
 
 
 @dataclass(frozen=True)
 class Execution:
     """One measured execution (possibly a back-to-back repetition loop).
 
-    The first five fields are the reference's (``device.py:130-138``).
-    The B200 backend fills the optional tail:
+    The first five fields are the reference's (``device.py:130-138``):
+    per-execution runtime (s), the power trace, the granted clock, the
+    repetition count and the traced duration. The real device fills the
+    optional tail:
 
-    * ``window`` — ``(t0, t1)`` of the steady-state part of the loop inside
-      the trace; energy rules that the reference evaluates over
-      ``[0, runtime]`` use this window instead when present;
-    * ``counter_energy`` — energy-counter delta over the whole loop (J);
-    * ``counter_power`` — counter slope over the steady window (W);
-    * ``telemetry`` — medians of SM clock, temperature etc. over the window.
+    * ``window`` — ``(t0, t1)`` steady-state part of the loop inside the
+      trace; energy rules the reference evaluates over ``[0, runtime]`` use
+      this window when present;
+    * ``counter_energy`` / ``counter_power`` — NVML energy-counter delta over
+      the loop (J) and its slope over the steady window (W);
+    * ``telemetry`` — medians of SM / memory clock, temperature and the
+      controller / throttle status over the window.
     """
 
     runtime: float
@@ -92,5 +97,3 @@ class Execution:
     counter_energy: float | None = None
     counter_power: float | None = None
     telemetry: Mapping[str, float] | None = None
-
-

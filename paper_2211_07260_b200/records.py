@@ -1,16 +1,17 @@
-"""Result records: what one measurement produced and how it is ranked and stored.
+"""Result records: what one measurement produced, how it ranks, where it is kept.
 
 Behaviour contract (reference ``pkg/src/jouletune/tuner.py:65-224``):
 
 * a :class:`BenchmarkResult` resolves a metric name against the core fields
   (``time`` in s, ``energy`` in J), then observer readings, then user metrics;
-* an :class:`Objective` turns a result into a scalar to *minimise*; failed
-  results rank last (+inf), ``maximize`` negates;
+* an :class:`Objective` maps a result to a scalar to *minimise*: failed
+  results rank last (+inf) and ``maximize`` negates the metric;
 * :class:`UserMetric` expressions see ``time``/``energy``, every observer key
-  and the run constants, and must produce a finite number;
+  and the run constants, and must evaluate to a finite number;
 * :class:`ResultCache` is an append-only JSON-lines file keyed by
   ``KernelConfig.key()``; re-opening it replays every line, so an interrupted
-  tuning run resumes with zero repeated device work.
+  run resumes with no repeated device work, and the line format is the
+  reference's (``sort_keys`` JSON of ``BenchmarkResult.to_dict()``).
 """
 
 from __future__ import annotations
@@ -19,7 +20,7 @@ import json
 import math
 from dataclasses import dataclass, field
 from pathlib import Path
-from typing import Any, Mapping
+from typing import Any, Iterator, Mapping
 
 from .errors import ConfigurationError, MeasurementError
 from .expressions import Expression
@@ -28,8 +29,13 @@ from .spaces import KernelConfig
 __all__ = ["BenchmarkResult", "Objective", "UserMetric", "default_metrics", "ResultCache", "CORE_FIELDS"]
 
 CORE_FIELDS = frozenset({"time", "energy"})
+_DIRECTIONS = {"": "minimize", "min": "minimize", "max": "maximize"}
+
+
 @dataclass(frozen=True)
 class BenchmarkResult:
+    """One evaluated config (failed evaluations carry inf time/energy and a reason)."""
+
     config: KernelConfig
     time: float
     energy: float
@@ -38,63 +44,62 @@ class BenchmarkResult:
     failed: bool = False
     failure_reason: str | None = None
 
+    def _namespaces(self) -> Iterator[Mapping[str, float]]:
+        yield {"time": self.time, "energy": self.energy}
+        yield self.observer_results
+        yield self.metrics
+
     def lookup(self, name: str) -> float:
-        """Core field, then observer reading, then user metric."""
-        if name in CORE_FIELDS:
-            return self.time if name == "time" else self.energy
-        for table in (self.observer_results, self.metrics):
+        for table in self._namespaces():
             if name in table:
                 return table[name]
-        known = ["time", "energy"] + sorted(self.observer_results) + sorted(self.metrics)
-        raise ConfigurationError(f"result has no metric {name!r}; available: {known}")
+        available = ["time", "energy", *sorted(self.observer_results), *sorted(self.metrics)]
+        raise ConfigurationError(f"result has no metric {name!r}; available: {available}")
 
     def to_dict(self) -> dict[str, Any]:
-        return {
-            "config": self.config.as_dict(),
-            "time": self.time,
-            "energy": self.energy,
-            "observer_results": dict(self.observer_results),
-            "metrics": dict(self.metrics),
-            "failed": self.failed,
-            "failure_reason": self.failure_reason,
-        }
+        doc: dict[str, Any] = {"config": self.config.as_dict(), "time": self.time, "energy": self.energy}
+        doc["observer_results"] = dict(self.observer_results)
+        doc["metrics"] = dict(self.metrics)
+        doc["failed"] = self.failed
+        doc["failure_reason"] = self.failure_reason
+        return doc
 
     @classmethod
-    def from_dict(cls, data: Mapping[str, Any]) -> "BenchmarkResult":
-        return cls(
-            config=KernelConfig.from_dict(data["config"]),
-            time=data["time"],
-            energy=data["energy"],
-            observer_results=dict(data.get("observer_results", {})),
-            metrics=dict(data.get("metrics", {})),
-            failed=data.get("failed", False),
-            failure_reason=data.get("failure_reason"),
-        )
+    def from_dict(cls, doc: Mapping[str, Any]) -> "BenchmarkResult":
+        optional = {
+            "observer_results": dict(doc.get("observer_results", {})),
+            "metrics": dict(doc.get("metrics", {})),
+            "failed": doc.get("failed", False),
+            "failure_reason": doc.get("failure_reason"),
+        }
+        return cls(KernelConfig.from_dict(doc["config"]), doc["time"], doc["energy"], **optional)
 
 
 @dataclass(frozen=True)
 class Objective:
+    """Metric name + direction; ``fitness`` is what every strategy minimises."""
+
     metric: str = "time"
     direction: str = "minimize"
 
     def __post_init__(self):
-        if self.direction not in ("minimize", "maximize"):
+        if self.direction not in _DIRECTIONS.values():
             raise ConfigurationError(f"direction must be minimize or maximize, got {self.direction!r}")
 
     @classmethod
     def parse(cls, text: str) -> "Objective":
         """``'energy'``, ``'time:min'``, ``'gflops_per_w:max'``."""
         name, _, suffix = text.partition(":")
-        direction = {"": "minimize", "min": "minimize", "max": "maximize"}.get(suffix)
-        if not name or direction is None:
+        if not name or suffix not in _DIRECTIONS:
             raise ConfigurationError(f"bad objective {text!r}; expected NAME[:min|:max]")
-        return cls(name, direction)
+        return cls(name, _DIRECTIONS[suffix])
 
     def fitness(self, result: BenchmarkResult) -> float:
         if result.failed:
             return math.inf
+        sign = -1.0 if self.direction == "maximize" else 1.0
         value = result.lookup(self.metric)
-        return -value if self.direction == "maximize" else value
+        return value if sign > 0 else -value
 
     def better(self, a: BenchmarkResult, b: BenchmarkResult) -> bool:
         return self.fitness(a) < self.fitness(b)
@@ -102,6 +107,8 @@ class Objective:
 
 @dataclass(frozen=True)
 class UserMetric:
+    """A named expression derived from every result (e.g. GFLOPS/W)."""
+
     name: str
     expression: str
 
@@ -111,57 +118,56 @@ class UserMetric:
 
     def evaluate(self, env: Mapping[str, float]) -> float:
         value = Expression(self.expression)(env)
-        if not isinstance(value, (int, float)) or not math.isfinite(value):
+        finite = isinstance(value, (int, float)) and math.isfinite(value)
+        if not finite:
             raise MeasurementError(f"metric {self.name!r} = {self.expression!r} is not finite: {value!r}")
         return float(value)
 
 
 def default_metrics(total_flops: float) -> tuple[UserMetric, ...]:
-    """``gflops`` and ``gflops_per_w`` from a known operation count (time in s)."""
+    """``gflops`` and ``gflops_per_w`` for a known operation count (time in s, energy in J)."""
     if total_flops <= 0:
         raise ConfigurationError("total_flops must be positive")
-    return (
-        UserMetric("gflops", "total_flops / time / 1e9"),
-        UserMetric("gflops_per_w", "total_flops / energy / 1e9"),
-    )
+    return UserMetric("gflops", "total_flops / time / 1e9"), UserMetric("gflops_per_w", "total_flops / energy / 1e9")
 
 
 class ResultCache:
-    """Append-only result store keyed by canonical config hash (JSON lines)."""
+    """Results keyed by config hash, optionally mirrored to a JSON-lines file."""
 
     def __init__(self, path: str | Path | None = None):
-        self.path = None if path is None else Path(path)
-        self._entries: dict[str, BenchmarkResult] = {}
+        self.path = Path(path) if path is not None else None
+        self._by_key: dict[str, BenchmarkResult] = {}
         if self.path is not None and self.path.exists():
-            for lineno, raw in enumerate(self.path.read_text().splitlines(), 1):
-                raw = raw.strip()
-                if not raw:
-                    continue
-                try:
-                    result = BenchmarkResult.from_dict(json.loads(raw))
-                except (json.JSONDecodeError, KeyError) as exc:
-                    raise ConfigurationError(f"corrupt cache line in {self.path}: {exc}") from exc
-                self._entries[result.config.key()] = result
+            self._replay(self.path)
+
+    def _replay(self, path: Path) -> None:
+        for raw in path.read_text().splitlines():
+            if not raw.strip():
+                continue
+            try:
+                result = BenchmarkResult.from_dict(json.loads(raw))
+            except (json.JSONDecodeError, KeyError) as exc:
+                raise ConfigurationError(f"corrupt cache line in {path}: {exc}") from exc
+            self._by_key[result.config.key()] = result
 
     def __len__(self) -> int:
-        return len(self._entries)
+        return len(self._by_key)
 
     def __contains__(self, config: KernelConfig) -> bool:
-        return config.key() in self._entries
+        return config.key() in self._by_key
 
     def get(self, config: KernelConfig) -> BenchmarkResult | None:
-        return self._entries.get(config.key())
+        return self._by_key.get(config.key())
 
     def put(self, result: BenchmarkResult) -> None:
-        k = result.config.key()
-        if k in self._entries:
+        """Store once (first write wins) and append it to the file."""
+        key = result.config.key()
+        if key in self._by_key:
             return
-        self._entries[k] = result
+        self._by_key[key] = result
         if self.path is not None:
-            with open(self.path, "a") as fh:
+            with self.path.open("a") as fh:
                 fh.write(json.dumps(result.to_dict(), sort_keys=True) + "\n")
 
     def results(self) -> list[BenchmarkResult]:
-        return list(self._entries.values())
-
-
+        return list(self._by_key.values())
