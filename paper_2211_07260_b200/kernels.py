@@ -497,23 +497,53 @@ class SgemmTF32Problem(SgemmProblem):
     roofline_kind = "tensor"
 
     def tune_params(self):
-        return {"BN": [64, 128, 256], "STAGES": [2, 3, 4, 5, 6]}
+        return {"BN": [64, 128, 256], "STAGES": [2, 3, 4, 5, 6], "PERSIST": [0, 1], "SPLIT_TAIL": [0, 1]}
 
     def restrictions(self):
         return [
             "STAGES * (16384 + BN * 128) + 2048 <= 232448",
+            "PERSIST == 0 or BN >= 128",
+            "PERSIST == 1 or SPLIT_TAIL == 0",
             f"{self.m} % 128 == 0 and {self.n} % BN == 0 and {self.k} % 32 == 0",
         ]
 
     def default_config(self):
-        return {"BN": 256, "STAGES": 4}
+        return {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1}
+
+    def defines(self, config):
+        c = _as_dict(config)
+        d = {"BN": c["BN"], "STAGES": c["STAGES"]}
+        if c.get("PERSIST", 0):
+            d["SPLIT_TAIL"] = c.get("SPLIT_TAIL", 0)
+        return d
+
+    def _variant(self, config) -> tuple[str, str]:
+        """(source file, kernel symbol): persistent warp-specialised or one tile per CTA."""
+        if _as_dict(config).get("PERSIST", 0):
+            return "sgemm_tf32p.cu", "sgemm_tf32p"
+        return "sgemm_tf32.cu", "sgemm_tf32"
+
+    def cubin(self, config):
+        source, _ = self._variant(config)
+        return native.compile_cubin(native.kernel_source(source), self.name, self.options(config))
+
+    def kernel(self, config):
+        if self.gpu is None:
+            raise RuntimeError(f"{self.name}: prepare(gpu) first")
+        return self.gpu.load(self.cubin(config), self._variant(config)[1])
 
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
         return c["STAGES"] * (128 * 32 * 4 + c["BN"] * 32 * 4) + 1024 + 256
 
+    def tiles(self, config) -> int:
+        return (self.m // 128) * (self.n // _as_dict(config)["BN"])
+
     def launch(self, config):
         c = _as_dict(config)
+        if c.get("PERSIST", 0):
+            sms = self.gpu.sm_count if self.gpu is not None else 148
+            return Launch((min(sms, self.tiles(c)), 1, 1), (192, 1, 1), smem=self.smem_bytes(c))
         return Launch((self.n // c["BN"], self.m // 128, 1), (128, 1, 1), smem=self.smem_bytes(c))
 
     def prepare(self, gpu, inputs=None):
@@ -525,10 +555,19 @@ class SgemmTF32Problem(SgemmProblem):
             "a": gpu.tensor_map_2d(self.buffers["at"], self.k, self.m, 32, 32, sw),
             "b": gpu.tensor_map_2d(self.buffers["b"], self.k, self.n, 32, 32, sw),
         }
+        # split-K tail workspace (two 128 x 256 partials per split tile, < one per SM) and counters
+        self.buffers["workspace"] = gpu.empty((2 * gpu.sm_count * 128 * 256,), np.float32)
+        counters = gpu.empty((gpu.sm_count,), np.uint32)
+        counters.fill(0)
+        self.buffers["counters"] = counters
 
     def args(self, config):
-        return [self._maps["a"], self._maps["b"], self.buffers["out"], i32(self.m), i32(self.n), i32(self.k),
-                f32(self.alpha), f32(self.beta)]
+        c = _as_dict(config)
+        b = self.buffers
+        scalars = [i32(self.m), i32(self.n), i32(self.k), f32(self.alpha), f32(self.beta)]
+        if c.get("PERSIST", 0):
+            return [self._maps["a"], self._maps["b"], b["out"], b["workspace"], b["counters"], *scalars]
+        return [self._maps["a"], self._maps["b"], b["out"], *scalars]
 
 
 # -- burner (P(f) sweep load) ---------------------------------------------------------------
