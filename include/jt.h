@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define JT_ABI_VERSION 1
+#define JT_ABI_VERSION 2
 
 /* Status codes and the Python exception each maps to (native.py):         */
 typedef enum {
@@ -157,7 +157,14 @@ int jt_bench(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const
 int jt_events_reserve(jt_ctx *ctx, int n);
 int jt_event_record(jt_ctx *ctx, int index);
 int jt_event_elapsed(jt_ctx *ctx, int start, int stop, double *seconds);
-/* Async copies on the context stream (host memory should be pinned). */
+/* Streams: index 0 is the context's own; jt_streams_reserve(n) makes 1..n-1.
+ * jt_stream_select routes subsequent launches, async copies, memsets, event
+ * records and timed loops to that stream (copy/compute overlap for the
+ * host-buffer suite entry points); jt_synchronize waits for all of them. */
+int jt_streams_reserve(jt_ctx *ctx, int n);
+int jt_stream_select(jt_ctx *ctx, int index);
+int jt_stream_wait_event(jt_ctx *ctx, int event_index);   /* selected stream waits on event */
+/* Async copies on the selected stream (host memory should be pinned). */
 int jt_h2d_async(jt_ctx *ctx, unsigned long long dst, const void *src, size_t bytes);
 int jt_d2h_async(jt_ctx *ctx, void *dst, unsigned long long src, size_t bytes);
 /* Overwrite a scratch buffer larger than L2 (126 MB on B200). */

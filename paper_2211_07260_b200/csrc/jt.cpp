@@ -94,6 +94,7 @@ double real_now() {
     X(cuStreamCreate) \
     X(cuStreamDestroy) \
     X(cuStreamSynchronize) \
+    X(cuStreamWaitEvent) \
     X(cuTensorMapEncodeTiled)
 
 struct Driver {
@@ -265,7 +266,9 @@ struct jt_ctx {
     int ordinal = 0;
     CUdevice dev = 0;
     CUcontext cu = nullptr;
-    CUstream stream = nullptr;
+    CUstream stream = nullptr;             // stream 0: the context's own
+    std::vector<CUstream> lanes;           // streams 1..n (jt_streams_reserve)
+    int cur = 0;                           // stream launches / copies / events go to
     CUevent ev_a = nullptr, ev_b = nullptr;
     CUdeviceptr flush_buf = 0;
     size_t flush_bytes = 0;
@@ -289,6 +292,8 @@ struct jt_ctx {
 };
 
 namespace {
+
+inline CUstream active(const jt_ctx *c) { return c->cur == 0 ? c->stream : c->lanes[c->cur - 1]; }
 
 std::mutex g_open_mu;
 std::set<jt_ctx *> g_open;
@@ -421,7 +426,7 @@ int launch_on(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, void **params) 
         cfg.blockDimY = s->block[1];
         cfg.blockDimZ = s->block[2];
         cfg.sharedMemBytes = s->smem_bytes;
-        cfg.hStream = c->stream;
+        cfg.hStream = active(c);
         CUlaunchAttribute attr;
         std::memset(&attr, 0, sizeof attr);
         attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
@@ -434,7 +439,7 @@ int launch_on(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, void **params) 
         return JT_OK;
     }
     CU_TRY(D.p_cuLaunchKernel(k->fn, s->grid[0], s->grid[1], s->grid[2], s->block[0], s->block[1], s->block[2],
-                          s->smem_bytes, c->stream, params, nullptr),
+                          s->smem_bytes, active(c), params, nullptr),
            "cuLaunchKernel");
     return JT_OK;
 }
@@ -578,6 +583,10 @@ int jt_close(jt_ctx *c) {
     reset_controls(c);
     D.p_cuCtxSetCurrent(c->cu);
     D.p_cuStreamSynchronize(c->stream);
+    for (CUstream st : c->lanes) {
+        D.p_cuStreamSynchronize(st);
+        D.p_cuStreamDestroy(st);
+    }
     for (jt_kernel *k : c->kernels) delete k;
     for (jt_module *m : c->modules) {
         D.p_cuModuleUnload(m->mod);
@@ -634,27 +643,54 @@ int jt_host_free(jt_ctx *c, void *hptr) {
 
 int jt_h2d(jt_ctx *c, unsigned long long dst, const void *src, size_t bytes) {
     if (int e = bind(c)) return e;
-    CU_TRY(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, c->stream), "cuMemcpyHtoDAsync");
-    CU_TRY(D.p_cuStreamSynchronize(c->stream), "h2d sync");
+    CU_TRY(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, active(c)), "cuMemcpyHtoDAsync");
+    CU_TRY(D.p_cuStreamSynchronize(active(c)), "h2d sync");
     return JT_OK;
 }
 
 int jt_d2h(jt_ctx *c, void *dst, unsigned long long src, size_t bytes) {
     if (int e = bind(c)) return e;
-    CU_TRY(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, c->stream), "cuMemcpyDtoHAsync");
-    CU_TRY(D.p_cuStreamSynchronize(c->stream), "d2h sync");
+    CU_TRY(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, active(c)), "cuMemcpyDtoHAsync");
+    CU_TRY(D.p_cuStreamSynchronize(active(c)), "d2h sync");
     return JT_OK;
 }
 
 int jt_memset_d8(jt_ctx *c, unsigned long long dst, unsigned char value, size_t bytes) {
     if (int e = bind(c)) return e;
-    CU_TRY(D.p_cuMemsetD8Async((CUdeviceptr)dst, value, bytes, c->stream), "cuMemsetD8Async");
+    CU_TRY(D.p_cuMemsetD8Async((CUdeviceptr)dst, value, bytes, active(c)), "cuMemsetD8Async");
     return JT_OK;
 }
 
 int jt_synchronize(jt_ctx *c) {
     if (int e = bind(c)) return e;
     CU_TRY(D.p_cuStreamSynchronize(c->stream), "cuStreamSynchronize");
+    for (CUstream st : c->lanes) CU_TRY(D.p_cuStreamSynchronize(st), "cuStreamSynchronize");
+    return JT_OK;
+}
+
+int jt_streams_reserve(jt_ctx *c, int n) {
+    if (int e = bind(c)) return e;
+    if (n < 1 || n > 64) return fail(JT_EINVAL, "bad stream count %d", n);
+    while ((int)c->lanes.size() + 1 < n) {
+        CUstream st;
+        CU_TRY(D.p_cuStreamCreate(&st, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+        c->lanes.push_back(st);
+    }
+    return JT_OK;
+}
+
+int jt_stream_select(jt_ctx *c, int index) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    if (index < 0 || index > (int)c->lanes.size()) return fail(JT_EINVAL, "stream %d not reserved", index);
+    c->cur = index;
+    return JT_OK;
+}
+
+int jt_stream_wait_event(jt_ctx *c, int event_index) {
+    if (int e = bind(c)) return e;
+    if (event_index < 0 || event_index >= (int)c->events.size())
+        return fail(JT_EINVAL, "event %d not reserved", event_index);
+    CU_TRY(D.p_cuStreamWaitEvent(active(c), c->events[event_index], 0), "cuStreamWaitEvent");
     return JT_OK;
 }
 
@@ -764,10 +800,10 @@ int jt_time(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *arg
     if (int e = check_shape(s)) return e;
     std::vector<void *> params;
     if (int e = pack_args(args, n_args, params)) return e;
-    CU_TRY(D.p_cuEventRecord(c->ev_a, c->stream), "cuEventRecord");
+    CU_TRY(D.p_cuEventRecord(c->ev_a, active(c)), "cuEventRecord");
     for (int i = 0; i < reps; ++i)
         if (int e = launch_on(c, k, s, params.data())) return e;
-    CU_TRY(D.p_cuEventRecord(c->ev_b, c->stream), "cuEventRecord");
+    CU_TRY(D.p_cuEventRecord(c->ev_b, active(c)), "cuEventRecord");
     CU_TRY(D.p_cuEventSynchronize(c->ev_b), "kernel execution");
     float ms = 0.f;
     CU_TRY(D.p_cuEventElapsedTime(&ms, c->ev_a, c->ev_b), "cuEventElapsedTime");
@@ -798,9 +834,9 @@ int jt_bench(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *ar
     };
     // probe launch (also the warm-up): untimed by the loop, timed by events
     CUresult r;
-    if ((r = D.p_cuEventRecord(c->ev_a, c->stream)) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
+    if ((r = D.p_cuEventRecord(c->ev_a, active(c))) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
     if (int e = launch_on(c, k, s, params.data())) return finish(e);
-    if ((r = D.p_cuEventRecord(c->ev_b, c->stream)) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
+    if ((r = D.p_cuEventRecord(c->ev_b, active(c))) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
     if ((r = D.p_cuEventSynchronize(c->ev_b)) != CUDA_SUCCESS) return finish(cu_fail(r, "kernel execution"));
     float ms = 0.f;
     D.p_cuEventElapsedTime(&ms, c->ev_a, c->ev_b);
@@ -810,10 +846,10 @@ int jt_bench(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *ar
     int reps = (int)std::min<long>(std::max<long>(want, min_reps), max_reps);
 
     out->host_t_enqueue = mono_now();
-    if ((r = D.p_cuEventRecord(c->ev_a, c->stream)) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
+    if ((r = D.p_cuEventRecord(c->ev_a, active(c))) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
     for (int i = 0; i < reps; ++i)
         if (int e = launch_on(c, k, s, params.data())) return finish(e);
-    if ((r = D.p_cuEventRecord(c->ev_b, c->stream)) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
+    if ((r = D.p_cuEventRecord(c->ev_b, active(c))) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
     if ((r = D.p_cuEventSynchronize(c->ev_b)) != CUDA_SUCCESS) return finish(cu_fail(r, "kernel execution"));
     out->host_t_done = mono_now();
     D.p_cuEventElapsedTime(&ms, c->ev_a, c->ev_b);
@@ -838,7 +874,7 @@ int jt_events_reserve(jt_ctx *c, int n) {
 int jt_event_record(jt_ctx *c, int index) {
     if (int e = bind(c)) return e;
     if (index < 0 || index >= (int)c->events.size()) return fail(JT_EINVAL, "event %d not reserved", index);
-    CU_TRY(D.p_cuEventRecord(c->events[index], c->stream), "cuEventRecord");
+    CU_TRY(D.p_cuEventRecord(c->events[index], active(c)), "cuEventRecord");
     return JT_OK;
 }
 
@@ -855,13 +891,13 @@ int jt_event_elapsed(jt_ctx *c, int start, int stop, double *seconds) {
 
 int jt_h2d_async(jt_ctx *c, unsigned long long dst, const void *src, size_t bytes) {
     if (int e = bind(c)) return e;
-    CU_TRY(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, c->stream), "cuMemcpyHtoDAsync");
+    CU_TRY(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, active(c)), "cuMemcpyHtoDAsync");
     return JT_OK;
 }
 
 int jt_d2h_async(jt_ctx *c, void *dst, unsigned long long src, size_t bytes) {
     if (int e = bind(c)) return e;
-    CU_TRY(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, c->stream), "cuMemcpyDtoHAsync");
+    CU_TRY(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, active(c)), "cuMemcpyDtoHAsync");
     return JT_OK;
 }
 
@@ -871,7 +907,7 @@ int jt_l2_flush(jt_ctx *c) {
         c->flush_bytes = std::max<size_t>((size_t)c->info.l2_bytes * 2, (size_t)256 << 20);
         CU_TRY(D.p_cuMemAlloc(&c->flush_buf, c->flush_bytes), "alloc L2 flush buffer");
     }
-    CU_TRY(D.p_cuMemsetD8Async(c->flush_buf, 0x5a, c->flush_bytes, c->stream), "L2 flush");
+    CU_TRY(D.p_cuMemsetD8Async(c->flush_buf, 0x5a, c->flush_bytes, active(c)), "L2 flush");
     return JT_OK;
 }
 

@@ -18,7 +18,7 @@ import numpy as np
 from . import native
 from .native import ARG_BLOB, ARG_F32, ARG_F64, ARG_I32, ARG_I64, ARG_PTR, JTArg, JTBenchResult, JTLaunchShape, JTSample, check
 
-__all__ = ["GPU", "DeviceArray", "Kernel", "Launch", "BenchRun", "i32", "f32", "f64", "i64"]
+__all__ = ["GPU", "DeviceArray", "DeviceSlice", "rows", "Kernel", "Launch", "BenchRun", "i32", "f32", "f64", "i64"]
 
 
 class _Scalar:
@@ -90,6 +90,27 @@ class DeviceArray:
             self.ptr = 0
 
 
+class DeviceSlice:
+    """A byte range of a :class:`DeviceArray` (kernel argument / async-copy endpoint; not owning)."""
+
+    __slots__ = ("gpu", "ptr", "nbytes", "shape", "dtype")
+
+    def __init__(self, base: DeviceArray, offset: int, nbytes: int, shape=None):
+        if offset < 0 or nbytes < 0 or offset + nbytes > base.nbytes:
+            raise ValueError(f"slice [{offset}, {offset + nbytes}) outside a {base.nbytes}-byte buffer")
+        self.gpu = base.gpu
+        self.ptr = base.ptr + offset
+        self.nbytes = nbytes
+        self.dtype = base.dtype
+        self.shape = tuple(shape) if shape is not None else (nbytes // base.dtype.itemsize,)
+
+
+def rows(base: DeviceArray, r0: int, r1: int) -> DeviceSlice:
+    """Rows [r0, r1) of a row-major device array (its shape[1:] is the row)."""
+    row = int(np.prod(base.shape[1:])) * base.dtype.itemsize if len(base.shape) > 1 else base.dtype.itemsize
+    return DeviceSlice(base, r0 * row, (r1 - r0) * row, (r1 - r0, *base.shape[1:]))
+
+
 @dataclass(frozen=True)
 class Launch:
     grid: tuple[int, int, int]
@@ -118,7 +139,7 @@ class Launch:
 def _pack(args: Sequence) -> ctypes.Array:
     arr = (JTArg * max(len(args), 1))()
     for i, a in enumerate(args):
-        if isinstance(a, DeviceArray):
+        if isinstance(a, (DeviceArray, DeviceSlice)):
             arr[i].kind = ARG_PTR
             arr[i].v.ptr = a.ptr
         elif isinstance(a, Blob):
@@ -244,6 +265,17 @@ class GPU:
         out = ctypes.c_double()
         check(native.lib().jt_event_elapsed(self.handle, int(start), int(stop), ctypes.byref(out)), "jt_event_elapsed")
         return out.value
+
+    # -- streams: 0 = the context's own; copies / launches / events follow the selected one
+    def reserve_streams(self, n: int) -> None:
+        check(native.lib().jt_streams_reserve(self.handle, int(n)), "jt_streams_reserve")
+
+    def use_stream(self, index: int) -> None:
+        check(native.lib().jt_stream_select(self.handle, int(index)), "jt_stream_select")
+
+    def wait_event(self, index: int) -> None:
+        """The selected stream waits for event ``index`` (recorded on any stream)."""
+        check(native.lib().jt_stream_wait_event(self.handle, int(index)), "jt_stream_wait_event")
 
     def h2d_async(self, dst: "DeviceArray", host: np.ndarray) -> None:
         check(native.lib().jt_h2d_async(self.handle, dst.ptr, host.ctypes.data, host.nbytes), "jt_h2d_async")

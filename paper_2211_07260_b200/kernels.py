@@ -30,7 +30,7 @@ from typing import Any, Mapping
 import numpy as np
 
 from . import native
-from .gpu import GPU, DeviceArray, Kernel, Launch, f32, i32
+from .gpu import GPU, DeviceArray, Kernel, Launch, f32, i32, rows
 from .spaces import KernelConfig, SearchSpace
 
 __all__ = [
@@ -43,6 +43,20 @@ __all__ = [
     "PROBLEMS",
     "make_problem",
 ]
+
+
+@dataclass
+class Strip:
+    """One stage of a host-buffer pipeline: H2D copies, one launch, D2H copies.
+
+    Consecutive strips run on three streams (H2D / compute / D2H) so the
+    copies of strip i+1 and i-1 overlap the launch of strip i.
+    """
+
+    h2d: list  # [(DeviceSlice, host ndarray)]
+    launch: Launch
+    args: list
+    d2h: list  # [(host ndarray, DeviceSlice)]
 
 
 @dataclass
@@ -127,6 +141,10 @@ class KernelProblem:
 
     def fetch_output(self) -> np.ndarray:
         return self.buffers["out"].download()
+
+    def strips(self, config, uploads: Mapping[str, np.ndarray], out: np.ndarray, n: int) -> list[Strip] | None:
+        """Split one host-buffer call into ~n independent strips (None: not splittable)."""
+        return None
 
     # -- compilation ------------------------------------------------------------
     def options(self, config: Mapping[str, Any]) -> list[str]:
@@ -218,10 +236,10 @@ class PnPolyProblem(KernelProblem):
             "VERTICES": self.n_vertices,
         }
 
-    def launch(self, config):
+    def launch(self, config, n_points: int | None = None):
         c = _as_dict(config)
         per_block = c["block_size_x"] * c["tile"]
-        tiles = max(1, math.ceil(self.n_points / per_block))
+        tiles = max(1, math.ceil((self.n_points if n_points is None else n_points) / per_block))
         if c.get("persist", 0):
             sms = self.gpu.sm_count if self.gpu is not None else 148
             resident = max(1, 2048 // c["block_size_x"])  # thread-limited residency per SM
@@ -287,6 +305,21 @@ class PnPolyProblem(KernelProblem):
         b = self.buffers
         packed = b["packed3"] if _as_dict(config).get("asm", 0) >= 3 else b["packed"]
         return [b["out"], b["points"], i32(self.n_points), b[f"edges{m}"], b[f"ybounds{m}"], packed]
+
+    def strips(self, config, uploads, out, n):
+        """Point chunks (multiples of one block's tile): each is an independent launch."""
+        c = _as_dict(config)
+        points, per_block = uploads["points"], c["block_size_x"] * c["tile"]
+        size = max(per_block, math.ceil(self.n_points / n / per_block) * per_block)
+        tail = self.args(config)[3:]
+        plan = []
+        for p0 in range(0, self.n_points, size):
+            p1 = min(self.n_points, p0 + size)
+            dst = rows(self.buffers["points"], p0, p1)
+            res = rows(self.buffers["out"], p0, p1)
+            plan.append(Strip([(dst, points[p0:p1])], self.launch(c, p1 - p0), [res, dst, i32(p1 - p0), *tail],
+                              [(out[p0:p1], res)]))
+        return plan
 
     def bind(self, kernel, config):
         c = _as_dict(config)
@@ -382,6 +415,24 @@ class Conv2DProblem(KernelProblem):
 
     def args(self, config):
         return [self.buffers["out"], self.buffers["image"]]
+
+    def strips(self, config, uploads, out, n):
+        """Bands of output rows (multiples of the block's tile height). Band i uploads only
+        the input rows band i-1 has not (its halo of FH-1 rows is already resident)."""
+        c = _as_dict(config)
+        image, th = uploads["image"], c["block_size_y"] * c["tile_size_y"]
+        band = max(th, math.ceil(self.height / n / th) * th)
+        shape = self.launch(c)
+        plan, uploaded = [], 0
+        for r0 in range(0, self.height, band):
+            r1 = min(self.height, r0 + band)
+            need = r1 + self.fh - 1
+            h2d = [(rows(self.buffers["image"], uploaded, need), image[uploaded:need])]
+            uploaded = need
+            res = rows(self.buffers["out"], r0, r1)
+            launch = Launch((shape.grid[0], (r1 - r0) // th, 1), shape.block)
+            plan.append(Strip(h2d, launch, [res, rows(self.buffers["image"], r0, need)], [(out[r0:r1], res)]))
+        return plan
 
     def bind(self, kernel, config):
         kernel.set_global("d_filter", self.inputs["filter"])

@@ -52,17 +52,60 @@ class Runner:
         self.launch_shape = problem.launch(self.config)
         self.args = problem.args(self.config)
 
-    def run(self, uploads: Mapping[str, np.ndarray], out: np.ndarray | None = None) -> np.ndarray:
-        """H2D each named input buffer, launch once, D2H the output (one stream)."""
+    # event indices below EVENT_BASE are left to callers (bench.py)
+    EVENT_BASE = 64
+    H2D, COMPUTE, D2H = 1, 0, 2
+
+    def run(self, uploads: Mapping[str, np.ndarray], out: np.ndarray | None = None, *,
+            strips: int | None = None) -> np.ndarray:
+        """H2D the inputs, launch, D2H the output.
+
+        With ``strips`` > 1 and a problem that splits (conv2d bands, pnpoly
+        chunks) the call is pipelined over three streams: the H2D of strip
+        i+1 and the D2H of strip i-1 overlap the launch of strip i, so a
+        PCIe-bound call costs about max(H2D, D2H) instead of their sum.
+        """
+        dst = self.problem.buffers["out"]
+        if out is None:
+            out = np.empty(dst.shape, dtype=dst.dtype)
+        if strips and strips > 1:
+            uploads = {k: np.ascontiguousarray(v) for k, v in uploads.items()}
+            plan = self.problem.strips(self.config, uploads, out, strips)
+            if plan:
+                return self._pipelined(plan, out)
+        return self._single(uploads, out)
+
+    def _pipelined(self, plan, out: np.ndarray) -> np.ndarray:
+        gpu, base = self.gpu, self.EVENT_BASE
+        gpu.reserve_streams(3)
+        gpu.reserve_events(base + 2 * len(plan))
+        self.problem.bind(self.kernel, self.config)
+        try:
+            for i, strip in enumerate(plan):
+                gpu.use_stream(self.H2D)
+                for dev, host in strip.h2d:
+                    gpu.h2d_async(dev, host)
+                gpu.record(base + 2 * i)
+                gpu.use_stream(self.COMPUTE)
+                gpu.wait_event(base + 2 * i)
+                gpu.launch(self.kernel, strip.launch, strip.args)
+                gpu.record(base + 2 * i + 1)
+                gpu.use_stream(self.D2H)
+                gpu.wait_event(base + 2 * i + 1)
+                for host, dev in strip.d2h:
+                    gpu.d2h_async(host, dev)
+        finally:
+            gpu.use_stream(self.COMPUTE)
+            gpu.synchronize()
+        return out
+
+    def _single(self, uploads: Mapping[str, np.ndarray], out: np.ndarray) -> np.ndarray:
         gpu = self.gpu
         for name, host in uploads.items():
             gpu.h2d_async(self.problem.buffers[name], np.ascontiguousarray(host))
         self.problem.bind(self.kernel, self.config)
         gpu.launch(self.kernel, self.launch_shape, self.args)
-        dst = self.problem.buffers["out"]
-        if out is None:
-            out = np.empty(dst.shape, dtype=dst.dtype)
-        gpu.d2h_async(out, dst)
+        gpu.d2h_async(out, self.problem.buffers["out"])
         gpu.synchronize()
         return out
 
@@ -84,8 +127,17 @@ def _runner(name: str, key: tuple, config, problem_kwargs: dict, inputs: dict, o
     return hit
 
 
-def conv2d(image: np.ndarray, filt: np.ndarray, *, config=None, out=None, ordinal: int = 0) -> np.ndarray:
-    """Valid-mode 2D correlation of a pre-padded float32 image with a 17x17-style filter."""
+# Measured on the B200 pool's PCIe Gen5 x16 (scripts/e2e_probe.py): concurrent H2D + D2H reach
+# ~90 GB/s combined but every extra strip costs ~25 us of copy-engine turnaround, so a few
+# large strips win: conv2d 4096^2 2.58 -> 1.97 ms at 4 bands, pnpoly 20M 6.30 -> 4.08 ms at 6 chunks.
+CONV2D_STRIPS = 4
+PNPOLY_STRIPS = 6
+
+
+def conv2d(image: np.ndarray, filt: np.ndarray, *, config=None, out=None, ordinal: int = 0,
+           strips: int = CONV2D_STRIPS) -> np.ndarray:
+    """Valid-mode 2D correlation of a pre-padded float32 image with a 17x17-style filter
+    (``strips`` row bands pipelined over copy/compute streams; 1 = one launch)."""
     image = np.asarray(image, dtype=np.float32)
     filt = np.asarray(filt, dtype=np.float32)
     fh, fw = filt.shape
@@ -93,18 +145,20 @@ def conv2d(image: np.ndarray, filt: np.ndarray, *, config=None, out=None, ordina
     r = _runner("conv2d", (h, w, fh, fw), config, {"width": w, "height": h, "fw": fw, "fh": fh},
                 {"image": image, "filter": filt}, ordinal)
     r.problem.inputs["filter"] = filt
-    return r.run({"image": image}, out)
+    return r.run({"image": image}, out, strips=strips)
 
 
-def pnpoly(points: np.ndarray, vx: np.ndarray, vy: np.ndarray, *, config=None, out=None, ordinal: int = 0):
-    """int32 inside/outside bitmap for float32 points (n, 2) against a polygon."""
+def pnpoly(points: np.ndarray, vx: np.ndarray, vy: np.ndarray, *, config=None, out=None, ordinal: int = 0,
+           strips: int = PNPOLY_STRIPS):
+    """int32 inside/outside bitmap for float32 points (n, 2) against a polygon
+    (``strips`` point chunks pipelined over copy/compute streams; 1 = one launch)."""
     points = np.asarray(points, dtype=np.float32)
     vx = np.asarray(vx, dtype=np.float32)
     vy = np.asarray(vy, dtype=np.float32)
     key = (points.shape[0], vx.size, vx.tobytes(), vy.tobytes())
     r = _runner("pnpoly", key, config, {"n_points": points.shape[0], "n_vertices": vx.size},
                 {"points": points, "vx": vx, "vy": vy}, ordinal)
-    return r.run({"points": points}, out)
+    return r.run({"points": points}, out, strips=strips)
 
 
 def sgemm(a: np.ndarray, b: np.ndarray, c: np.ndarray, alpha: float = 1.0, beta: float = 0.0, *, config=None,

@@ -219,11 +219,36 @@ def test_suite_host_api_matches_oracles():
     assert O.sgemm_error(c, O.sgemm(si["a"], si["b"], si["c0"], 1.0, 0.5)) <= O.SGEMM_TOL
 
 
+def test_suite_pipelined_strips_match_single_launch():
+    """Pipelined host calls (bands / chunks over 3 streams) give the single-launch bits."""
+    from paper_2211_07260_b200 import suite
+    from paper_2211_07260_b200.kernels import Conv2DProblem, PnPolyProblem
+
+    ci = Conv2DProblem(width=512, height=496).host_inputs()  # 31 tile rows: ragged last band
+    one = suite.conv2d(ci["image"], ci["filter"], strips=1)
+    for n in (2, 5, 16):
+        np.testing.assert_array_equal(suite.conv2d(ci["image"], ci["filter"], strips=n), one)
+    assert O.conv2d_error(one, O.conv2d(ci["image"], ci["filter"]), ci["image"], ci["filter"]) <= O.CONV_TOL
+    img_pinned = suite.pinned(ci["image"].shape)
+    img_pinned[...] = ci["image"]
+    out_pinned = suite.pinned(one.shape)
+    suite.conv2d(img_pinned, ci["filter"], out=out_pinned, strips=8)
+    np.testing.assert_array_equal(out_pinned, one)
+    pi = PnPolyProblem(n_points=1_000_003).host_inputs()  # not a multiple of any chunk
+    want = O.pnpoly(pi["points"], pi["vx"], pi["vy"], 3)
+    for n in (1, 3, 16):
+        np.testing.assert_array_equal(suite.pnpoly(pi["points"], pi["vx"], pi["vy"], strips=n), want)
+
+
 # -- SGEMM on tcgen05 (TF32, its own tolerance) -------------------------------------------------
 
 
-@pytest.mark.parametrize("cfg", [{"BN": 64, "STAGES": 3}, {"BN": 128, "STAGES": 6}, {"BN": 256, "STAGES": 2},
-                                 {"BN": 256, "STAGES": 4}], ids=str)
+TF32_CONFIGS = [{"BN": 64, "STAGES": 3}, {"BN": 128, "STAGES": 6}, {"BN": 256, "STAGES": 2}, {"BN": 256, "STAGES": 4},
+                {"BN": 128, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 0},
+                {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1}]
+
+
+@pytest.mark.parametrize("cfg", TF32_CONFIGS, ids=str)
 @pytest.mark.parametrize("mnk,beta", [((256, 256, 256), 0.5), ((384, 512, 96), 0.0)])
 def test_sgemm_tf32_tcgen05_within_tf32_tolerance(gpu, cfg, mnk, beta):
     from paper_2211_07260_b200.kernels import SgemmTF32Problem
@@ -249,3 +274,23 @@ def test_sgemm_tf32_full_size(gpu):
     cfg = tuned.best_config("sgemm_tf32") or p.default_config()
     ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
     assert O.sgemm_error(run_once(gpu, p, cfg), ref) <= O.SGEMM_TF32_TOL
+
+
+@pytest.mark.parametrize("cfg", [{"BN": 128, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1},
+                                 {"BN": 256, "STAGES": 3, "PERSIST": 1, "SPLIT_TAIL": 1}], ids=str)
+def test_sgemm_tf32_persistent_split_tail(gpu, cfg):
+    """More tiles than SMs with a short last wave: the tail tiles are split along K over two
+    CTAs and reduced through the workspace. Relaunching must keep the result (the per-tile
+    arrival counters only grow; their parity marks the second finisher)."""
+    from paper_2211_07260_b200.kernels import SgemmTF32Problem
+
+    p = SgemmTF32Problem(m=2304, n=2304, k=256, beta=0.5)
+    p.prepare(gpu)
+    tiles = p.tiles(cfg)
+    assert tiles > gpu.sm_count and 0 < 2 * (tiles % gpu.sm_count) <= gpu.sm_count  # the split path runs
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    first = run_once(gpu, p, cfg)
+    assert O.sgemm_error(first, ref) <= O.SGEMM_TF32_TOL
+    for _ in range(2):
+        np.testing.assert_array_equal(run_once(gpu, p, cfg), first)  # deterministic split-K reduction
+
