@@ -42,6 +42,13 @@
 //                 5: ASM 3 with sign(d_k ^ d_{k-1}) taken from an FMUL (IEEE
 //                 product sign): 4 FMA-pipe + 1 LOP3 per edge-point.
 //                 6: ASM 5 on point pairs (FADD2/FMUL2/FFMA2). Same formulation 3.
+//                 7: ASM 3 with EDGE pairs in the packed f32x2 lanes and the
+//                 point's coordinates as the broadcast scalar operand: per
+//                 point and 2 edges FADD2 d, FFMA2 x, FADD2 e, then 1.5 LOP3
+//                 per edge. The pairs come straight out of LDS.64 of the
+//                 structure-of-arrays table {vy0..3, sl0..3, ic0..3} per 4
+//                 edges, so no register shuffling: 3 issue slots per
+//                 edge-point (1.5 FMA-pipe + 1.5 ALU). Same formulation 3.
 //
 // Edge table (built on the host in float32, see kernels.py): per edge k from
 // vertex k-1 (cyclic) to vertex k, a float4 {vy_k, a, b, c} and a float2
@@ -89,9 +96,20 @@
 #if ASM == 5 && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
 #error "ASM=5 needs POLY_SMEM=1, METHOD=2 and TILE in {2,4,6,8}"
 #endif
+#if ASM == 7 && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
+#error "ASM=7 needs POLY_SMEM=1, METHOD=2 and TILE in {2,4,6,8}"
+#endif
 // packed records {ymin, ymax, slope, icpt} (METHOD 2) padded
 // to a multiple of 4 with never-spanning dummies {+inf, -inf, 0, 0}
 #define NPACK (((VERTICES) + 3) / 4 * 4)
+// ASM 7 table: edges padded to a multiple of 8 (two 4-edge groups per loop
+// trip), 12 floats per 4-edge group
+#define NPAIR8 (((VERTICES) + 7) / 8 * 8)
+#if ASM == 7
+#define TAB_VEC4 (NPAIR8 * 3 / 4)
+#else
+#define TAB_VEC4 NPACK
+#endif
 
 #if ASM == 1 || ASM == 2
 #define PT_X(PY) "fma.rn.f32 x, sl, %" PY ", ic;\n"
@@ -331,29 +349,34 @@
 // Blackwell's packed f32x2 ops (FADD2 / FFMA2, each lane IEEE .rn, no ftz),
 // halving FMA-pipe issue; the sign-bit LOP3s stay per point on the ALU pipe.
 #if TILE == 4
-#define S4_REGS ".reg .b64 vy2, sl2, ic2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1;\n" \
+#define S4_REGS ".reg .b64 pxq0, pyq0, pxq1, pyq1, zz;\n.reg .u32 zr;\n.reg .b64 vy2, sl2, ic2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1;\n" \
     ".reg .b32 lo0, hi0, lo1, hi1, lo2, hi2, t0a, t0b, t1a, t1b, t2a, t2b, t3a, t3b;\n" \
     ".reg .f32 vy, sl, ic, z, vyl;\n"
-#define S4_INIT "mov.b32 vyl, %10;\n" \
+#define S4_INIT "mov.u32 zr, %%tid.y;\n" "cvt.u64.u32 zz, zr;\n" \
+    "xor.b64 pxq0, %4, zz;\n" \
+    "xor.b64 pyq0, %6, zz;\n" \
+    "xor.b64 pxq1, %5, zz;\n" \
+    "xor.b64 pyq1, %7, zz;\n" \
+    "mov.b32 vyl, %10;\n" \
     "mov.b64 vy2, {vyl, vyl};\n" \
-    "sub.rn.f32x2 dp0, %6, vy2;\n" \
-    "sub.rn.f32x2 dp1, %7, vy2;\n"
+    "sub.rn.f32x2 dp0, pyq0, vy2;\n" \
+    "sub.rn.f32x2 dp1, pyq1, vy2;\n"
 #define S4_BODY \
     "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2, {sl, sl};\n" \
     "mov.b64 ic2, {ic, ic};\n" \
-    "sub.rn.f32x2 dA0, %6, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %6, ic2;\n" \
-    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "sub.rn.f32x2 dA0, pyq0, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq0, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {lo0, hi0}, dA0;\n" \
     "mov.b64 {lo1, hi1}, dp0;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
     "lop3.b32 t0a, lo0, lo1, lo2, 0x28;\n" \
     "lop3.b32 t1a, hi0, hi1, hi2, 0x28;\n" \
-    "sub.rn.f32x2 dA1, %7, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %7, ic2;\n" \
-    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "sub.rn.f32x2 dA1, pyq1, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq1, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {lo0, hi0}, dA1;\n" \
     "mov.b64 {lo1, hi1}, dp1;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -363,9 +386,9 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2, {sl, sl};\n" \
     "mov.b64 ic2, {ic, ic};\n" \
-    "sub.rn.f32x2 dB0, %6, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %6, ic2;\n" \
-    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "sub.rn.f32x2 dB0, pyq0, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq0, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {lo0, hi0}, dB0;\n" \
     "mov.b64 {lo1, hi1}, dA0;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -373,9 +396,9 @@
     "lop3.b32 t1b, hi0, hi1, hi2, 0x28;\n" \
     "lop3.b32 %0, %0, t0a, t0b, 0x96;\n" \
     "lop3.b32 %1, %1, t1a, t1b, 0x96;\n" \
-    "sub.rn.f32x2 dB1, %7, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %7, ic2;\n" \
-    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "sub.rn.f32x2 dB1, pyq1, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq1, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {lo0, hi0}, dB1;\n" \
     "mov.b64 {lo1, hi1}, dA1;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -387,17 +410,17 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2, {sl, sl};\n" \
     "mov.b64 ic2, {ic, ic};\n" \
-    "sub.rn.f32x2 dA0, %6, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %6, ic2;\n" \
-    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "sub.rn.f32x2 dA0, pyq0, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq0, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {lo0, hi0}, dA0;\n" \
     "mov.b64 {lo1, hi1}, dB0;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
     "lop3.b32 t0a, lo0, lo1, lo2, 0x28;\n" \
     "lop3.b32 t1a, hi0, hi1, hi2, 0x28;\n" \
-    "sub.rn.f32x2 dA1, %7, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %7, ic2;\n" \
-    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "sub.rn.f32x2 dA1, pyq1, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq1, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {lo0, hi0}, dA1;\n" \
     "mov.b64 {lo1, hi1}, dB1;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -407,9 +430,9 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2, {sl, sl};\n" \
     "mov.b64 ic2, {ic, ic};\n" \
-    "sub.rn.f32x2 dp0, %6, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %6, ic2;\n" \
-    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "sub.rn.f32x2 dp0, pyq0, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq0, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {lo0, hi0}, dp0;\n" \
     "mov.b64 {lo1, hi1}, dA0;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -417,9 +440,9 @@
     "lop3.b32 t1b, hi0, hi1, hi2, 0x28;\n" \
     "lop3.b32 %0, %0, t0a, t0b, 0x96;\n" \
     "lop3.b32 %1, %1, t1a, t1b, 0x96;\n" \
-    "sub.rn.f32x2 dp1, %7, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %7, ic2;\n" \
-    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "sub.rn.f32x2 dp1, pyq1, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq1, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {lo0, hi0}, dp1;\n" \
     "mov.b64 {lo1, hi1}, dA1;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -430,47 +453,56 @@
 #define S4_BASE "8"
 #define S4_SPAN "9"
 #elif TILE == 8
-#define S4_REGS ".reg .b64 vy2, sl2, ic2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3;\n" \
+#define S4_REGS ".reg .b64 pxq0, pyq0, pxq1, pyq1, pxq2, pyq2, pxq3, pyq3, zz;\n.reg .u32 zr;\n.reg .b64 vy2, sl2, ic2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3;\n" \
     ".reg .b32 lo0, hi0, lo1, hi1, lo2, hi2, t0a, t0b, t1a, t1b, t2a, t2b, t3a, t3b, t4a, t4b, t5a, t5b, t6a, t6b, t7a, t7b;\n" \
     ".reg .f32 vy, sl, ic, z, vyl;\n"
-#define S4_INIT "mov.b32 vyl, %18;\n" \
+#define S4_INIT "mov.u32 zr, %%tid.y;\n" "cvt.u64.u32 zz, zr;\n" \
+    "xor.b64 pxq0, %8, zz;\n" \
+    "xor.b64 pyq0, %12, zz;\n" \
+    "xor.b64 pxq1, %9, zz;\n" \
+    "xor.b64 pyq1, %13, zz;\n" \
+    "xor.b64 pxq2, %10, zz;\n" \
+    "xor.b64 pyq2, %14, zz;\n" \
+    "xor.b64 pxq3, %11, zz;\n" \
+    "xor.b64 pyq3, %15, zz;\n" \
+    "mov.b32 vyl, %18;\n" \
     "mov.b64 vy2, {vyl, vyl};\n" \
-    "sub.rn.f32x2 dp0, %12, vy2;\n" \
-    "sub.rn.f32x2 dp1, %13, vy2;\n" \
-    "sub.rn.f32x2 dp2, %14, vy2;\n" \
-    "sub.rn.f32x2 dp3, %15, vy2;\n"
+    "sub.rn.f32x2 dp0, pyq0, vy2;\n" \
+    "sub.rn.f32x2 dp1, pyq1, vy2;\n" \
+    "sub.rn.f32x2 dp2, pyq2, vy2;\n" \
+    "sub.rn.f32x2 dp3, pyq3, vy2;\n"
 #define S4_BODY \
     "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2, {sl, sl};\n" \
     "mov.b64 ic2, {ic, ic};\n" \
-    "sub.rn.f32x2 dA0, %12, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %12, ic2;\n" \
-    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "sub.rn.f32x2 dA0, pyq0, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq0, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {lo0, hi0}, dA0;\n" \
     "mov.b64 {lo1, hi1}, dp0;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
     "lop3.b32 t0a, lo0, lo1, lo2, 0x28;\n" \
     "lop3.b32 t1a, hi0, hi1, hi2, 0x28;\n" \
-    "sub.rn.f32x2 dA1, %13, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %13, ic2;\n" \
-    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "sub.rn.f32x2 dA1, pyq1, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq1, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {lo0, hi0}, dA1;\n" \
     "mov.b64 {lo1, hi1}, dp1;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
     "lop3.b32 t2a, lo0, lo1, lo2, 0x28;\n" \
     "lop3.b32 t3a, hi0, hi1, hi2, 0x28;\n" \
-    "sub.rn.f32x2 dA2, %14, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %14, ic2;\n" \
-    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "sub.rn.f32x2 dA2, pyq2, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq2, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq2, x2;\n" \
     "mov.b64 {lo0, hi0}, dA2;\n" \
     "mov.b64 {lo1, hi1}, dp2;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
     "lop3.b32 t4a, lo0, lo1, lo2, 0x28;\n" \
     "lop3.b32 t5a, hi0, hi1, hi2, 0x28;\n" \
-    "sub.rn.f32x2 dA3, %15, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %15, ic2;\n" \
-    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "sub.rn.f32x2 dA3, pyq3, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq3, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq3, x2;\n" \
     "mov.b64 {lo0, hi0}, dA3;\n" \
     "mov.b64 {lo1, hi1}, dp3;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -480,9 +512,9 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2, {sl, sl};\n" \
     "mov.b64 ic2, {ic, ic};\n" \
-    "sub.rn.f32x2 dB0, %12, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %12, ic2;\n" \
-    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "sub.rn.f32x2 dB0, pyq0, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq0, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {lo0, hi0}, dB0;\n" \
     "mov.b64 {lo1, hi1}, dA0;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -490,9 +522,9 @@
     "lop3.b32 t1b, hi0, hi1, hi2, 0x28;\n" \
     "lop3.b32 %0, %0, t0a, t0b, 0x96;\n" \
     "lop3.b32 %1, %1, t1a, t1b, 0x96;\n" \
-    "sub.rn.f32x2 dB1, %13, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %13, ic2;\n" \
-    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "sub.rn.f32x2 dB1, pyq1, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq1, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {lo0, hi0}, dB1;\n" \
     "mov.b64 {lo1, hi1}, dA1;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -500,9 +532,9 @@
     "lop3.b32 t3b, hi0, hi1, hi2, 0x28;\n" \
     "lop3.b32 %2, %2, t2a, t2b, 0x96;\n" \
     "lop3.b32 %3, %3, t3a, t3b, 0x96;\n" \
-    "sub.rn.f32x2 dB2, %14, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %14, ic2;\n" \
-    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "sub.rn.f32x2 dB2, pyq2, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq2, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq2, x2;\n" \
     "mov.b64 {lo0, hi0}, dB2;\n" \
     "mov.b64 {lo1, hi1}, dA2;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -510,9 +542,9 @@
     "lop3.b32 t5b, hi0, hi1, hi2, 0x28;\n" \
     "lop3.b32 %4, %4, t4a, t4b, 0x96;\n" \
     "lop3.b32 %5, %5, t5a, t5b, 0x96;\n" \
-    "sub.rn.f32x2 dB3, %15, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %15, ic2;\n" \
-    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "sub.rn.f32x2 dB3, pyq3, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq3, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq3, x2;\n" \
     "mov.b64 {lo0, hi0}, dB3;\n" \
     "mov.b64 {lo1, hi1}, dA3;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -524,33 +556,33 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2, {sl, sl};\n" \
     "mov.b64 ic2, {ic, ic};\n" \
-    "sub.rn.f32x2 dA0, %12, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %12, ic2;\n" \
-    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "sub.rn.f32x2 dA0, pyq0, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq0, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {lo0, hi0}, dA0;\n" \
     "mov.b64 {lo1, hi1}, dB0;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
     "lop3.b32 t0a, lo0, lo1, lo2, 0x28;\n" \
     "lop3.b32 t1a, hi0, hi1, hi2, 0x28;\n" \
-    "sub.rn.f32x2 dA1, %13, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %13, ic2;\n" \
-    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "sub.rn.f32x2 dA1, pyq1, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq1, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {lo0, hi0}, dA1;\n" \
     "mov.b64 {lo1, hi1}, dB1;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
     "lop3.b32 t2a, lo0, lo1, lo2, 0x28;\n" \
     "lop3.b32 t3a, hi0, hi1, hi2, 0x28;\n" \
-    "sub.rn.f32x2 dA2, %14, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %14, ic2;\n" \
-    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "sub.rn.f32x2 dA2, pyq2, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq2, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq2, x2;\n" \
     "mov.b64 {lo0, hi0}, dA2;\n" \
     "mov.b64 {lo1, hi1}, dB2;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
     "lop3.b32 t4a, lo0, lo1, lo2, 0x28;\n" \
     "lop3.b32 t5a, hi0, hi1, hi2, 0x28;\n" \
-    "sub.rn.f32x2 dA3, %15, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %15, ic2;\n" \
-    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "sub.rn.f32x2 dA3, pyq3, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq3, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq3, x2;\n" \
     "mov.b64 {lo0, hi0}, dA3;\n" \
     "mov.b64 {lo1, hi1}, dB3;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -560,9 +592,9 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2, {sl, sl};\n" \
     "mov.b64 ic2, {ic, ic};\n" \
-    "sub.rn.f32x2 dp0, %12, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %12, ic2;\n" \
-    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "sub.rn.f32x2 dp0, pyq0, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq0, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {lo0, hi0}, dp0;\n" \
     "mov.b64 {lo1, hi1}, dA0;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -570,9 +602,9 @@
     "lop3.b32 t1b, hi0, hi1, hi2, 0x28;\n" \
     "lop3.b32 %0, %0, t0a, t0b, 0x96;\n" \
     "lop3.b32 %1, %1, t1a, t1b, 0x96;\n" \
-    "sub.rn.f32x2 dp1, %13, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %13, ic2;\n" \
-    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "sub.rn.f32x2 dp1, pyq1, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq1, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {lo0, hi0}, dp1;\n" \
     "mov.b64 {lo1, hi1}, dA1;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -580,9 +612,9 @@
     "lop3.b32 t3b, hi0, hi1, hi2, 0x28;\n" \
     "lop3.b32 %2, %2, t2a, t2b, 0x96;\n" \
     "lop3.b32 %3, %3, t3a, t3b, 0x96;\n" \
-    "sub.rn.f32x2 dp2, %14, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %14, ic2;\n" \
-    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "sub.rn.f32x2 dp2, pyq2, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq2, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq2, x2;\n" \
     "mov.b64 {lo0, hi0}, dp2;\n" \
     "mov.b64 {lo1, hi1}, dA2;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -590,9 +622,9 @@
     "lop3.b32 t5b, hi0, hi1, hi2, 0x28;\n" \
     "lop3.b32 %4, %4, t4a, t4b, 0x96;\n" \
     "lop3.b32 %5, %5, t5a, t5b, 0x96;\n" \
-    "sub.rn.f32x2 dp3, %15, vy2;\n" \
-    "fma.rn.f32x2 x2, sl2, %15, ic2;\n" \
-    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "sub.rn.f32x2 dp3, pyq3, vy2;\n" \
+    "fma.rn.f32x2 x2, sl2, pyq3, ic2;\n" \
+    "sub.rn.f32x2 e2, pxq3, x2;\n" \
     "mov.b64 {lo0, hi0}, dp3;\n" \
     "mov.b64 {lo1, hi1}, dA3;\n" \
     "mov.b64 {lo2, hi2}, e2;\n" \
@@ -607,6 +639,122 @@
     "{\n" S4_REGS ".reg .u32 ptr, end;\n.reg .pred s;\n" S4_INIT                       \
     "mov.u32 ptr, %" S4_BASE ";\nadd.u32 end, ptr, %" S4_SPAN ";\n" "PNPOLY_S4_LOOP:\n" \
     S4_BODY "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_S4_LOOP;\n}\n"
+#endif
+#if ASM == 7
+// One 4-edge group for one point. vyA = {vy0, vy1}, vyB = {vy2, vy3} (same
+// for sl / ic) come from LDS.64, so every f32x2 operand is an aligned pair;
+// the point's px / py enter as broadcast scalars. PREV holds py - vy of the
+// vertex before this group; LAST receives py - vy3 (chain to the next group).
+// The six FMA-pipe ops of point t+1 are interleaved one-to-one with the six
+// ALU LOP3s of point t (register set S = t % 2), so every warp's stream
+// alternates pipes instead of bursting one pipe at a time.
+#define S7_F1(S, PX, PY) "mov.b64 py2" S ", {%" PY ", %" PY "};\n" "mov.b64 px2" S ", {%" PX ", %" PX "};\n" \
+                         "sub.rn.f32x2 dA" S ", py2" S ", vyA;\n"
+#define S7_F2(S) "fma.rn.f32x2 xA" S ", slA, py2" S ", icA;\n"
+#define S7_F3(S) "sub.rn.f32x2 eA" S ", px2" S ", xA" S ";\n"
+#define S7_F4(S) "sub.rn.f32x2 dB" S ", py2" S ", vyB;\n"
+#define S7_F5(S) "fma.rn.f32x2 xB" S ", slB, py2" S ", icB;\n"
+#define S7_F6(S, LAST) "sub.rn.f32x2 eB" S ", px2" S ", xB" S ";\n"                                    \
+    "mov.b64 {d0" S ", d1" S "}, dA" S ";\n" "mov.b64 {d2" S ", " LAST "}, dB" S ";\n"                   \
+    "mov.b64 {e0" S ", e1" S "}, eA" S ";\n" "mov.b64 {e2" S ", e3" S "}, eB" S ";\n"
+#define S7_L1(S, PREV) "lop3.b32 t0" S ", d0" S ", " PREV ", e0" S ", 0x28;\n"
+#define S7_L2(S) "lop3.b32 t1" S ", d1" S ", d0" S ", e1" S ", 0x28;\n"
+#define S7_L3(S, ACC) "lop3.b32 %" ACC ", %" ACC ", t0" S ", t1" S ", 0x96;\n"
+#define S7_L4(S) "lop3.b32 t0" S ", d2" S ", d1" S ", e2" S ", 0x28;\n"
+#define S7_L5(S, LAST) "lop3.b32 t1" S ", " LAST ", d2" S ", e3" S ", 0x28;\n"
+#define S7_HEAD(S, PX, PY, LAST) S7_F1(S, PX, PY) S7_F2(S) S7_F3(S) S7_F4(S) S7_F5(S) S7_F6(S, LAST)
+#define S7_TAIL(S, ACC, PREV, LAST) S7_L1(S, PREV) S7_L2(S) S7_L3(S, ACC) S7_L4(S) S7_L5(S, LAST) S7_L3(S, ACC)
+#define S7_STEP(NS, NPX, NPY, NLAST, CS, CACC, CPREV, CLAST)                                         \
+    S7_F1(NS, NPX, NPY) S7_L1(CS, CPREV) S7_F2(NS) S7_L2(CS) S7_F3(NS) S7_L3(CS, CACC)               \
+    S7_F4(NS) S7_L4(CS) S7_F5(NS) S7_L5(CS, CLAST) S7_F6(NS, NLAST) S7_L3(CS, CACC)
+#define S7_LOAD(OFF)                                            \
+    "ld.shared.v2.b64 {vyA, vyB}, [ptr+" OFF "];\n"             \
+    "ld.shared.v2.b64 {slA, slB}, [ptr+" OFF "+16];\n"          \
+    "ld.shared.v2.b64 {icA, icB}, [ptr+" OFF "+32];\n"
+#define S7_INIT1(I, PY, VL) "sub.rn.f32 dp" #I ", %" PY ", %" VL ";\n"
+#if TILE == 2
+#define S7_GROUP_P \
+    S7_HEAD("0", "2", "4", "dq0") \
+    S7_STEP("1", "3", "5", "dq1", "0", "0", "dp0", "dq0") \
+    S7_TAIL("1", "1", "dp1", "dq1")
+#define S7_GROUP_Q \
+    S7_HEAD("0", "2", "4", "dp0") \
+    S7_STEP("1", "3", "5", "dp1", "0", "0", "dq0", "dp0") \
+    S7_TAIL("1", "1", "dq1", "dp1")
+#define S7_INIT S7_INIT1(0, "4", "8") S7_INIT1(1, "5", "8")
+#define S7_BASE "6"
+#define S7_SPAN "7"
+#elif TILE == 4
+#define S7_GROUP_P \
+    S7_HEAD("0", "4", "8", "dq0") \
+    S7_STEP("1", "5", "9", "dq1", "0", "0", "dp0", "dq0") \
+    S7_STEP("0", "6", "10", "dq2", "1", "1", "dp1", "dq1") \
+    S7_STEP("1", "7", "11", "dq3", "0", "2", "dp2", "dq2") \
+    S7_TAIL("1", "3", "dp3", "dq3")
+#define S7_GROUP_Q \
+    S7_HEAD("0", "4", "8", "dp0") \
+    S7_STEP("1", "5", "9", "dp1", "0", "0", "dq0", "dp0") \
+    S7_STEP("0", "6", "10", "dp2", "1", "1", "dq1", "dp1") \
+    S7_STEP("1", "7", "11", "dp3", "0", "2", "dq2", "dp2") \
+    S7_TAIL("1", "3", "dq3", "dp3")
+#define S7_INIT S7_INIT1(0, "8", "14") S7_INIT1(1, "9", "14") S7_INIT1(2, "10", "14") S7_INIT1(3, "11", "14")
+#define S7_BASE "12"
+#define S7_SPAN "13"
+#elif TILE == 6
+#define S7_GROUP_P \
+    S7_HEAD("0", "6", "12", "dq0") \
+    S7_STEP("1", "7", "13", "dq1", "0", "0", "dp0", "dq0") \
+    S7_STEP("0", "8", "14", "dq2", "1", "1", "dp1", "dq1") \
+    S7_STEP("1", "9", "15", "dq3", "0", "2", "dp2", "dq2") \
+    S7_STEP("0", "10", "16", "dq4", "1", "3", "dp3", "dq3") \
+    S7_STEP("1", "11", "17", "dq5", "0", "4", "dp4", "dq4") \
+    S7_TAIL("1", "5", "dp5", "dq5")
+#define S7_GROUP_Q \
+    S7_HEAD("0", "6", "12", "dp0") \
+    S7_STEP("1", "7", "13", "dp1", "0", "0", "dq0", "dp0") \
+    S7_STEP("0", "8", "14", "dp2", "1", "1", "dq1", "dp1") \
+    S7_STEP("1", "9", "15", "dp3", "0", "2", "dq2", "dp2") \
+    S7_STEP("0", "10", "16", "dp4", "1", "3", "dq3", "dp3") \
+    S7_STEP("1", "11", "17", "dp5", "0", "4", "dq4", "dp4") \
+    S7_TAIL("1", "5", "dq5", "dp5")
+#define S7_INIT S7_INIT1(0, "12", "20") S7_INIT1(1, "13", "20") S7_INIT1(2, "14", "20") S7_INIT1(3, "15", "20") S7_INIT1(4, "16", "20") S7_INIT1(5, "17", "20")
+#define S7_BASE "18"
+#define S7_SPAN "19"
+#elif TILE == 8
+#define S7_GROUP_P \
+    S7_HEAD("0", "8", "16", "dq0") \
+    S7_STEP("1", "9", "17", "dq1", "0", "0", "dp0", "dq0") \
+    S7_STEP("0", "10", "18", "dq2", "1", "1", "dp1", "dq1") \
+    S7_STEP("1", "11", "19", "dq3", "0", "2", "dp2", "dq2") \
+    S7_STEP("0", "12", "20", "dq4", "1", "3", "dp3", "dq3") \
+    S7_STEP("1", "13", "21", "dq5", "0", "4", "dp4", "dq4") \
+    S7_STEP("0", "14", "22", "dq6", "1", "5", "dp5", "dq5") \
+    S7_STEP("1", "15", "23", "dq7", "0", "6", "dp6", "dq6") \
+    S7_TAIL("1", "7", "dp7", "dq7")
+#define S7_GROUP_Q \
+    S7_HEAD("0", "8", "16", "dp0") \
+    S7_STEP("1", "9", "17", "dp1", "0", "0", "dq0", "dp0") \
+    S7_STEP("0", "10", "18", "dp2", "1", "1", "dq1", "dp1") \
+    S7_STEP("1", "11", "19", "dp3", "0", "2", "dq2", "dp2") \
+    S7_STEP("0", "12", "20", "dp4", "1", "3", "dq3", "dp3") \
+    S7_STEP("1", "13", "21", "dp5", "0", "4", "dq4", "dp4") \
+    S7_STEP("0", "14", "22", "dp6", "1", "5", "dq5", "dp5") \
+    S7_STEP("1", "15", "23", "dp7", "0", "6", "dq6", "dp6") \
+    S7_TAIL("1", "7", "dq7", "dp7")
+#define S7_INIT S7_INIT1(0, "16", "26") S7_INIT1(1, "17", "26") S7_INIT1(2, "18", "26") S7_INIT1(3, "19", "26") S7_INIT1(4, "20", "26") S7_INIT1(5, "21", "26") S7_INIT1(6, "22", "26") S7_INIT1(7, "23", "26")
+#define S7_BASE "24"
+#define S7_SPAN "25"
+#endif
+#define S7_SETS ".reg .b64 py20, px20, dA0, dB0, xA0, xB0, eA0, eB0;\n" ".reg .b32 d00, d10, d20, e00, e10, e20, e30, t00, t10;\n" ".reg .b64 py21, px21, dA1, dB1, xA1, xB1, eA1, eB1;\n" ".reg .b32 d01, d11, d21, e01, e11, e21, e31, t01, t11;\n" ".reg .b64 py22, px22, dA2, dB2, xA2, xB2, eA2, eB2;\n" ".reg .b32 d02, d12, d22, e02, e12, e22, e32, t02, t12;\n" ".reg .b64 py23, px23, dA3, dB3, xA3, xB3, eA3, eB3;\n" ".reg .b32 d03, d13, d23, e03, e13, e23, e33, t03, t13;\n" ".reg .b64 py24, px24, dA4, dB4, xA4, xB4, eA4, eB4;\n" ".reg .b32 d04, d14, d24, e04, e14, e24, e34, t04, t14;\n" ".reg .b64 py25, px25, dA5, dB5, xA5, xB5, eA5, eB5;\n" ".reg .b32 d05, d15, d25, e05, e15, e25, e35, t05, t15;\n" ".reg .b64 py26, px26, dA6, dB6, xA6, xB6, eA6, eB6;\n" ".reg .b32 d06, d16, d26, e06, e16, e26, e36, t06, t16;\n" ".reg .b64 py27, px27, dA7, dB7, xA7, xB7, eA7, eB7;\n" ".reg .b32 d07, d17, d27, e07, e17, e27, e37, t07, t17;\n" 
+#define S7_ASM                                                                                   \
+    "{\n"                                                                                        \
+    ".reg .b64 vyA, vyB, slA, slB, icA, icB;\n"                                                 \
+    S7_SETS                                                                                      \
+    ".reg .b32 dp0, dp1, dp2, dp3, dp4, dp5, dp6, dp7, dq0, dq1, dq2, dq3, dq4, dq5, dq6, dq7;\n" \
+    ".reg .u32 ptr, end;\n.reg .pred s;\n" S7_INIT                                               \
+    "mov.u32 ptr, %" S7_BASE ";\nadd.u32 end, ptr, %" S7_SPAN ";\n"                              \
+    "PNPOLY_S7_LOOP:\n" S7_LOAD("0") S7_GROUP_P S7_LOAD("48") S7_GROUP_Q                         \
+    "add.u32 ptr, ptr, 96;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_S7_LOOP;\n}\n"
 #endif
 #if ASM == 5
 // ASM 3 with the sign XOR of consecutive (py - vy) moved to the FMA pipe:
@@ -1081,30 +1229,35 @@
 #if ASM == 6
 // ASM 5 on point pairs with packed f32x2 (FADD2 / FMUL2 / FFMA2).
 #if TILE == 4
-#define S6_REGS ".reg .b64 sl2b, ic2b, vy2, m2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1;\n" \
+#define S6_REGS ".reg .b64 pxq0, pyq0, pxq1, pyq1, zz;\n.reg .u32 zr;\n.reg .b64 sl2b, ic2b, vy2, m2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1;\n" \
     ".reg .b32 mlo, mhi, elo, ehi;\n" \
     ".reg .f32 vy, sl, ic, z, vyl;\n"
-#define S6_INIT "mov.b32 vyl, %10;\n" \
+#define S6_INIT "mov.u32 zr, %%tid.y;\n" "cvt.u64.u32 zz, zr;\n" \
+    "xor.b64 pxq0, %4, zz;\n" \
+    "xor.b64 pyq0, %6, zz;\n" \
+    "xor.b64 pxq1, %5, zz;\n" \
+    "xor.b64 pyq1, %7, zz;\n" \
+    "mov.b32 vyl, %10;\n" \
     "mov.b64 vy2, {vyl, vyl};\n" \
-    "sub.rn.f32x2 dp0, %6, vy2;\n" \
-    "sub.rn.f32x2 dp1, %7, vy2;\n"
+    "sub.rn.f32x2 dp0, pyq0, vy2;\n" \
+    "sub.rn.f32x2 dp1, pyq1, vy2;\n"
 #define S6_BODY \
     "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2b, {sl, sl};\n" \
     "mov.b64 ic2b, {ic, ic};\n" \
-    "sub.rn.f32x2 dA0, %6, vy2;\n" \
+    "sub.rn.f32x2 dA0, pyq0, vy2;\n" \
     "mul.rn.f32x2 m2, dA0, dp0;\n" \
-    "fma.rn.f32x2 x2, sl2b, %6, ic2b;\n" \
-    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq0, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
     "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dA1, %7, vy2;\n" \
+    "sub.rn.f32x2 dA1, pyq1, vy2;\n" \
     "mul.rn.f32x2 m2, dA1, dp1;\n" \
-    "fma.rn.f32x2 x2, sl2b, %7, ic2b;\n" \
-    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq1, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
@@ -1113,18 +1266,18 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2b, {sl, sl};\n" \
     "mov.b64 ic2b, {ic, ic};\n" \
-    "sub.rn.f32x2 dB0, %6, vy2;\n" \
+    "sub.rn.f32x2 dB0, pyq0, vy2;\n" \
     "mul.rn.f32x2 m2, dB0, dA0;\n" \
-    "fma.rn.f32x2 x2, sl2b, %6, ic2b;\n" \
-    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq0, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
     "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dB1, %7, vy2;\n" \
+    "sub.rn.f32x2 dB1, pyq1, vy2;\n" \
     "mul.rn.f32x2 m2, dB1, dA1;\n" \
-    "fma.rn.f32x2 x2, sl2b, %7, ic2b;\n" \
-    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq1, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
@@ -1133,18 +1286,18 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2b, {sl, sl};\n" \
     "mov.b64 ic2b, {ic, ic};\n" \
-    "sub.rn.f32x2 dA0, %6, vy2;\n" \
+    "sub.rn.f32x2 dA0, pyq0, vy2;\n" \
     "mul.rn.f32x2 m2, dA0, dB0;\n" \
-    "fma.rn.f32x2 x2, sl2b, %6, ic2b;\n" \
-    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq0, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
     "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dA1, %7, vy2;\n" \
+    "sub.rn.f32x2 dA1, pyq1, vy2;\n" \
     "mul.rn.f32x2 m2, dA1, dB1;\n" \
-    "fma.rn.f32x2 x2, sl2b, %7, ic2b;\n" \
-    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq1, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
@@ -1153,18 +1306,18 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2b, {sl, sl};\n" \
     "mov.b64 ic2b, {ic, ic};\n" \
-    "sub.rn.f32x2 dp0, %6, vy2;\n" \
+    "sub.rn.f32x2 dp0, pyq0, vy2;\n" \
     "mul.rn.f32x2 m2, dp0, dA0;\n" \
-    "fma.rn.f32x2 x2, sl2b, %6, ic2b;\n" \
-    "sub.rn.f32x2 e2, %4, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq0, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
     "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dp1, %7, vy2;\n" \
+    "sub.rn.f32x2 dp1, pyq1, vy2;\n" \
     "mul.rn.f32x2 m2, dp1, dA1;\n" \
-    "fma.rn.f32x2 x2, sl2b, %7, ic2b;\n" \
-    "sub.rn.f32x2 e2, %5, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq1, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
@@ -1172,48 +1325,57 @@
 #define S6_BASE "8"
 #define S6_SPAN "9"
 #elif TILE == 8
-#define S6_REGS ".reg .b64 sl2b, ic2b, vy2, m2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3;\n" \
+#define S6_REGS ".reg .b64 pxq0, pyq0, pxq1, pyq1, pxq2, pyq2, pxq3, pyq3, zz;\n.reg .u32 zr;\n.reg .b64 sl2b, ic2b, vy2, m2, x2, e2, dp0, dA0, dB0, dp1, dA1, dB1, dp2, dA2, dB2, dp3, dA3, dB3;\n" \
     ".reg .b32 mlo, mhi, elo, ehi;\n" \
     ".reg .f32 vy, sl, ic, z, vyl;\n"
-#define S6_INIT "mov.b32 vyl, %18;\n" \
+#define S6_INIT "mov.u32 zr, %%tid.y;\n" "cvt.u64.u32 zz, zr;\n" \
+    "xor.b64 pxq0, %8, zz;\n" \
+    "xor.b64 pyq0, %12, zz;\n" \
+    "xor.b64 pxq1, %9, zz;\n" \
+    "xor.b64 pyq1, %13, zz;\n" \
+    "xor.b64 pxq2, %10, zz;\n" \
+    "xor.b64 pyq2, %14, zz;\n" \
+    "xor.b64 pxq3, %11, zz;\n" \
+    "xor.b64 pyq3, %15, zz;\n" \
+    "mov.b32 vyl, %18;\n" \
     "mov.b64 vy2, {vyl, vyl};\n" \
-    "sub.rn.f32x2 dp0, %12, vy2;\n" \
-    "sub.rn.f32x2 dp1, %13, vy2;\n" \
-    "sub.rn.f32x2 dp2, %14, vy2;\n" \
-    "sub.rn.f32x2 dp3, %15, vy2;\n"
+    "sub.rn.f32x2 dp0, pyq0, vy2;\n" \
+    "sub.rn.f32x2 dp1, pyq1, vy2;\n" \
+    "sub.rn.f32x2 dp2, pyq2, vy2;\n" \
+    "sub.rn.f32x2 dp3, pyq3, vy2;\n"
 #define S6_BODY \
     "ld.shared.v4.f32 {vy, sl, ic, z}, [ptr+0];\n" \
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2b, {sl, sl};\n" \
     "mov.b64 ic2b, {ic, ic};\n" \
-    "sub.rn.f32x2 dA0, %12, vy2;\n" \
+    "sub.rn.f32x2 dA0, pyq0, vy2;\n" \
     "mul.rn.f32x2 m2, dA0, dp0;\n" \
-    "fma.rn.f32x2 x2, sl2b, %12, ic2b;\n" \
-    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq0, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
     "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dA1, %13, vy2;\n" \
+    "sub.rn.f32x2 dA1, pyq1, vy2;\n" \
     "mul.rn.f32x2 m2, dA1, dp1;\n" \
-    "fma.rn.f32x2 x2, sl2b, %13, ic2b;\n" \
-    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq1, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
     "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dA2, %14, vy2;\n" \
+    "sub.rn.f32x2 dA2, pyq2, vy2;\n" \
     "mul.rn.f32x2 m2, dA2, dp2;\n" \
-    "fma.rn.f32x2 x2, sl2b, %14, ic2b;\n" \
-    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq2, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq2, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %4, %4, mlo, elo, 0x78;\n" \
     "lop3.b32 %5, %5, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dA3, %15, vy2;\n" \
+    "sub.rn.f32x2 dA3, pyq3, vy2;\n" \
     "mul.rn.f32x2 m2, dA3, dp3;\n" \
-    "fma.rn.f32x2 x2, sl2b, %15, ic2b;\n" \
-    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq3, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq3, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %6, %6, mlo, elo, 0x78;\n" \
@@ -1222,34 +1384,34 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2b, {sl, sl};\n" \
     "mov.b64 ic2b, {ic, ic};\n" \
-    "sub.rn.f32x2 dB0, %12, vy2;\n" \
+    "sub.rn.f32x2 dB0, pyq0, vy2;\n" \
     "mul.rn.f32x2 m2, dB0, dA0;\n" \
-    "fma.rn.f32x2 x2, sl2b, %12, ic2b;\n" \
-    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq0, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
     "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dB1, %13, vy2;\n" \
+    "sub.rn.f32x2 dB1, pyq1, vy2;\n" \
     "mul.rn.f32x2 m2, dB1, dA1;\n" \
-    "fma.rn.f32x2 x2, sl2b, %13, ic2b;\n" \
-    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq1, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
     "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dB2, %14, vy2;\n" \
+    "sub.rn.f32x2 dB2, pyq2, vy2;\n" \
     "mul.rn.f32x2 m2, dB2, dA2;\n" \
-    "fma.rn.f32x2 x2, sl2b, %14, ic2b;\n" \
-    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq2, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq2, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %4, %4, mlo, elo, 0x78;\n" \
     "lop3.b32 %5, %5, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dB3, %15, vy2;\n" \
+    "sub.rn.f32x2 dB3, pyq3, vy2;\n" \
     "mul.rn.f32x2 m2, dB3, dA3;\n" \
-    "fma.rn.f32x2 x2, sl2b, %15, ic2b;\n" \
-    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq3, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq3, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %6, %6, mlo, elo, 0x78;\n" \
@@ -1258,34 +1420,34 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2b, {sl, sl};\n" \
     "mov.b64 ic2b, {ic, ic};\n" \
-    "sub.rn.f32x2 dA0, %12, vy2;\n" \
+    "sub.rn.f32x2 dA0, pyq0, vy2;\n" \
     "mul.rn.f32x2 m2, dA0, dB0;\n" \
-    "fma.rn.f32x2 x2, sl2b, %12, ic2b;\n" \
-    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq0, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
     "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dA1, %13, vy2;\n" \
+    "sub.rn.f32x2 dA1, pyq1, vy2;\n" \
     "mul.rn.f32x2 m2, dA1, dB1;\n" \
-    "fma.rn.f32x2 x2, sl2b, %13, ic2b;\n" \
-    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq1, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
     "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dA2, %14, vy2;\n" \
+    "sub.rn.f32x2 dA2, pyq2, vy2;\n" \
     "mul.rn.f32x2 m2, dA2, dB2;\n" \
-    "fma.rn.f32x2 x2, sl2b, %14, ic2b;\n" \
-    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq2, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq2, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %4, %4, mlo, elo, 0x78;\n" \
     "lop3.b32 %5, %5, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dA3, %15, vy2;\n" \
+    "sub.rn.f32x2 dA3, pyq3, vy2;\n" \
     "mul.rn.f32x2 m2, dA3, dB3;\n" \
-    "fma.rn.f32x2 x2, sl2b, %15, ic2b;\n" \
-    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq3, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq3, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %6, %6, mlo, elo, 0x78;\n" \
@@ -1294,34 +1456,34 @@
     "mov.b64 vy2, {vy, vy};\n" \
     "mov.b64 sl2b, {sl, sl};\n" \
     "mov.b64 ic2b, {ic, ic};\n" \
-    "sub.rn.f32x2 dp0, %12, vy2;\n" \
+    "sub.rn.f32x2 dp0, pyq0, vy2;\n" \
     "mul.rn.f32x2 m2, dp0, dA0;\n" \
-    "fma.rn.f32x2 x2, sl2b, %12, ic2b;\n" \
-    "sub.rn.f32x2 e2, %8, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq0, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq0, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %0, %0, mlo, elo, 0x78;\n" \
     "lop3.b32 %1, %1, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dp1, %13, vy2;\n" \
+    "sub.rn.f32x2 dp1, pyq1, vy2;\n" \
     "mul.rn.f32x2 m2, dp1, dA1;\n" \
-    "fma.rn.f32x2 x2, sl2b, %13, ic2b;\n" \
-    "sub.rn.f32x2 e2, %9, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq1, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq1, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %2, %2, mlo, elo, 0x78;\n" \
     "lop3.b32 %3, %3, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dp2, %14, vy2;\n" \
+    "sub.rn.f32x2 dp2, pyq2, vy2;\n" \
     "mul.rn.f32x2 m2, dp2, dA2;\n" \
-    "fma.rn.f32x2 x2, sl2b, %14, ic2b;\n" \
-    "sub.rn.f32x2 e2, %10, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq2, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq2, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %4, %4, mlo, elo, 0x78;\n" \
     "lop3.b32 %5, %5, mhi, ehi, 0x78;\n" \
-    "sub.rn.f32x2 dp3, %15, vy2;\n" \
+    "sub.rn.f32x2 dp3, pyq3, vy2;\n" \
     "mul.rn.f32x2 m2, dp3, dA3;\n" \
-    "fma.rn.f32x2 x2, sl2b, %15, ic2b;\n" \
-    "sub.rn.f32x2 e2, %11, x2;\n" \
+    "fma.rn.f32x2 x2, sl2b, pyq3, ic2b;\n" \
+    "sub.rn.f32x2 e2, pxq3, x2;\n" \
     "mov.b64 {mlo, mhi}, m2;\n" \
     "mov.b64 {elo, ehi}, e2;\n" \
     "lop3.b32 %6, %6, mlo, elo, 0x78;\n" \
@@ -1356,8 +1518,8 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #if ASM
     // packed records, NPACK entries (ASM 1/2: {ymin, ymax, slope, icpt};
     // ASM 3: {vy_k, slope, icpt, 0})
-    __shared__ __align__(16) float4 s_packed[NPACK];
-    for (int k = threadIdx.x; k < NPACK; k += BLOCK_SIZE_X) s_packed[k] = g_packed[k];
+    __shared__ __align__(16) float4 s_packed[TAB_VEC4];
+    for (int k = threadIdx.x; k < TAB_VEC4; k += BLOCK_SIZE_X) s_packed[k] = g_packed[k];
     __syncthreads();
 #elif POLY_SMEM
     __shared__ float4 s_edges[VERTICES];
@@ -1451,11 +1613,13 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
         for (int t = 0; t < TILE; ++t) inside[t] = acc[t] >> 31;
     }
-#elif ASM == 3 || ASM == 5
+#elif ASM == 3 || ASM == 5 || ASM == 7
 #if ASM == 3
 #define SS_ASM S3_ASM
-#else
+#elif ASM == 5
 #define SS_ASM S5_ASM
+#else
+#define SS_ASM S7_ASM
 #endif
     unsigned inside[TILE];
     {
@@ -1463,8 +1627,13 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
         for (int t = 0; t < TILE; ++t) acc[t] = 0u;
         const unsigned sbase = (unsigned)__cvta_generic_to_shared(s_packed);
+#if ASM == 7
+        const unsigned span = NPAIR8 * 12u;  // 4-edge groups of 12 floats
+        const float vy_last = reinterpret_cast<const float *>(s_packed)[(VERTICES - 1) / 4 * 12 + (VERTICES - 1) % 4];
+#else
         const unsigned span = NPACK * 16u;
         const float vy_last = s_packed[VERTICES - 1].x;
+#endif
 #if TILE == 2
         asm volatile(SS_ASM : "+r"(acc[0]), "+r"(acc[1]) : "f"(px[0]), "f"(px[1]), "f"(py[0]), "f"(py[1]),
                      "r"(sbase), "r"(span), "f"(vy_last));

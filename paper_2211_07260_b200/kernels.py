@@ -199,7 +199,7 @@ class PnPolyProblem(KernelProblem):
             "method": [0, 1, 2],
             "between": [0, 1],
             "poly_smem": [0, 1],
-            "asm": [0, 1, 2, 3, 4, 5, 6],
+            "asm": [0, 1, 2, 3, 4, 5, 6, 7],
             "persist": [0, 1],
         }
 
@@ -213,8 +213,8 @@ class PnPolyProblem(KernelProblem):
         ]
 
     def default_config(self):
-        return {"block_size_x": 256, "tile": 8, "vec": 2, "method": 2, "between": 0, "poly_smem": 1, "asm": 4,
-                "persist": 1}
+        return {"block_size_x": 256, "tile": 8, "vec": 2, "method": 2, "between": 0, "poly_smem": 1, "asm": 7,
+                "persist": 0}
 
     @staticmethod
     def formula(config) -> int:
@@ -269,6 +269,7 @@ class PnPolyProblem(KernelProblem):
             self.buffers[f"ybounds{m}"] = gpu.array(yb)
         self.buffers["packed"] = gpu.array(self.packed_table())
         self.buffers["packed3"] = gpu.array(self.chain_table())
+        self.buffers["packed7"] = gpu.array(self.pair_table())
 
     def chain_table(self) -> np.ndarray:
         """{vy_k, slope, icpt, 0} per edge for the sign-bit chain (ASM=3),
@@ -283,6 +284,21 @@ class PnPolyProblem(KernelProblem):
         table[:n, 1] = edges[:, 2]
         table[:n, 2] = edges[:, 1]
         return table
+
+    def pair_table(self) -> np.ndarray:
+        """ASM=7 structure-of-arrays chain table: per group of 4 edges the 12
+        floats {vy0..3, slope0..3, icpt0..3}, edges padded to a multiple of 8
+        with the chain's zero-length continuation (vy of the last vertex,
+        slope = icpt = 0). Pure repacking of chain_table()."""
+        edges, _ = self._tables[2]
+        n = edges.shape[0]
+        n8 = (n + 7) // 8 * 8
+        chain = np.zeros((n8, 3), dtype=np.float32)
+        chain[:, 0] = edges[n - 1, 0]
+        chain[:n, 0] = edges[:, 0]
+        chain[:n, 1] = edges[:, 2]
+        chain[:n, 2] = edges[:, 1]
+        return np.ascontiguousarray(chain.reshape(n8 // 4, 4, 3).transpose(0, 2, 1)).reshape(-1)
 
     def packed_table(self) -> np.ndarray:
         """{ymin, ymax, slope, icpt} per edge (METHOD 2), padded to a multiple
@@ -303,7 +319,8 @@ class PnPolyProblem(KernelProblem):
     def args(self, config):
         m = _as_dict(config)["method"]
         b = self.buffers
-        packed = b["packed3"] if _as_dict(config).get("asm", 0) >= 3 else b["packed"]
+        asm = _as_dict(config).get("asm", 0)
+        packed = b["packed7"] if asm == 7 else b["packed3"] if asm >= 3 else b["packed"]
         return [b["out"], b["points"], i32(self.n_points), b[f"edges{m}"], b[f"ybounds{m}"], packed]
 
     def strips(self, config, uploads, out, n):

@@ -52,7 +52,7 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
                 "method": [2],
                 "between": [0],
                 "poly_smem": [1],
-                "asm": [3, 5],
+                "asm": [3, 7],
                 "persist": [0, 1],
             },
             "restrictions": [],
