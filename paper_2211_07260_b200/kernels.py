@@ -565,18 +565,20 @@ class SgemmTF32Problem(SgemmProblem):
     roofline_kind = "tensor"
 
     def tune_params(self):
-        return {"BN": [64, 128, 256], "STAGES": [2, 3, 4, 5, 6], "PERSIST": [0, 1], "SPLIT_TAIL": [0, 1]}
+        return {"BN": [64, 128, 256], "STAGES": [2, 3, 4, 5, 6], "PERSIST": [0, 1], "SPLIT_TAIL": [0, 1],
+                "PAIR": [0, 1]}
 
     def restrictions(self):
         return [
-            "STAGES * (16384 + BN * 128) + 2048 <= 232448",
+            "STAGES * (16384 + BN * 128 / (1 + PAIR)) + 2048 <= 232448",
             "PERSIST == 0 or BN >= 128",
             "PERSIST == 1 or SPLIT_TAIL == 0",
-            f"{self.m} % 128 == 0 and {self.n} % BN == 0 and {self.k} % 32 == 0",
+            "PAIR == 0 or (PERSIST == 0 and BN >= 128)",
+            f"{self.m} % (128 * (1 + PAIR)) == 0 and {self.n} % BN == 0 and {self.k} % 32 == 0",
         ]
 
     def default_config(self):
-        return {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1}
+        return {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1, "PAIR": 0}
 
     def defines(self, config):
         c = _as_dict(config)
@@ -586,8 +588,12 @@ class SgemmTF32Problem(SgemmProblem):
         return d
 
     def _variant(self, config) -> tuple[str, str]:
-        """(source file, kernel symbol): persistent warp-specialised or one tile per CTA."""
-        if _as_dict(config).get("PERSIST", 0):
+        """(source file, kernel symbol): CTA-pair (cta_group::2), persistent warp-specialised, or one
+        tile per CTA."""
+        c = _as_dict(config)
+        if c.get("PAIR", 0):
+            return "sgemm_tf32c2.cu", "sgemm_tf32c2"
+        if c.get("PERSIST", 0):
             return "sgemm_tf32p.cu", "sgemm_tf32p"
         return "sgemm_tf32.cu", "sgemm_tf32"
 
@@ -602,13 +608,17 @@ class SgemmTF32Problem(SgemmProblem):
 
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
-        return c["STAGES"] * (128 * 32 * 4 + c["BN"] * 32 * 4) + 1024 + 256
+        b_stage = c["BN"] * 32 * 4 // (2 if c.get("PAIR", 0) else 1)
+        return c["STAGES"] * (128 * 32 * 4 + b_stage) + 1024 + 256
 
     def tiles(self, config) -> int:
         return (self.m // 128) * (self.n // _as_dict(config)["BN"])
 
     def launch(self, config):
         c = _as_dict(config)
+        if c.get("PAIR", 0):  # one 256 x BN tile per CTA pair (cluster of 2 on one TPC)
+            return Launch((2 * (self.n // c["BN"]), self.m // 256, 1), (128, 1, 1), smem=self.smem_bytes(c),
+                          cluster_x=2)
         if c.get("PERSIST", 0):
             sms = self.gpu.sm_count if self.gpu is not None else 148
             return Launch((min(sms, self.tiles(c)), 1, 1), (192, 1, 1), smem=self.smem_bytes(c))

@@ -244,20 +244,22 @@ def test_suite_pipelined_strips_match_single_launch():
 # -- SGEMM on tcgen05 (TF32, its own tolerance) -------------------------------------------------
 
 
-TF32_CONFIGS = [{"BN": 64, "STAGES": 3}, {"BN": 128, "STAGES": 6}, {"BN": 256, "STAGES": 2}, {"BN": 256, "STAGES": 4},
-                {"BN": 128, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 0},
-                {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1}]
+_TF32 = {"PERSIST": 0, "SPLIT_TAIL": 0, "PAIR": 0}
+TF32_CONFIGS = [_TF32 | c for c in (
+    {"BN": 64, "STAGES": 3}, {"BN": 128, "STAGES": 6}, {"BN": 256, "STAGES": 2}, {"BN": 256, "STAGES": 4},
+    {"BN": 128, "STAGES": 4, "PERSIST": 1}, {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1},
+    {"BN": 128, "STAGES": 6, "PAIR": 1}, {"BN": 256, "STAGES": 4, "PAIR": 1})]
 
 
 @pytest.mark.parametrize("cfg", TF32_CONFIGS, ids=str)
-@pytest.mark.parametrize("mnk,beta", [((256, 256, 256), 0.5), ((384, 512, 96), 0.0)])
+@pytest.mark.parametrize("mnk,beta", [((256, 256, 256), 0.5), ((384, 512, 96), 0.0), ((512, 768, 160), 1.0)])
 def test_sgemm_tf32_tcgen05_within_tf32_tolerance(gpu, cfg, mnk, beta):
     from paper_2211_07260_b200.kernels import SgemmTF32Problem
 
     m, n, k = mnk
-    if n % cfg["BN"]:
-        pytest.skip("N not a multiple of BN")
     p = SgemmTF32Problem(m=m, n=n, k=k, beta=beta)
+    if not p.is_valid(cfg):
+        pytest.skip("shape not a multiple of this config's tile")
     p.prepare(gpu)
     got = run_once(gpu, p, cfg)
     ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
@@ -277,8 +279,8 @@ def test_sgemm_tf32_full_size(gpu):
     assert O.sgemm_error(run_once(gpu, p, cfg), ref) <= O.SGEMM_TF32_TOL
 
 
-@pytest.mark.parametrize("cfg", [{"BN": 128, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1},
-                                 {"BN": 256, "STAGES": 3, "PERSIST": 1, "SPLIT_TAIL": 1}], ids=str)
+@pytest.mark.parametrize("cfg", [{"BN": 128, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1, "PAIR": 0},
+                                 {"BN": 256, "STAGES": 3, "PERSIST": 1, "SPLIT_TAIL": 1, "PAIR": 0}], ids=str)
 def test_sgemm_tf32_persistent_split_tail(gpu, cfg):
     """More tiles than SMs with a short last wave: the tail tiles are split along K over two
     CTAs and reduced through the workspace. Relaunching must keep the result (the per-tile
