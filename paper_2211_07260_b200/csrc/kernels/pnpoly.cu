@@ -49,6 +49,12 @@
 //                 structure-of-arrays table {vy0..3, sl0..3, ic0..3} per 4
 //                 edges, so no register shuffling: 3 issue slots per
 //                 edge-point (1.5 FMA-pipe + 1.5 ALU). Same formulation 3.
+//                 8: ASM 7's arithmetic written in C++ over the same table
+//                 held in __constant__ memory (POLY_SMEM=0): the edge pairs
+//                 are warp-uniform loads, so ptxas can feed them to FADD2 /
+//                 FFMA2 as uniform-register operands and the f32x2 ops read
+//                 fewer vector registers (register-read bandwidth, not the
+//                 FMA pipe, is what holds ASM 7's dispatch back).
 //
 // Edge table (built on the host in float32, see kernels.py): per edge k from
 // vertex k-1 (cyclic) to vertex k, a float4 {vy_k, a, b, c} and a float2
@@ -99,13 +105,16 @@
 #if ASM == 7 && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
 #error "ASM=7 needs POLY_SMEM=1, METHOD=2 and TILE in {2,4,6,8}"
 #endif
+#if ASM == 8 && !(POLY_SMEM == 0 && METHOD == 2)
+#error "ASM=8 needs POLY_SMEM=0 and METHOD=2"
+#endif
 // packed records {ymin, ymax, slope, icpt} (METHOD 2) padded
 // to a multiple of 4 with never-spanning dummies {+inf, -inf, 0, 0}
 #define NPACK (((VERTICES) + 3) / 4 * 4)
 // ASM 7 table: edges padded to a multiple of 8 (two 4-edge groups per loop
 // trip), 12 floats per 4-edge group
 #define NPAIR8 (((VERTICES) + 7) / 8 * 8)
-#if ASM == 7
+#if ASM == 7 || ASM == 8
 #define TAB_VEC4 (NPAIR8 * 3 / 4)
 #else
 #define TAB_VEC4 NPACK
@@ -1500,6 +1509,22 @@
 
 __constant__ float4 c_edges[VERTICES];
 __constant__ float2 c_ybounds[VERTICES];
+#if ASM == 8
+// the ASM 7 pair table: per 4-edge group {vy0..3}, {sl0..3}, {ic0..3}
+__constant__ ulonglong2 c_pairs[TAB_VEC4];
+
+// {a, a} - b and s * {a, a} + c on packed f32x2 lanes (IEEE .rn per lane, no ftz)
+__device__ __forceinline__ unsigned long long f2_sub_bcast(float a, unsigned long long b) {
+    unsigned long long r;
+    asm("{\n.reg .b64 aa;\nmov.b64 aa, {%1, %1};\nsub.rn.f32x2 %0, aa, %2;\n}" : "=l"(r) : "f"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2_fma_bcast(unsigned long long sl, float a, unsigned long long c) {
+    unsigned long long r;
+    asm("{\n.reg .b64 aa;\nmov.b64 aa, {%2, %2};\nfma.rn.f32x2 %0, %1, aa, %3;\n}" : "=l"(r) : "l"(sl), "f"(a), "l"(c));
+    return r;
+}
+#endif
 
 __device__ __forceinline__ float crossing_x(float4 e, float py) {
 #if METHOD == 0
@@ -1515,7 +1540,7 @@ extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X)
 pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
        const float4 *__restrict__ g_edges, const float2 *__restrict__ g_ybounds,
        const float4 *__restrict__ g_packed) {
-#if ASM
+#if ASM && ASM != 8
     // packed records, NPACK entries (ASM 1/2: {ymin, ymax, slope, icpt};
     // ASM 3: {vy_k, slope, icpt, 0})
     __shared__ __align__(16) float4 s_packed[TAB_VEC4];
@@ -1610,6 +1635,35 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
                      : "l"(pxp[0]), "l"(pxp[1]), "l"(pxp[2]), "l"(pxp[3]), "l"(pyp[0]), "l"(pyp[1]), "l"(pyp[2]),
                        "l"(pyp[3]), "r"(sbase), "r"(span), "f"(vy_last));
 #endif
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) inside[t] = acc[t] >> 31;
+    }
+#elif ASM == 8
+    unsigned inside[TILE];
+    {
+        unsigned acc[TILE], dp[TILE];
+        const float vy_last = reinterpret_cast<const float *>(c_pairs)[(VERTICES - 1) / 4 * 12 + (VERTICES - 1) % 4];
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) {
+            acc[t] = 0u;
+            dp[t] = __float_as_uint(__fsub_rn(py[t], vy_last));
+        }
+#pragma unroll 2
+        for (int g = 0; g < NPAIR8 / 4; ++g) {
+            const ulonglong2 vy = c_pairs[3 * g], sl = c_pairs[3 * g + 1], ic = c_pairs[3 * g + 2];
+#pragma unroll
+            for (int t = 0; t < TILE; ++t) {
+                const unsigned long long dA = f2_sub_bcast(py[t], vy.x), dB = f2_sub_bcast(py[t], vy.y);
+                const unsigned long long eA = f2_sub_bcast(px[t], f2_fma_bcast(sl.x, py[t], ic.x));
+                const unsigned long long eB = f2_sub_bcast(px[t], f2_fma_bcast(sl.y, py[t], ic.y));
+                const unsigned d0 = (unsigned)dA, d1 = (unsigned)(dA >> 32);
+                const unsigned d2 = (unsigned)dB, d3 = (unsigned)(dB >> 32);
+                // crossing bit of each edge = sign((py - vy_k) ^ (py - vy_{k-1})) & sign(px - x_k)
+                acc[t] ^= ((d0 ^ dp[t]) & (unsigned)eA) ^ ((d1 ^ d0) & (unsigned)(eA >> 32));
+                acc[t] ^= ((d2 ^ d1) & (unsigned)eB) ^ ((d3 ^ d2) & (unsigned)(eB >> 32));
+                dp[t] = d3;
+            }
+        }
 #pragma unroll
         for (int t = 0; t < TILE; ++t) inside[t] = acc[t] >> 31;
     }

@@ -199,15 +199,16 @@ class PnPolyProblem(KernelProblem):
             "method": [0, 1, 2],
             "between": [0, 1],
             "poly_smem": [0, 1],
-            "asm": [0, 1, 2, 3, 4, 5, 6, 7],
+            "asm": [0, 1, 2, 3, 4, 5, 6, 7, 8],
             "persist": [0, 1],
         }
 
     def restrictions(self):
         return [
             "vec == 1 or tile % 2 == 0",
-            "asm == 0 or (poly_smem == 1 and method == 2)",
-            "asm == 0 or asm == 3 or (between == 1 and tile != 8)",
+            "asm == 0 or method == 2",
+            "asm == 0 or (asm == 8 and poly_smem == 0) or (asm != 8 and poly_smem == 1)",
+            "asm == 0 or asm >= 3 or (between == 1 and tile != 8)",
             "asm < 3 or (between == 0 and tile != 1)",
             "(asm != 4 and asm != 6) or (vec == 2 and (tile == 4 or tile == 8))",
         ]
@@ -340,6 +341,9 @@ class PnPolyProblem(KernelProblem):
 
     def bind(self, kernel, config):
         c = _as_dict(config)
+        if c.get("asm", 0) == 8:
+            kernel.set_global("c_pairs", self.pair_table())
+            return
         if not c["poly_smem"]:
             edges, yb = self._tables[c["method"]]
             kernel.set_global("c_edges", edges)

@@ -17,7 +17,7 @@ want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 3)
 # usage: time_pnpoly.py [ASMS [TILES [BLOCKS]]]   e.g.  time_pnpoly.py 3,7 4,8 128,256,512
 lists = [[int(v) for v in a.split(",")] for a in sys.argv[1:4]]
 asms, tiles, blocks = lists + [[3, 7], [4, 8], [128, 256, 512]][len(lists):]
-configs = [dict(block_size_x=b, tile=t, vec=2, method=2, between=0, poly_smem=1, asm=a, persist=ps)
+configs = [dict(block_size_x=b, tile=t, vec=2, method=2, between=0, poly_smem=int(a != 8), asm=a, persist=ps)
            for a, b, t, ps in itertools.product(asms, blocks, tiles, (0, 1))]
 peak_slots = gpu.sm_count * 128 * 1965e6
 for cfg in configs:
