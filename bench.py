@@ -209,9 +209,12 @@ def kernel_profile(name: str, config: dict):
     return entry.get("dram_bytes_per_launch")
 
 
-def tf32_peak_gflops() -> float:
+def tf32_peak_gflops(sustained: bool = False) -> float:
+    """Dense TF32 peak = half the MEASURED dense bf16 rate (same tcgen05 cycles, K=8 vs K=16 per MMA).
+    ``sustained``: the back-to-back figure (power-capped clocks), for kernels timed in long loops."""
     peaks = ROOT / "MEASURED_PEAKS.json"
-    bf16 = json.loads(peaks.read_text()).get("bf16_tflops", 1590.0) if peaks.exists() else 1590.0
+    doc = json.loads(peaks.read_text()) if peaks.exists() else {}
+    bf16 = doc.get("bf16_tflops_sustained" if sustained else "bf16_tflops") or doc.get("bf16_tflops", 1590.0)
     return bf16 / 2.0 * 1e3
 
 
@@ -238,11 +241,14 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 0.6):
         "sm_mhz": summ["sm_mhz"],
     }
     if prob.roofline_kind == "tensor":
-        # dense TF32 = half the measured dense bf16 rate (same tcgen05 cycles, K=8 vs K=16 per MMA)
-        peak = tf32_peak_gflops()
+        # a >= 0.6 s back-to-back loop runs at the power cap: the sustained measured peak is the
+        # denominator (the burst one is reported beside it)
+        peak = tf32_peak_gflops(sustained=True)
         out["roofline_frac"] = round(rate / peak, 4)
         out["roofline_peak_gflops"] = peak
-        out["roofline_basis"] = "MEASURED_PEAKS bf16_tflops / 2 (tcgen05 kind::tf32 issues K=8 per MMA vs K=16)"
+        out["roofline_frac_vs_burst"] = round(rate / tf32_peak_gflops(), 4)
+        out["roofline_basis"] = ("MEASURED_PEAKS bf16_tflops_sustained / 2 (tcgen05 kind::tf32 issues K=8 per MMA vs "
+                                 "K=16; loop runs power-capped like the sustained bf16 measurement)")
     elif summ["sm_mhz"]:
         peak = fp32_peak_tflops(gpu.sm_count, summ["sm_mhz"]) * 1e3
         if prob.roofline_kind == "issue":
