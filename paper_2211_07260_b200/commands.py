@@ -1,4 +1,4 @@
-"""Command line: ``simulate-sweep``, ``fit``, ``tune``, ``steer``.
+"""Command line: ``simulate-sweep``, ``fit``, ``tune``, ``steer``, ``analyze``.
 
 Behaviour contract (reference ``pkg/src/jouletune/cli.py``): the same
 subcommands, flags, report documents (``report.json`` / model JSON / sweep
@@ -18,8 +18,10 @@ Additions for the real GPU:
   before writing the CSV; a ``.meta.json`` sidecar keeps the raw records;
 * ``--observer nvml`` selects the NVML energy-counter observer.
 
-``analyze`` (Pareto / fitness-flow-graph analysis) is out of scope
-(post-hoc CPU analysis, not on the measured path).
+``analyze`` reads any result cache, simulated or B200:
+``--mode pareto`` writes the performance / efficiency front and
+``--mode difficulty`` the proportion-of-centrality curve of the space's
+fitness flow graph (reference ``cli.py:367-443``).
 """
 
 from __future__ import annotations
@@ -34,7 +36,7 @@ from typing import Any
 
 import numpy as np
 
-from . import __version__, pmodel, recipes, records, search, steering
+from . import __version__, landscape, pmodel, recipes, records, search, steering
 from .errors import ConfigurationError, JouleTuneError
 from .hardware import CLOCK_PARAM
 from .observer_hooks import AveragedPowerObserver, InstantPowerObserver, NVMLObserver
@@ -266,6 +268,50 @@ def cmd_steer(args) -> int:
     return _run_tuning(m, steered, {"steering": info}, device=device)
 
 
+# -- analyze ------------------------------------------------------------------------------------
+
+
+def cmd_analyze(args) -> int:
+    pareto = args.mode == "pareto"
+    m = RunManifest(
+        "analyze", cache=args.cache, space=args.space, objective=args.objective, out=args.out, seed=args.seed,
+        mode=args.mode, performance=args.performance if pareto else None,
+        efficiency=args.efficiency if pareto else None, weights=None if pareto else args.weights,
+        p_max=None if pareto else args.p_max, p_steps=None if pareto else args.p_steps,
+    )
+    m.validate()
+    results = [r for r in records.ResultCache(args.cache).results() if not r.failed]
+    if not results:
+        raise JouleTuneError(f"cache {args.cache} holds no successful results")
+    out_dir = Path(args.out or ".")
+    out_dir.mkdir(parents=True, exist_ok=True)
+    if pareto:
+        points = [landscape.ParetoPoint(r.config, r.lookup(args.performance), r.lookup(args.efficiency))
+                  for r in results]
+        front = landscape.pareto_front(points)
+        landscape.write_pareto_csv(points, front, out_dir / "pareto.csv")
+        body = {"points": len(points), "front_size": len(front),
+                "front": [{"config": p.config.as_dict(), "performance": p.performance, "efficiency": p.efficiency}
+                          for p in front]}
+        _write_report({**m.header(), **body}, out_dir / "analyze.json")
+        print(f"pareto front: {len(front)} of {len(points)} points -> {out_dir}")
+        return 0
+    if args.space is None:
+        raise ConfigurationError("--space is required for difficulty analysis")
+    space = SearchSpace.from_json(args.space)
+    objective = records.Objective.parse(args.objective or "energy")
+    graph = landscape.build_ffg(space, {r.config: objective.fitness(r) for r in results})
+    weights = landscape.minima_arrival_distribution(graph, mode=args.weights)
+    curve = landscape.proportion_of_centrality(graph, weights, np.linspace(1.0, args.p_max, args.p_steps).tolist())
+    landscape.write_centrality_csv(curve, out_dir / "difficulty.csv")
+    body = {"objective": f"{objective.metric}:{objective.direction}", "nodes": len(graph.nodes),
+            "edges": graph.edge_count(), "minima": len(graph.minima), "f_optimal": curve.f_optimal,
+            "weights_mode": args.weights}
+    _write_report({**m.header(), **body}, out_dir / "analyze.json")
+    print(f"difficulty: {len(graph.minima)} local optima over {len(graph.nodes)} configs -> {out_dir}")
+    return 0
+
+
 # -- parser (flag tables) ----------------------------------------------------------------------
 
 _TUNING_FLAGS = [
@@ -303,6 +349,19 @@ _COMMANDS = {
     "steer": ("tune with the clock parameter reduced to the model band", cmd_steer, _TUNING_FLAGS + [
         ("--model", dict(required=True, help="fitted model JSON")),
         ("--pct", dict(type=float, default=0.10)),
+    ]),
+    "analyze": ("analyze a result cache", cmd_analyze, [
+        ("--cache", dict(required=True)),
+        ("--mode", dict(choices=["pareto", "difficulty"], required=True)),
+        ("--space", dict(default=None, help="needed for difficulty")),
+        ("--objective", dict(default=None)),
+        ("--performance", dict(default="gflops")),
+        ("--efficiency", dict(default="gflops_per_w")),
+        ("--weights", dict(choices=list(landscape.WEIGHT_MODES), default="absorbing")),
+        ("--p-max", dict(type=float, default=1.5)),
+        ("--p-steps", dict(type=int, default=26)),
+        ("--out", dict(default=None)),
+        ("--seed", dict(type=int, default=0)),
     ]),
 }
 

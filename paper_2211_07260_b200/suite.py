@@ -20,7 +20,7 @@ from . import tuned
 from .gpu import GPU
 from .kernels import KernelProblem, make_problem
 
-__all__ = ["Runner", "conv2d", "pnpoly", "sgemm", "pinned", "device"]
+__all__ = ["Runner", "conv2d", "pnpoly", "sgemm", "sgemm_tf32", "pinned", "device"]
 
 _lock = threading.Lock()
 _gpus: dict[int, GPU] = {}
@@ -164,12 +164,24 @@ def pnpoly(points: np.ndarray, vx: np.ndarray, vy: np.ndarray, *, config=None, o
 def sgemm(a: np.ndarray, b: np.ndarray, c: np.ndarray, alpha: float = 1.0, beta: float = 0.0, *, config=None,
           ordinal: int = 0) -> np.ndarray:
     """alpha * a @ b + beta * c in FP32 (a is staged column-major, as BLAS 'N')."""
+    return _gemm("sgemm", a, b, c, alpha, beta, config, ordinal)
+
+
+def sgemm_tf32(a: np.ndarray, b: np.ndarray, c: np.ndarray, alpha: float = 1.0, beta: float = 0.0, *, config=None,
+               ordinal: int = 0) -> np.ndarray:
+    """The same product on the tcgen05 tensor cores: TF32 inputs, FP32 accumulation
+    (oracle SGEMM_TF32_TOL). Shapes must be multiples of the config's tile (M % 128 or
+    % 256 for the CTA-pair kernel, N % BN, K % 32)."""
+    return _gemm("sgemm_tf32", a, b, c, alpha, beta, config, ordinal)
+
+
+def _gemm(name, a, b, c, alpha, beta, config, ordinal) -> np.ndarray:
     a = np.asarray(a, dtype=np.float32)
     b = np.asarray(b, dtype=np.float32)
     c = np.asarray(c, dtype=np.float32)
     m, k = a.shape
     n = b.shape[1]
-    r = _runner("sgemm", (m, n, k, float(alpha), float(beta)), config,
+    r = _runner(name, (m, n, k, float(alpha), float(beta)), config,
                 {"m": m, "n": n, "k": k, "alpha": float(alpha), "beta": float(beta)}, {"a": a, "b": b, "c0": c},
                 ordinal)
     at = a.T if a.flags.f_contiguous else np.ascontiguousarray(a.T)

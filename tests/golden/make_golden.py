@@ -148,6 +148,25 @@ def main():
             "model": json.loads((tmp / "model.json").read_text()),
             "steer_report": json.loads((tmp / "steer" / "report.json").read_text()),
         }
+        # analyze over the steer run's cache: Pareto front and both difficulty weightings
+        band = gold["cli"]["steer_report"]["steering"]["band"]
+        steered = J.SearchSpace.from_dict(gold["spaces"]["a100_mimic_space"]).with_values("nvml_gr_clock", band)
+        (tmp / "steered.json").write_text(json.dumps(steered.to_dict()))
+        cache = str(tmp / "steer" / "cache.jsonl")
+        analyze = {}
+        for label, extra in (("pareto", ["--mode", "pareto"]),
+                             ("absorbing", ["--mode", "difficulty", "--space", str(tmp / "steered.json")]),
+                             ("pagerank", ["--mode", "difficulty", "--space", str(tmp / "steered.json"),
+                                           "--weights", "pagerank", "--p-max", "2.0", "--p-steps", "11"]),
+                             ("time", ["--mode", "difficulty", "--space", str(tmp / "steered.json"),
+                                       "--objective", "time"])):
+            out = tmp / f"analyze_{label}"
+            rc = cli_main(["analyze", "--cache", cache, "--out", str(out), *extra])
+            doc = json.loads((out / "analyze.json").read_text())
+            csv_name = "pareto.csv" if label == "pareto" else "difficulty.csv"
+            analyze[label] = {"rc": rc, "report": {k: v for k, v in doc.items() if not k.startswith("manifest")},
+                              "manifest_keys": sorted(doc["manifest"]), "csv": (out / csv_name).read_text()}
+        gold["analyze"] = analyze
     OUT.write_text(json.dumps(gold, indent=None, separators=(",", ":")) + "\n")
     print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB)")
 

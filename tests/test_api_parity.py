@@ -194,3 +194,66 @@ def test_live_reference_fit_parity(reference):
             got = PM.fit(ours, tdp=1000.0)
         for k, v in ref.to_dict().items():
             assert _close(getattr(got, k), v, rel=1e-9), (trial, k)
+
+
+def test_cli_analyze_matches_reference(golden, spec_file, tmp_path):
+    """``analyze`` (Pareto front, difficulty curve under both weightings) on the
+    steer run's cache: same reports and CSVs as the reference (analysis.py, cli.py:367-443)."""
+    spec = str(spec_file("a100_mimic"))
+    space_path = tmp_path / "space.json"
+    space_path.write_text(json.dumps(golden["spaces"]["a100_mimic_space"]))
+    assert cli_main(["simulate-sweep", "--device", spec, "--out", str(tmp_path / "sweep.csv"), "--points", "25"]) == 0
+    assert cli_main(["fit", "--samples", str(tmp_path / "sweep.csv"), "--device", spec, "--out",
+                     str(tmp_path / "model.json")]) == 0
+    assert cli_main(["steer", "--space", str(space_path), "--device", spec, "--model", str(tmp_path / "model.json"),
+                     "--out", str(tmp_path / "steer"), "--observer", "instant", "--total-flops", "1.374e11"]) == 0
+    band = golden["cli"]["steer_report"]["steering"]["band"]
+    steered = B.SearchSpace.from_dict(golden["spaces"]["a100_mimic_space"]).with_values("nvml_gr_clock", band)
+    (tmp_path / "steered.json").write_text(json.dumps(steered.to_dict()))
+    cache = str(tmp_path / "steer" / "cache.jsonl")
+    runs = {"pareto": ["--mode", "pareto"],
+            "absorbing": ["--mode", "difficulty", "--space", str(tmp_path / "steered.json")],
+            "pagerank": ["--mode", "difficulty", "--space", str(tmp_path / "steered.json"), "--weights", "pagerank",
+                         "--p-max", "2.0", "--p-steps", "11"],
+            "time": ["--mode", "difficulty", "--space", str(tmp_path / "steered.json"), "--objective", "time"]}
+    for label, extra in runs.items():
+        want = golden["analyze"][label]
+        out = tmp_path / f"analyze_{label}"
+        assert cli_main(["analyze", "--cache", cache, "--out", str(out), *extra]) == want["rc"] == 0
+        doc = json.loads((out / "analyze.json").read_text())
+        assert sorted(doc["manifest"]) == want["manifest_keys"], label
+        body = {k: v for k, v in doc.items() if not k.startswith("manifest")}
+        assert body.keys() == want["report"].keys(), label
+        for k, v in want["report"].items():
+            if isinstance(v, float):
+                assert _close(body[k], v), (label, k)
+            else:
+                assert body[k] == v, (label, k)
+        csv_name = "pareto.csv" if label == "pareto" else "difficulty.csv"
+        assert (out / csv_name).read_text() == want["csv"], label
+
+
+def test_landscape_units():
+    """Pareto and flow-graph rules on hand-checkable cases."""
+    from paper_2211_07260_b200 import landscape as L
+
+    K = lambda **kw: B.KernelConfig.from_dict(kw)  # noqa: E731
+    pts = [L.ParetoPoint(K(i=i), p, e) for i, (p, e) in enumerate([(3, 1), (2, 2), (2, 2), (1, 3), (1, 1), (3, 0.5)])]
+    front = L.pareto_front(pts)
+    assert [(p.performance, p.efficiency) for p in front] == [(3, 1), (2, 2), (1, 3)]
+    assert front[1] is pts[1]  # duplicate coordinates: first occurrence only
+    assert L.dominates(pts[0], pts[5]) and not L.dominates(pts[1], pts[2]) and not L.dominates(pts[0], pts[1])
+    space = B.SearchSpace.from_dict({"parameters": {"a": [0, 1], "b": [0, 1]}})
+    fit = {K(a=0, b=0): 1.0, K(a=1, b=1): 1.5, K(a=0, b=1): 3.0, K(a=1, b=0): 2.0}
+    g = L.build_ffg(space, fit)
+    assert set(g.minima) == {K(a=0, b=0), K(a=1, b=1)} and g.edge_count() == 4
+    w = L.minima_arrival_distribution(g)  # each transient node splits 1/2 : 1/2, each sink keeps its own walk
+    assert w[K(a=0, b=0)] == pytest.approx(0.5) and w[K(a=1, b=1)] == pytest.approx(0.5)
+    pr = L.minima_arrival_distribution(g, mode="pagerank")
+    assert sum(pr.values()) == pytest.approx(1.0) and pr[K(a=0, b=0)] == pytest.approx(pr[K(a=1, b=1)])
+    curve = L.proportion_of_centrality(g, w, [1.0, 1.4, 1.5])
+    assert curve.f_optimal == 1.0 and curve.proportions == pytest.approx((0.5, 0.5, 1.0))
+    with pytest.raises(B.AnalysisError):
+        L.build_ffg(space, {K(a=0, b=0): 1.0})
+    with pytest.raises(B.ConfigurationError):
+        L.minima_arrival_distribution(g, mode="random")

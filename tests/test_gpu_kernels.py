@@ -221,6 +221,10 @@ def test_suite_host_api_matches_oracles():
     c = suite.sgemm(si["a"], si["b"], si["c0"], 1.0, 0.5, config=SgemmProblem().default_config() | {
         "MWG": 64, "NWG": 64, "MDIMC": 16, "NDIMC": 16, "MDIMA": 16, "NDIMB": 16})
     assert O.sgemm_error(c, O.sgemm(si["a"], si["b"], si["c0"], 1.0, 0.5)) <= O.SGEMM_TOL
+    ti = SgemmProblem(m=512, n=256, k=96).host_inputs()
+    t = suite.sgemm_tf32(ti["a"], ti["b"], ti["c0"], 1.0, 0.5)  # tuned CTA-pair config fits 512 x 256
+    err = O.sgemm_error(t, O.sgemm(ti["a"], ti["b"], ti["c0"], 1.0, 0.5))
+    assert 1e-6 < err <= O.SGEMM_TF32_TOL
 
 
 def test_suite_pipelined_strips_match_single_launch():
