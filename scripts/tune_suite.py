@@ -87,7 +87,7 @@ def oracle_check(problem, cfg) -> tuple[bool, float]:
     return err <= (O.SGEMM_TF32_TOL if problem.name == "sgemm_tf32" else O.SGEMM_TOL), err
 
 
-CONFIRM_ENERGY, CONFIRM_TIME, CONFIRM_ROUNDS, CONFIRM_WINDOW = 5, 3, 3, 1.0
+CONFIRM_ENERGY, CONFIRM_TIME, CONFIRM_ROUNDS, CONFIRM_WINDOW, CONFIRM_SETTLE = 5, 3, 3, 1.0, 0.25
 
 
 def confirm(dev, problem, leaders) -> list[dict]:
@@ -99,11 +99,15 @@ def confirm(dev, problem, leaders) -> list[dict]:
             seen.add(r.config.key())
             configs.append(r)
     samples = {r.config.key(): [] for r in configs}
-    for _ in range(CONFIRM_ROUNDS):
-        for r in configs:
-            ex = dev.execute(r.config, duration_hint=CONFIRM_WINDOW)
-            if ex.counter_power:
-                samples[r.config.key()].append((ex.runtime, ex.counter_power, ex.telemetry))
+    settle, dev.settle = dev.settle, CONFIRM_SETTLE  # energy window starts after the power ramp
+    try:
+        for _ in range(CONFIRM_ROUNDS):
+            for r in configs:
+                ex = dev.execute(r.config, duration_hint=CONFIRM_WINDOW)
+                if ex.counter_power:
+                    samples[r.config.key()].append((ex.runtime, ex.counter_power, ex.telemetry))
+    finally:
+        dev.settle = settle
     out = []
     for r in configs:
         got = samples[r.config.key()]
@@ -178,7 +182,8 @@ def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | No
         "clock_mode": dev.clock_mode or "not requested",
         "time_optimal": dict(by_time),
         "energy_optimal": dict(by_energy),
-        "confirm": {"rounds": CONFIRM_ROUNDS, "window_s": CONFIRM_WINDOW, "candidates": confirmed},
+        "confirm": {"rounds": CONFIRM_ROUNDS, "window_s": CONFIRM_WINDOW, "settle_s": CONFIRM_SETTLE,
+                    "candidates": confirmed},
     }
     # correctness gate on the two winners
     for key in ("time_optimal", "energy_optimal"):
