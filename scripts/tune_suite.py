@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import shutil
 import os
 import sys
 import time
@@ -236,6 +237,11 @@ def main():
         TUNED_PATH.write_text(json.dumps(data, indent=1) + "\n")
     Path("gpurun_out").mkdir(exist_ok=True)
     Path("gpurun_out/tuned_b200.json").write_text(json.dumps(data, indent=1) + "\n")
+    mirror = Path("gpurun_out/results")
+    if RESULTS.resolve() != mirror.resolve():  # caches come back from the GPU box only under gpurun_out/
+        mirror.mkdir(parents=True, exist_ok=True)
+        for f in RESULTS.glob("cache_*.jsonl"):
+            shutil.copy(f, mirror / f.name)
     gpu.close()
 
 
