@@ -218,7 +218,7 @@ def tf32_peak_gflops(sustained: bool = False) -> float:
     return bf16 / 2.0 * 1e3
 
 
-def measure_tuned(gpu, name: str, objective: str, seconds: float = 0.6):
+def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: float = 0.25):
     from paper_2211_07260_b200 import tuned
     from paper_2211_07260_b200.gpu import fp32_peak_tflops
     from paper_2211_07260_b200.kernels import make_problem
@@ -229,7 +229,7 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 0.6):
     k = prob.kernel(cfg)
     prob.bind(k, cfg)
     run = gpu.bench(k, prob.launch(cfg), prob.args(cfg), min_seconds=seconds)
-    summ = summarize_samples(run.samples, run.loop_t0 + 0.1, run.loop_t1)
+    summ = summarize_samples(run.samples, run.loop_t0 + settle, run.loop_t1)  # past the power ramp
     rate = prob.total_flops / run.per_launch_s / 1e9
     out = {
         "config": cfg,
@@ -241,7 +241,7 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 0.6):
         "sm_mhz": summ["sm_mhz"],
     }
     if prob.roofline_kind == "tensor":
-        # a >= 0.6 s back-to-back loop runs at the power cap: the sustained measured peak is the
+        # a >= 1 s back-to-back loop runs at the power cap: the sustained measured peak is the
         # denominator (the burst one is reported beside it)
         peak = tf32_peak_gflops(sustained=True)
         out["roofline_frac"] = round(rate / peak, 4)
