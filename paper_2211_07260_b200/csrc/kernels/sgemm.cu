@@ -17,6 +17,14 @@
 //                   1: strided by MDIMC*VWM (NDIMC*VWN) -> conflict-free smem
 //   SA, SB          1: stage the A (B) tile in shared memory (double buffered);
 //                   0: read fragments straight from global memory through L1
+//   ASYNC           (B200 addition, not a CLBlast knob) 0: CLBlast's staging
+//                   through registers (global -> registers -> shared, two
+//                   static buffers); 2 or 3: that many shared-memory stages
+//                   filled by cp.async (LDGSTS) straight from global memory,
+//                   one __syncthreads per k-tile. Frees the KWA*MWA/VWM +
+//                   KWB*NWB/VWN staging registers per thread and lets the
+//                   copy of tile t+ASYNC-1 overlap the FFMAs of tile t.
+//                   Needs SA = SB = 1 (dynamic shared memory, up to 227 KB).
 //
 // Requirements (the tuning-space restrictions, kernels.py):
 //   MWG % (MDIMC*VWM) == 0, NWG % (NDIMC*VWN) == 0,
@@ -65,6 +73,15 @@
 #ifndef SB
 #define SB 1
 #endif
+#ifndef ASYNC
+#define ASYNC 0
+#endif
+#if ASYNC && !(SA && SB)
+#error "ASYNC staging needs SA = SB = 1"
+#endif
+#if ASYNC == 1 || ASYNC > 4
+#error "ASYNC must be 0, 2, 3 or 4"
+#endif
 
 #define THREADS (MDIMC * NDIMC)
 #define MWI (MWG / MDIMC)
@@ -112,6 +129,21 @@ __device__ __forceinline__ int frag_n(int tn, int w) {
 #endif
 }
 
+#if ASYNC
+// one VW-float vector global -> shared without a register round trip
+template <typename T>
+__device__ __forceinline__ void cp_async(T *dst, const T *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if constexpr (sizeof(T) == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"((int)sizeof(T)) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+#endif
+
 extern "C" __global__ void __launch_bounds__(THREADS)
 sgemm(const int M, const int N, const int K, const float alpha, const float beta,
       const float *__restrict__ at, const float *__restrict__ b, float *__restrict__ c) {
@@ -119,6 +151,16 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
     const int tm = tid % MDIMC, tn = tid / MDIMC;
     const int m0 = blockIdx.x * MWG, n0 = blockIdx.y * NWG;
 
+#if ASYNC
+    // ASYNC stages of {A tile, B tile} in dynamic shared memory
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
+    typedef vm_t a_tile_t[KWG][MWG / VWM];
+    typedef vn_t b_tile_t[KWG][NWG / VWN];
+    a_tile_t *a_sm = reinterpret_cast<a_tile_t *>(smem_dyn);
+    b_tile_t *b_sm = reinterpret_cast<b_tile_t *>(smem_dyn + ASYNC * sizeof(a_tile_t));
+    const int ma = tid % MDIMA, ka = tid / MDIMA;
+    const int nb = tid % NDIMB, kb = tid / NDIMB;
+#else
 #if SA
     __shared__ __align__(16) vm_t a_sm[2][KWG][MWG / VWM];
     const int ma = tid % MDIMA, ka = tid / MDIMA;
@@ -128,6 +170,8 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
     __shared__ __align__(16) vn_t b_sm[2][KWG][NWG / VWN];
     const int nb = tid % NDIMB, kb = tid / NDIMB;
     vn_t b_reg[KWB][NWB / VWN];
+#endif
+
 #endif
 
     float acc[MWI][NWI];
@@ -140,6 +184,72 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
     const vn_t *b_v = reinterpret_cast<const vn_t *>(b);
     const int lda_v = M / VWM, ldb_v = N / VWN;
 
+    // one KWG-deep k-tile of FFMAs from stage `buf` (SA/SB = 0: fragments from global at k0)
+    auto mac_tile = [&](const int buf, const int k0) {
+#pragma unroll 1
+        for (int kw = 0; kw < KWG; kw += KWI) {
+#pragma unroll
+            for (int ki = 0; ki < KWI; ++ki) {
+                const int k = kw + ki;
+                vm_t af[MWI / VWM];
+                vn_t bf[NWI / VWN];
+#pragma unroll
+                for (int w = 0; w < MWI / VWM; ++w) {
+#if SA
+                    af[w] = a_sm[buf][k][frag_m(tm, w)];
+#else
+                    af[w] = __ldg(at_v + (size_t)(k0 + k) * lda_v + m0 / VWM + frag_m(tm, w));
+#endif
+                }
+#pragma unroll
+                for (int w = 0; w < NWI / VWN; ++w) {
+#if SB
+                    bf[w] = b_sm[buf][k][frag_n(tn, w)];
+#else
+                    bf[w] = __ldg(b_v + (size_t)(k0 + k) * ldb_v + n0 / VWN + frag_n(tn, w));
+#endif
+                }
+#pragma unroll
+                for (int i = 0; i < MWI; ++i)
+#pragma unroll
+                    for (int j = 0; j < NWI; ++j)
+                        acc[i][j] = fmaf(lane(af[i / VWM], i % VWM), lane(bf[j / VWN], j % VWN), acc[i][j]);
+            }
+        }
+    };
+    const int tiles = K / KWG;
+
+#if ASYNC
+    // global -> shared copies of k-tile `tile` into stage `buf`, same thread mapping as CLBlast's loads
+    auto issue = [&](int tile, int buf) {
+        const int k0 = tile * KWG;
+#pragma unroll
+        for (int kk = 0; kk < KWA; ++kk)
+#pragma unroll
+            for (int mv = 0; mv < MWA / VWM; ++mv)
+                cp_async(&a_sm[buf][ka + kk * KDIMA][ma + mv * MDIMA],
+                         at_v + (size_t)(k0 + ka + kk * KDIMA) * lda_v + m0 / VWM + ma + mv * MDIMA);
+#pragma unroll
+        for (int kk = 0; kk < KWB; ++kk)
+#pragma unroll
+            for (int nv = 0; nv < NWB / VWN; ++nv)
+                cp_async(&b_sm[buf][kb + kk * KDIMB][nb + nv * NDIMB],
+                         b_v + (size_t)(k0 + kb + kk * KDIMB) * ldb_v + n0 / VWN + nb + nv * NDIMB);
+    };
+#pragma unroll
+    for (int s = 0; s < ASYNC - 1; ++s) {
+        if (s < tiles) issue(s, s);
+        cp_async_commit();  // empty groups keep the wait_group arithmetic uniform
+    }
+#pragma unroll 1
+    for (int t = 0; t < tiles; ++t) {
+        cp_async_wait<ASYNC - 2>();  // this thread's copies of tile t have landed
+        __syncthreads();             // everyone's have; and everyone is done with tile t-1's stage
+        if (t + ASYNC - 1 < tiles) issue(t + ASYNC - 1, (t + ASYNC - 1) % ASYNC);  // refill tile t-1's stage
+        cp_async_commit();
+        mac_tile(t % ASYNC, t * KWG);
+    }
+#else
     auto fetch = [&](int k0) {
 #if SA
 #pragma unroll
@@ -171,7 +281,6 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
 #endif
     };
 
-    const int tiles = K / KWG;
 #if SA || SB
     fetch(0);
     stash(0);
@@ -184,41 +293,14 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
 #if SA || SB
         if (t + 1 < tiles) fetch(k0 + KWG);
 #endif
-#pragma unroll 1
-        for (int kw = 0; kw < KWG; kw += KWI) {
-#pragma unroll
-            for (int ki = 0; ki < KWI; ++ki) {
-                const int k = kw + ki;
-                vm_t af[MWI / VWM];
-                vn_t bf[NWI / VWN];
-#pragma unroll
-                for (int w = 0; w < MWI / VWM; ++w) {
-#if SA
-                    af[w] = a_sm[buf][k][frag_m(tm, w)];
-#else
-                    af[w] = __ldg(at_v + (size_t)(k0 + k) * lda_v + m0 / VWM + frag_m(tm, w));
-#endif
-                }
-#pragma unroll
-                for (int w = 0; w < NWI / VWN; ++w) {
-#if SB
-                    bf[w] = b_sm[buf][k][frag_n(tn, w)];
-#else
-                    bf[w] = __ldg(b_v + (size_t)(k0 + k) * ldb_v + n0 / VWN + frag_n(tn, w));
-#endif
-                }
-#pragma unroll
-                for (int i = 0; i < MWI; ++i)
-#pragma unroll
-                    for (int j = 0; j < NWI; ++j)
-                        acc[i][j] = fmaf(lane(af[i / VWM], i % VWM), lane(bf[j / VWN], j % VWN), acc[i][j]);
-            }
-        }
+        mac_tile(buf, k0);
 #if SA || SB
         if (t + 1 < tiles) stash(buf ^ 1);
         __syncthreads();
 #endif
     }
+
+#endif
 
     // epilogue: C = alpha * acc + beta * C, VWN-wide row segments
 #pragma unroll

@@ -490,13 +490,13 @@ class SgemmProblem(KernelProblem):
                 "MWG": [64, 128, 256], "NWG": [64, 128, 256], "KWG": [8, 16, 32],
                 "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32, 64], "NDIMB": [8, 16, 32, 64],
                 "KWI": [1, 2, 4, 8], "VWM": [1, 2, 4], "VWN": [1, 2, 4], "STRM": [0, 1], "STRN": [0, 1],
-                "SA": [0, 1], "SB": [0, 1],
+                "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3, 4],
             }
         return {
             "MWG": [16, 32, 64, 128], "NWG": [16, 32, 64, 128], "KWG": [16, 32],
             "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32], "NDIMB": [8, 16, 32],
             "KWI": [2, 8], "VWM": [1, 2, 4, 8], "VWN": [1, 2, 4, 8], "STRM": [0, 1], "STRN": [0, 1],
-            "SA": [0, 1], "SB": [0, 1],
+            "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3],
         }
 
     def restrictions(self):
@@ -513,21 +513,26 @@ class SgemmProblem(KernelProblem):
             "(MDIMC * NDIMC) % MDIMA == 0",
             "(MDIMC * NDIMC) % NDIMB == 0",
             "VWM <= 4 and VWN <= 4",
-            "(SA * KWG * MWG + SB * KWG * NWG) * 2 * 4 <= 48 * 1024",
+            # ASYNC = 0: CLBlast's two static buffers (48 KB); ASYNC = S: S cp.async stages (dynamic, 227 KB)
+            "ASYNC == 0 or (SA == 1 and SB == 1)",
+            "(ASYNC == 0 and (SA * KWG * MWG + SB * KWG * NWG) * 2 * 4 <= 48 * 1024)"
+            " or (ASYNC > 0 and KWG * (MWG + NWG) * 4 * ASYNC <= 227 * 1024)",
             "(MWG / MDIMC) * (NWG / NDIMC) <= 128",
             f"{self.m} % MWG == 0 and {self.n} % NWG == 0 and {self.k} % KWG == 0",
         ]
 
     def default_config(self):
         return {"MWG": 128, "NWG": 128, "KWG": 16, "MDIMC": 16, "NDIMC": 16, "MDIMA": 32, "NDIMB": 32,
-                "KWI": 2, "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1}
+                "KWI": 2, "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 0}
 
     def defines(self, config):
         return dict(_as_dict(config))
 
     def launch(self, config):
         c = _as_dict(config)
-        return Launch((self.m // c["MWG"], self.n // c["NWG"], 1), (c["MDIMC"] * c["NDIMC"], 1, 1))
+        stages = c.get("ASYNC", 0)
+        smem = c["KWG"] * (c["MWG"] + c["NWG"]) * 4 * stages  # dynamic cp.async stages (0: static buffers)
+        return Launch((self.m // c["MWG"], self.n // c["NWG"], 1), (c["MDIMC"] * c["NDIMC"], 1, 1), smem=smem)
 
     def host_inputs(self):
         a = np.random.default_rng(self.seed).uniform(-1.0, 1.0, (self.m, self.k)).astype(np.float32)

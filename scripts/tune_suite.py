@@ -66,11 +66,11 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
             "parameters": {
                 "MWG": [64, 128], "NWG": [64, 128], "KWG": [16, 32], "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32],
                 "MDIMA": [16, 32], "NDIMB": [16, 32], "KWI": [2, 8], "VWM": [2, 4], "VWN": [2, 4],
-                "STRM": [0, 1], "STRN": [0, 1], "SA": [1], "SB": [1],
+                "STRM": [0, 1], "STRN": [0, 1], "SA": [1], "SB": [1], "ASYNC": [0, 2, 3],
             },
             "restrictions": problem.restrictions(),
         }
-        return doc, "random", 300
+        return doc, "random", 400
     raise ValueError(name)
 
 

@@ -171,6 +171,11 @@ SGEMM_CONFIGS = [
     dict(MWG=128, NWG=64, KWG=16, MDIMC=16, NDIMC=8, MDIMA=32, NDIMB=8, KWI=2, VWM=2, VWN=2, SA=0, SB=1),
     dict(MWG=32, NWG=32, KWG=16, MDIMC=8, NDIMC=8, MDIMA=8, NDIMB=8, KWI=8, VWM=4, VWN=4, SA=0, SB=0),
     dict(MWG=128, NWG=128, KWG=16, MDIMC=32, NDIMC=8, MDIMA=32, NDIMB=32, KWI=2, VWM=4, VWN=4, STRM=0, STRN=1),
+    # cp.async stages (ASYNC): 2 and 3 stages, vector widths 1 / 2 / 4 (4-, 8- and 16-byte copies)
+    dict(MWG=128, NWG=128, KWG=32, MDIMC=16, NDIMC=16, MDIMA=32, NDIMB=32, KWI=8, VWM=4, VWN=4, ASYNC=2),
+    dict(MWG=128, NWG=64, KWG=32, MDIMC=16, NDIMC=8, MDIMA=16, NDIMB=16, KWI=8, VWM=4, VWN=4, STRN=0, ASYNC=3),
+    dict(MWG=64, NWG=64, KWG=16, MDIMC=16, NDIMC=16, MDIMA=16, NDIMB=16, KWI=2, VWM=1, VWN=2, STRM=0, ASYNC=2),
+    dict(MWG=32, NWG=64, KWG=16, MDIMC=8, NDIMC=8, MDIMA=8, NDIMB=16, KWI=8, VWM=2, VWN=1, ASYNC=3),
 ]
 
 
