@@ -88,6 +88,14 @@ def oracle_check(problem, cfg) -> tuple[bool, float]:
     return err <= (O.SGEMM_TF32_TOL if problem.name == "sgemm_tf32" else O.SGEMM_TOL), err
 
 
+SEEDS = {
+    "sgemm": [
+        {"MWG": 128, "NWG": 128, "KWG": 32, "MDIMC": 16, "NDIMC": 16, "MDIMA": 32, "NDIMB": 32, "KWI": 8, "VWM": 4,
+         "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 2},
+        {"MWG": 128, "NWG": 64, "KWG": 32, "MDIMC": 16, "NDIMC": 8, "MDIMA": 16, "NDIMB": 16, "KWI": 8, "VWM": 4,
+         "VWN": 4, "STRM": 1, "STRN": 0, "SA": 1, "SB": 1, "ASYNC": 2},
+    ],
+}
 CONFIRM_ENERGY, CONFIRM_TIME, CONFIRM_ROUNDS, CONFIRM_WINDOW, CONFIRM_SETTLE = 5, 3, 3, 1.0, 0.25
 
 
@@ -162,8 +170,15 @@ def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | No
         constants={"total_flops": problem.total_flops},
         cache=cache,
     )
+    # known-good seeds (hand-explored, scripts/time_sgemm.py) join the sampled configs
+    seeded = []
+    for seed_cfg in SEEDS.get(name, []):
+        one = SearchSpace.from_dict({"parameters": {k: [v] for k, v in seed_cfg.items()}})
+        seeded += run_strategy(TuningRun(one, "exhaustive", Objective("energy")), dev, [NVMLObserver(duration)],
+                               user_metrics=metrics, constants={"total_flops": problem.total_flops},
+                               cache=cache).history
     tune_s = time.time() - t0
-    ok = [r for r in outcome.history if not r.failed]
+    ok = [r for r in outcome.history + seeded if not r.failed]
     # The sweep's 0.4 s windows see only ~4 energy-counter updates, so near-equal configs
     # rank by noise. Re-measure the leaders with longer windows, interleaved round-robin
     # (so thermal drift hits every candidate alike), and pick the winners by median.
