@@ -249,14 +249,86 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: 
         out["roofline_frac_vs_burst"] = round(rate / tf32_peak_gflops(), 4)
         out["roofline_basis"] = ("MEASURED_PEAKS bf16_tflops_sustained / 2 (tcgen05 kind::tf32 issues K=8 per MMA vs "
                                  "K=16; loop runs power-capped like the sustained bf16 measurement)")
+    elif prob.roofline_kind == "hbm":
+        peaks = ROOT / "MEASURED_PEAKS.json"
+        hbm = (json.loads(peaks.read_text()) if peaks.exists() else {}).get("hbm_gbs") or 7700.0
+        gbs = prob.algorithmic_bytes / run.per_launch_s / 1e9
+        out["roofline_frac"] = round(gbs / hbm, 4)
+        out["roofline_basis"] = (f"HBM: {prob.algorithmic_bytes / 1e6:.1f} MB algorithmic (points + bitmap) per launch "
+                                 f"= {gbs:.0f} GB/s vs {hbm} GB/s (MEASURED_PEAKS hbm_gbs)")
     elif summ["sm_mhz"]:
         peak = fp32_peak_tflops(gpu.sm_count, summ["sm_mhz"]) * 1e3
         if prob.roofline_kind == "issue":
             peak /= 2.0  # 1 lane-instruction slot per lane per clock, not 2 flop/FFMA
         out["roofline_frac"] = round(rate / peak, 4)
-    if name == "pnpoly":
-        out["edge_tests_per_s"] = round(prob.edge_tests / run.per_launch_s, 1)
+    if name in ("pnpoly", "pnpoly_slab"):
+        out["edge_tests_per_s"] = round(prob.edge_tests / run.per_launch_s, 1)  # brute-force-equivalent
+    if name == "pnpoly_slab":
+        out["edges_evaluated_per_point"] = round(prob.useful_edge_tests() / prob.n_points, 2)
     for b in prob.buffers.values():
+        b.free()
+    return out
+
+
+#: the sharded tuning leg: a fixed slice of the conv2d space (strong scaling over ranks)
+TUNE_SPACE = {"block_size_x": [32, 64], "block_size_y": [4, 8], "tile_size_x": [2, 4, 8], "tile_size_y": [1, 2, 4],
+              "use_shmem": [0, 1], "use_padding": [0]}
+TUNE_WINDOW_S = 0.2  # launch loop per point: >= 2 energy-counter updates (~100 ms cadence)
+
+
+def tuning_leg(gpu, dist: Dist) -> dict:
+    """Tuning throughput: this rank's shard of a fixed (config) space through the reference API.
+
+    ``partition.plan`` deals the configs over the ranks (LPT); each
+    rank measures its shard on its own GPU with the NVML observer
+    (``run_strategy``'s evaluator, energy objective), writes a JSONL shard, and
+    rank 0 merges them on the filesystem after a barrier. Compilation happens
+    before the timed region. points/s = all points / slowest shard's seconds.
+    """
+    import tempfile
+
+    from paper_2211_07260_b200 import NVMLObserver, Objective, SearchSpace, default_metrics, partition
+    from paper_2211_07260_b200.b200 import B200Device
+    from paper_2211_07260_b200.kernels import make_problem
+
+    problem = make_problem("conv2d")
+    space = SearchSpace.from_dict({"parameters": TUNE_SPACE, "restrictions": problem.restrictions()})
+    shards = partition.plan(space, dist.world)
+    mine = shards[dist.rank]
+    with ThreadPoolExecutor(8) as pool:
+        list(pool.map(lambda c: problem.cubin({**problem.default_config(), **c.as_dict()}), mine.configs))
+    base = os.environ.get("BENCH_TUNE_DIR") or os.path.join(tempfile.gettempdir(),
+                                                            f"bench_tune_{os.environ.get('MASTER_PORT', 'solo')}")
+    workdir = Path(base)
+    if dist.rank == 0:
+        workdir.mkdir(parents=True, exist_ok=True)
+        for f in workdir.iterdir():
+            f.unlink()
+    dist.barrier()
+    device = B200Device(problem, gpu=gpu, min_window=TUNE_WINDOW_S)
+    stats = partition.run_shard(mine, device, [NVMLObserver(TUNE_WINDOW_S)], out=workdir / f"shard{dist.rank}.jsonl",
+                                user_metrics=default_metrics(problem.total_flops),
+                                constants={"total_flops": problem.total_flops})
+    dist.barrier()
+    slowest = dist.max(stats["seconds"])
+    points = len(space.enumerate())
+    out = {"space": "conv2d slice " + json.dumps(TUNE_SPACE, separators=(",", ":")), "points": points,
+           "window_s": TUNE_WINDOW_S, "points_per_s": round(points / slowest, 3), "slowest_shard_s": round(slowest, 2),
+           "shard_points": [s.points() for s in shards],
+           "timing": "wall clock of each rank's shard loop (compile excluded), max over ranks"}
+    if dist.rank == 0:
+        merged = partition.merge(space, [workdir / f"shard{r}.jsonl" for r in range(dist.world)],
+                                 objective=Objective("energy"))
+        ok = [r for r in merged.history if not r.failed]
+        best_t = min(ok, key=lambda r: r.time)
+        out["failed"] = len(merged.history) - len(ok)
+        out["energy_optimal"] = {"config": merged.best.config.as_dict(),
+                                 "gflops_per_w": round(merged.best.metrics.get("gflops_per_w", 0.0), 2),
+                                 "gflops": round(merged.best.metrics.get("gflops", 0.0), 1)}
+        out["time_optimal"] = {"config": best_t.config.as_dict(),
+                               "gflops_per_w": round(best_t.metrics.get("gflops_per_w", 0.0), 2),
+                               "gflops": round(best_t.metrics.get("gflops", 0.0), 1)}
+    for b in problem.buffers.values():
         b.free()
     return out
 
@@ -332,10 +404,12 @@ def run_ours(args, dist: Dist) -> int:
     e2e_single = e2e_rate(1)
     e2e_value = e2e_rate(E2E_STRIPS)
 
+    tuning = None if args.no_tune else tuning_leg(gpu, dist)
+
     # per-kernel tuned summaries (time- and energy-optimal) on this rank's GPU
     per_kernel = {}
     if dist.rank == 0 and not args.quick:
-        for name in ("conv2d", "pnpoly", "sgemm", "sgemm_tf32"):
+        for name in ("conv2d", "pnpoly", "pnpoly_slab", "sgemm", "sgemm_tf32"):
             per_kernel[name] = {obj: measure_tuned(gpu, name, obj) for obj in ("time_optimal", "energy_optimal")}
 
     cpu = None
@@ -399,6 +473,8 @@ def run_ours(args, dist: Dist) -> int:
             "gpu_launches": args.steps,
             "per_kernel": per_kernel,
         }
+        if tuning:
+            line["tuning"] = tuning
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))
@@ -413,6 +489,7 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--quick", action="store_true", help="skip per-kernel and CPU-baseline legs")
+    ap.add_argument("--no-tune", action="store_true", help="skip the sharded tuning-throughput leg")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

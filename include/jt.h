@@ -192,6 +192,37 @@ int jt_power_limit_reset(jt_ctx *ctx);
  * ybounds[2k..2k+1] = {min, max} of the edge's y range. Computed in IEEE
  * float32 with explicit fmaf so the device and the oracle see the same bits. */
 int jt_pnpoly_edges(const float *vx, const float *vy, int n, int method, float *edges, float *ybounds);
+/* PnPoly slab tables for csrc/kernels/pnpoly_slab.cu (exact point location
+ * by y-slab; the bitmap is bit-identical to the brute-force METHOD 2 crossing
+ * test). The sorted distinct vertex ordinates u[0..nu) cut the plane into
+ * nu+1 slabs; slab r = #{u <= py} holds exactly the edges whose y-range
+ * spans every py in [u[r-1], u[r]). `buckets` uniform y-buckets give each
+ * point a starting rank that the kernel corrects by exact compares.
+ * xbuckets = 0: each slab lists its edges as {slope, icpt} pairs (the
+ *   jt_pnpoly_edges METHOD 2 bits), padded to a multiple of `pad` with
+ *   never-crossing {0, -inf} fillers; the kernel tests every listed edge.
+ * xbuckets > 0: each slab's edges sorted by lo, the smallest computed crossing
+ *   abscissa fma(slope, py, icpt) over the slab (fma is monotone in py, so it
+ *   is the smaller of the two end values), with pmax = running max of hi; the
+ *   kernel counts {lo > px} (certain crossings) from a starting position
+ *   (xbuckets uniform x-buckets per slab over [lo_min, lo_max], uint16
+ *   positions) corrected by exact compares, and evaluates only edges with
+ *   lo <= px < hi. Records {slope, icpt, hi, 0}; {x0, xscale} per slab.
+ * Table words (4 B): u at u_off (nu floats), guess at guess_off (buckets
+ * int32), slab starts at band_off (nu+2 int32, in edges); x-search only:
+ * {x0, xscale} float pairs at xpar_off, uint16 [nu+1][xb+1] bucket starts at
+ * xst_off, lo / pmax at xlo_off / pmax_off; pairs / records at pair_off.
+ * table == NULL: fill `info` only (size query). The reference has no PnPoly
+ * code; this serves the B200 PnPoly suite. */
+typedef struct {
+    int nu, ng, ne, max_band;
+    int u_off, guess_off, band_off, pair_off, words;
+    float ybase, yscale;
+    int xlo_off, pmax_off, xpar_off, xst_off, xb;
+} jt_slab_info;
+int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pad, int xbuckets, float *table,
+                    long long capacity, jt_slab_info *info);
+
 /* TMA descriptor (CUtensorMap, 128 bytes written to out128) for a row-major
  * fp32 matrix [rows][cols] at dptr, tiles of box_rows x box_cols elements.
  * `swizzle` is a CUtensorMapSwizzle value: 0 none, 1 32B, 2 64B, 3 128B,

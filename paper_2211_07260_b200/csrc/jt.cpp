@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1006,6 +1007,156 @@ int jt_pnpoly_edges(const float *vx, const float *vy, int n, int method, float *
         }
         ybounds[2 * k] = std::min(vy[k], vy[p]);
         ybounds[2 * k + 1] = std::max(vy[k], vy[p]);
+    }
+    return JT_OK;
+}
+
+int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pad, int xbuckets, float *table,
+                    long long capacity, jt_slab_info *info) {
+    if (!vx || !vy || !info || n < 3) return fail(JT_EINVAL, "polygon needs >= 3 vertices");
+    if (buckets < 1 || buckets > (1 << 20)) return fail(JT_EINVAL, "bucket count %d out of range", buckets);
+    if (pad < 1 || pad > 64) return fail(JT_EINVAL, "band padding %d out of range", pad);
+    if (xbuckets < 0 || xbuckets > 4096) return fail(JT_EINVAL, "x-bucket count %d out of range", xbuckets);
+    const bool xsearch = xbuckets > 0;
+    // METHOD 2 edge records, bit for bit those of jt_pnpoly_edges
+    std::vector<float> slope(n), icpt(n), ylo(n), yhi(n);
+    for (int k = 0; k < n; ++k) {
+        if (std::isnan(vy[k]) || std::isnan(vx[k])) return fail(JT_EINVAL, "vertex %d is NaN", k);
+        const int p = (k + n - 1) % n;
+        const float dx = vx[p] - vx[k];
+        const float dy = vy[p] - vy[k];
+        volatile float s = dx / dy;
+        slope[k] = s;
+        icpt[k] = std::fmaf(-slope[k], vy[k], vx[k]);
+        ylo[k] = std::min(vy[k], vy[p]);
+        yhi[k] = std::max(vy[k], vy[p]);
+    }
+    // distinct vertex ordinates (IEEE equality: -0.0 == +0.0)
+    std::vector<float> u(vy, vy + n);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end(), [](float a, float b) { return a == b; }), u.end());
+    const int nu = (int)u.size();
+    // slab r = #{u <= py}: r = 0 and r = nu span nothing; slab r in [1, nu-1]
+    // holds every edge with ylo <= u[r-1] and yhi >= u[r], i.e. every edge
+    // whose (vy_k > py) != (vy_j > py) for all py in [u[r-1], u[r])
+    if (xsearch) pad = 1;
+    std::vector<int> off(nu + 2, 0);
+    std::vector<int> members;
+    std::vector<float> xlo, xhi;
+    int max_band = 0;
+    for (int r = 0; r <= nu; ++r) {
+        off[r] = (int)members.size();
+        if (r == 0 || r == nu) continue;
+        const size_t first = members.size();
+        for (int k = 0; k < n; ++k)
+            if (ylo[k] <= u[r - 1] && yhi[k] >= u[r]) members.push_back(k);
+        if (xsearch) {
+            // fma(slope, py, icpt) is monotone in py (a correctly rounded
+            // monotone function), so over the slab's py in [u[r-1], pred(u[r])]
+            // each edge's computed crossing abscissa lies in [lo, hi], its two
+            // end values. px < lo: the edge certainly crosses; px >= hi: it
+            // certainly does not; otherwise the kernel evaluates it. A NaN end
+            // value widens the interval to (-inf, +inf).
+            const float top = std::nextafter(u[r], -INFINITY);
+            std::vector<float> los, his;
+            for (size_t i = first; i < members.size(); ++i) {
+                const int k = members[i];
+                const float a = std::fmaf(slope[k], u[r - 1], icpt[k]);
+                const float b = std::fmaf(slope[k], top, icpt[k]);
+                const bool nan = std::isnan(a) || std::isnan(b);
+                los.push_back(nan ? -INFINITY : std::min(a, b));
+                his.push_back(nan ? INFINITY : std::max(a, b));
+            }
+            std::vector<int> idx(los.size());
+            for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+            std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return los[a] < los[b]; });
+            std::vector<int> sorted(idx.size());
+            for (size_t i = 0; i < idx.size(); ++i) {
+                sorted[i] = members[first + idx[i]];
+                xlo.push_back(los[idx[i]]);
+                xhi.push_back(his[idx[i]]);
+            }
+            std::copy(sorted.begin(), sorted.end(), members.begin() + first);
+        }
+        int cnt = (int)(members.size() - first);
+        for (; cnt % pad; ++cnt) members.push_back(-1);  // never-crossing filler
+        max_band = std::max(max_band, cnt);
+    }
+    off[nu + 1] = (int)members.size();
+    const int ne = (int)members.size();
+    auto up4 = [](long long w) { return (w + 3) / 4 * 4; };
+    info->nu = nu;
+    info->ng = buckets;
+    info->ne = ne;
+    info->max_band = max_band;
+    info->u_off = 0;
+    info->guess_off = (int)up4(nu);
+    info->band_off = info->guess_off + (int)up4(buckets);
+    info->xb = xbuckets;
+    if (xsearch) {
+        info->xpar_off = info->band_off + (int)up4(nu + 2);                 // {x0, xscale} per slab
+        info->xst_off = info->xpar_off + (int)up4(2 * (nu + 1));            // uint16 [nu+1][xb+1]
+        info->xlo_off = info->xst_off + (int)up4(((long long)(nu + 1) * (xbuckets + 1) + 1) / 2);
+        info->pmax_off = info->xlo_off + (int)up4(ne);
+        info->pair_off = info->pmax_off + (int)up4(ne);  // records {slope, icpt, hi, 0}
+        info->words = info->pair_off + 4 * ne;
+        if (max_band > 65535) return fail(JT_EINVAL, "slab of %d edges exceeds the uint16 x-bucket index", max_band);
+    } else {
+        info->xpar_off = info->xst_off = 0;
+        info->xlo_off = info->pmax_off = 0;
+        info->pair_off = info->band_off + (int)up4(nu + 2);  // pairs {slope, icpt}
+        info->words = info->pair_off + 2 * ne;
+    }
+    info->ybase = u[0];
+    info->yscale = nu > 1 && u[nu - 1] > u[0] ? (float)buckets / (u[nu - 1] - u[0]) : 0.f;
+    if (!table) return JT_OK;  // size query
+    if (capacity < info->words) return fail(JT_EINVAL, "slab table needs %d words, got %lld", info->words, capacity);
+    std::memset(table, 0, sizeof(float) * info->words);
+    std::memcpy(table + info->u_off, u.data(), sizeof(float) * nu);
+    int32_t *guess = reinterpret_cast<int32_t *>(table + info->guess_off);
+    for (int g = 0; g < buckets; ++g) {  // a starting rank only: the kernel corrects it exactly
+        const double y = (double)u[0] + (g + 0.5) / (info->yscale > 0 ? (double)info->yscale : 1.0);
+        guess[g] = (int)(std::upper_bound(u.begin(), u.end(), y, [](double a, float b) { return a < b; }) - u.begin());
+    }
+    std::memcpy(table + info->band_off, off.data(), sizeof(int) * (nu + 2));
+    if (xsearch) {
+        float *lo = table + info->xlo_off, *pm = table + info->pmax_off, *rec = table + info->pair_off;
+        float *xpar = table + info->xpar_off;
+        uint16_t *xst = reinterpret_cast<uint16_t *>(table + info->xst_off);
+        for (int r = 1; r < nu; ++r) {
+            float run = -INFINITY;
+            for (int i = off[r]; i < off[r + 1]; ++i) {
+                run = std::max(run, xhi[i]);
+                lo[i] = xlo[i];
+                pm[i] = run;  // max hi over the slab's edges up to and including i
+            }
+            // x-buckets: a starting position for #{lo <= px}, corrected exactly by the kernel
+            const int cnt = off[r + 1] - off[r];
+            if (!cnt) continue;
+            const float x0 = xlo[off[r]], x1 = xlo[off[r + 1] - 1];
+            const float scale = std::isfinite(x0) && std::isfinite(x1) && x1 > x0 ? (float)xbuckets / (x1 - x0) : 0.f;
+            xpar[2 * r] = std::isfinite(x0) ? x0 : 0.f;
+            xpar[2 * r + 1] = scale;
+            for (int k = 0; k <= xbuckets; ++k) {
+                const double edge = scale > 0 ? (double)x0 + k / (double)scale : -INFINITY;
+                int c = 0;
+                while (c < cnt && (double)xlo[off[r] + c] <= edge) ++c;
+                xst[(size_t)r * (xbuckets + 1) + k] = (uint16_t)c;
+            }
+        }
+        for (int i = 0; i < ne; ++i) {
+            const int k = members[i];
+            rec[4 * i] = slope[k];
+            rec[4 * i + 1] = icpt[k];
+            rec[4 * i + 2] = xhi[i];
+        }
+        return JT_OK;
+    }
+    float *pairs = table + info->pair_off;
+    for (int i = 0; i < ne; ++i) {
+        const int k = members[i];
+        pairs[2 * i] = k < 0 ? 0.f : slope[k];
+        pairs[2 * i + 1] = k < 0 ? -INFINITY : icpt[k];  // fma(0, py, -inf) = -inf: px < x never holds
     }
     return JT_OK;
 }

@@ -36,6 +36,7 @@ from .spaces import KernelConfig, SearchSpace
 __all__ = [
     "KernelProblem",
     "PnPolyProblem",
+    "PnPolySlabProblem",
     "Conv2DProblem",
     "SgemmProblem",
     "SgemmTF32Problem",
@@ -348,6 +349,158 @@ class PnPolyProblem(KernelProblem):
             edges, yb = self._tables[c["method"]]
             kernel.set_global("c_edges", edges)
             kernel.set_global("c_ybounds", yb)
+
+
+@dataclass
+class PnPolySlabProblem(PnPolyProblem):
+    """PnPoly by y-slab point location (csrc/kernels/pnpoly_slab.cu).
+
+    Same inputs and the same bitmap as :class:`PnPolyProblem` at METHOD 2
+    (bit for bit: the skipped edges are exactly those whose y-test fails), but
+    a different amount of work, so it is reported as its own kernel: its
+    roofline is HBM (the 240 MB of points and bitmap), and ``total_flops``
+    keeps the brute-force edge-test count so GFLOP/s compares 1:1 with the
+    brute-force kernel on the same output.
+    """
+
+    name: str = "pnpoly_slab"
+    source: str = "pnpoly_slab.cu"
+    symbol: str = "pnpoly_slab"
+
+    roofline_kind = "hbm"
+    #: slab lists are padded to a multiple of this (4 edges per trip of the edge loop)
+    pad = 4
+
+    def tune_params(self):
+        return {
+            "block_size_x": [128, 256, 512, 1024],
+            "tile": [1, 2, 4, 8],
+            "sort": [0, 1],
+            "pairs_smem": [0, 1],
+            "xbuckets": [0, 4, 8, 16],
+            "buckets": [1024, 4096],
+        }
+
+    def restrictions(self):
+        info = self.slab_info(4096)
+        xinfo = self.slab_info(4096, 4)
+        nu1 = info.nu + 1
+        head = (info.nu + 3) // 4 * 4 + (info.nu + 2 + 3) // 4 * 4
+        # x-search words past the slab starts: {x0, xscale}, uint16 bucket starts, lo, pmax
+        xfix = (2 * nu1 + 3) // 4 * 4 + 4 + 2 * ((xinfo.ne + 3) // 4 * 4)
+        limit = 227 * 1024
+        return [
+            "block_size_x * tile <= 8192",
+            "xbuckets == 0 or (sort == 0 and pairs_smem == 0)",
+            f"({head} + buckets + pairs_smem * {2 * info.ne} + sort * ({(info.nu + 4) // 4 * 4} + "
+            f"5 * block_size_x * tile) + (xbuckets > 0) * ({xfix} + {nu1} * (xbuckets + 1) / 2)) * 4 <= {limit}",
+        ]
+
+    def default_config(self):
+        return {"block_size_x": 1024, "tile": 8, "sort": 1, "pairs_smem": 0, "xbuckets": 0, "buckets": 4096}
+
+    @staticmethod
+    def formula(config) -> int:
+        return 2
+
+    def defines(self, config):
+        c = _as_dict(config)
+        return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "SORT": c["sort"],
+                "PAIRS_SMEM": c["pairs_smem"], "XSEARCH": int(c.get("xbuckets", 0) > 0)}
+
+    def _polygon(self):
+        inputs = getattr(self, "inputs", None)
+        if inputs is None:
+            inputs = self.host_inputs() if self.n_points <= (1 << 20) else self._vertices_only()
+        return inputs["vx"], inputs["vy"]
+
+    def _vertices_only(self):
+        rng = np.random.default_rng(self.seed)
+        theta = np.sort(rng.uniform(0.0, 2.0 * np.pi, self.n_vertices))
+        radius = 0.5 + 0.3 * rng.uniform(0.0, 1.0, self.n_vertices)
+        return {"vx": (radius * np.cos(theta)).astype(np.float32), "vy": (radius * np.sin(theta)).astype(np.float32)}
+
+    def slab_table(self, buckets: int, xbuckets: int = 0):
+        cache = self.__dict__.setdefault("_slab_tables", {})
+        if (buckets, xbuckets) not in cache:
+            vx, vy = self._polygon()
+            cache[buckets, xbuckets] = native.pnpoly_slabs(vx, vy, buckets, self.pad, xbuckets)
+        return cache[buckets, xbuckets]
+
+    def slab_info(self, buckets: int, xbuckets: int = 0):
+        return self.slab_table(buckets, xbuckets)[1]
+
+    def smem_bytes(self, config) -> int:
+        c = _as_dict(config)
+        info = self.slab_info(c["buckets"], c.get("xbuckets", 0))
+        words = info.words if c["pairs_smem"] else info.pair_off
+        if c["sort"]:
+            words += (info.nu + 4) // 4 * 4 + 5 * c["block_size_x"] * c["tile"]
+        return 4 * words
+
+    def launch(self, config, n_points: int | None = None):
+        c = _as_dict(config)
+        chunk = c["block_size_x"] * c["tile"]
+        chunks = max(1, math.ceil((self.n_points if n_points is None else n_points) / chunk))
+        smem = self.smem_bytes(c)
+        sms = self.gpu.sm_count if self.gpu is not None else 148
+        resident = max(1, min(2048 // c["block_size_x"], (228 * 1024) // (smem + 1024)))
+        return Launch((min(chunks, sms * resident), 1, 1), (c["block_size_x"], 1, 1), smem)
+
+    def prepare(self, gpu, inputs=None):
+        self.gpu = gpu
+        inputs = inputs or self.host_inputs()
+        self.inputs = inputs
+        self.__dict__.pop("_slab_tables", None)
+        self.buffers = {
+            "out": gpu.empty((self.n_points,), np.int32),
+            "points": gpu.array(inputs["points"], slack=16),
+        }
+
+    def _table_buffer(self, buckets: int, xbuckets: int):
+        key = f"slabs{buckets}x{xbuckets}"
+        if key not in self.buffers:
+            self.buffers[key] = self.gpu.array(self.slab_table(buckets, xbuckets)[0])
+        return self.buffers[key]
+
+    def _tail(self, c):
+        xb = c.get("xbuckets", 0)
+        info = self.slab_info(c["buckets"], xb)
+        staged = info.words if c["pairs_smem"] else info.pair_off
+        return [self._table_buffer(c["buckets"], xb), i32(info.nu), i32(info.ng), i32(info.band_off),
+                i32(info.pair_off), i32(staged), f32(info.ybase), f32(info.yscale), i32(info.xlo_off),
+                i32(info.pmax_off), i32(info.xpar_off), i32(info.xst_off), i32(info.xb)]
+
+    def args(self, config):
+        c = _as_dict(config)
+        return [self.buffers["out"], self.buffers["points"], i32(self.n_points), *self._tail(c)]
+
+    def strips(self, config, uploads, out, n):
+        c = _as_dict(config)
+        points, per_block = uploads["points"], c["block_size_x"] * c["tile"]
+        size = max(per_block, math.ceil(self.n_points / n / per_block) * per_block)
+        tail = self._tail(c)
+        plan = []
+        for p0 in range(0, self.n_points, size):
+            p1 = min(self.n_points, p0 + size)
+            dst = rows(self.buffers["points"], p0, p1)
+            res = rows(self.buffers["out"], p0, p1)
+            plan.append(Strip([(dst, points[p0:p1])], self.launch(c, p1 - p0), [res, dst, i32(p1 - p0), *tail],
+                              [(out[p0:p1], res)]))
+        return plan
+
+    def bind(self, kernel, config):
+        pass
+
+    def useful_edge_tests(self) -> float:
+        """Edges listed for the points' slabs on this input (incl. padding): what the
+        edge-loop variants (xbuckets=0) evaluate per point."""
+        info = self.slab_info(4096)
+        table = self.slab_table(4096)[0]
+        u = table[info.u_off:info.u_off + info.nu]
+        band = table[info.band_off:info.band_off + info.nu + 2].view(np.int32)
+        r = np.searchsorted(u, self.inputs["points"][:, 1], side="right")
+        return float((band[r + 1] - band[r]).astype(np.int64).sum())
 
 
 # -- Conv2D -------------------------------------------------------------------------------
@@ -701,7 +854,7 @@ class BurnerProblem(KernelProblem):
         return [self.buffers["sink"], i32(self.iters), f32(1.0)]
 
 
-PROBLEMS = {"pnpoly": PnPolyProblem, "conv2d": Conv2DProblem, "sgemm": SgemmProblem, "sgemm_tf32": SgemmTF32Problem,
+PROBLEMS = {"pnpoly": PnPolyProblem, "pnpoly_slab": PnPolySlabProblem, "conv2d": Conv2DProblem, "sgemm": SgemmProblem, "sgemm_tf32": SgemmTF32Problem,
             "burner": BurnerProblem}
 
 

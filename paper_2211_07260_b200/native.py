@@ -53,8 +53,18 @@ EXPORTS = (
     "jt_app_clocks_set", "jt_app_clocks_reset", "jt_power_limit_set", "jt_power_limit_reset",
     "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
     "jt_h2d_async", "jt_d2h_async", "jt_tensor_map_2d", "jt_streams_reserve", "jt_stream_select",
-    "jt_stream_wait_event",
+    "jt_stream_wait_event", "jt_pnpoly_slabs",
 )
+
+
+class JTSlabInfo(ctypes.Structure):
+    _fields_ = [
+        ("nu", ctypes.c_int), ("ng", ctypes.c_int), ("ne", ctypes.c_int), ("max_band", ctypes.c_int),
+        ("u_off", ctypes.c_int), ("guess_off", ctypes.c_int), ("band_off", ctypes.c_int), ("pair_off", ctypes.c_int),
+        ("words", ctypes.c_int), ("ybase", ctypes.c_float), ("yscale", ctypes.c_float),
+        ("xlo_off", ctypes.c_int), ("pmax_off", ctypes.c_int), ("xpar_off", ctypes.c_int), ("xst_off", ctypes.c_int),
+        ("xb", ctypes.c_int),
+    ]
 
 
 class JTDeviceInfo(ctypes.Structure):
@@ -226,6 +236,8 @@ def _declare(lib) -> None:
         "jt_power_limit_set": (c.c_int, [P, c.c_uint]),
         "jt_power_limit_reset": (c.c_int, [P]),
         "jt_pnpoly_edges": (c.c_int, [P, P, c.c_int, c.c_int, P, P]),
+        "jt_pnpoly_slabs": (c.c_int, [P, P, c.c_int, c.c_int, c.c_int, c.c_int, P, c.c_longlong,
+                                      c.POINTER(JTSlabInfo)]),
         "jt_module_set_global": (c.c_int, [P, P, c.c_char_p, P, c.c_size_t]),
     }
     for name, (res, args) in sig.items():
@@ -349,3 +361,20 @@ def pnpoly_edges(vx, vy, method: int):
         "jt_pnpoly_edges",
     )
     return edges, ybounds
+
+
+def pnpoly_slabs(vx, vy, buckets: int, pad: int, xbuckets: int = 0):
+    """Slab table for csrc/kernels/pnpoly_slab.cu (libjt ``jt_pnpoly_slabs``):
+    returns (table as float32 words, JTSlabInfo)."""
+    import numpy as np
+
+    vx = np.ascontiguousarray(vx, dtype=np.float32)
+    vy = np.ascontiguousarray(vy, dtype=np.float32)
+    info = JTSlabInfo()
+    L = lib()
+    check(L.jt_pnpoly_slabs(vx.ctypes.data, vy.ctypes.data, vx.size, int(buckets), int(pad), int(xbuckets), None, 0,
+                            ctypes.byref(info)), "jt_pnpoly_slabs")
+    table = np.zeros(info.words, dtype=np.float32)
+    check(L.jt_pnpoly_slabs(vx.ctypes.data, vy.ctypes.data, vx.size, int(buckets), int(pad), int(xbuckets), table.ctypes.data,
+                            table.size, ctypes.byref(info)), "jt_pnpoly_slabs")
+    return table, info

@@ -1,0 +1,99 @@
+"""PnPoly slab kernel (csrc/kernels/pnpoly_slab.cu) on the B200 through libjt:
+bit-exact against the brute-force oracle formulation 2 (oracle/pnpoly_oracle.c)."""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import kernels_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SLAB_CONFIGS = (
+    [dict(block_size_x=b, tile=t, sort=s, pairs_smem=ps, xbuckets=0, buckets=4096)
+     for b, t, s, ps in itertools.product((128, 512, 1024), (1, 4, 8), (0, 1), (0, 1))
+     if not (ps and s and b * t > 2048)]
+    + [dict(block_size_x=256, tile=8, sort=1, pairs_smem=0, xbuckets=0, buckets=1024),
+       dict(block_size_x=1024, tile=8, sort=1, pairs_smem=0, xbuckets=0, buckets=1024)]
+    + [dict(block_size_x=b, tile=t, sort=0, pairs_smem=0, xbuckets=x, buckets=g)
+       for b, t, x, g in itertools.product((128, 512, 1024), (1, 4, 8), (4, 16), (1024, 4096))]
+)
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    from paper_2211_07260_b200.gpu import GPU
+
+    g = GPU(0)
+    yield g
+    g.close()
+
+
+def run_once(gpu, problem, cfg):
+    k = problem.kernel(cfg)
+    problem.reset_output()
+    gpu.launch(k, problem.launch(cfg), problem.args(cfg))
+    gpu.synchronize()
+    return problem.fetch_output()
+
+
+@pytest.fixture(scope="module")
+def slab_small(gpu):
+    from paper_2211_07260_b200.kernels import PnPolySlabProblem
+
+    p = PnPolySlabProblem(n_points=1_000_003)
+    p.prepare(gpu)
+    return p, O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
+
+
+@pytest.mark.parametrize("cfg", SLAB_CONFIGS, ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
+def test_slab_bit_exact_across_configs(gpu, slab_small, cfg):
+    p, want = slab_small
+    assert p.is_valid(cfg)
+    got = run_once(gpu, p, cfg)
+    assert np.array_equal(got, want), f"{int((got != want).sum())} points differ"
+
+
+@pytest.mark.parametrize("n", [1, 7, 4097])
+def test_slab_tiny_and_ragged_inputs(gpu, n):
+    from paper_2211_07260_b200.kernels import PnPolySlabProblem
+
+    p = PnPolySlabProblem(n_points=n)
+    p.prepare(gpu)
+    for cfg in (p.default_config(), dict(p.default_config(), sort=0, tile=1)):
+        np.testing.assert_array_equal(run_once(gpu, p, cfg),
+                                      O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2))
+
+
+def test_slab_degenerate_points_and_polygon(gpu):
+    """Points on vertices / edges / at vertex ordinates, +-0.0, +-inf and NaN
+    coordinates; a polygon with horizontal edges and a repeated vertex."""
+    from paper_2211_07260_b200.kernels import PnPolySlabProblem
+
+    vx = np.array([0.0, 0.5, 0.5, 1.0, 1.0, 0.0, 0.0], np.float32)
+    vy = np.array([0.0, 0.0, 0.25, 0.25, 1.0, 1.0, 1.0], np.float32)
+    special = [0.0, -0.0, np.inf, -np.inf, np.nan, 0.25, 0.75, -0.5, 1.5]
+    xs = np.concatenate([vx, vx + 1e-7, vx - 1e-7, special]).astype(np.float32)
+    ys = np.concatenate([vy, vy + 1e-7, vy - 1e-7, special]).astype(np.float32)
+    pts = np.array([[x, y] for x in xs for y in ys], np.float32)
+    p = PnPolySlabProblem(n_points=len(pts), n_vertices=vx.size)
+    p.prepare(gpu, {"points": pts, "vx": vx, "vy": vy})
+    want = O.pnpoly(pts, vx, vy, 2)
+    for cfg in SLAB_CONFIGS[::3]:
+        np.testing.assert_array_equal(run_once(gpu, p, cfg), want, err_msg=str(cfg))
+
+
+def test_slab_matches_brute_force_kernel_full_size(gpu):
+    """20 M points x 600 vertices: the slab bitmap equals the oracle's formulation 2
+    (the precomputed slope / intercept form the brute-force METHOD 2 kernel computes)."""
+    from paper_2211_07260_b200 import tuned
+    from paper_2211_07260_b200.kernels import PnPolySlabProblem
+
+    p = PnPolySlabProblem()
+    p.prepare(gpu)
+    want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
+    for cfg in {str(c): c for c in [p.default_config(), tuned.best_config("pnpoly_slab"),
+                                    tuned.best_config("pnpoly_slab", "energy_optimal")] if c}.values():
+        got = run_once(gpu, p, cfg)
+        assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ ({cfg})"

@@ -1,0 +1,151 @@
+"""CPU checks of the PnPoly slab table (libjt ``jt_pnpoly_slabs``, no GPU needed).
+
+The slab kernel is bit-exact with the brute-force METHOD 2 kernel iff, for
+every point, the list of slab r = #{u <= py} is exactly the set of edges whose
+y-test ``(vy_k > py) != (vy_j > py)`` holds, with the same slope / intercept
+bits. Both are checked here on the benchmark polygon and on degenerate ones.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2211_07260_b200 import native
+from paper_2211_07260_b200.kernels import PnPolySlabProblem
+
+
+def _decode(table, info):
+    u = table[info.u_off:info.u_off + info.nu]
+    guess = table[info.guess_off:info.guess_off + info.ng].view(np.int32)
+    band = table[info.band_off:info.band_off + info.nu + 2].view(np.int32)
+    pairs = table[info.pair_off:info.pair_off + 2 * info.ne].reshape(-1, 2)
+    return u, guess, band, pairs
+
+
+def _kernel_rank(py, u, guess, info):
+    """slab_of() of pnpoly_slab.cu, step for step in float32."""
+    if math.isnan(py):
+        return 0
+    f = np.float32(np.float32(py) - np.float32(info.ybase)) * np.float32(info.yscale)
+    g = int(np.clip(np.trunc(np.nan_to_num(f, posinf=2**31 - 1, neginf=-2**31)), -2**31, 2**31 - 1))
+    r = guess[min(max(g, 0), info.ng - 1)]
+    while r < info.nu and u[r] <= py:
+        r += 1
+    while r > 0 and u[r - 1] > py:
+        r -= 1
+    return int(r)
+
+
+POLYGONS = {
+    "benchmark": None,
+    "horizontal+repeated": (np.array([0.0, 0.5, 0.5, 1.0, 1.0, 0.0, 0.0], np.float32),
+                            np.array([0.0, 0.0, 0.25, 0.25, 1.0, 1.0, 1.0], np.float32)),
+    "signed-zeros": (np.array([-1.0, 1.0, 1.0, -1.0], np.float32), np.array([-0.0, 0.0, 1.0, 1.0], np.float32)),
+    "comb": (np.array([0, 4, 4, 3, 3, 2, 2, 1, 1, 0], np.float32),
+             np.array([0, 0, 3, 3, 1, 1, 3, 3, 1, 1], np.float32)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(POLYGONS))
+@pytest.mark.parametrize("buckets", [1, 7, 4096])
+def test_slab_lists_equal_the_y_test(name, buckets):
+    if POLYGONS[name] is None:
+        p = PnPolySlabProblem(n_points=4096)
+        vx, vy = p._polygon()
+    else:
+        vx, vy = POLYGONS[name]
+    table, info = native.pnpoly_slabs(vx, vy, buckets, 4)
+    u, guess, band, pairs = _decode(table, info)
+    edges, _ = native.pnpoly_edges(vx, vy, 2)  # {vy_k, icpt, slope, 0}: the brute-force kernel's bits
+    n = vx.size
+    prev = np.roll(vy, 1)
+    rng = np.random.default_rng(0)
+    probes = np.concatenate([vy, np.nextafter(vy, np.inf), np.nextafter(vy, -np.inf),
+                             rng.uniform(vy.min() - 1, vy.max() + 1, 300).astype(np.float32),
+                             np.array([np.inf, -np.inf, np.nan, 0.0, -0.0], np.float32)]).astype(np.float32)
+    for py in probes:
+        r = _kernel_rank(py, u, guess, info)
+        assert r == (0 if math.isnan(py) else int(np.searchsorted(u, py, side="right")))
+        listed = pairs[band[r]:band[r + 1]]
+        assert len(listed) % 4 == 0
+        real = listed[~np.isneginf(listed[:, 1])]
+        fillers = listed[np.isneginf(listed[:, 1])]
+        assert np.all(fillers[:, 0] == 0)
+        spans = [k for k in range(n) if (vy[k] > py) != (prev[k] > py)]
+        want = np.array([[edges[k, 2], edges[k, 1]] for k in spans], np.float32).reshape(-1, 2)
+        assert real.view(np.uint32).tolist() == want.view(np.uint32).tolist(), (name, float(py), r)
+    assert info.max_band == max(band[r + 1] - band[r] for r in range(info.nu + 1))
+
+
+def test_slab_table_size_query_and_errors():
+    vx = np.array([0, 1, 0], np.float32)
+    vy = np.array([0, 0, 1], np.float32)
+    table, info = native.pnpoly_slabs(vx, vy, 16, 4)
+    assert info.words == table.size and info.nu == 2 and info.ne == 4
+    with pytest.raises(Exception):
+        native.pnpoly_slabs(vx[:2], vy[:2], 16, 4)
+    with pytest.raises(Exception):
+        native.pnpoly_slabs(vx, vy, 0, 4)
+
+
+def test_slab_space_fits_shared_memory():
+    p = PnPolySlabProblem()
+    for cfg in p.space().enumerate():
+        assert p.smem_bytes(cfg.as_dict()) <= 227 * 1024
+    assert p.is_valid(p.default_config())
+
+
+@pytest.mark.parametrize("name", sorted(POLYGONS))
+def test_xsearch_table_decides_like_the_brute_force_test(name):
+    """x-search layout: per slab, lo sorted ascending, pmax = running max of hi, and for
+    every probe point the kernel's decision procedure (count lo > px, then evaluate the
+    undecided edges walking back while pmax > px) equals the brute-force parity.
+    The fma is emulated exactly in float64 (a float32 x float32 product is exact)."""
+    if POLYGONS[name] is None:
+        p = PnPolySlabProblem(n_points=4096)
+        vx, vy = p._polygon()
+    else:
+        vx, vy = POLYGONS[name]
+    table, info = native.pnpoly_slabs(vx, vy, 64, 4, 8)
+    u, guess, band, _ = _decode(table, info)
+    xlo = table[info.xlo_off:info.xlo_off + info.ne]
+    pmax = table[info.pmax_off:info.pmax_off + info.ne]
+    rec = table[info.pair_off:info.pair_off + 4 * info.ne].reshape(-1, 4)
+    for r in range(1, info.nu):
+        lo, pm = xlo[band[r]:band[r + 1]], pmax[band[r]:band[r + 1]]
+        assert np.all(np.diff(lo) >= 0) and np.all(pm == np.maximum.accumulate(rec[band[r]:band[r + 1], 2]))
+        assert np.all(rec[band[r]:band[r + 1], 2] >= lo)
+    xst = table[info.xst_off:].view(np.uint16)[:(info.nu + 1) * (info.xb + 1)].reshape(info.nu + 1, info.xb + 1)
+    for r in range(1, info.nu):
+        cnt = band[r + 1] - band[r]
+        assert np.all(np.diff(xst[r].astype(int)) >= 0) and xst[r].max() <= cnt
+    edges, _ = native.pnpoly_edges(vx, vy, 2)
+    prev = np.roll(vy, 1)
+
+    def fma32(a, b, c):  # exact product in float64, one rounding of the sum: equals fmaf
+        return np.float32(np.float64(a) * np.float64(b) + np.float64(c))
+
+    rng = np.random.default_rng(1)
+    span = float(max(abs(vx).max(), abs(vy).max())) + 0.5
+    pts = rng.uniform(-span, span, (3000, 2)).astype(np.float32)
+    pts[:len(vx), 1] = vy  # points exactly at vertex ordinates / abscissae
+    pts[len(vx):2 * len(vx), 0] = vx
+    for px, py in pts:
+        want = 0
+        for k in range(vx.size):
+            if (vy[k] > py) != (prev[k] > py) and px < fma32(edges[k, 2], py, edges[k, 1]):
+                want ^= 1
+        r = int(np.searchsorted(u, py, side="right"))
+        got = 0
+        if 0 < r < info.nu:
+            b, c = band[r], band[r + 1] - band[r]
+            pos = int(np.sum(xlo[b:b + c] <= px))
+            got = (c - pos) & 1
+            j = pos - 1
+            while j >= 0 and pmax[b + j] > px:
+                sl, ic, hi, _ = rec[b + j]
+                if hi > px and px < fma32(sl, py, ic):
+                    got ^= 1
+                j -= 1
+        assert got == want, (name, float(px), float(py))
