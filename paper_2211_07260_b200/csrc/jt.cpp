@@ -1011,6 +1011,42 @@ int jt_pnpoly_edges(const float *vx, const float *vy, int n, int method, float *
     return JT_OK;
 }
 
+// The kernel's bucket index, op for op: min(max(__float2int_rz((v - base) * scale), 0), hi)
+// with cvt.rzi.s32 semantics (NaN -> 0, saturation at the int range). This
+// file is built with -ffp-contract=off, so (v - base) * scale rounds twice,
+// like __fsub_rn / __fmul_rn on the device.
+static int slab_bucket(float v, float base, float scale, int hi) {
+    const float f = (v - base) * scale;
+    long long k;
+    if (std::isnan(f)) k = 0;
+    else if (f >= 2147483647.f) k = 2147483647LL;
+    else if (f <= -2147483648.f) k = -2147483648LL;
+    else k = (long long)std::trunc(f);
+    return (int)std::min<long long>(std::max<long long>(k, 0), hi);
+}
+
+// Bucket starts with an exactness flag. vals: sorted ascending; bucket(v) is
+// monotone in v, so #{vals <= v} is constant over bucket g unless some value
+// and its float predecessor share bucket g. Exact buckets get that count and
+// `flag`; the others get #{bucket(val) < g} (a start the kernel corrects).
+static void slab_bucket_starts(const float *vals, int m, float base, float scale, int hi, unsigned flag,
+                               std::vector<unsigned> &out) {
+    out.assign(hi + 1, 0u);
+    std::vector<char> split(hi + 1, 0);
+    std::vector<int> at(m);
+    for (int i = 0; i < m; ++i) {
+        at[i] = slab_bucket(vals[i], base, scale, hi);
+        if (slab_bucket(std::nextafter(vals[i], -INFINITY), base, scale, hi) == at[i]) split[at[i]] = 1;
+    }
+    int below = 0, upto = 0;  // #{at < g}, #{at <= g}
+    for (int g = 0; g <= hi; ++g) {
+        while (below < m && at[below] < g) ++below;
+        upto = std::max(upto, below);
+        while (upto < m && at[upto] <= g) ++upto;
+        out[g] = split[g] ? (unsigned)below : ((unsigned)upto | flag);
+    }
+}
+
 int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pad, int xbuckets, float *table,
                     long long capacity, jt_slab_info *info) {
     if (!vx || !vy || !info || n < 3) return fail(JT_EINVAL, "polygon needs >= 3 vertices");
@@ -1094,13 +1130,13 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
     info->band_off = info->guess_off + (int)up4(buckets);
     info->xb = xbuckets;
     if (xsearch) {
-        info->xpar_off = info->band_off + (int)up4(nu + 2);                 // {x0, xscale} per slab
-        info->xst_off = info->xpar_off + (int)up4(2 * (nu + 1));            // uint16 [nu+1][xb+1]
+        info->xpar_off = info->band_off + (int)up4(nu + 2);                 // {b, cnt, x0, xscale} per slab
+        info->xst_off = info->xpar_off + 4 * (nu + 1);                      // uint16 [nu+1][xb+1]
         info->xlo_off = info->xst_off + (int)up4(((long long)(nu + 1) * (xbuckets + 1) + 1) / 2);
         info->pmax_off = info->xlo_off + (int)up4(ne);
         info->pair_off = info->pmax_off + (int)up4(ne);  // records {slope, icpt, hi, 0}
         info->words = info->pair_off + 4 * ne;
-        if (max_band > 65535) return fail(JT_EINVAL, "slab of %d edges exceeds the uint16 x-bucket index", max_band);
+        if (max_band > 32767) return fail(JT_EINVAL, "slab of %d edges exceeds the 15-bit x-bucket index", max_band);
     } else {
         info->xpar_off = info->xst_off = 0;
         info->xlo_off = info->pmax_off = 0;
@@ -1113,16 +1149,16 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
     if (capacity < info->words) return fail(JT_EINVAL, "slab table needs %d words, got %lld", info->words, capacity);
     std::memset(table, 0, sizeof(float) * info->words);
     std::memcpy(table + info->u_off, u.data(), sizeof(float) * nu);
-    int32_t *guess = reinterpret_cast<int32_t *>(table + info->guess_off);
-    for (int g = 0; g < buckets; ++g) {  // a starting rank only: the kernel corrects it exactly
-        const double y = (double)u[0] + (g + 0.5) / (info->yscale > 0 ? (double)info->yscale : 1.0);
-        guess[g] = (int)(std::upper_bound(u.begin(), u.end(), y, [](double a, float b) { return a < b; }) - u.begin());
-    }
+    // rank = #{u <= py} per y-bucket; bit 31 set: exact for every py of the bucket
+    std::vector<unsigned> starts;
+    slab_bucket_starts(u.data(), nu, info->ybase, info->yscale, buckets - 1, 0x80000000u, starts);
+    std::memcpy(table + info->guess_off, starts.data(), sizeof(unsigned) * buckets);
     std::memcpy(table + info->band_off, off.data(), sizeof(int) * (nu + 2));
     if (xsearch) {
         float *lo = table + info->xlo_off, *pm = table + info->pmax_off, *rec = table + info->pair_off;
         float *xpar = table + info->xpar_off;
         uint16_t *xst = reinterpret_cast<uint16_t *>(table + info->xst_off);
+        std::vector<unsigned> xs;
         for (int r = 1; r < nu; ++r) {
             float run = -INFINITY;
             for (int i = off[r]; i < off[r + 1]; ++i) {
@@ -1130,19 +1166,20 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
                 lo[i] = xlo[i];
                 pm[i] = run;  // max hi over the slab's edges up to and including i
             }
-            // x-buckets: a starting position for #{lo <= px}, corrected exactly by the kernel
+            // slab record {first edge, edge count, x0, xscale}; x-buckets: pos = #{lo <= px}
+            // per bucket, bit 15 set where it is exact (else a start the kernel corrects)
             const int cnt = off[r + 1] - off[r];
+            int32_t *srec = reinterpret_cast<int32_t *>(xpar + 4 * r);
+            srec[0] = off[r];
+            srec[1] = cnt;
             if (!cnt) continue;
             const float x0 = xlo[off[r]], x1 = xlo[off[r + 1] - 1];
             const float scale = std::isfinite(x0) && std::isfinite(x1) && x1 > x0 ? (float)xbuckets / (x1 - x0) : 0.f;
-            xpar[2 * r] = std::isfinite(x0) ? x0 : 0.f;
-            xpar[2 * r + 1] = scale;
-            for (int k = 0; k <= xbuckets; ++k) {
-                const double edge = scale > 0 ? (double)x0 + k / (double)scale : -INFINITY;
-                int c = 0;
-                while (c < cnt && (double)xlo[off[r] + c] <= edge) ++c;
-                xst[(size_t)r * (xbuckets + 1) + k] = (uint16_t)c;
-            }
+            const float base = std::isfinite(x0) ? x0 : 0.f;
+            xpar[4 * r + 2] = base;
+            xpar[4 * r + 3] = scale;
+            slab_bucket_starts(xlo.data() + off[r], cnt, base, scale, xbuckets, 0x8000u, xs);
+            for (int k = 0; k <= xbuckets; ++k) xst[(size_t)r * (xbuckets + 1) + k] = (uint16_t)xs[k];
         }
         for (int i = 0; i < ne; ++i) {
             const int k = members[i];

@@ -37,8 +37,12 @@
 //                 by the host with the same fmaf). Edges with lo > px cross
 //                 for every py of the slab, edges with hi <= px for none, so
 //                 parity = (#{lo > px} + crossings among lo <= px < hi) & 1.
-//                 pos = #{lo <= px} starts from a per-slab uniform x-bucket
-//                 (the table's xbuckets) and is corrected by exact compares;
+//                 pos = #{lo <= px} comes from a per-slab uniform x-bucket
+//                 (the table's xbuckets), exact where no lo falls inside the
+//                 bucket (flagged by the host), else corrected by compares;
+//                 the slab rank likewise comes from a y-bucket
+//                 (EXACT_FLAGS=0: ignore the host's exactness flags and
+//                 always run the correcting compares);
 //                 the undecided edges (about 0.05 per point on the benchmark
 //                 polygon) are found by walking back from pos while the
 //                 running max of hi (pmax) exceeds px, and are evaluated with
@@ -58,6 +62,9 @@
 #ifndef XSEARCH
 #define XSEARCH 0
 #endif
+#ifndef EXACT_FLAGS
+#define EXACT_FLAGS 1
+#endif
 #if XSEARCH && (SORT || PAIRS_SMEM)
 #error "XSEARCH=1 takes SORT=0 and PAIRS_SMEM=0"
 #endif
@@ -70,7 +77,9 @@ __device__ __forceinline__ int slab_of(float py, const float *u, const int *gues
     // any starting rank will do: the two loops below make it exact
     int g = __float2int_rz((py - ybase) * yscale);
     g = min(max(g, 0), ng - 1);
-    int r = guess[g];
+    const int gv = guess[g];  // bit 31: the rank is exact for every py of this bucket
+    int r = gv & 0x7fffffff;
+    if (gv < 0) return r;
     while (r < nu && u[r] <= py) ++r;
     while (r > 0 && u[r - 1] > py) --r;
     return r;
@@ -155,9 +164,9 @@ __device__ __forceinline__ int lds_u16(unsigned a) {
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
     return v;
 }
-__device__ __forceinline__ float2 lds_f32x2(unsigned a) {
-    float2 v;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+__device__ __forceinline__ float4 lds_f32x4(unsigned a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
     return v;
 }
 
@@ -174,18 +183,24 @@ __device__ __forceinline__ int xsearch_point(float px, float py, const XTables &
     if (!(px == px) || !(py == py)) return 0;  // NaN: every compare is false
     int g = __float2int_rz(__fmul_rn(__fsub_rn(py, T.ybase), T.yscale));
     g = min(max(g, 0), T.ng - 1);
-    int r = lds_s32(T.guess + 4u * g);
-    while (r < T.nu && lds_f32(T.u + 4u * r) <= py) ++r;
-    while (r > 0 && lds_f32(T.u + 4u * r - 4u) > py) --r;
+    const int gv = lds_s32(T.guess + 4u * g);  // bit 31: the rank is exact for this bucket
+    int r = gv & 0x7fffffff;
+    if (!EXACT_FLAGS || gv >= 0) {
+        while (r < T.nu && lds_f32(T.u + 4u * r) <= py) ++r;
+        while (r > 0 && lds_f32(T.u + 4u * r - 4u) > py) --r;
+    }
     if (r == 0 || r >= T.nu) return 0;  // below / above every vertex: no edge spans
-    const int b = lds_s32(T.band + 4u * r), cnt = lds_s32(T.band + 4u * r + 4u) - b;
-    const float2 xp = lds_f32x2(T.xpar + 8u * r);
-    int k = __float2int_rz(__fmul_rn(__fsub_rn(px, xp.x), xp.y));
+    const float4 sr = lds_f32x4(T.xpar + 16u * r);  // {first edge, count, x0, xscale}
+    const int b = __float_as_int(sr.x), cnt = __float_as_int(sr.y);
+    int k = __float2int_rz(__fmul_rn(__fsub_rn(px, sr.z), sr.w));
     k = min(max(k, 0), T.xb);
-    int pos = lds_u16(T.xst + 2u * (r * (T.xb + 1) + k));  // a start; made exact below
+    const int w = lds_u16(T.xst + 2u * (r * (T.xb + 1) + k));  // bit 15: pos is exact
+    int pos = w & 0x7fff;
     const unsigned lo = T.xlo + 4u * b;
-    while (pos < cnt && lds_f32(lo + 4u * pos) <= px) ++pos;
-    while (pos > 0 && lds_f32(lo + 4u * pos - 4u) > px) --pos;
+    if (!EXACT_FLAGS || !(w & 0x8000)) {
+        while (pos < cnt && lds_f32(lo + 4u * pos) <= px) ++pos;
+        while (pos > 0 && lds_f32(lo + 4u * pos - 4u) > px) --pos;
+    }
     int in = (cnt - pos) & 1;  // lo > px: crosses for every py of the slab
     // undecided: lo <= px < hi; pmax[j] = max hi over the slab's first j+1 edges
     for (int j = pos - 1; j >= 0 && lds_f32(T.pmax + 4u * (b + j)) > px; --j) {

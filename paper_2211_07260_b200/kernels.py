@@ -378,6 +378,7 @@ class PnPolySlabProblem(PnPolyProblem):
             "sort": [0, 1],
             "pairs_smem": [0, 1],
             "xbuckets": [0, 4, 8, 16],
+            "exact_flags": [0, 1],
             "buckets": [1024, 4096],
         }
 
@@ -386,18 +387,20 @@ class PnPolySlabProblem(PnPolyProblem):
         xinfo = self.slab_info(4096, 4)
         nu1 = info.nu + 1
         head = (info.nu + 3) // 4 * 4 + (info.nu + 2 + 3) // 4 * 4
-        # x-search words past the slab starts: {x0, xscale}, uint16 bucket starts, lo, pmax
-        xfix = (2 * nu1 + 3) // 4 * 4 + 4 + 2 * ((xinfo.ne + 3) // 4 * 4)
+        # x-search words past the slab starts: slab records, uint16 bucket starts, lo, pmax
+        xfix = 4 * nu1 + 4 + 2 * ((xinfo.ne + 3) // 4 * 4)
         limit = 227 * 1024
         return [
             "block_size_x * tile <= 8192",
             "xbuckets == 0 or (sort == 0 and pairs_smem == 0)",
+            "xbuckets > 0 or exact_flags == 1",
             f"({head} + buckets + pairs_smem * {2 * info.ne} + sort * ({(info.nu + 4) // 4 * 4} + "
             f"5 * block_size_x * tile) + (xbuckets > 0) * ({xfix} + {nu1} * (xbuckets + 1) / 2)) * 4 <= {limit}",
         ]
 
     def default_config(self):
-        return {"block_size_x": 1024, "tile": 8, "sort": 1, "pairs_smem": 0, "xbuckets": 0, "buckets": 4096}
+        return {"block_size_x": 1024, "tile": 8, "sort": 1, "pairs_smem": 0, "xbuckets": 0, "exact_flags": 1,
+                "buckets": 4096}
 
     @staticmethod
     def formula(config) -> int:
@@ -406,7 +409,8 @@ class PnPolySlabProblem(PnPolyProblem):
     def defines(self, config):
         c = _as_dict(config)
         return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "SORT": c["sort"],
-                "PAIRS_SMEM": c["pairs_smem"], "XSEARCH": int(c.get("xbuckets", 0) > 0)}
+                "PAIRS_SMEM": c["pairs_smem"], "XSEARCH": int(c.get("xbuckets", 0) > 0),
+                "EXACT_FLAGS": c.get("exact_flags", 1)}
 
     def _polygon(self):
         inputs = getattr(self, "inputs", None)

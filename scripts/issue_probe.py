@@ -1,0 +1,157 @@
+"""Issue-rate microbenchmarks behind the PnPoly brute-force ceiling.
+
+Each probe is a loop of independent chains of one instruction form (inline
+PTX, so ptxas emits exactly that SASS op), run by 148 x 4 blocks of 256
+threads (16 warps per SMSP). Every warp times its loop with clock64; the
+issue rate per SMSP is warps_per_smsp x instructions_per_iteration x iters /
+cycles. Forms:
+
+  ffma_rrr   FFMA with three distinct register sources
+  ffma_rri   FFMA with an immediate multiplicand (2 register sources)
+  fadd_rr    FADD, two register sources
+  fadd2_bc   FADD2 {s, s} - pair (the ASM 7 form: broadcast scalar + pair)
+  ffma2_bc   FFMA2 pair * {s, s} + pair
+  lop3_rrr   LOP3 with three register sources
+  lop3_rri   LOP3 with two register sources and an immediate
+  mix_f2_lop one FADD2 (broadcast form) + one 3-register LOP3 per chain step
+  mix_f_lop  one FADD + one 3-register LOP3 per chain step
+
+The SASS op counts of each probe's loop (cuobjdump) are printed with it, so a
+rate can be read per SASS instruction actually issued.
+
+    python scripts/issue_probe.py            (prints one JSON line per form)
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2211_07260_b200 import native  # noqa: E402
+from paper_2211_07260_b200.gpu import GPU, Launch, f32, i32  # noqa: E402
+
+CHAINS = 8
+UNROLL = 4  # body repeats per loop trip (the 3-instruction loop overhead is amortised)
+FORMS = {
+    # name: (per-chain PTX body using %c (chain reg) and per-chain invariants, instrs per chain per iter, regs)
+    "ffma_rrr": ("fma.rn.f32 c{k}, c{k}, x{k}, y{k};", 1),
+    "ffma_rri": ("fma.rn.f32 c{k}, c{k}, 0f3F800001, y{k};", 1),
+    "fadd_rr": ("add.rn.f32 c{k}, c{k}, x{k};", 1),
+    "fadd2_bc": ("mov.b64 t{k}, {{s, s}};\nsub.rn.f32x2 p{k}, t{k}, p{k};", 1),
+    "ffma2_bc": ("mov.b64 t{k}, {{s, s}};\nfma.rn.f32x2 p{k}, p{k}, t{k}, q{k};", 1),
+    "lop3_rrr": ("lop3.b32 u{k}, u{k}, v{k}, w{k}, 0x96;", 1),
+    "lop3_rri": ("lop3.b32 u{k}, u{k}, v{k}, 0x5A5A5A5A, 0x96;", 1),
+    "mix_f2_lop": ("mov.b64 t{k}, {{s, s}};\nsub.rn.f32x2 p{k}, t{k}, p{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x96;", 2),
+    "mix_f_lop": ("add.rn.f32 c{k}, c{k}, x{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x96;", 2),
+}
+
+TEMPLATE = r"""
+extern "C" __global__ void __launch_bounds__(256) probe(unsigned long long *cycles, float *sink, int iters, float s_in) {
+    unsigned long long t0, t1;
+    float out;
+    asm volatile("{\n"
+        ".reg .f32 s, %s;\n.reg .b32 %s;\n.reg .b64 %s;\n.reg .pred lp;\n.reg .s32 it;\n"
+        "mov.f32 s, %%3;\n"
+        %s
+        "mov.u64 %%0, %%clock64;\n"
+        "mov.s32 it, %%4;\n"
+        "LOOP:\n"
+        %s
+        "sub.s32 it, it, 1;\n"
+        "setp.gt.s32 lp, it, 0;\n"
+        "@lp bra LOOP;\n"
+        "mov.u64 %%1, %%clock64;\n"
+        %s
+        "}\n" : "=l"(t0), "=l"(t1), "=f"(out) : "f"(s_in + 0.001f * threadIdx.x), "r"(iters));
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if ((threadIdx.x & 31) == 0) cycles[gw] = t1 - t0;
+    if (out == 12345.f) sink[threadIdx.x] = out;
+}
+"""
+
+
+def kernel_source(body: str) -> str:
+    f32 = ", ".join(f"c{k}, x{k}, y{k}" for k in range(CHAINS))
+    b32 = ", ".join(f"u{k}, v{k}, w{k}" for k in range(CHAINS))
+    b64 = ", ".join(f"p{k}, q{k}, t{k}" for k in range(CHAINS))
+    init = ""
+    for k in range(CHAINS):
+        init += (f"add.f32 c{k}, s, 0f3F8{k}0000;\nadd.f32 x{k}, s, 0f3F9{k}0000;\nadd.f32 y{k}, s, 0f3FA{k}0000;\n"
+                 f"mov.b32 u{k}, c{k};\nmov.b32 v{k}, x{k};\nmov.b32 w{k}, y{k};\n"
+                 f"mov.b64 p{k}, {{x{k}, y{k}}};\nmov.b64 q{k}, {{y{k}, c{k}}};\nmov.b64 t{k}, {{s, s}};\n")
+    loop = "".join(body.format(k=k) + "\n" for _ in range(UNROLL) for k in range(CHAINS))
+    fold = "mov.f32 %2, c0;\n"
+    for k in range(CHAINS):
+        fold += (f"add.f32 %2, %2, c{k};\nadd.f32 %2, %2, x{k};\nadd.f32 %2, %2, y{k};\n"
+                 f"{{ .reg .f32 a, b; mov.b64 {{a, b}}, p{k}; add.f32 %2, %2, a; add.f32 %2, %2, b; "
+                 f"mov.b64 {{a, b}}, q{k}; add.f32 %2, %2, a; }}\n"
+                 f"{{ .reg .b32 z; xor.b32 z, u{k}, v{k}; xor.b32 z, z, w{k}; cvt.rn.f32.u32 x{k}, z; "
+                 f"add.f32 %2, %2, x{k}; }}\n")
+    return TEMPLATE % (f32, b32, b64, cstr(init), cstr(loop), cstr(fold))
+
+
+def cstr(ptx: str) -> str:
+    """Multi-line PTX as concatenated C string literals."""
+    return "".join(f'"{line}\\n"\n' for line in ptx.splitlines() if line.strip())
+
+
+def loop_ops(cubin: bytes) -> dict:
+    """SASS op histogram of the timed loop (branch target .. backward branch)."""
+    import re
+    import subprocess
+    import tempfile
+    from collections import Counter
+
+    with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
+        f.write(cubin)
+        f.flush()
+        sass = subprocess.run(["cuobjdump", "-sass", f.name], capture_output=True, text=True).stdout
+    rows = []
+    for line in sass.splitlines():
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
+        if m:
+            rows.append((int(m.group(1), 16), m.group(2).strip()))
+    for i, (addr, ins) in enumerate(rows):
+        m = re.search(r"BRA(?:\.U)?\s+(?:!?U?P\d+,\s*)?0x([0-9a-f]+)", ins)
+        if m and m.group(1) and int(m.group(1), 16) < addr:
+            start = int(m.group(1), 16)
+            body = [x for a, x in rows if start <= a <= addr]
+            return dict(Counter((x.split()[1] if x.startswith("@") else x.split()[0]) for x in body))
+    return {}
+
+
+def main():
+    gpu = GPU(0)
+    sms = gpu.sm_count
+    blocks, threads, iters = sms * 4, 256, 4096
+    warps_per_smsp = blocks * threads // 32 / (sms * 4)
+    cycles = gpu.empty((blocks * threads // 32,), np.uint64)
+    sink = gpu.empty((threads,), np.float32)
+    for name, (body, per_chain) in FORMS.items():
+        src = kernel_source(body)
+        cubin = native.compile_cubin(src, f"probe_{name}", native._nvrtc_options({}))
+        k = gpu.load(cubin, "probe")
+        launch = Launch((blocks, 1, 1), (threads, 1, 1))
+        args = [cycles, sink, i32(iters), f32(1.5)]
+        gpu.launch(k, launch, args)
+        gpu.synchronize()
+        gpu.launch(k, launch, args)
+        gpu.synchronize()
+        cyc = cycles.download().astype(np.float64)
+        instrs = per_chain * CHAINS * UNROLL * iters
+        per_smsp = warps_per_smsp * instrs / float(np.median(cyc))
+        ops = loop_ops(cubin)
+        issued = sum(ops.values()) * iters * warps_per_smsp / float(np.median(cyc))
+        print(json.dumps({"form": name, "instrs_per_trip_per_warp": per_chain * CHAINS * UNROLL,
+                          "sass_loop_ops": ops, "sass_issue_per_smsp_per_cycle": round(issued, 3),
+                          "warp_instr_per_smsp_per_cycle": round(per_smsp, 3),
+                          "median_cycles": float(np.median(cyc)), "warps_per_smsp": warps_per_smsp}), flush=True)
+    gpu.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -16,8 +16,8 @@ SLAB_CONFIGS = (
      if not (ps and s and b * t > 2048)]
     + [dict(block_size_x=256, tile=8, sort=1, pairs_smem=0, xbuckets=0, buckets=1024),
        dict(block_size_x=1024, tile=8, sort=1, pairs_smem=0, xbuckets=0, buckets=1024)]
-    + [dict(block_size_x=b, tile=t, sort=0, pairs_smem=0, xbuckets=x, buckets=g)
-       for b, t, x, g in itertools.product((128, 512, 1024), (1, 4, 8), (4, 16), (1024, 4096))]
+    + [dict(block_size_x=b, tile=t, sort=0, pairs_smem=0, xbuckets=x, exact_flags=f, buckets=g)
+       for b, t, x, f, g in itertools.product((128, 512, 1024), (1, 4, 8), (4, 16), (0, 1), (1024, 4096))]
 )
 
 
@@ -97,3 +97,19 @@ def test_slab_matches_brute_force_kernel_full_size(gpu):
                                     tuned.best_config("pnpoly_slab", "energy_optimal")] if c}.values():
         got = run_once(gpu, p, cfg)
         assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ ({cfg})"
+
+
+@pytest.mark.parametrize("strips", [1, 5])
+def test_slab_host_api_matches_brute_force(gpu, strips):
+    """suite.pnpoly(algorithm="slab") through pinned host buffers equals the brute-force call."""
+    from paper_2211_07260_b200 import suite
+    from paper_2211_07260_b200.kernels import PnPolyProblem
+
+    inp = PnPolyProblem(n_points=1_500_007).host_inputs()
+    pts = suite.pinned(inp["points"].shape, np.float32)
+    pts[...] = inp["points"]
+    slab = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips, algorithm="slab").copy()
+    brute = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips,
+                         config=dict(PnPolyProblem().default_config(), asm=0, method=2)).copy()
+    np.testing.assert_array_equal(slab, brute)
+    np.testing.assert_array_equal(slab, O.pnpoly(inp["points"], inp["vx"], inp["vy"], 2))

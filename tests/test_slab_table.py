@@ -23,13 +23,25 @@ def _decode(table, info):
     return u, guess, band, pairs
 
 
-def _kernel_rank(py, u, guess, info):
-    """slab_of() of pnpoly_slab.cu, step for step in float32."""
+def _bucket(v, base, scale, hi):
+    """min(max(__float2int_rz(__fmul_rn(__fsub_rn(v, base), scale)), 0), hi) in float32."""
+    with np.errstate(invalid="ignore", over="ignore"):
+        f = np.float32(np.float32(v) - np.float32(base)) * np.float32(scale)
+    g = 0 if math.isnan(f) else int(np.clip(np.trunc(np.nan_to_num(f, posinf=2**31 - 1, neginf=-2**31)),
+                                            -2**31, 2**31 - 1))
+    return min(max(g, 0), hi)
+
+
+def _kernel_rank(py, u, guess, info, check_exact=True):
+    """The kernel's slab rank: y-bucket start (bit 31 = exact), else corrected by compares."""
     if math.isnan(py):
         return 0
-    f = np.float32(np.float32(py) - np.float32(info.ybase)) * np.float32(info.yscale)
-    g = int(np.clip(np.trunc(np.nan_to_num(f, posinf=2**31 - 1, neginf=-2**31)), -2**31, 2**31 - 1))
-    r = guess[min(max(g, 0), info.ng - 1)]
+    gv = int(guess[_bucket(py, info.ybase, info.yscale, info.ng - 1)]) & 0xFFFFFFFF
+    r = gv & 0x7FFFFFFF
+    if gv & 0x80000000:
+        if check_exact:  # the flag promises the corrected value is already there
+            assert r == int(np.searchsorted(u, np.float32(py), side="right"))
+        return r
     while r < info.nu and u[r] <= py:
         r += 1
     while r > 0 and u[r - 1] > py:
@@ -117,9 +129,11 @@ def test_xsearch_table_decides_like_the_brute_force_test(name):
         assert np.all(np.diff(lo) >= 0) and np.all(pm == np.maximum.accumulate(rec[band[r]:band[r + 1], 2]))
         assert np.all(rec[band[r]:band[r + 1], 2] >= lo)
     xst = table[info.xst_off:].view(np.uint16)[:(info.nu + 1) * (info.xb + 1)].reshape(info.nu + 1, info.xb + 1)
+    srec = table[info.xpar_off:info.xpar_off + 4 * (info.nu + 1)].reshape(-1, 4)
     for r in range(1, info.nu):
         cnt = band[r + 1] - band[r]
-        assert np.all(np.diff(xst[r].astype(int)) >= 0) and xst[r].max() <= cnt
+        assert srec[r, :2].view(np.int32).tolist() == [band[r], cnt]
+        assert np.all((xst[r] & 0x7FFF) <= cnt)
     edges, _ = native.pnpoly_edges(vx, vy, 2)
     prev = np.roll(vy, 1)
 
@@ -136,11 +150,14 @@ def test_xsearch_table_decides_like_the_brute_force_test(name):
         for k in range(vx.size):
             if (vy[k] > py) != (prev[k] > py) and px < fma32(edges[k, 2], py, edges[k, 1]):
                 want ^= 1
-        r = int(np.searchsorted(u, py, side="right"))
+        r = 0 if math.isnan(py) else _kernel_rank(py, u, guess, info)
         got = 0
-        if 0 < r < info.nu:
+        if 0 < r < info.nu and not math.isnan(px):
             b, c = band[r], band[r + 1] - band[r]
             pos = int(np.sum(xlo[b:b + c] <= px))
+            w = int(xst[r, _bucket(px, srec[r, 2], srec[r, 3], info.xb)])
+            if w & 0x8000:  # flagged exact: the bucket's start must already be the count
+                assert (w & 0x7FFF) == pos, (name, float(px), float(py))
             got = (c - pos) & 1
             j = pos - 1
             while j >= 0 and pmax[b + j] > px:
