@@ -18,6 +18,10 @@
 //                 (identical booleans; different instruction shapes)
 //   POLY_SMEM     0: edge table in __constant__ memory; 1: staged in shared memory
 //   VERTICES      polygon size (compile-time so the edge loop is counted)
+//   MIN_BLOCKS    (optional) __launch_bounds__ minimum resident blocks per SM,
+//                 capping registers so more warps fit. Swept by
+//                 scripts/time_pnpoly_minb.py: no gain (occupancy is not what
+//                 limits ASM 7), so it is not in the tuning space.
 //   (launch)      persist=1 in the tuning space sizes the grid to the SMs'
 //                 residency and the kernel strides over point tiles
 //   ASM           1: hand-written PTX edge loop (needs BETWEEN=1, POLY_SMEM=1,
@@ -1536,7 +1540,11 @@ __device__ __forceinline__ float crossing_x(float4 e, float py) {
 #endif
 }
 
+#ifdef MIN_BLOCKS
+extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X, MIN_BLOCKS)
+#else
 extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X)
+#endif
 pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
        const float4 *__restrict__ g_edges, const float2 *__restrict__ g_ybounds,
        const float4 *__restrict__ g_packed) {

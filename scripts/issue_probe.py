@@ -15,6 +15,8 @@ cycles. Forms:
   lop3_rri   LOP3 with two register sources and an immediate
   mix_f2_lop one FADD2 (broadcast form) + one 3-register LOP3 per chain step
   mix_f_lop  one FADD + one 3-register LOP3 per chain step
+  asm7_edge2 the ASM 7 step for one point and two edges: FADD2, FFMA2, FADD2
+             (broadcast scalar operands) and three 3-register LOP3s
 
 The SASS op counts of each probe's loop (cuobjdump) are printed with it, so a
 rate can be read per SASS instruction actually issued.
@@ -47,6 +49,9 @@ FORMS = {
     "lop3_rri": ("lop3.b32 u{k}, u{k}, v{k}, 0x5A5A5A5A, 0x96;", 1),
     "mix_f2_lop": ("mov.b64 t{k}, {{s, s}};\nsub.rn.f32x2 p{k}, t{k}, p{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x96;", 2),
     "mix_f_lop": ("add.rn.f32 c{k}, c{k}, x{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x96;", 2),
+    "asm7_edge2": ("mov.b64 t{k}, {{s, s}};\nsub.rn.f32x2 p{k}, t{k}, p{k};\nfma.rn.f32x2 q{k}, p{k}, t{k}, q{k};\n"
+                   "sub.rn.f32x2 p{k}, t{k}, q{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x28;\n"
+                   "lop3.b32 v{k}, u{k}, v{k}, w{k}, 0x28;\nlop3.b32 w{k}, u{k}, v{k}, w{k}, 0x96;", 6),
 }
 
 TEMPLATE = r"""
@@ -68,7 +73,9 @@ extern "C" __global__ void __launch_bounds__(256) probe(unsigned long long *cycl
         %s
         "}\n" : "=l"(t0), "=l"(t1), "=f"(out) : "f"(s_in + 0.001f * threadIdx.x), "r"(iters));
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if ((threadIdx.x & 31) == 0) cycles[gw] = t1 - t0;
+    unsigned smid;
+    asm volatile("mov.u32 %%0, %%%%smid;" : "=r"(smid));
+    if ((threadIdx.x & 31) == 0) cycles[gw] = ((unsigned long long)smid << 48) | (t1 - t0);
     if (out == 12345.f) sink[threadIdx.x] = out;
 }
 """
@@ -141,11 +148,21 @@ def main():
         gpu.synchronize()
         gpu.launch(k, launch, args)
         gpu.synchronize()
-        cyc = cycles.download().astype(np.float64)
+        raw = cycles.download()
+        sm = (raw >> np.uint64(48)).astype(np.int64)
+        cyc = (raw & np.uint64((1 << 48) - 1)).astype(np.float64)
+        # per SM: warps resident there / 4 SMSPs, over the slowest warp's cycles on that SM
+        # (the block scheduler need not spread blocks evenly)
         instrs = per_chain * CHAINS * UNROLL * iters
-        per_smsp = warps_per_smsp * instrs / float(np.median(cyc))
         ops = loop_ops(cubin)
-        issued = sum(ops.values()) * iters * warps_per_smsp / float(np.median(cyc))
+        rates, issued_rates = [], []
+        for s_id in np.unique(sm):
+            w = sm == s_id
+            rates.append(w.sum() / 4.0 * instrs / cyc[w].max())
+            issued_rates.append(w.sum() / 4.0 * sum(ops.values()) * iters / cyc[w].max())
+        per_smsp = float(np.median(rates))
+        issued = float(np.median(issued_rates))
+        warps_per_smsp = float(np.median(np.bincount(sm)[np.unique(sm)])) / 4.0
         print(json.dumps({"form": name, "instrs_per_trip_per_warp": per_chain * CHAINS * UNROLL,
                           "sass_loop_ops": ops, "sass_issue_per_smsp_per_cycle": round(issued, 3),
                           "warp_instr_per_smsp_per_cycle": round(per_smsp, 3),
