@@ -211,7 +211,8 @@ int jt_pnpoly_edges(const float *vx, const float *vy, int n, int method, float *
  * Table words (4 B): u at u_off (nu floats), guess at guess_off (buckets
  * int32), slab starts at band_off (nu+2 int32, in edges); x-search only:
  * {x0, xscale} float pairs at xpar_off, uint16 [nu+1][xb+1] bucket starts at
- * xst_off, lo / pmax at xlo_off / pmax_off; pairs / records at pair_off.
+ * xst_off, lo / pmax at xlo_off / pmax_off and their conservatively rounded
+ * binary16 copy at half_off; pairs / records at pair_off.
  * table == NULL: fill `info` only (size query). The reference has no PnPoly
  * code; this serves the B200 PnPoly suite. */
 typedef struct {
@@ -219,6 +220,7 @@ typedef struct {
     int u_off, guess_off, band_off, pair_off, words;
     float ybase, yscale;
     int xlo_off, pmax_off, xpar_off, xst_off, xb;
+    int half_off;  /* x-search only: per edge (pmax as binary16 rounded up) << 16 | (lo rounded down) */
 } jt_slab_info;
 int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pad, int xbuckets, float *table,
                     long long capacity, jt_slab_info *info);

@@ -1025,6 +1025,30 @@ static int slab_bucket(float v, float base, float scale, int hi) {
     return (int)std::min<long long>(std::max<long long>(k, 0), hi);
 }
 
+// float32 -> IEEE binary16 bits, rounded toward -inf (dir < 0) or +inf (dir > 0):
+// the result, read back as a float, is <= (resp. >=) v. Overflow goes to +-inf.
+static uint16_t half_round(float v, int dir) {
+    if (std::isnan(v)) return 0x7e00;
+    auto to_float = [](uint16_t h) -> float {
+        const int s = h >> 15, e = (h >> 10) & 31, m = h & 1023;
+        float f = e == 0 ? std::ldexp((float)m, -24) : e == 31 ? (m ? NAN : INFINITY) : std::ldexp(1024.f + m, e - 25);
+        return s ? -f : f;
+    };
+    // nearest-ish candidate by scanning the ordered code space with a binary search on magnitude
+    const float a = std::fabs(v);
+    uint16_t lo = 0, hi = 0x7c00;  // +0 .. +inf
+    while (lo < hi) {  // smallest magnitude code >= a
+        const uint16_t mid = (uint16_t)((lo + hi) / 2);
+        if (to_float(mid) >= a) hi = mid; else lo = (uint16_t)(mid + 1);
+    }
+    uint16_t up = lo;                                               // |h| >= a
+    uint16_t dn = to_float(up) == a ? up : (uint16_t)(up - 1);      // |h| <= a
+    const bool neg = std::signbit(v);
+    // magnitude rounding direction flips for negative values
+    const uint16_t mag = (dir > 0) != neg ? up : dn;
+    return (uint16_t)(mag | (neg ? 0x8000 : 0));
+}
+
 // Bucket starts with an exactness flag. vals: sorted ascending; bucket(v) is
 // monotone in v, so #{vals <= v} is constant over bucket g unless some value
 // and its float predecessor share bucket g. Exact buckets get that count and
@@ -1132,13 +1156,15 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
     if (xsearch) {
         info->xpar_off = info->band_off + (int)up4(nu + 2);                 // {b, cnt, x0, xscale} per slab
         info->xst_off = info->xpar_off + 4 * (nu + 1);                      // uint16 [nu+1][xb+1]
-        info->xlo_off = info->xst_off + (int)up4(((long long)(nu + 1) * (xbuckets + 1) + 1) / 2);
+        // compact copy first: one word per edge, lo rounded down | pmax rounded up to binary16
+        info->half_off = info->xst_off + (int)up4(((long long)(nu + 1) * (xbuckets + 1) + 1) / 2);
+        info->xlo_off = info->half_off + (int)up4(ne);
         info->pmax_off = info->xlo_off + (int)up4(ne);
         info->pair_off = info->pmax_off + (int)up4(ne);  // records {slope, icpt, hi, 0}
         info->words = info->pair_off + 4 * ne;
         if (max_band > 32767) return fail(JT_EINVAL, "slab of %d edges exceeds the 15-bit x-bucket index", max_band);
     } else {
-        info->xpar_off = info->xst_off = 0;
+        info->xpar_off = info->xst_off = info->half_off = 0;
         info->xlo_off = info->pmax_off = 0;
         info->pair_off = info->band_off + (int)up4(nu + 2);  // pairs {slope, icpt}
         info->words = info->pair_off + 2 * ne;
@@ -1186,6 +1212,10 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
             rec[4 * i] = slope[k];
             rec[4 * i + 1] = icpt[k];
             rec[4 * i + 2] = xhi[i];
+        }
+        uint32_t *half = reinterpret_cast<uint32_t *>(table + info->half_off);
+        for (int i = 0; i < ne; ++i) {  // conservative: lo never above, pmax never below the float32 value
+            half[i] = (uint32_t)half_round(lo[i], -1) | ((uint32_t)half_round(pm[i], +1) << 16);
         }
         return JT_OK;
     }

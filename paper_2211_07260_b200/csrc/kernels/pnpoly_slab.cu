@@ -42,7 +42,11 @@
 //                 bucket (flagged by the host), else corrected by compares;
 //                 the slab rank likewise comes from a y-bucket
 //                 (EXACT_FLAGS=0: ignore the host's exactness flags and
-//                 always run the correcting compares);
+//                 always run the correcting compares); HALF=1 stages lo / pmax
+//                 as binary16 rounded down / up (half the shared memory, two
+//                 CTAs per SM): a too-small lo or too-large pmax only sends more
+//                 edges through the exact re-evaluation, so the bitmap is
+//                 unchanged;
 //                 the undecided edges (about 0.05 per point on the benchmark
 //                 polygon) are found by walking back from pos while the
 //                 running max of hi (pmax) exceeds px, and are evaluated with
@@ -64,6 +68,9 @@
 #endif
 #ifndef EXACT_FLAGS
 #define EXACT_FLAGS 1
+#endif
+#ifndef HALF
+#define HALF 0
 #endif
 #if XSEARCH && (SORT || PAIRS_SMEM)
 #error "XSEARCH=1 takes SORT=0 and PAIRS_SMEM=0"
@@ -164,6 +171,18 @@ __device__ __forceinline__ int lds_u16(unsigned a) {
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ float lds_f16(unsigned a) {
+    float v;
+    asm volatile("{\n.reg .b16 h;\nld.shared.b16 h, [%1];\ncvt.f32.f16 %0, h;\n}" : "=f"(v) : "r"(a));
+    return v;
+}
+#if HALF
+#define LO_AT(i) lds_f16(T.xlo + 4u * (i))
+#define PMAX_AT(i) lds_f16(T.xlo + 4u * (i) + 2u)
+#else
+#define LO_AT(i) lds_f32(T.xlo + 4u * (i))
+#define PMAX_AT(i) lds_f32(T.pmax + 4u * (i))
+#endif
 __device__ __forceinline__ float4 lds_f32x4(unsigned a) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -196,14 +215,13 @@ __device__ __forceinline__ int xsearch_point(float px, float py, const XTables &
     k = min(max(k, 0), T.xb);
     const int w = lds_u16(T.xst + 2u * (r * (T.xb + 1) + k));  // bit 15: pos is exact
     int pos = w & 0x7fff;
-    const unsigned lo = T.xlo + 4u * b;
     if (!EXACT_FLAGS || !(w & 0x8000)) {
-        while (pos < cnt && lds_f32(lo + 4u * pos) <= px) ++pos;
-        while (pos > 0 && lds_f32(lo + 4u * pos - 4u) > px) --pos;
+        while (pos < cnt && LO_AT(b + pos) <= px) ++pos;
+        while (pos > 0 && LO_AT(b + pos - 1) > px) --pos;
     }
     int in = (cnt - pos) & 1;  // lo > px: crosses for every py of the slab
     // undecided: lo <= px < hi; pmax[j] = max hi over the slab's first j+1 edges
-    for (int j = pos - 1; j >= 0 && lds_f32(T.pmax + 4u * (b + j)) > px; --j) {
+    for (int j = pos - 1; j >= 0 && PMAX_AT(b + j) > px; --j) {
         const float4 q = __ldg(T.recs + b + j);
         if (q.z > px) in ^= (px < __fmaf_rn(q.x, py, q.y)) ? 1 : 0;
     }
@@ -214,10 +232,15 @@ __device__ __forceinline__ int xsearch_point(float px, float py, const XTables &
 extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X)
 pnpoly_slab(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, const float *__restrict__ table,
             int nu, int ng, int band_off, int pair_off, int staged_words, float ybase, float yscale,
-            int xlo_off, int pmax_off, int xpar_off, int xst_off, int xb) {
+            int xlo_off, int pmax_off, int xpar_off, int xst_off, int xb, int arr_off, int arr_words) {
+    // stage table words [0, staged_words), then [arr_off, arr_off + arr_words) right after them
+    // (x-search: the lo / pmax arrays of the chosen precision); xlo_off / pmax_off are
+    // shared-memory word offsets
     extern __shared__ __align__(16) float smem[];
     for (int i = threadIdx.x; i < staged_words / 4; i += BLOCK_SIZE_X)
         reinterpret_cast<float4 *>(smem)[i] = __ldg(reinterpret_cast<const float4 *>(table) + i);
+    for (int i = threadIdx.x; i < arr_words / 4; i += BLOCK_SIZE_X)
+        reinterpret_cast<float4 *>(smem)[staged_words / 4 + i] = __ldg(reinterpret_cast<const float4 *>(table) + arr_off / 4 + i);
     const float *u = smem;
     const int *guess = reinterpret_cast<const int *>(smem + ((nu + 3) & ~3));
     const int *band = reinterpret_cast<const int *>(smem + band_off);
@@ -272,7 +295,7 @@ pnpoly_slab(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, 
 #endif
 #if SORT
     __shared__ int warp_tot[32];
-    int *hist = reinterpret_cast<int *>(smem + staged_words);              // nu + 1 counters
+    int *hist = reinterpret_cast<int *>(smem + staged_words + arr_words);  // nu + 1 counters
     float4 *sorted = reinterpret_cast<float4 *>(hist + ((nu + 4) & ~3));  // CHUNK records
     int *result = reinterpret_cast<int *>(sorted + CHUNK);                 // CHUNK results
 #endif

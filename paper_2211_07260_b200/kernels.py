@@ -379,6 +379,7 @@ class PnPolySlabProblem(PnPolyProblem):
             "pairs_smem": [0, 1],
             "xbuckets": [0, 4, 8, 16],
             "exact_flags": [0, 1],
+            "half": [0, 1],
             "buckets": [1024, 4096],
         }
 
@@ -387,20 +388,24 @@ class PnPolySlabProblem(PnPolyProblem):
         xinfo = self.slab_info(4096, 4)
         nu1 = info.nu + 1
         head = (info.nu + 3) // 4 * 4 + (info.nu + 2 + 3) // 4 * 4
-        # x-search words past the slab starts: slab records, uint16 bucket starts, lo, pmax
-        xfix = 4 * nu1 + 4 + 2 * ((xinfo.ne + 3) // 4 * 4)
+        # x-search words past the slab starts: slab records, uint16 bucket starts, lo + pmax
+        # (two float32 arrays, or one word per edge with HALF)
+        xfix = 4 * nu1 + 4
+        ne4 = (xinfo.ne + 3) // 4 * 4
         limit = 227 * 1024
         return [
             "block_size_x * tile <= 8192",
             "xbuckets == 0 or (sort == 0 and pairs_smem == 0)",
             "xbuckets > 0 or exact_flags == 1",
+            "xbuckets > 0 or half == 0",
             f"({head} + buckets + pairs_smem * {2 * info.ne} + sort * ({(info.nu + 4) // 4 * 4} + "
-            f"5 * block_size_x * tile) + (xbuckets > 0) * ({xfix} + {nu1} * (xbuckets + 1) / 2)) * 4 <= {limit}",
+            f"5 * block_size_x * tile) + (xbuckets > 0) * ({xfix} + (2 - half) * {ne4} + {nu1} * (xbuckets + 1) / 2)) * 4"
+            f" <= {limit}",
         ]
 
     def default_config(self):
         return {"block_size_x": 1024, "tile": 8, "sort": 1, "pairs_smem": 0, "xbuckets": 0, "exact_flags": 1,
-                "buckets": 4096}
+                "half": 0, "buckets": 4096}
 
     @staticmethod
     def formula(config) -> int:
@@ -410,7 +415,7 @@ class PnPolySlabProblem(PnPolyProblem):
         c = _as_dict(config)
         return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "SORT": c["sort"],
                 "PAIRS_SMEM": c["pairs_smem"], "XSEARCH": int(c.get("xbuckets", 0) > 0),
-                "EXACT_FLAGS": c.get("exact_flags", 1)}
+                "EXACT_FLAGS": c.get("exact_flags", 1), "HALF": c.get("half", 0)}
 
     def _polygon(self):
         inputs = getattr(self, "inputs", None)
@@ -437,7 +442,7 @@ class PnPolySlabProblem(PnPolyProblem):
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
         info = self.slab_info(c["buckets"], c.get("xbuckets", 0))
-        words = info.words if c["pairs_smem"] else info.pair_off
+        words = sum(self._stage(c, info))
         if c["sort"]:
             words += (info.nu + 4) // 4 * 4 + 5 * c["block_size_x"] * c["tile"]
         return 4 * words
@@ -467,13 +472,26 @@ class PnPolySlabProblem(PnPolyProblem):
             self.buffers[key] = self.gpu.array(self.slab_table(buckets, xbuckets)[0])
         return self.buffers[key]
 
+    @staticmethod
+    def _stage(c, info):
+        """(words staged from the table's start, words of the second staged range)."""
+        if c.get("xbuckets", 0):
+            if c.get("half", 0):
+                return info.xlo_off, 0  # header + the binary16 lo|pmax words
+            return info.half_off, info.pair_off - info.xlo_off  # header, then float32 lo and pmax
+        return (info.words if c["pairs_smem"] else info.pair_off), 0
+
     def _tail(self, c):
         xb = c.get("xbuckets", 0)
         info = self.slab_info(c["buckets"], xb)
-        staged = info.words if c["pairs_smem"] else info.pair_off
+        staged, arr_words = self._stage(c, info)
+        # x-search arrays as shared-memory word offsets (see pnpoly_slab.cu)
+        xlo_s = info.half_off
+        pmax_s = info.half_off + (info.pmax_off - info.xlo_off)
         return [self._table_buffer(c["buckets"], xb), i32(info.nu), i32(info.ng), i32(info.band_off),
-                i32(info.pair_off), i32(staged), f32(info.ybase), f32(info.yscale), i32(info.xlo_off),
-                i32(info.pmax_off), i32(info.xpar_off), i32(info.xst_off), i32(info.xb)]
+                i32(info.pair_off), i32(staged), f32(info.ybase), f32(info.yscale), i32(xlo_s),
+                i32(pmax_s), i32(info.xpar_off), i32(info.xst_off), i32(info.xb), i32(info.xlo_off),
+                i32(arr_words)]
 
     def args(self, config):
         c = _as_dict(config)

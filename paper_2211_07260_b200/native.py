@@ -63,7 +63,7 @@ class JTSlabInfo(ctypes.Structure):
         ("u_off", ctypes.c_int), ("guess_off", ctypes.c_int), ("band_off", ctypes.c_int), ("pair_off", ctypes.c_int),
         ("words", ctypes.c_int), ("ybase", ctypes.c_float), ("yscale", ctypes.c_float),
         ("xlo_off", ctypes.c_int), ("pmax_off", ctypes.c_int), ("xpar_off", ctypes.c_int), ("xst_off", ctypes.c_int),
-        ("xb", ctypes.c_int),
+        ("xb", ctypes.c_int), ("half_off", ctypes.c_int),
     ]
 
 

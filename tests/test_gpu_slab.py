@@ -16,8 +16,8 @@ SLAB_CONFIGS = (
      if not (ps and s and b * t > 2048)]
     + [dict(block_size_x=256, tile=8, sort=1, pairs_smem=0, xbuckets=0, buckets=1024),
        dict(block_size_x=1024, tile=8, sort=1, pairs_smem=0, xbuckets=0, buckets=1024)]
-    + [dict(block_size_x=b, tile=t, sort=0, pairs_smem=0, xbuckets=x, exact_flags=f, buckets=g)
-       for b, t, x, f, g in itertools.product((128, 512, 1024), (1, 4, 8), (4, 16), (0, 1), (1024, 4096))]
+    + [dict(block_size_x=b, tile=t, sort=0, pairs_smem=0, xbuckets=x, exact_flags=f, half=h, buckets=g)
+       for b, t, x, f, h, g in itertools.product((128, 512, 1024), (1, 4, 8), (4, 16), (0, 1), (0, 1), (1024, 4096))]
 )
 
 
@@ -113,3 +113,44 @@ def test_slab_host_api_matches_brute_force(gpu, strips):
                          config=dict(PnPolyProblem().default_config(), asm=0, method=2)).copy()
     np.testing.assert_array_equal(slab, brute)
     np.testing.assert_array_equal(slab, O.pnpoly(inp["points"], inp["vx"], inp["vy"], 2))
+
+
+@pytest.mark.parametrize("shape", ["star3000", "convex50", "comb"])
+def test_slab_other_polygons(gpu, shape):
+    """Slab kernel on polygons unlike the benchmark one: a 3000-vertex star (long slab
+    lists), a 50-vertex convex polygon (2 edges per slab) and a comb with shared
+    vertex ordinates and horizontal edges."""
+    from paper_2211_07260_b200.kernels import PnPolySlabProblem
+
+    rng = np.random.default_rng(11)
+    if shape == "star3000":
+        th = np.sort(rng.uniform(0, 2 * np.pi, 3000))
+        rad = 0.4 + 0.5 * rng.uniform(0, 1, 3000)
+    elif shape == "convex50":
+        th = np.sort(rng.uniform(0, 2 * np.pi, 50))
+        rad = np.full(50, 0.9)
+    if shape == "comb":
+        vx = np.array([0, 4, 4, 3, 3, 2, 2, 1, 1, 0], np.float32) / 4 - 0.5
+        vy = np.array([0, 0, 3, 3, 1, 1, 3, 3, 1, 1], np.float32) / 3 - 0.5
+    else:
+        vx, vy = (rad * np.cos(th)).astype(np.float32), (rad * np.sin(th)).astype(np.float32)
+    pts = rng.uniform(-1, 1, (300_001, 2)).astype(np.float32)
+    pts[:vx.size] = np.stack([vx, vy], 1)  # exactly on the vertices
+    p = PnPolySlabProblem(n_points=len(pts), n_vertices=vx.size)
+    p.prepare(gpu, {"points": pts, "vx": vx, "vy": vy})
+    want = O.pnpoly(pts, vx, vy, 2)
+    cfgs = [c for c in SLAB_CONFIGS[::4] if p.is_valid(c)] + [p.default_config()]
+    assert cfgs
+    for cfg in cfgs:
+        np.testing.assert_array_equal(run_once(gpu, p, cfg), want, err_msg=f"{shape} {cfg}")
+
+
+def test_slab_through_tune_kernel():
+    """The paper-style facade tunes the slab kernel as a built-in problem."""
+    from paper_2211_07260_b200 import tune_kernel
+
+    rows, outcome = tune_kernel("pnpoly_slab", tune_params={"block_size_x": [512, 1024], "tile": [2], "sort": [0],
+                                                            "pairs_smem": [0], "xbuckets": [16], "exact_flags": [0],
+                                                            "half": [0, 1], "buckets": [4096]},
+                                problem_kwargs={"n_points": 1 << 20}, duration=0.05)
+    assert len(rows) == 4 and not any(r["failed"] for r in rows) and outcome.best.metrics["gflops"] > 0

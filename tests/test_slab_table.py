@@ -166,3 +166,23 @@ def test_xsearch_table_decides_like_the_brute_force_test(name):
                     got ^= 1
                 j -= 1
         assert got == want, (name, float(px), float(py))
+
+
+@pytest.mark.parametrize("name", sorted(POLYGONS))
+def test_half_copy_is_conservative_and_tight(name):
+    """The binary16 copy: lo rounded toward -inf, pmax toward +inf, each the closest
+    such binary16 value (so the HALF kernel only re-evaluates a few more edges)."""
+    if POLYGONS[name] is None:
+        vx, vy = PnPolySlabProblem(n_points=4096)._polygon()
+    else:
+        vx, vy = POLYGONS[name]
+    table, info = native.pnpoly_slabs(vx, vy, 64, 4, 8)
+    h = table[info.half_off:info.half_off + info.ne].view(np.uint32)
+    lo16 = (h & 0xFFFF).astype(np.uint16).view(np.float16)
+    pm16 = (h >> 16).astype(np.uint16).view(np.float16)
+    lo = table[info.xlo_off:info.xlo_off + info.ne]
+    pm = table[info.pmax_off:info.pmax_off + info.ne]
+    assert np.all(lo16.astype(np.float32) <= lo) and np.all(pm16.astype(np.float32) >= pm)
+    with np.errstate(over="ignore"):
+        assert np.all(np.nextafter(lo16, np.float16(np.inf)).astype(np.float32) > lo)
+        assert np.all(np.nextafter(pm16, np.float16(-np.inf)).astype(np.float32) < pm)
