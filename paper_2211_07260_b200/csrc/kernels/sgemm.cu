@@ -25,6 +25,12 @@
 //                   KWB*NWB/VWN staging registers per thread and lets the
 //                   copy of tile t+ASYNC-1 overlap the FFMAs of tile t.
 //                   Needs SA = SB = 1 (dynamic shared memory, up to 227 KB).
+//   FMA2            (B200 addition) 1: the outer product issues packed
+//                   FFMA2 on pairs of N-adjacent accumulators with the A
+//                   element as a broadcast scalar: half the FFMA issue slots
+//                   for the same FMA-pipe work, leaving issue bandwidth for
+//                   the fragment loads. Per element the same fma.rn sequence,
+//                   so the result is bit-identical to FMA2 = 0. Needs VWN even.
 //
 // Requirements (the tuning-space restrictions, kernels.py):
 //   MWG % (MDIMC*VWM) == 0, NWG % (NDIMC*VWN) == 0,
@@ -83,6 +89,12 @@
 #error "ASYNC must be 0, 2, 3 or 4"
 #endif
 
+#ifndef FMA2
+#define FMA2 0
+#endif
+#if FMA2 && (VWN % 2)
+#error "FMA2 needs an even VWN (accumulator pairs inside one B vector)"
+#endif
 #define THREADS (MDIMC * NDIMC)
 #define MWI (MWG / MDIMC)
 #define NWI (NWG / NDIMC)
@@ -144,6 +156,16 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 #endif
 
+#if FMA2
+// acc2 = {b0, b1} * {a, a} + acc2 per lane (fma.rn.f32x2): the accumulator pair lives in
+// one 64-bit register pair, the A element is the broadcast scalar operand
+__device__ __forceinline__ void fma2(unsigned long long &acc2, float a, float b0, float b1) {
+    asm("{\n.reg .b64 aa, bb;\nmov.b64 aa, {%1, %1};\nmov.b64 bb, {%2, %3};\nfma.rn.f32x2 %0, bb, aa, %0;\n}"
+        : "+l"(acc2)
+        : "f"(a), "f"(b0), "f"(b1));
+}
+#endif
+
 extern "C" __global__ void __launch_bounds__(THREADS)
 sgemm(const int M, const int N, const int K, const float alpha, const float beta,
       const float *__restrict__ at, const float *__restrict__ b, float *__restrict__ c) {
@@ -174,11 +196,19 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
 
 #endif
 
+#if FMA2
+    unsigned long long acc2[MWI][NWI / 2];
+#pragma unroll
+    for (int i = 0; i < MWI; ++i)
+#pragma unroll
+        for (int j = 0; j < NWI / 2; ++j) acc2[i][j] = 0ull;
+#else
     float acc[MWI][NWI];
 #pragma unroll
     for (int i = 0; i < MWI; ++i)
 #pragma unroll
         for (int j = 0; j < NWI; ++j) acc[i][j] = 0.f;
+#endif
 
     const vm_t *at_v = reinterpret_cast<const vm_t *>(at);
     const vn_t *b_v = reinterpret_cast<const vn_t *>(b);
@@ -212,8 +242,14 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
 #pragma unroll
                 for (int i = 0; i < MWI; ++i)
 #pragma unroll
+#if FMA2
+                    for (int j = 0; j < NWI; j += 2)
+                        fma2(acc2[i][j / 2], lane(af[i / VWM], i % VWM), lane(bf[j / VWN], j % VWN),
+                             lane(bf[j / VWN], j % VWN + 1));
+#else
                     for (int j = 0; j < NWI; ++j)
                         acc[i][j] = fmaf(lane(af[i / VWM], i % VWM), lane(bf[j / VWN], j % VWN), acc[i][j]);
+#endif
             }
         }
     };
@@ -302,6 +338,16 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
 
 #endif
 
+#if FMA2
+    float acc[MWI][NWI];
+#pragma unroll
+    for (int i = 0; i < MWI; ++i)
+#pragma unroll
+        for (int j = 0; j < NWI; j += 2) {
+            acc[i][j] = __uint_as_float((unsigned)acc2[i][j / 2]);
+            acc[i][j + 1] = __uint_as_float((unsigned)(acc2[i][j / 2] >> 32));
+        }
+#endif
     // epilogue: C = alpha * acc + beta * C, VWN-wide row segments
 #pragma unroll
     for (int i = 0; i < MWI; ++i) {

@@ -665,13 +665,13 @@ class SgemmProblem(KernelProblem):
                 "MWG": [64, 128, 256], "NWG": [64, 128, 256], "KWG": [8, 16, 32],
                 "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32, 64], "NDIMB": [8, 16, 32, 64],
                 "KWI": [1, 2, 4, 8], "VWM": [1, 2, 4], "VWN": [1, 2, 4], "STRM": [0, 1], "STRN": [0, 1],
-                "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3, 4],
+                "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3, 4], "FMA2": [0, 1],
             }
         return {
             "MWG": [16, 32, 64, 128], "NWG": [16, 32, 64, 128], "KWG": [16, 32],
             "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32], "NDIMB": [8, 16, 32],
             "KWI": [2, 8], "VWM": [1, 2, 4, 8], "VWN": [1, 2, 4, 8], "STRM": [0, 1], "STRN": [0, 1],
-            "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3],
+            "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3], "FMA2": [0, 1],
         }
 
     def restrictions(self):
@@ -694,6 +694,7 @@ class SgemmProblem(KernelProblem):
             " or (ASYNC > 0 and KWG * (MWG + NWG) * 4 * ASYNC <= 227 * 1024)",
             "(MWG / MDIMC) * (NWG / NDIMC) <= 128",
             f"{self.m} % MWG == 0 and {self.n} % NWG == 0 and {self.k} % KWG == 0",
+            "FMA2 == 0 or VWN % 2 == 0",
         ]
 
     def default_config(self):
