@@ -16,7 +16,13 @@
 //
 // Tunables (-D): BLOCK_X, BLOCK_Y, TILE_X (1,2,4,8), TILE_Y, USE_SMEM (stage
 // the input tile in shared memory, else read through L1 with __ldg),
-// PAD (extra floats per smem row, multiple of 4), IMAGE_W, IMAGE_H, FW, FH.
+// PAD (extra floats per smem row, multiple of 4), IMAGE_W, IMAGE_H, FW, FH,
+// FMA2 (B200 addition): accumulators in x-adjacent pairs; for even filter
+// columns j the pair {in[x+j], in[x+j+1]} is an aligned register pair, so one
+// packed FFMA2 (filter coefficient as the broadcast operand, held in a uniform
+// register) does two FMAs; odd columns stay scalar. Half the issue slots of
+// the even-column FMAs, the same fma.rn per output in the same order: the
+// result is bit-identical to FMA2 = 0. Needs an even TILE_X.
 #ifndef BLOCK_X
 #define BLOCK_X 32
 #endif
@@ -46,6 +52,12 @@
 #endif
 #ifndef FH
 #define FH 17
+#endif
+#ifndef FMA2
+#define FMA2 0
+#endif
+#if FMA2 && (TILE_X % 2)
+#error "FMA2 needs an even TILE_X"
 #endif
 
 #if ((FW - 1) % 4) != 0 || (PAD % 4) != 0
@@ -95,6 +107,22 @@ __device__ __forceinline__ void load_segment(float (&r)[SEG + 3], const float *p
     }
 }
 
+#if FMA2
+// {acc.lo, acc.hi} += {x0, x1} * {f, f} as one fma.rn.f32x2
+__device__ __forceinline__ void fma2(unsigned long long &acc, float f, float x0, float x1) {
+    asm("{\n.reg .b64 ff, xx;\nmov.b64 ff, {%1, %1};\nmov.b64 xx, {%2, %3};\nfma.rn.f32x2 %0, xx, ff, %0;\n}"
+        : "+l"(acc)
+        : "f"(f), "f"(x0), "f"(x1));
+}
+// the same two FMAs as scalar fma.rn (x0 / x1 need not form an aligned pair)
+__device__ __forceinline__ void fma_split(unsigned long long &acc, float f, float x0, float x1) {
+    asm("{\n.reg .f32 lo, hi;\nmov.b64 {lo, hi}, %0;\nfma.rn.f32 lo, %2, %1, lo;\nfma.rn.f32 hi, %3, %1, hi;\n"
+        "mov.b64 %0, {lo, hi};\n}"
+        : "+l"(acc)
+        : "f"(f), "f"(x0), "f"(x1));
+}
+#endif
+
 extern "C" __global__ void __launch_bounds__(BLOCK_X *BLOCK_Y)
 conv2d(float *__restrict__ out, const float *__restrict__ in) {
     const int x0 = blockIdx.x * OUT_TW;
@@ -136,11 +164,19 @@ conv2d(float *__restrict__ out, const float *__restrict__ in) {
     constexpr int PITCH = IN_W;
 #endif
 
+#if FMA2
+    unsigned long long acc2[TILE_Y][TILE_X / 2];
+#pragma unroll
+    for (int ty = 0; ty < TILE_Y; ++ty)
+#pragma unroll
+        for (int tx = 0; tx < TILE_X / 2; ++tx) acc2[ty][tx] = 0ull;
+#else
     float acc[TILE_Y][TILE_X];
 #pragma unroll
     for (int ty = 0; ty < TILE_Y; ++ty)
 #pragma unroll
         for (int tx = 0; tx < TILE_X; ++tx) acc[ty][tx] = 0.f;
+#endif
 
     // Input row r (relative to the thread patch) feeds output rows ty with
     // filter row i = r - ty in [0, FH).
@@ -154,12 +190,32 @@ conv2d(float *__restrict__ out, const float *__restrict__ in) {
             if (i >= 0 && i < FH) {
 #pragma unroll
                 for (int j = 0; j < FW; ++j)
+#if FMA2
+#pragma unroll
+                    for (int tx = 0; tx < TILE_X; tx += 2) {
+                        if ((j & 1) == 0)
+                            fma2(acc2[ty][tx / 2], d_filter[i * FW + j], seg[tx + j], seg[tx + j + 1]);
+                        else
+                            fma_split(acc2[ty][tx / 2], d_filter[i * FW + j], seg[tx + j], seg[tx + j + 1]);
+                    }
+#else
 #pragma unroll
                     for (int tx = 0; tx < TILE_X; ++tx) acc[ty][tx] = fmaf(seg[tx + j], d_filter[i * FW + j], acc[ty][tx]);
+#endif
             }
         }
     }
 
+#if FMA2
+    float acc[TILE_Y][TILE_X];
+#pragma unroll
+    for (int ty = 0; ty < TILE_Y; ++ty)
+#pragma unroll
+        for (int tx = 0; tx < TILE_X; tx += 2) {
+            acc[ty][tx] = __uint_as_float((unsigned)acc2[ty][tx / 2]);
+            acc[ty][tx + 1] = __uint_as_float((unsigned)(acc2[ty][tx / 2] >> 32));
+        }
+#endif
     const int ox = x0 + threadIdx.x * TILE_X;
     const int oy = y0 + threadIdx.y * TILE_Y;
 #pragma unroll

@@ -556,6 +556,7 @@ class Conv2DProblem(KernelProblem):
             "tile_size_y": [1, 2, 4, 8],
             "use_shmem": [0, 1],
             "use_padding": [0, 1],
+            "fma2": [0, 1],
         }
 
     def restrictions(self):
@@ -565,6 +566,7 @@ class Conv2DProblem(KernelProblem):
             f"{self.width} % (block_size_x * tile_size_x) == 0",
             f"{self.height} % (block_size_y * tile_size_y) == 0",
             "use_shmem == 1 or use_padding == 0",
+            "fma2 == 0 or tile_size_x % 2 == 0",
             f"use_shmem == 0 or (block_size_y * tile_size_y + {self.fh - 1}) * "
             f"(block_size_x * tile_size_x + {self.fw - 1} + 4 * use_padding) * 4 <= 48000",
         ]
@@ -582,6 +584,7 @@ class Conv2DProblem(KernelProblem):
             "TILE_Y": c["tile_size_y"],
             "USE_SMEM": c["use_shmem"],
             "PAD": 4 * c["use_padding"],
+            "FMA2": c.get("fma2", 0),
             "IMAGE_W": self.width,
             "IMAGE_H": self.height,
             "FW": self.fw,

@@ -66,7 +66,7 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
             "parameters": {
                 "MWG": [64, 128], "NWG": [64, 128], "KWG": [16, 32], "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32],
                 "MDIMA": [16, 32], "NDIMB": [16, 32], "KWI": [2, 8], "VWM": [2, 4], "VWN": [2, 4],
-                "STRM": [0, 1], "STRN": [0, 1], "SA": [1], "SB": [1], "ASYNC": [0, 2, 3],
+                "STRM": [0, 1], "STRN": [0, 1], "SA": [1], "SB": [1], "ASYNC": [0, 2, 3], "FMA2": [0, 1],
             },
             "restrictions": problem.restrictions(),
         }
@@ -91,9 +91,14 @@ def oracle_check(problem, cfg) -> tuple[bool, float]:
 SEEDS = {
     "sgemm": [
         {"MWG": 128, "NWG": 128, "KWG": 32, "MDIMC": 16, "NDIMC": 16, "MDIMA": 32, "NDIMB": 32, "KWI": 8, "VWM": 4,
-         "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 2},
+         "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 2, "FMA2": 0},
+        # round-1 winners with the packed FFMA2 outer product (scripts/time_sgemm_fma2.py)
+        {"MWG": 128, "NWG": 128, "KWG": 16, "MDIMC": 8, "NDIMC": 16, "MDIMA": 16, "NDIMB": 16, "KWI": 2, "VWM": 4,
+         "VWN": 2, "STRM": 1, "STRN": 0, "SA": 1, "SB": 1, "ASYNC": 3, "FMA2": 1},
+        {"MWG": 128, "NWG": 128, "KWG": 32, "MDIMC": 8, "NDIMC": 16, "MDIMA": 16, "NDIMB": 16, "KWI": 8, "VWM": 4,
+         "VWN": 2, "STRM": 1, "STRN": 0, "SA": 1, "SB": 1, "ASYNC": 2, "FMA2": 1},
         {"MWG": 128, "NWG": 64, "KWG": 32, "MDIMC": 16, "NDIMC": 8, "MDIMA": 16, "NDIMB": 16, "KWI": 8, "VWM": 4,
-         "VWN": 4, "STRM": 1, "STRN": 0, "SA": 1, "SB": 1, "ASYNC": 2},
+         "VWN": 4, "STRM": 1, "STRN": 0, "SA": 1, "SB": 1, "ASYNC": 2, "FMA2": 0},
     ],
 }
 CONFIRM_ENERGY, CONFIRM_TIME, CONFIRM_ROUNDS, CONFIRM_WINDOW, CONFIRM_SETTLE = 5, 3, 3, 1.0, 0.25

@@ -149,6 +149,22 @@ def test_conv2d_within_fp32_tolerance(gpu, cfg, shape):
     assert err <= O.CONV_TOL
 
 
+@pytest.mark.parametrize("cfg", [c for c in CONV_CONFIGS if c["tile_size_x"] % 2 == 0],
+                         ids=lambda c: "-".join(str(v) for v in c.values()))
+def test_conv2d_fma2_bit_identical_to_scalar(gpu, cfg):
+    """fma2=1 (packed FFMA2 on even filter columns) computes the same fma.rn sequence per
+    output as fma2=0, so the images agree bit for bit (and with the oracle's tolerance)."""
+    from paper_2211_07260_b200.kernels import Conv2DProblem
+
+    p = Conv2DProblem(width=512, height=256)
+    p.prepare(gpu)
+    scalar = run_once(gpu, p, dict(cfg, fma2=0)).copy()
+    packed = run_once(gpu, p, dict(cfg, fma2=1))
+    assert np.array_equal(scalar.view(np.uint32), packed.view(np.uint32))
+    ref = O.conv2d(p.inputs["image"], p.inputs["filter"])
+    assert O.conv2d_error(packed, ref, p.inputs["image"], p.inputs["filter"]) <= O.CONV_TOL
+
+
 def test_conv2d_full_size_tuned(gpu):
     from paper_2211_07260_b200 import tuned
     from paper_2211_07260_b200.kernels import Conv2DProblem
@@ -191,6 +207,22 @@ def test_sgemm_within_fp32_tolerance(gpu, overrides, mnk, beta):
     got = run_once(gpu, p, cfg)
     ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
     assert O.sgemm_error(got, ref) <= O.SGEMM_TOL
+
+
+@pytest.mark.parametrize("overrides", [c for c in SGEMM_CONFIGS if c.get("VWN", 4) % 2 == 0],
+                         ids=lambda c: str(sorted(c.items())))
+def test_sgemm_fma2_bit_identical_to_scalar(gpu, overrides):
+    """FMA2=1 (packed FFMA2 outer product) gives C bit for bit equal to FMA2=0."""
+    from paper_2211_07260_b200.kernels import SgemmProblem
+
+    p = SgemmProblem(m=512, n=512, k=512, beta=0.5)
+    p.prepare(gpu)
+    cfg = {**p.default_config(), **overrides}
+    scalar = run_once(gpu, p, dict(cfg, FMA2=0)).copy()
+    packed = run_once(gpu, p, dict(cfg, FMA2=1))
+    assert np.array_equal(scalar.view(np.uint32), packed.view(np.uint32))
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    assert O.sgemm_error(packed, ref) <= O.SGEMM_TOL
 
 
 def test_sgemm_full_size_tuned(gpu):
