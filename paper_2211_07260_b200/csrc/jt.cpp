@@ -1049,6 +1049,12 @@ static uint16_t half_round(float v, int dir) {
     return (uint16_t)(mag | (neg ? 0x8000 : 0));
 }
 
+static float half_value(uint16_t h) {
+    const int e = (h >> 10) & 31, m = h & 1023;
+    const float f = e == 0 ? std::ldexp((float)m, -24) : e == 31 ? (m ? NAN : INFINITY) : std::ldexp(1024.f + m, e - 25);
+    return (h >> 15) ? -f : f;
+}
+
 // Bucket starts with an exactness flag. vals: sorted ascending; bucket(v) is
 // monotone in v, so #{vals <= v} is constant over bucket g unless some value
 // and its float predecessor share bucket g. Exact buckets get that count and
@@ -1214,9 +1220,23 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
             rec[4 * i + 2] = xhi[i];
         }
         uint32_t *half = reinterpret_cast<uint32_t *>(table + info->half_off);
+        std::vector<float> lo16(ne);
         for (int i = 0; i < ne; ++i) {  // conservative: lo never above, pmax never below the float32 value
-            half[i] = (uint32_t)half_round(lo[i], -1) | ((uint32_t)half_round(pm[i], +1) << 16);
+            const uint16_t l = half_round(lo[i], -1);
+            half[i] = (uint32_t)l | ((uint32_t)half_round(pm[i], +1) << 16);
+            lo16[i] = half_value(l);
         }
+        // skip pointer (record word 3): the largest j < i in the slab with hi_j > lo16_i, else -1.
+        // The kernel visits undecided candidates (j < pos with hi_j > px) from pos - 1 down; every
+        // visited j has lo16_j <= px, so an edge strictly between skip(j) and j (hi <= lo16_j <= px)
+        // can never be one. lo16 (<= lo) keeps this valid for both the float32 and the HALF tables.
+        int32_t *recw = reinterpret_cast<int32_t *>(rec);
+        for (int r = 1; r < nu; ++r)
+            for (int i = off[r]; i < off[r + 1]; ++i) {
+                int j = i - 1;
+                while (j >= off[r] && !(xhi[j] > lo16[i])) --j;
+                recw[4 * i + 3] = j >= off[r] ? j - off[r] : -1;
+            }
         return JT_OK;
     }
     float *pairs = table + info->pair_off;

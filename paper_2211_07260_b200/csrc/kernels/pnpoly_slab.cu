@@ -49,8 +49,10 @@
 //                 unchanged;
 //                 the undecided edges (about 0.05 per point on the benchmark
 //                 polygon) are found by walking back from pos while the
-//                 running max of hi (pmax) exceeds px, and are evaluated with
-//                 the brute-force formula.
+//                 running max of hi (pmax) exceeds px, jumping along each
+//                 record's skip pointer (the next lower edge whose hi exceeds
+//                 this edge's lo), and are evaluated with the brute-force
+//                 formula.
 #ifndef BLOCK_SIZE_X
 #define BLOCK_SIZE_X 512
 #endif
@@ -221,9 +223,11 @@ __device__ __forceinline__ int xsearch_point(float px, float py, const XTables &
     }
     int in = (cnt - pos) & 1;  // lo > px: crosses for every py of the slab
     // undecided: lo <= px < hi; pmax[j] = max hi over the slab's first j+1 edges
-    for (int j = pos - 1; j >= 0 && PMAX_AT(b + j) > px; --j) {
-        const float4 q = __ldg(T.recs + b + j);
+    // (the walk follows each record's skip pointer: the next lower edge whose hi can exceed px)
+    for (int j = pos - 1; j >= 0 && PMAX_AT(b + j) > px;) {
+        const float4 q = __ldg(T.recs + b + j);  // {slope, icpt, hi, skip}
         if (q.z > px) in ^= (px < __fmaf_rn(q.x, py, q.y)) ? 1 : 0;
+        j = __float_as_int(q.w);
     }
     return in;
 }

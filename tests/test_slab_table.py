@@ -140,6 +140,21 @@ def test_xsearch_table_decides_like_the_brute_force_test(name):
     def fma32(a, b, c):  # exact product in float64, one rounding of the sum: equals fmaf
         return np.float32(np.float64(a) * np.float64(b) + np.float64(c))
 
+    hw = table[info.half_off:info.half_off + info.ne].view(np.uint32)
+    lo16 = (hw & 0xFFFF).astype(np.uint16).view(np.float16).astype(np.float32)
+    pm16 = (hw >> 16).astype(np.uint16).view(np.float16).astype(np.float32)
+
+    def walk(b, pos, c, xlo_t, pm_t, px, py):
+        """The kernel's parity: certain crossings + the undecided edges along the skip chain."""
+        got = (c - pos) & 1
+        j = pos - 1
+        while j >= 0 and pm_t[b + j] > px:
+            sl, ic, hi, skip = rec[b + j]
+            if hi > px and px < fma32(sl, py, ic):
+                got ^= 1
+            j = int(np.float32(skip).view(np.int32))
+        return got
+
     rng = np.random.default_rng(1)
     span = float(max(abs(vx).max(), abs(vy).max())) + 0.5
     pts = rng.uniform(-span, span, (3000, 2)).astype(np.float32)
@@ -158,13 +173,11 @@ def test_xsearch_table_decides_like_the_brute_force_test(name):
             w = int(xst[r, _bucket(px, srec[r, 2], srec[r, 3], info.xb)])
             if w & 0x8000:  # flagged exact: the bucket's start must already be the count
                 assert (w & 0x7FFF) == pos, (name, float(px), float(py))
-            got = (c - pos) & 1
-            j = pos - 1
-            while j >= 0 and pmax[b + j] > px:
-                sl, ic, hi, _ = rec[b + j]
-                if hi > px and px < fma32(sl, py, ic):
-                    got ^= 1
-                j -= 1
+            got = walk(b, pos, c, xlo_t=None, pm_t=pmax, px=px, py=py)
+            # HALF tables: pos over binary16 lo (rounded down), walk bounded by binary16 pmax (up)
+            pos16 = int(np.sum(lo16[b:b + c] <= px))
+            got16 = walk(b, pos16, c, xlo_t=None, pm_t=pm16, px=px, py=py)
+            assert got16 == want, ("half", name, float(px), float(py))
         assert got == want, (name, float(px), float(py))
 
 
