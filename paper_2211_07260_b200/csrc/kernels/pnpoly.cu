@@ -660,10 +660,9 @@
 // vertex before this group; LAST receives py - vy3 (chain to the next group).
 // The six FMA-pipe ops of point t+1 are interleaved one-to-one with the six
 // ALU LOP3s of point t (register set S = t % 2), so every warp's stream
-// alternates pipes instead of bursting one pipe at a time. (a ^ b) & c is
-// symmetric in a, b: the vertex difference shared by two consecutive edges
-// sits in the same operand slot of both LOP3s, so the operand-reuse cache
-// can serve its second read.
+// alternates pipes instead of bursting one pipe at a time. (Putting the
+// vertex difference shared by consecutive edges in the same LOP3 operand slot
+// lets ptxas set operand-reuse flags on 16 LOP3s; measured: no speed-up.)
 #define S7_F1(S, PX, PY) "mov.b64 py2" S ", {%" PY ", %" PY "};\n" "mov.b64 px2" S ", {%" PX ", %" PX "};\n" \
                          "sub.rn.f32x2 dA" S ", py2" S ", vyA;\n"
 #define S7_F2(S) "fma.rn.f32x2 xA" S ", slA, py2" S ", icA;\n"
@@ -674,10 +673,10 @@
     "mov.b64 {d0" S ", d1" S "}, dA" S ";\n" "mov.b64 {d2" S ", " LAST "}, dB" S ";\n"                   \
     "mov.b64 {e0" S ", e1" S "}, eA" S ";\n" "mov.b64 {e2" S ", e3" S "}, eB" S ";\n"
 #define S7_L1(S, PREV) "lop3.b32 t0" S ", d0" S ", " PREV ", e0" S ", 0x28;\n"
-#define S7_L2(S) "lop3.b32 t1" S ", d0" S ", d1" S ", e1" S ", 0x28;\n"
+#define S7_L2(S) "lop3.b32 t1" S ", d1" S ", d0" S ", e1" S ", 0x28;\n"
 #define S7_L3(S, ACC) "lop3.b32 %" ACC ", %" ACC ", t0" S ", t1" S ", 0x96;\n"
 #define S7_L4(S) "lop3.b32 t0" S ", d2" S ", d1" S ", e2" S ", 0x28;\n"
-#define S7_L5(S, LAST) "lop3.b32 t1" S ", d2" S ", " LAST ", e3" S ", 0x28;\n"
+#define S7_L5(S, LAST) "lop3.b32 t1" S ", " LAST ", d2" S ", e3" S ", 0x28;\n"
 #define S7_HEAD(S, PX, PY, LAST) S7_F1(S, PX, PY) S7_F2(S) S7_F3(S) S7_F4(S) S7_F5(S) S7_F6(S, LAST)
 #define S7_TAIL(S, ACC, PREV, LAST) S7_L1(S, PREV) S7_L2(S) S7_L3(S, ACC) S7_L4(S) S7_L5(S, LAST) S7_L3(S, ACC)
 #define S7_STEP(NS, NPX, NPY, NLAST, CS, CACC, CPREV, CLAST)                                         \
