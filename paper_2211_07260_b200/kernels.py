@@ -573,7 +573,7 @@ class Conv2DProblem(KernelProblem):
 
     def default_config(self):
         return {"block_size_x": 32, "block_size_y": 4, "tile_size_x": 4, "tile_size_y": 4, "use_shmem": 1,
-                "use_padding": 0}
+                "use_padding": 0, "fma2": 0}
 
     def defines(self, config):
         c = _as_dict(config)
@@ -674,7 +674,7 @@ class SgemmProblem(KernelProblem):
             "MWG": [16, 32, 64, 128], "NWG": [16, 32, 64, 128], "KWG": [16, 32],
             "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32], "NDIMB": [8, 16, 32],
             "KWI": [2, 8], "VWM": [1, 2, 4, 8], "VWN": [1, 2, 4, 8], "STRM": [0, 1], "STRN": [0, 1],
-            "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3], "FMA2": [0, 1],
+            "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3, 4], "FMA2": [0, 1],
         }
 
     def restrictions(self):
@@ -702,7 +702,7 @@ class SgemmProblem(KernelProblem):
 
     def default_config(self):
         return {"MWG": 128, "NWG": 128, "KWG": 16, "MDIMC": 16, "NDIMC": 16, "MDIMA": 32, "NDIMB": 32,
-                "KWI": 2, "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 0}
+                "KWI": 2, "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 0, "FMA2": 0}
 
     def defines(self, config):
         return dict(_as_dict(config))

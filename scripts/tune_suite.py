@@ -71,6 +71,17 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
             "restrictions": problem.restrictions(),
         }
         return doc, "random", 400
+    if name == "sgemm_wide":  # FMA2 only, larger CTA tiles (round-1 follow-up sweep)
+        doc = {
+            "parameters": {
+                "MWG": [128, 256], "NWG": [128, 256], "KWG": [8, 16, 32], "MDIMC": [8, 16, 32],
+                "NDIMC": [8, 16, 32], "MDIMA": [16, 32], "NDIMB": [16, 32], "KWI": [2, 8], "VWM": [2, 4],
+                "VWN": [2, 4], "STRM": [0, 1], "STRN": [0, 1], "SA": [1], "SB": [1], "ASYNC": [2, 3, 4],
+                "FMA2": [1],
+            },
+            "restrictions": problem.restrictions(),
+        }
+        return doc, "random", 300
     raise ValueError(name)
 
 
@@ -147,7 +158,7 @@ def confirm(dev, problem, leaders) -> list[dict]:
 
 
 def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | None) -> dict:
-    problem = make_problem(name)
+    problem = make_problem("sgemm" if name == "sgemm_wide" else name)
     doc, strategy, budget = curated_space(name, problem)
     space = SearchSpace.from_dict(doc)
     if clocks:
@@ -177,7 +188,8 @@ def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | No
     )
     # known-good seeds (hand-explored, scripts/time_sgemm.py) join the sampled configs
     seeded = []
-    for seed_cfg in SEEDS.get(name, []):
+    for seed_cfg in SEEDS.get(name, []) + ([] if name != "sgemm_wide" else [
+            {**c, "FMA2": 1} for c in [tuned_entry_config("sgemm")] if c]):
         one = SearchSpace.from_dict({"parameters": {k: [v] for k, v in seed_cfg.items()}})
         seeded += run_strategy(TuningRun(one, "exhaustive", Objective("energy")), dev, [NVMLObserver(duration)],
                                user_metrics=metrics, constants={"total_flops": problem.total_flops},
@@ -225,6 +237,13 @@ def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | No
     return entry
 
 
+def tuned_entry_config(kernel):
+    """The currently tuned time-optimal config of `kernel` (re-measured as a seed)."""
+    data = json.loads(TUNED_PATH.read_text()) if TUNED_PATH.exists() else {}
+    cfg = data.get(kernel, {}).get("time_optimal", {}).get("config")
+    return {k: v for k, v in cfg.items() if not k.startswith("nvml_")} if cfg else None
+
+
 def _try_compile(problem, cfg):
     try:
         problem.cubin({**problem.default_config(), **cfg})
@@ -253,7 +272,14 @@ def main():
         print("clock control:", probe.clock_mode, "->", clocks, flush=True)
     data = json.loads(TUNED_PATH.read_text()) if TUNED_PATH.exists() else {}
     for name in args.kernels.split(","):
-        data[name] = tune(gpu, name, args.duration, args.seed, clocks)
+        entry = tune(gpu, name, args.duration, args.seed, clocks)
+        if name == "sgemm_wide":  # a follow-up sweep of the sgemm space: keep whichever wins
+            old = data.get("sgemm")
+            if old and old["time_optimal"]["time_s"] <= entry["time_optimal"]["time_s"]:
+                data["sgemm_wide_sweep"] = entry
+                continue
+            name = "sgemm"
+        data[name] = entry
         TUNED_PATH.write_text(json.dumps(data, indent=1) + "\n")
     Path("gpurun_out").mkdir(exist_ok=True)
     Path("gpurun_out/tuned_b200.json").write_text(json.dumps(data, indent=1) + "\n")
