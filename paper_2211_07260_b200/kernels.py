@@ -761,7 +761,7 @@ class SgemmTF32Problem(SgemmProblem):
             "STAGES * (16384 + BN * 128 / (1 + PAIR)) + 2048 <= 232448",
             "PERSIST == 0 or BN >= 128",
             "PERSIST == 1 or SPLIT_TAIL == 0",
-            "PAIR == 0 or (PERSIST == 0 and BN >= 128)",
+            "PAIR == 0 or (BN >= 128 and SPLIT_TAIL == 0)",
             f"{self.m} % (128 * (1 + PAIR)) == 0 and {self.n} % BN == 0 and {self.k} % 32 == 0",
         ]
 
@@ -771,7 +771,7 @@ class SgemmTF32Problem(SgemmProblem):
     def defines(self, config):
         c = _as_dict(config)
         d = {"BN": c["BN"], "STAGES": c["STAGES"]}
-        if c.get("PERSIST", 0):
+        if c.get("PERSIST", 0) and not c.get("PAIR", 0):
             d["SPLIT_TAIL"] = c.get("SPLIT_TAIL", 0)
         return d
 
@@ -779,6 +779,8 @@ class SgemmTF32Problem(SgemmProblem):
         """(source file, kernel symbol): CTA-pair (cta_group::2), persistent warp-specialised, or one
         tile per CTA."""
         c = _as_dict(config)
+        if c.get("PAIR", 0) and c.get("PERSIST", 0):
+            return "sgemm_tf32c2p.cu", "sgemm_tf32c2p"
         if c.get("PAIR", 0):
             return "sgemm_tf32c2.cu", "sgemm_tf32c2"
         if c.get("PERSIST", 0):
@@ -804,6 +806,10 @@ class SgemmTF32Problem(SgemmProblem):
 
     def launch(self, config):
         c = _as_dict(config)
+        if c.get("PAIR", 0) and c.get("PERSIST", 0):  # persistent CTA pairs, one per TPC
+            sms = self.gpu.sm_count if self.gpu is not None else 148
+            pairs = min(sms // 2, (self.m // 256) * (self.n // c["BN"]))
+            return Launch((2 * pairs, 1, 1), (192, 1, 1), smem=self.smem_bytes(c), cluster_x=2)
         if c.get("PAIR", 0):  # one 256 x BN tile per CTA pair (cluster of 2 on one TPC)
             return Launch((2 * (self.n // c["BN"]), self.m // 256, 1), (128, 1, 1), smem=self.smem_bytes(c),
                           cluster_x=2)
@@ -831,7 +837,7 @@ class SgemmTF32Problem(SgemmProblem):
         c = _as_dict(config)
         b = self.buffers
         scalars = [i32(self.m), i32(self.n), i32(self.k), f32(self.alpha), f32(self.beta)]
-        if c.get("PERSIST", 0):
+        if c.get("PERSIST", 0) and not c.get("PAIR", 0):
             return [self._maps["a"], self._maps["b"], b["out"], b["workspace"], b["counters"], *scalars]
         return [self._maps["a"], self._maps["b"], b["out"], *scalars]
 
