@@ -19,10 +19,18 @@
 //     through its shared::cluster address), so the MMA never overwrites an
 //     accumulator either CTA is still reading;
 //   * tcgen05.commit ... multicast::cluster frees a stage in both CTAs and
-//     signals both epilogues.
+//     signals both epilogues;
+//   * SPLIT_TAIL: tiles = q * pairs + r. A static persistent schedule still
+//     leaves r pairs with one tile more than the others; when 2r <= pairs
+//     the r leftover tiles are split into two K halves run by 2r pairs.
+//     Each CTA of a half-pair stores its 128 partial rows to a workspace and
+//     bumps a counter per (tile, CTA rank); the second finisher sums the two
+//     halves in a fixed order (deterministic) and writes C. No CTA waits on
+//     another; counters only grow (odd = partner done), so relaunches need
+//     no reset.
 //
 // Storage and operand layout as sgemm_tf32c2.cu. Tunables (-D): BN (128,
-// 256), STAGES. Requires M % 256 == 0, N % BN == 0, K % 32 == 0. Launch:
+// 256), STAGES, SPLIT_TAIL. Requires M % 256 == 0, N % BN == 0, K % 32 == 0. Launch:
 // grid (2 * pairs, 1, 1), 192 threads, cluster (2, 1, 1).
 #ifndef BN
 #define BN 256
@@ -38,6 +46,9 @@
 #define STAGE_BYTES (A_STAGE_BYTES + B_STAGE_BYTES)
 #define TMEM_COLS (2 * BN)
 #define EPI_THREADS 128
+#ifndef SPLIT_TAIL
+#define SPLIT_TAIL 1
+#endif
 
 #if BN != 128 && BN != 256
 #error "BN must be 128 or 256"
@@ -103,6 +114,28 @@ __host__ __device__ constexpr unsigned instr_desc() {
            ((unsigned)(256 >> 4) << 24);
 }
 
+// A work unit: a tile and a K range; part 0 = whole tile, 1/2 = split halves.
+struct Unit {
+    int tile, k_begin, k_end, part;
+};
+// The static schedule of one pair, computed arithmetically.
+struct Schedule {
+    int dp_units, split_unit, dp_tiles, k_tiles, pair;
+    __device__ Schedule(int pair_, int pairs, int tiles, int k_tiles_) : k_tiles(k_tiles_), pair(pair_) {
+        const int full_waves = tiles / pairs, rest = tiles - full_waves * pairs;
+        const bool split = SPLIT_TAIL && rest > 0 && 2 * rest <= pairs && k_tiles >= 2;
+        dp_tiles = split ? full_waves * pairs : tiles;
+        dp_units = pair < dp_tiles ? (dp_tiles - 1 - pair) / pairs + 1 : 0;
+        split_unit = (split && pair < 2 * rest) ? 1 : 0;
+    }
+    __device__ int count() const { return dp_units + split_unit; }
+    __device__ Unit at(int i, int pairs) const {
+        if (i < dp_units) return Unit{pair + i * pairs, 0, k_tiles, 0};
+        const int half = pair & 1, mid = k_tiles / 2;
+        return Unit{dp_tiles + (pair >> 1), half ? mid : 0, half ? k_tiles : mid, 1 + half};
+    }
+};
+
 #define TMEM_LD32(taddr, v)                                                                                        \
     asm volatile(                                                                                                  \
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, " \
@@ -115,7 +148,8 @@ __host__ __device__ constexpr unsigned instr_desc() {
 
 extern "C" __global__ void __launch_bounds__(192, 1)
 sgemm_tf32c2p(const __grid_constant__ TensorMap map_a, const __grid_constant__ TensorMap map_b, float *__restrict__ c,
-              const int M, const int N, const int K, const float alpha, const float beta) {
+              float *__restrict__ workspace, unsigned *__restrict__ counters, const int M, const int N, const int K,
+              const float alpha, const float beta) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = (unsigned char *)(((unsigned long long)smem_raw + 1023) & ~1023ull);
     unsigned long long *full = (unsigned long long *)(smem + STAGES * STAGE_BYTES);
@@ -123,13 +157,15 @@ sgemm_tf32c2p(const __grid_constant__ TensorMap map_a, const __grid_constant__ T
     unsigned long long *tmem_full = empty + STAGES;  // [2]
     unsigned long long *tmem_empty = tmem_full + 2;  // [2], the leader's counts both CTAs
     unsigned *tmem_slot = (unsigned *)(tmem_empty + 2);
+    unsigned *reduce_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
     const int tiles_m = M / 256, tiles = tiles_m * (N / BN), k_tiles = K / BK;
-    const int n_units = pair < tiles ? (tiles - 1 - pair) / pairs + 1 : 0;
+    const Schedule sched(pair, pairs, tiles, k_tiles);
+    const int n_units = sched.count();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -158,10 +194,10 @@ sgemm_tf32c2p(const __grid_constant__ TensorMap map_a, const __grid_constant__ T
         if (lane == 0) {  // ---- TMA producer (both CTAs) ----
             int g = 0;
             for (int u = 0; u < n_units; ++u) {
-                const int tile = pair + u * pairs;
-                const int m0 = (tile % tiles_m) * 256, n0 = (tile / tiles_m) * BN;
+                const Unit unit = sched.at(u, pairs);
+                const int m0 = (unit.tile % tiles_m) * 256, n0 = (unit.tile / tiles_m) * BN;
                 const int m_own = m0 + (int)rank * BM, n_own = n0 + (int)rank * BN_HALF;
-                for (int kt = 0; kt < k_tiles; ++kt, ++g) {
+                for (int kt = unit.k_begin; kt < unit.k_end; ++kt, ++g) {
                     const int s = g % STAGES;
                     mbar_wait(smem_u32(&empty[s]), ((g / STAGES) & 1) ^ 1);
                     const unsigned bar_local = smem_u32(&full[s]);
@@ -182,18 +218,19 @@ sgemm_tf32c2p(const __grid_constant__ TensorMap map_a, const __grid_constant__ T
             const unsigned idesc = instr_desc();
             int g = 0;
             for (int u = 0; u < n_units; ++u) {
+                const Unit unit = sched.at(u, pairs);
                 const int acc = u & 1;
                 mbar_wait(smem_u32(&tmem_empty[acc]), ((u >> 1) & 1) ^ 1);  // both epilogues drained it
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const unsigned d_tmem = tmem + acc * BN;
-                for (int kt = 0; kt < k_tiles; ++kt, ++g) {
+                for (int kt = unit.k_begin; kt < unit.k_end; ++kt, ++g) {
                     const int s = g % STAGES;
                     mbar_wait(smem_u32(&full[s]), (g / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const unsigned a_base = smem_u32(smem + s * STAGE_BYTES), b_base = a_base + A_STAGE_BYTES;
 #pragma unroll
                     for (int kk = 0; kk < BK / 8; ++kk) {
-                        const unsigned accumulate = (kt | kk) ? 1u : 0u;
+                        const unsigned accumulate = (kt != unit.k_begin || kk) ? 1u : 0u;
                         asm volatile(
                             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                             "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
@@ -218,14 +255,58 @@ sgemm_tf32c2p(const __grid_constant__ TensorMap map_a, const __grid_constant__ T
         const int quarter = warp & 3;
         const int epi_tid = threadIdx.x - 64;
         for (int u = 0; u < n_units; ++u) {
+            const Unit unit = sched.at(u, pairs);
             const int acc = u & 1;
-            const int tile = pair + u * pairs;
-            const int m0 = (tile % tiles_m) * 256, n0 = (tile / tiles_m) * BN;
+            const int m0 = (unit.tile % tiles_m) * 256, n0 = (unit.tile / tiles_m) * BN;
             mbar_wait(smem_u32(&tmem_full[acc]), (u >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const int row = m0 + (int)rank * BM + quarter * 32 + lane;
-            float *crow = c + (size_t)row * N + n0;
+            const int local_row = (int)rank * BM + quarter * 32 + lane;  // row within the 256-row tile
+            float *crow = c + (size_t)(m0 + local_row) * N + n0;
             const unsigned lane_base = tmem + acc * BN + ((unsigned)(quarter * 32) << 16);
+            if (unit.part) {
+                // split-K half: publish this CTA's 128 partial rows, the second finisher reduces
+                const int slot = unit.tile - sched.dp_tiles;
+                const size_t half_stride = (size_t)256 * BN;
+                float *h0 = workspace + (size_t)2 * slot * half_stride + (size_t)local_row * BN;
+                float *mine = h0 + (unit.part - 1) * half_stride;
+#pragma unroll 1
+                for (int col = 0; col < BN; col += 32) {
+                    unsigned v[32];
+                    TMEM_LD32(lane_base + col, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    float4 *dst = reinterpret_cast<float4 *>(mine + col);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                named_sync(1, EPI_THREADS);
+                if (epi_tid == 0) mbar_arrive_cluster(map_to_rank(smem_u32(&tmem_empty[acc]), 0));
+                __threadfence();
+                named_sync(1, EPI_THREADS);
+                if (epi_tid == 0) *reduce_flag = atomicAdd(&counters[2 * slot + rank], 1u);
+                named_sync(1, EPI_THREADS);
+                const unsigned arrived_before = *reduce_flag;
+                named_sync(1, EPI_THREADS);  // everyone read the flag before the next unit reuses it
+                if (arrived_before & 1u) {   // second finisher: fixed order half 0 + half 1
+                    __threadfence();
+                    const float *h1 = h0 + half_stride;
+#pragma unroll 1
+                    for (int col = 0; col < BN; col += 4) {
+                        const float4 p0 = __ldcg(reinterpret_cast<const float4 *>(h0 + col));
+                        const float4 p1 = __ldcg(reinterpret_cast<const float4 *>(h1 + col));
+                        float4 *dst = reinterpret_cast<float4 *>(crow + col);
+                        float4 o = beta != 0.f ? *dst : make_float4(0.f, 0.f, 0.f, 0.f);
+                        o.x = fmaf(alpha, p0.x + p1.x, beta * o.x);
+                        o.y = fmaf(alpha, p0.y + p1.y, beta * o.y);
+                        o.z = fmaf(alpha, p0.z + p1.z, beta * o.z);
+                        o.w = fmaf(alpha, p0.w + p1.w, beta * o.w);
+                        *dst = o;
+                    }
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int col = 0; col < BN; col += 32) {
                 unsigned v[32];

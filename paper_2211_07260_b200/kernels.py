@@ -761,7 +761,8 @@ class SgemmTF32Problem(SgemmProblem):
             "STAGES * (16384 + BN * 128 / (1 + PAIR)) + 2048 <= 232448",
             "PERSIST == 0 or BN >= 128",
             "PERSIST == 1 or SPLIT_TAIL == 0",
-            "PAIR == 0 or (BN >= 128 and SPLIT_TAIL == 0)",
+            "PAIR == 0 or BN >= 128",
+            "PAIR == 0 or PERSIST == 1 or SPLIT_TAIL == 0",
             f"{self.m} % (128 * (1 + PAIR)) == 0 and {self.n} % BN == 0 and {self.k} % 32 == 0",
         ]
 
@@ -771,7 +772,7 @@ class SgemmTF32Problem(SgemmProblem):
     def defines(self, config):
         c = _as_dict(config)
         d = {"BN": c["BN"], "STAGES": c["STAGES"]}
-        if c.get("PERSIST", 0) and not c.get("PAIR", 0):
+        if c.get("PERSIST", 0):
             d["SPLIT_TAIL"] = c.get("SPLIT_TAIL", 0)
         return d
 
@@ -837,7 +838,7 @@ class SgemmTF32Problem(SgemmProblem):
         c = _as_dict(config)
         b = self.buffers
         scalars = [i32(self.m), i32(self.n), i32(self.k), f32(self.alpha), f32(self.beta)]
-        if c.get("PERSIST", 0) and not c.get("PAIR", 0):
+        if c.get("PERSIST", 0):
             return [self._maps["a"], self._maps["b"], b["out"], b["workspace"], b["counters"], *scalars]
         return [self._maps["a"], self._maps["b"], b["out"], *scalars]
 
