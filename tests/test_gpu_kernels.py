@@ -292,11 +292,15 @@ _TF32 = {"PERSIST": 0, "SPLIT_TAIL": 0, "PAIR": 0}
 TF32_CONFIGS = [_TF32 | c for c in (
     {"BN": 64, "STAGES": 3}, {"BN": 128, "STAGES": 6}, {"BN": 256, "STAGES": 2}, {"BN": 256, "STAGES": 4},
     {"BN": 128, "STAGES": 4, "PERSIST": 1}, {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1},
-    {"BN": 128, "STAGES": 6, "PAIR": 1}, {"BN": 256, "STAGES": 4, "PAIR": 1})]
+    {"BN": 128, "STAGES": 6, "PAIR": 1}, {"BN": 256, "STAGES": 4, "PAIR": 1},
+    # persistent CTA pairs (sgemm_tf32c2p.cu), with and without the split-K tail
+    {"BN": 256, "STAGES": 4, "PAIR": 1, "PERSIST": 1}, {"BN": 128, "STAGES": 5, "PAIR": 1, "PERSIST": 1},
+    {"BN": 256, "STAGES": 5, "PAIR": 1, "PERSIST": 1, "SPLIT_TAIL": 1})]
 
 
 @pytest.mark.parametrize("cfg", TF32_CONFIGS, ids=str)
-@pytest.mark.parametrize("mnk,beta", [((256, 256, 256), 0.5), ((384, 512, 96), 0.0), ((512, 768, 160), 1.0)])
+@pytest.mark.parametrize("mnk,beta", [((256, 256, 256), 0.5), ((384, 512, 96), 0.0), ((512, 768, 160), 1.0),
+                                      ((2560, 2048, 1024), 0.5)])
 def test_sgemm_tf32_tcgen05_within_tf32_tolerance(gpu, cfg, mnk, beta):
     from paper_2211_07260_b200.kernels import SgemmTF32Problem
 
@@ -310,6 +314,9 @@ def test_sgemm_tf32_tcgen05_within_tf32_tolerance(gpu, cfg, mnk, beta):
     err = O.sgemm_error(got, ref)
     assert err <= O.SGEMM_TF32_TOL
     assert err > 1e-6  # really TF32 inputs, not an FP32 path
+    if cfg.get("SPLIT_TAIL"):  # the split-K reduction has a fixed order: a relaunch gives the same bits
+        again = run_once(gpu, p, cfg)
+        assert np.array_equal(got.view(np.uint32), again.view(np.uint32))
 
 
 def test_sgemm_tf32_full_size(gpu):
