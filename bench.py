@@ -138,6 +138,34 @@ def cpu_conv_rate(budget_s: float, threads: int, rows_per_task: int = 32):
     return flops / dt / 1e9, done_rows, dt
 
 
+def cpu_kernel_rates() -> dict:
+    """The CPU oracle ports of the other kernels on bounded samples of their BASELINE workloads
+    (host cores, the same run), for the per-kernel GPU / CPU ratio. Test infrastructure as the
+    reported baseline only."""
+    from oracle import kernels_oracle as O
+    from paper_2211_07260_b200.kernels import PnPolyProblem, SgemmProblem
+
+    out = {}
+    threads = O.host_threads()
+    p = PnPolyProblem()
+    inp = p.host_inputs()
+    n = 2_000_000
+    t0 = time.perf_counter()
+    O.pnpoly(inp["points"][:n], inp["vx"], inp["vy"], 2, threads=threads)
+    dt = time.perf_counter() - t0
+    out["pnpoly"] = {"value": round(3.0 * n * p.n_vertices / dt / 1e9, 3), "unit": "GFLOP/s (3 ops per edge test)",
+                     "cores": threads, "kind": "port",
+                     "sample": f"{n} of 20 M points x 600 edges ({dt:.1f} s), C float32 crossing test, formulation 2"}
+    s = SgemmProblem(m=2048, n=2048, k=2048)
+    inp = s.host_inputs()
+    t0 = time.perf_counter()
+    O.sgemm(inp["a"], inp["b"], inp["c0"], s.alpha, s.beta)
+    dt = time.perf_counter() - t0
+    out["sgemm"] = {"value": round(s.total_flops / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                    "sample": f"2048^3 ({dt:.1f} s), numpy float64 matmul oracle (OpenBLAS threads)"}
+    return out
+
+
 def run_reference(args, dist: Dist) -> int:
     if dist.rank != 0:
         return 0
@@ -416,7 +444,9 @@ def run_ours(args, dist: Dist) -> int:
             per_kernel[name] = {obj: measure_tuned(gpu, name, obj) for obj in ("time_optimal", "energy_optimal")}
 
     cpu = None
+    cpu_kernels = None
     if dist.rank == 0 and dist.world == 1 and not args.quick:
+        cpu_kernels = cpu_kernel_rates()
         threads = len(os.sched_getaffinity(0))
         rate, rows, dt = cpu_conv_rate(budget_s=10.0, threads=threads)
         cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
@@ -480,6 +510,8 @@ def run_ours(args, dist: Dist) -> int:
             line["tuning"] = tuning
         if cpu:
             line["cpu_baseline"] = cpu
+        if cpu_kernels:
+            line["cpu_per_kernel"] = cpu_kernels
         print(json.dumps(line))
     gpu.close()
     return 0
