@@ -36,7 +36,7 @@ from typing import Any, Callable, Mapping
 import numpy as np
 
 from .hardware import EXECUTION_PARAMS, DeviceSpec, DeviceState, Execution, PowerSample
-from .errors import CapabilityError, ConfigurationError, DomainError
+from .errors import CapabilityError, DomainError
 from .gpu import ENERGY, E_STAMP, GPU, MEM_MHZ, P_INST, REASONS, SM_MHZ, SW_POWER_CAP, TEMP, T
 from .kernels import KernelProblem, make_problem
 from .spaces import KernelConfig, normalize_value

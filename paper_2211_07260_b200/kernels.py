@@ -30,7 +30,7 @@ from typing import Any, Mapping
 import numpy as np
 
 from . import native
-from .gpu import GPU, DeviceArray, Kernel, Launch, f32, i32, rows
+from .gpu import GPU, Kernel, Launch, f32, i32, rows
 from .spaces import KernelConfig, SearchSpace
 
 __all__ = [
