@@ -1248,6 +1248,129 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
     return JT_OK;
 }
 
+// Monotone integer key of a float (total order of the non-NaN floats, -0.0 < +0.0 by bits).
+static uint32_t float_key(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+static float key_float(uint32_t k) {
+    const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+// Smallest non-NaN float v with slab_bucket(v) >= k (+inf if none): bucket is monotone in v.
+static float bucket_first(int k, float base, float scale, int hi) {
+    uint32_t lo = float_key(-INFINITY), up = float_key(INFINITY);
+    if (slab_bucket(key_float(up), base, scale, hi) < k) return INFINITY;
+    while (lo < up) {
+        const uint32_t mid = lo + (up - lo) / 2;
+        if (slab_bucket(key_float(mid), base, scale, hi) >= k) up = mid; else lo = mid + 1;
+    }
+    return key_float(lo);
+}
+
+int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, float *params, uint32_t *bits,
+                   long long capacity, int *clean_cells) {
+    if (!vx || !vy || !params || n < 3) return fail(JT_EINVAL, "polygon needs >= 3 vertices");
+    if (gw < 1 || gh < 1 || (long long)gw * gh > (1LL << 26)) return fail(JT_EINVAL, "bad grid %d x %d", gw, gh);
+    const long long words = ((long long)gw * gh + 15) / 16;
+    // METHOD 2 edges and y-slabs, bit for bit those of jt_pnpoly_slabs
+    std::vector<float> slope(n), icpt(n), ylo(n), yhi(n);
+    float xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+    for (int k = 0; k < n; ++k) {
+        if (std::isnan(vy[k]) || std::isnan(vx[k])) return fail(JT_EINVAL, "vertex %d is NaN", k);
+        const int p = (k + n - 1) % n;
+        const float dx = vx[p] - vx[k];
+        const float dy = vy[p] - vy[k];
+        volatile float s = dx / dy;
+        slope[k] = s;
+        icpt[k] = std::fmaf(-slope[k], vy[k], vx[k]);
+        ylo[k] = std::min(vy[k], vy[p]);
+        yhi[k] = std::max(vy[k], vy[p]);
+        xmin = std::min(xmin, vx[k]), xmax = std::max(xmax, vx[k]);
+        ymin = std::min(ymin, vy[k]), ymax = std::max(ymax, vy[k]);
+    }
+    std::vector<float> u(vy, vy + n);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end(), [](float a, float b) { return a == b; }), u.end());
+    const int nu = (int)u.size();
+    // the cell of a point: (min(max(f2i_rz((px - x0) * sx), 0), gw - 1), same in y), float32 ops as the kernel
+    const float x0 = xmin, y0 = ymin;
+    const float sx = xmax > xmin ? (float)gw / (xmax - xmin) : 0.f;
+    const float sy = ymax > ymin ? (float)gh / (ymax - ymin) : 0.f;
+    params[0] = x0, params[1] = sx, params[2] = y0, params[3] = sy;
+    if (!bits) return JT_OK;
+    if (capacity < words) return fail(JT_EINVAL, "grid needs %lld words, got %lld", words, capacity);
+    std::memset(bits, 0, sizeof(uint32_t) * words);
+    // exact float ranges of the cells: [first(k), pred(first(k + 1))]
+    std::vector<float> cx0(gw + 1), cy0(gh + 1);
+    for (int k = 0; k <= gw; ++k) cx0[k] = k == 0 ? -INFINITY : bucket_first(k, x0, sx, gw - 1);
+    for (int k = 0; k <= gh; ++k) cy0[k] = k == 0 ? -INFINITY : bucket_first(k, y0, sy, gh - 1);
+    cx0[gw] = cy0[gh] = INFINITY;
+    // slab lists
+    std::vector<std::vector<int>> slab(nu + 1);
+    for (int r = 1; r < nu; ++r)
+        for (int k = 0; k < n; ++k)
+            if (ylo[k] <= u[r - 1] && yhi[k] >= u[r]) slab[r].push_back(k);
+    auto rank = [&](float y) { return (int)(std::upper_bound(u.begin(), u.end(), y) - u.begin()); };
+    int clean = 0;
+    std::vector<float> elo, ehi;
+    for (int cy = 0; cy < gh; ++cy) {
+        const float Y0 = cy0[cy], Y1 = cy0[cy + 1] == INFINITY ? INFINITY : std::nextafter(cy0[cy + 1], -INFINITY);
+        if (!(Y0 <= Y1)) continue;  // no float maps to this row
+        const int r0 = rank(Y0), r1 = rank(Y1);
+        // per slab of the row: the py sub-range and every edge's computed-x range over it
+        struct Part { int r; float lo_y, hi_y; };
+        std::vector<Part> parts;
+        for (int r = r0; r <= r1; ++r) {
+            const float a = r == r0 ? Y0 : u[r - 1];
+            const float b = r == r1 ? Y1 : std::nextafter(u[r], -INFINITY);
+            parts.push_back({r, a, b});
+        }
+        std::vector<std::vector<std::pair<float, float>>> ranges(parts.size());
+        bool row_nan = false;
+        for (size_t q = 0; q < parts.size(); ++q) {
+            const Part &P = parts[q];
+            if (P.r <= 0 || P.r >= nu) continue;
+            for (int k : slab[P.r]) {
+                const float a = std::fmaf(slope[k], P.lo_y, icpt[k]);
+                const float b = std::fmaf(slope[k], P.hi_y, icpt[k]);
+                if (std::isnan(a) || std::isnan(b)) row_nan = true;
+                ranges[q].push_back({std::min(a, b), std::max(a, b)});
+            }
+        }
+        if (row_nan) continue;  // leave the whole row to the exact search
+        for (int cx = 0; cx < gw; ++cx) {
+            const float X0 = cx0[cx], X1 = cx0[cx + 1] == INFINITY ? INFINITY : std::nextafter(cx0[cx + 1], -INFINITY);
+            if (!(X0 <= X1)) continue;
+            // every edge of every slab of the row must be decided for all px in [X0, X1]:
+            // X1 < lo (crosses for every point of the cell) or X0 >= hi (for none); and the
+            // number of crossings must have one parity in every slab the cell's rows span
+            int parity = -1;
+            bool ok = true;
+            for (size_t q = 0; q < parts.size() && ok; ++q) {
+                int cnt = 0;
+                for (const auto &lh : ranges[q]) {
+                    if (X1 < lh.first) ++cnt;
+                    else if (!(X0 >= lh.second)) { ok = false; break; }
+                }
+                if (ok) {
+                    if (parity < 0) parity = cnt & 1;
+                    else if (parity != (cnt & 1)) ok = false;
+                }
+            }
+            if (!ok) continue;
+            const long long cell = (long long)cy * gw + cx;
+            bits[cell >> 4] |= (1u | ((uint32_t)parity << 1)) << ((cell & 15) * 2);  // bit 0 clean, bit 1 inside
+            ++clean;
+        }
+    }
+    if (clean_cells) *clean_cells = clean;
+    return JT_OK;
+}
+
 int jt_tensor_map_2d(jt_ctx *c, unsigned long long dptr, unsigned long long rows, unsigned long long cols,
                      unsigned box_rows, unsigned box_cols, int swizzle, void *out128) {
     if (int e = bind(c)) return e;

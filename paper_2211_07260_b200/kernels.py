@@ -37,6 +37,7 @@ __all__ = [
     "KernelProblem",
     "PnPolyProblem",
     "PnPolySlabProblem",
+    "PnPolyGridProblem",
     "Conv2DProblem",
     "SgemmProblem",
     "SgemmTF32Problem",
@@ -525,6 +526,92 @@ class PnPolySlabProblem(PnPolyProblem):
         return float((band[r + 1] - band[r]).astype(np.int64).sum())
 
 
+@dataclass
+class PnPolyGridProblem(PnPolySlabProblem):
+    """PnPoly with a uniform-cell fast path (csrc/kernels/pnpoly_grid.cu).
+
+    The same bitmap as :class:`PnPolyProblem` at METHOD 2, bit for bit: a
+    GRID x GRID raster of cells (libjt ``jt_pnpoly_grid``) answers every point
+    whose cell is provably clean with one lookup; the others are queued per
+    warp and run the exact x-search of the slab kernel (its table read
+    through L1 / L2). Reported as its own kernel against the HBM roofline.
+    """
+
+    name: str = "pnpoly_grid"
+    source: str = "pnpoly_grid.cu"
+    symbol: str = "pnpoly_grid"
+
+    def tune_params(self):
+        return {
+            "block_size_x": [256, 512, 1024],
+            "tile": [1, 2, 4],
+            "grid": [256, 512],
+            "xbuckets": [8, 16],
+            "buckets": [1024, 4096],
+        }
+
+    def restrictions(self):
+        return [f"(grid * grid / 4 + block_size_x / 32 * {16 * 64}) <= {227 * 1024}"]
+
+    def default_config(self):
+        return {"block_size_x": 1024, "tile": 2, "grid": 512, "xbuckets": 16, "buckets": 4096}
+
+    def defines(self, config):
+        c = _as_dict(config)
+        return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"]}
+
+    def grid_table(self, g: int):
+        cache = self.__dict__.setdefault("_grid_tables", {})
+        if g not in cache:
+            vx, vy = self._polygon()
+            cache[g] = native.pnpoly_grid(vx, vy, g, g)
+        return cache[g]
+
+    def smem_bytes(self, config) -> int:
+        c = _as_dict(config)
+        words = (c["grid"] * c["grid"] + 15) // 16
+        return ((words + 3) // 4 * 4) * 4 + c["block_size_x"] // 32 * 64 * 16
+
+    def launch(self, config, n_points: int | None = None):
+        c = _as_dict(config)
+        chunk = c["block_size_x"] * c["tile"]
+        chunks = max(1, math.ceil((self.n_points if n_points is None else n_points) / chunk))
+        smem = self.smem_bytes(c)
+        sms = self.gpu.sm_count if self.gpu is not None else 148
+        resident = max(1, min(2048 // c["block_size_x"], (228 * 1024) // (smem + 1024)))
+        return Launch((min(chunks, sms * resident), 1, 1), (c["block_size_x"], 1, 1), smem)
+
+    def prepare(self, gpu, inputs=None):
+        super().prepare(gpu, inputs)
+        self.__dict__.pop("_grid_tables", None)
+
+    def _tail(self, c):
+        g = c["grid"]
+        key = f"grid{g}"
+        words, params, _ = self.grid_table(g)
+        if key not in self.buffers:
+            self.buffers[key] = self.gpu.array(words)
+        info = self.slab_info(c["buckets"], c["xbuckets"])
+        return [self.buffers[key], f32(params[0]), f32(params[1]), f32(params[2]), f32(params[3]),
+                self._table_buffer(c["buckets"], c["xbuckets"]), i32(info.nu), i32(info.ng), i32(info.xb),
+                f32(info.ybase), f32(info.yscale), i32(info.guess_off), i32(info.xpar_off), i32(info.xst_off),
+                i32(info.xlo_off), i32(info.pmax_off), i32(info.pair_off)]
+
+    def clean_fraction(self, g: int) -> float:
+        """Fraction of this input's points that land in a clean cell (the fast path)."""
+        words, prm, _ = self.grid_table(g)
+        pts = self.inputs["points"]
+
+        def cell(v, base, scale):
+            with np.errstate(invalid="ignore", over="ignore"):
+                f = (v.astype(np.float32) - np.float32(base)) * np.float32(scale)
+            k = np.trunc(np.nan_to_num(f, nan=0.0, posinf=2.0**31, neginf=-2.0**31))
+            return np.clip(k, 0, g - 1).astype(np.int64)
+
+        idx = cell(pts[:, 1], prm[2], prm[3]) * g + cell(pts[:, 0], prm[0], prm[1])
+        return float(((words[idx >> 4] >> ((idx & 15) * 2).astype(np.uint32)) & 1).mean())
+
+
 # -- Conv2D -------------------------------------------------------------------------------
 
 
@@ -887,7 +974,8 @@ class BurnerProblem(KernelProblem):
         return [self.buffers["sink"], i32(self.iters), f32(1.0)]
 
 
-PROBLEMS = {"pnpoly": PnPolyProblem, "pnpoly_slab": PnPolySlabProblem, "conv2d": Conv2DProblem, "sgemm": SgemmProblem, "sgemm_tf32": SgemmTF32Problem,
+PROBLEMS = {"pnpoly": PnPolyProblem, "pnpoly_slab": PnPolySlabProblem, "pnpoly_grid": PnPolyGridProblem,
+            "conv2d": Conv2DProblem, "sgemm": SgemmProblem, "sgemm_tf32": SgemmTF32Problem,
             "burner": BurnerProblem}
 
 

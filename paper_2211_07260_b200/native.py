@@ -53,7 +53,7 @@ EXPORTS = (
     "jt_app_clocks_set", "jt_app_clocks_reset", "jt_power_limit_set", "jt_power_limit_reset",
     "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
     "jt_h2d_async", "jt_d2h_async", "jt_tensor_map_2d", "jt_streams_reserve", "jt_stream_select",
-    "jt_stream_wait_event", "jt_pnpoly_slabs",
+    "jt_stream_wait_event", "jt_pnpoly_slabs", "jt_pnpoly_grid",
 )
 
 
@@ -238,6 +238,7 @@ def _declare(lib) -> None:
         "jt_pnpoly_edges": (c.c_int, [P, P, c.c_int, c.c_int, P, P]),
         "jt_pnpoly_slabs": (c.c_int, [P, P, c.c_int, c.c_int, c.c_int, c.c_int, P, c.c_longlong,
                                       c.POINTER(JTSlabInfo)]),
+        "jt_pnpoly_grid": (c.c_int, [P, P, c.c_int, c.c_int, c.c_int, P, P, c.c_longlong, c.POINTER(c.c_int)]),
         "jt_module_set_global": (c.c_int, [P, P, c.c_char_p, P, c.c_size_t]),
     }
     for name, (res, args) in sig.items():
@@ -378,3 +379,18 @@ def pnpoly_slabs(vx, vy, buckets: int, pad: int, xbuckets: int = 0):
     check(L.jt_pnpoly_slabs(vx.ctypes.data, vy.ctypes.data, vx.size, int(buckets), int(pad), int(xbuckets), table.ctypes.data,
                             table.size, ctypes.byref(info)), "jt_pnpoly_slabs")
     return table, info
+
+
+def pnpoly_grid(vx, vy, gw: int, gh: int):
+    """Uniform-cell fast-path bits for csrc/kernels/pnpoly_grid.cu (libjt ``jt_pnpoly_grid``):
+    returns (uint32 words, 2 bits per cell), params {x0, sx, y0, sy} and the clean-cell count."""
+    import numpy as np
+
+    vx = np.ascontiguousarray(vx, dtype=np.float32)
+    vy = np.ascontiguousarray(vy, dtype=np.float32)
+    params = np.zeros(4, dtype=np.float32)
+    words = np.zeros((gw * gh + 15) // 16, dtype=np.uint32)
+    clean = ctypes.c_int()
+    check(lib().jt_pnpoly_grid(vx.ctypes.data, vy.ctypes.data, vx.size, int(gw), int(gh), params.ctypes.data,
+                               words.ctypes.data, words.size, ctypes.byref(clean)), "jt_pnpoly_grid")
+    return words, params, clean.value

@@ -154,3 +154,86 @@ def test_slab_through_tune_kernel():
                                                             "half": [0, 1], "buckets": [4096]},
                                 problem_kwargs={"n_points": 1 << 20}, duration=0.05)
     assert len(rows) == 4 and not any(r["failed"] for r in rows) and outcome.best.metrics["gflops"] > 0
+
+
+# -- uniform-cell fast path in front of the slab search (csrc/kernels/pnpoly_grid.cu) ---------
+
+GRID_CONFIGS = [dict(block_size_x=b, tile=t, grid=g, xbuckets=x, buckets=4096)
+                for b, t, g, x in itertools.product((256, 1024), (1, 4), (256, 512), (8, 16))]
+
+
+@pytest.fixture(scope="module")
+def grid_small(gpu):
+    from paper_2211_07260_b200.kernels import PnPolyGridProblem
+
+    p = PnPolyGridProblem(n_points=1_000_003)
+    p.prepare(gpu)
+    return p, O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
+
+
+@pytest.mark.parametrize("cfg", GRID_CONFIGS, ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
+def test_grid_bit_exact_across_configs(gpu, grid_small, cfg):
+    p, want = grid_small
+    assert p.is_valid(cfg)
+    got = run_once(gpu, p, cfg)
+    assert np.array_equal(got, want), f"{int((got != want).sum())} points differ"
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 4097])
+def test_grid_tiny_and_ragged_inputs(gpu, n):
+    from paper_2211_07260_b200.kernels import PnPolyGridProblem
+
+    p = PnPolyGridProblem(n_points=n)
+    p.prepare(gpu)
+    for cfg in (p.default_config(), dict(p.default_config(), block_size_x=256, tile=1, grid=256)):
+        np.testing.assert_array_equal(run_once(gpu, p, cfg),
+                                      O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2))
+
+
+@pytest.mark.parametrize("shape", ["degenerate", "star3000", "convex50", "comb"])
+def test_grid_other_polygons_and_special_points(gpu, shape):
+    """Degenerate polygon with +-0, +-inf and NaN coordinates; the slab tests' other polygons;
+    points exactly on vertices and on cell borders."""
+    from paper_2211_07260_b200 import native
+    from paper_2211_07260_b200.kernels import PnPolyGridProblem
+
+    rng = np.random.default_rng(12)
+    if shape == "degenerate":
+        vx = np.array([0.0, 0.5, 0.5, 1.0, 1.0, 0.0, 0.0], np.float32)
+        vy = np.array([0.0, 0.0, 0.25, 0.25, 1.0, 1.0, 1.0], np.float32)
+    elif shape == "comb":
+        vx = np.array([0, 4, 4, 3, 3, 2, 2, 1, 1, 0], np.float32) / 4 - 0.5
+        vy = np.array([0, 0, 3, 3, 1, 1, 3, 3, 1, 1], np.float32) / 3 - 0.5
+    else:
+        m = 3000 if shape == "star3000" else 50
+        th = np.sort(rng.uniform(0, 2 * np.pi, m))
+        rad = 0.4 + 0.5 * rng.uniform(0, 1, m) if m == 3000 else np.full(m, 0.9)
+        vx, vy = (rad * np.cos(th)).astype(np.float32), (rad * np.sin(th)).astype(np.float32)
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 0.25, -0.5, 1.5], np.float32)
+    pts = [rng.uniform(-1.2, 1.2, (200_001, 2)).astype(np.float32), np.stack([vx, vy], 1),
+           np.array([[a, b] for a in special for b in special], np.float32)]
+    for g in (256, 512):
+        _, prm, _ = native.pnpoly_grid(vx, vy, g, g)
+        xs = (np.float32(prm[0]) + np.arange(g + 1, dtype=np.float32) / np.float32(prm[1])).astype(np.float32)
+        pts.append(np.stack([xs, rng.uniform(-1, 1, xs.size).astype(np.float32)], 1))
+    pts = np.ascontiguousarray(np.concatenate(pts).astype(np.float32))
+    p = PnPolyGridProblem(n_points=len(pts), n_vertices=vx.size)
+    p.prepare(gpu, {"points": pts, "vx": vx, "vy": vy})
+    want = O.pnpoly(pts, vx, vy, 2)
+    cfgs = [c for c in GRID_CONFIGS[::3] if p.is_valid(c)] + [p.default_config()]
+    for cfg in cfgs:
+        np.testing.assert_array_equal(run_once(gpu, p, cfg), want, err_msg=f"{shape} {cfg}")
+
+
+def test_grid_full_size_matches_brute_force(gpu):
+    from paper_2211_07260_b200 import tuned
+    from paper_2211_07260_b200.kernels import PnPolyGridProblem
+
+    p = PnPolyGridProblem()
+    p.prepare(gpu)
+    want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
+    for cfg in {str(c): c for c in [p.default_config(), tuned.best_config("pnpoly_grid"),
+                                    tuned.best_config("pnpoly_grid", "energy_optimal")] if c}.values():
+        got = run_once(gpu, p, cfg)
+        assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ ({cfg})"
+    assert p.clean_fraction(512) > 0.9

@@ -199,3 +199,51 @@ def test_half_copy_is_conservative_and_tight(name):
     with np.errstate(over="ignore"):
         assert np.all(np.nextafter(lo16, np.float16(np.inf)).astype(np.float32) > lo)
         assert np.all(np.nextafter(pm16, np.float16(-np.inf)).astype(np.float32) < pm)
+
+
+def _cell(v, base, scale, hi):
+    with np.errstate(invalid="ignore", over="ignore"):
+        f = (np.float32(v) - np.float32(base)) * np.float32(scale)
+    f = np.asarray(f, dtype=np.float32)
+    k = np.where(np.isnan(f), 0, np.trunc(np.nan_to_num(f, posinf=2.0**31, neginf=-2.0**31)))
+    return np.clip(np.clip(k, -2**31, 2**31 - 1), 0, hi).astype(np.int64)
+
+
+@pytest.mark.parametrize("name", sorted(POLYGONS))
+@pytest.mark.parametrize("g", [7, 64, 512])
+def test_grid_clean_cells_give_the_brute_force_parity(name, g):
+    """jt_pnpoly_grid: wherever a cell is flagged clean, its stored parity equals the
+    brute-force (formulation 2) bit of every point mapping to it - checked on random points,
+    points on/near vertices and cell borders, and points far outside."""
+    from oracle import kernels_oracle as O
+
+    if POLYGONS[name] is None:
+        vx, vy = PnPolySlabProblem(n_points=4096)._polygon()
+    else:
+        vx, vy = POLYGONS[name]
+    words, prm, clean = native.pnpoly_grid(vx, vy, g, g)
+    assert 0 <= clean <= g * g
+    rng = np.random.default_rng(3)
+    span = float(max(abs(vx).max(), abs(vy).max())) * 1.3
+    pts = [rng.uniform(-span, span, (200_000, 2)).astype(np.float32)]
+    vv = np.stack([vx, vy], 1).astype(np.float32)
+    for d in (0.0, 1e-7, -1e-7, 1e-3):
+        pts.append((vv + np.float32(d)).astype(np.float32))
+    # cell borders in x and y
+    xs = (np.float32(prm[0]) + np.arange(g + 1, dtype=np.float32) / np.float32(prm[1])).astype(np.float32)
+    ys = (np.float32(prm[2]) + np.arange(g + 1, dtype=np.float32) / np.float32(prm[3])).astype(np.float32)
+    bx = np.concatenate([xs, np.nextafter(xs, np.float32(np.inf)), np.nextafter(xs, np.float32(-np.inf))])
+    by = np.concatenate([ys, np.nextafter(ys, np.float32(np.inf)), np.nextafter(ys, np.float32(-np.inf))])
+    pts.append(np.stack([rng.choice(bx, 50_000), rng.uniform(-span, span, 50_000).astype(np.float32)], 1))
+    pts.append(np.stack([rng.uniform(-span, span, 50_000).astype(np.float32), rng.choice(by, 50_000)], 1))
+    pts.append(np.array([[1e30, 0], [-1e30, 0], [0, 1e30], [0, -1e30], [np.inf, 0], [-np.inf, 0]], np.float32))
+    pts = np.ascontiguousarray(np.concatenate(pts).astype(np.float32))
+    cx = _cell(pts[:, 0], prm[0], prm[1], g - 1)
+    cy = _cell(pts[:, 1], prm[2], prm[3], g - 1)
+    cell = cy * g + cx
+    code = (words[cell >> 4] >> ((cell & 15) * 2).astype(np.uint32)) & 3
+    want = O.pnpoly(pts, vx, vy, 2)
+    is_clean = (code & 1) == 1
+    assert np.array_equal((code[is_clean] >> 1).astype(np.int32), want[is_clean]), name
+    if name == "benchmark" and g == 512:
+        assert is_clean.mean() > 0.8  # the fast path is the common path
