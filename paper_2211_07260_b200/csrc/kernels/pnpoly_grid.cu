@@ -126,11 +126,11 @@ pnpoly_grid(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, 
             if (i < n) {
                 int res = 0;  // NaN coordinates: every compare is false, never inside
                 if (px == px && py == py) {
-                    int cx = __float2int_rz(__fmul_rn(__fsub_rn(px, gx0), gsx));
-                    int cy = __float2int_rz(__fmul_rn(__fsub_rn(py, gy0), gsy));
-                    cx = min(max(cx, 0), GRID - 1);
-                    cy = min(max(cy, 0), GRID - 1);
-                    const unsigned cell = (unsigned)(cy * GRID + cx);
+                    // min(max(f2i_rz(v), 0), GRID - 1) of the host's cell function, in one clamp:
+                    // cvt.rzi.u32 already maps NaN and negatives to 0
+                    const unsigned cx = min(__float2uint_rz(__fmul_rn(__fsub_rn(px, gx0), gsx)), GRID - 1u);
+                    const unsigned cy = min(__float2uint_rz(__fmul_rn(__fsub_rn(py, gy0), gsy)), GRID - 1u);
+                    const unsigned cell = cy * GRID + cx;
                     const unsigned code = (s_grid[cell >> 4] >> ((cell & 15u) * 2u)) & 3u;
                     slow = !(code & 1u);
                     res = (int)(code >> 1);

@@ -154,15 +154,18 @@ def pnpoly(points: np.ndarray, vx: np.ndarray, vy: np.ndarray, *, config=None, o
     (``strips`` point chunks pipelined over copy/compute streams; 1 = one launch).
 
     ``algorithm``: "brute" tests every edge (pnpoly.cu, the paper's kernel);
-    "slab" locates each point's y-slab and x-position first (pnpoly_slab.cu),
-    giving the brute-force METHOD 2 bitmap bit for bit at a fraction of the work."""
-    if algorithm not in ("brute", "slab"):
-        raise ValueError(f"algorithm must be 'brute' or 'slab', not {algorithm!r}")
+    "slab" locates each point's y-slab and x-position first (pnpoly_slab.cu);
+    "grid" answers points in provably clean cells with one lookup and runs the
+    slab search for the rest (pnpoly_grid.cu). All three give the brute-force
+    METHOD 2 bitmap bit for bit."""
+    names = {"brute": "pnpoly", "slab": "pnpoly_slab", "grid": "pnpoly_grid"}
+    if algorithm not in names:
+        raise ValueError(f"algorithm must be one of {sorted(names)}, not {algorithm!r}")
     points = np.asarray(points, dtype=np.float32)
     vx = np.asarray(vx, dtype=np.float32)
     vy = np.asarray(vy, dtype=np.float32)
     key = (points.shape[0], vx.size, vx.tobytes(), vy.tobytes())
-    name = "pnpoly" if algorithm == "brute" else "pnpoly_slab"
+    name = names[algorithm]
     r = _runner(name, key, config, {"n_points": points.shape[0], "n_vertices": vx.size},
                 {"points": points, "vx": vx, "vy": vy}, ordinal)
     return r.run({"points": points}, out, strips=strips)

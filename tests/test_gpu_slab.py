@@ -109,6 +109,8 @@ def test_slab_host_api_matches_brute_force(gpu, strips):
     pts = suite.pinned(inp["points"].shape, np.float32)
     pts[...] = inp["points"]
     slab = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips, algorithm="slab").copy()
+    grid = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips, algorithm="grid").copy()
+    np.testing.assert_array_equal(grid, slab)
     brute = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips,
                          config=dict(PnPolyProblem().default_config(), asm=0, method=2)).copy()
     np.testing.assert_array_equal(slab, brute)
