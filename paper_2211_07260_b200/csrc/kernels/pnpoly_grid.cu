@@ -48,6 +48,7 @@ struct SlabTable {
 
 // The exact search of pnpoly_slab.cu (XSEARCH), loads through the read-only path.
 __device__ __forceinline__ int slab_search(float px, float py, const SlabTable &T) {
+    if (!(px == px) || !(py == py)) return 0;  // NaN: every compare is false, never inside
     int g = __float2int_rz(__fmul_rn(__fsub_rn(py, T.ybase), T.yscale));
     g = min(max(g, 0), T.ng - 1);
     int r = __ldg(T.guess + g) & 0x7fffffff;
@@ -124,18 +125,18 @@ pnpoly_grid(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, 
             const float px = cur[t].x, py = cur[t].y;
             bool slow = false;
             if (i < n) {
-                int res = 0;  // NaN coordinates: every compare is false, never inside
-                if (px == px && py == py) {
-                    // min(max(f2i_rz(v), 0), GRID - 1) of the host's cell function, in one clamp:
-                    // cvt.rzi.u32 already maps NaN and negatives to 0
-                    const unsigned cx = min(__float2uint_rz(__fmul_rn(__fsub_rn(px, gx0), gsx)), GRID - 1u);
-                    const unsigned cy = min(__float2uint_rz(__fmul_rn(__fsub_rn(py, gy0), gsy)), GRID - 1u);
-                    const unsigned cell = cy * GRID + cx;
-                    const unsigned code = (s_grid[cell >> 4] >> ((cell & 15u) * 2u)) & 3u;
-                    slow = !(code & 1u);
-                    res = (int)(code >> 1);
-                }
-                if (!slow) bitmap[i] = res;
+                // min(max(f2i_rz(v), 0), GRID - 1) of the host's cell function, in one clamp:
+                // cvt.rzi.u32 already maps NaN and negatives to 0. A NaN coordinate lands in
+                // the first column (px) or row (py): a clean cell there has parity 0 (no edge
+                // spans below every vertex; every spanning edge crosses left of every vertex,
+                // and a closed polygon has an even number of them), which is the answer for
+                // NaN; an unclean one sends the point to slab_search, which returns 0.
+                const unsigned cx = min(__float2uint_rz(__fmul_rn(__fsub_rn(px, gx0), gsx)), GRID - 1u);
+                const unsigned cy = min(__float2uint_rz(__fmul_rn(__fsub_rn(py, gy0), gsy)), GRID - 1u);
+                const unsigned cell = cy * GRID + cx;
+                const unsigned code = (s_grid[cell >> 4] >> ((cell & 15u) * 2u)) & 3u;
+                slow = !(code & 1u);
+                if (!slow) bitmap[i] = (int)(code >> 1);
             }
             // queue the undecided points of this warp; search 32 at a time
             const unsigned need = __ballot_sync(0xffffffffu, slow);

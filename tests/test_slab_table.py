@@ -247,3 +247,20 @@ def test_grid_clean_cells_give_the_brute_force_parity(name, g):
     assert np.array_equal((code[is_clean] >> 1).astype(np.int32), want[is_clean]), name
     if name == "benchmark" and g == 512:
         assert is_clean.mean() > 0.8  # the fast path is the common path
+
+
+@pytest.mark.parametrize("name", sorted(POLYGONS))
+def test_grid_border_cells_are_zero_when_clean(name):
+    """pnpoly_grid.cu sends NaN coordinates to the first column / row without a NaN test:
+    every clean cell there must hold parity 0 (the NaN answer)."""
+    if POLYGONS[name] is None:
+        vx, vy = PnPolySlabProblem(n_points=4096)._polygon()
+    else:
+        vx, vy = POLYGONS[name]
+    for g in (7, 256, 512):
+        words, _, _ = native.pnpoly_grid(vx, vy, g, g)
+        code = lambda c: (int(words[c >> 4]) >> ((c & 15) * 2)) & 3  # noqa: E731
+        for k in range(g):
+            for c in (k * g, k):  # first column of row k, first row's cell k
+                if code(c) & 1:
+                    assert code(c) >> 1 == 0, (name, g, k)
