@@ -54,6 +54,11 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        # test hook: BENCH_SAME_GPU=1 puts every rank on cuda:0, so the N > 1 control flow
+        # (barriers, shard plan, gather, max over ranks) can be exercised on a 1-GPU box
+        # (its numbers are then meaningless)
+        if os.environ.get("BENCH_SAME_GPU") == "1":
+            self.local_rank = 0
         self.pg = None
         if self.world > 1:
             import torch.distributed as dist
