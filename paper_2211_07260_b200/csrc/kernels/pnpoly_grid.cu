@@ -18,8 +18,9 @@
 // lane busy.
 //
 // Tunables (-D): BLOCK_SIZE_X, TILE (points per thread per chunk, loaded one
-// chunk ahead), GRID (cells per side; the 2-bit raster is staged in shared
-// memory: GRID^2 / 4 bytes).
+// chunk ahead), GRID (cells per side), GRID_SMEM (1: the 2-bit raster is
+// staged in shared memory, GRID^2 / 4 bytes; 0: it is read through L1 from
+// global memory, which allows finer rasters and fewer queued points).
 #ifndef BLOCK_SIZE_X
 #define BLOCK_SIZE_X 1024
 #endif
@@ -28,6 +29,9 @@
 #endif
 #ifndef GRID
 #define GRID 512
+#endif
+#ifndef GRID_SMEM
+#define GRID_SMEM 1
 #endif
 #define CHUNK (BLOCK_SIZE_X * TILE)
 #define NWARPS (BLOCK_SIZE_X / 32)
@@ -78,11 +82,17 @@ pnpoly_grid(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, 
             float ybase, float yscale, int guess_off, int xpar_off, int xst_off, int xlo_off, int pmax_off,
             int rec_off) {
     extern __shared__ __align__(16) unsigned smem[];
+#if GRID_SMEM
     unsigned *s_grid = smem;
     float4 *queue = reinterpret_cast<float4 *>(smem + ((GRID_WORDS + 3) & ~3)) + (threadIdx.x >> 5) * QCAP;
     for (int i = threadIdx.x; i < GRID_WORDS / 4; i += BLOCK_SIZE_X)
         reinterpret_cast<uint4 *>(s_grid)[i] = __ldg(reinterpret_cast<const uint4 *>(grid) + i);
     for (int i = GRID_WORDS / 4 * 4 + threadIdx.x; i < GRID_WORDS; i += BLOCK_SIZE_X) s_grid[i] = __ldg(grid + i);
+#define GRID_WORD(w) s_grid[w]
+#else
+    float4 *queue = reinterpret_cast<float4 *>(smem) + (threadIdx.x >> 5) * QCAP;
+#define GRID_WORD(w) __ldg(grid + (w))
+#endif
     SlabTable T;
     T.u = table;
     T.guess = reinterpret_cast<const int *>(table + guess_off);
@@ -134,7 +144,7 @@ pnpoly_grid(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, 
                 const unsigned cx = min(__float2uint_rz(__fmul_rn(__fsub_rn(px, gx0), gsx)), GRID - 1u);
                 const unsigned cy = min(__float2uint_rz(__fmul_rn(__fsub_rn(py, gy0), gsy)), GRID - 1u);
                 const unsigned cell = cy * GRID + cx;
-                const unsigned code = (s_grid[cell >> 4] >> ((cell & 15u) * 2u)) & 3u;
+                const unsigned code = (GRID_WORD(cell >> 4) >> ((cell & 15u) * 2u)) & 3u;
                 slow = !(code & 1u);
                 if (!slow) bitmap[i] = (int)(code >> 1);
             }

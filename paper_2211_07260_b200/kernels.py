@@ -545,20 +545,22 @@ class PnPolyGridProblem(PnPolySlabProblem):
         return {
             "block_size_x": [256, 512, 1024],
             "tile": [1, 2, 4],
-            "grid": [256, 512],
+            "grid": [256, 512, 1024, 2048],
+            "grid_smem": [0, 1],
             "xbuckets": [8, 16],
             "buckets": [1024, 4096],
         }
 
     def restrictions(self):
-        return [f"(grid * grid / 4 + block_size_x / 32 * {16 * 64}) <= {227 * 1024}"]
+        return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * {16 * 64}) <= {227 * 1024}"]
 
     def default_config(self):
-        return {"block_size_x": 1024, "tile": 2, "grid": 512, "xbuckets": 16, "buckets": 4096}
+        return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "xbuckets": 16, "buckets": 4096}
 
     def defines(self, config):
         c = _as_dict(config)
-        return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"]}
+        return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"],
+                "GRID_SMEM": c.get("grid_smem", 1)}
 
     def grid_table(self, g: int):
         cache = self.__dict__.setdefault("_grid_tables", {})
@@ -569,7 +571,7 @@ class PnPolyGridProblem(PnPolySlabProblem):
 
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
-        words = (c["grid"] * c["grid"] + 15) // 16
+        words = (c["grid"] * c["grid"] + 15) // 16 if c.get("grid_smem", 1) else 0
         return ((words + 3) // 4 * 4) * 4 + c["block_size_x"] // 32 * 64 * 16
 
     def launch(self, config, n_points: int | None = None):

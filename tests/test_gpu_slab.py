@@ -160,8 +160,10 @@ def test_slab_through_tune_kernel():
 
 # -- uniform-cell fast path in front of the slab search (csrc/kernels/pnpoly_grid.cu) ---------
 
-GRID_CONFIGS = [dict(block_size_x=b, tile=t, grid=g, xbuckets=x, buckets=4096)
-                for b, t, g, x in itertools.product((256, 1024), (1, 4), (256, 512), (8, 16))]
+GRID_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, xbuckets=x, buckets=4096)
+                 for b, t, g, x in itertools.product((256, 1024), (1, 4), (256, 512), (8, 16))]
+                + [dict(block_size_x=b, tile=t, grid=g, grid_smem=0, xbuckets=16, buckets=1024)
+                   for b, t, g in itertools.product((256, 1024), (2,), (512, 1024, 2048))])
 
 
 @pytest.fixture(scope="module")
@@ -187,7 +189,8 @@ def test_grid_tiny_and_ragged_inputs(gpu, n):
 
     p = PnPolyGridProblem(n_points=n)
     p.prepare(gpu)
-    for cfg in (p.default_config(), dict(p.default_config(), block_size_x=256, tile=1, grid=256)):
+    for cfg in (p.default_config(), dict(p.default_config(), block_size_x=256, tile=1, grid=256),
+                dict(p.default_config(), grid=2048, grid_smem=0)):
         np.testing.assert_array_equal(run_once(gpu, p, cfg),
                                       O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2))
 
@@ -214,7 +217,7 @@ def test_grid_other_polygons_and_special_points(gpu, shape):
     special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 0.25, -0.5, 1.5], np.float32)
     pts = [rng.uniform(-1.2, 1.2, (200_001, 2)).astype(np.float32), np.stack([vx, vy], 1),
            np.array([[a, b] for a in special for b in special], np.float32)]
-    for g in (256, 512):
+    for g in (256, 512, 2048):
         _, prm, _ = native.pnpoly_grid(vx, vy, g, g)
         xs = (np.float32(prm[0]) + np.arange(g + 1, dtype=np.float32) / np.float32(prm[1])).astype(np.float32)
         pts.append(np.stack([xs, rng.uniform(-1, 1, xs.size).astype(np.float32)], 1))
