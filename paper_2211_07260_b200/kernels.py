@@ -842,7 +842,7 @@ class SgemmTF32Problem(SgemmProblem):
     roofline_kind = "tensor"
 
     def tune_params(self):
-        return {"BN": [64, 128, 256], "STAGES": [2, 3, 4, 5, 6], "PERSIST": [0, 1], "SPLIT_TAIL": [0, 1],
+        return {"BN": [64, 128, 256], "STAGES": [2, 3, 4, 5, 6, 7], "PERSIST": [0, 1], "SPLIT_TAIL": [0, 1],
                 "PAIR": [0, 1]}
 
     def restrictions(self):
