@@ -154,20 +154,20 @@ def cpu_kernel_rates() -> dict:
     threads = O.host_threads()
     p = PnPolyProblem()
     inp = p.host_inputs()
-    n = 2_000_000
+    n = p.n_points
     t0 = time.perf_counter()
     O.pnpoly(inp["points"][:n], inp["vx"], inp["vy"], 2, threads=threads)
     dt = time.perf_counter() - t0
     out["pnpoly"] = {"value": round(3.0 * n * p.n_vertices / dt / 1e9, 3), "unit": "GFLOP/s (3 ops per edge test)",
                      "cores": threads, "kind": "port",
-                     "sample": f"{n} of 20 M points x 600 edges ({dt:.1f} s), C float32 crossing test, formulation 2"}
-    s = SgemmProblem(m=2048, n=2048, k=2048)
+                     "sample": f"all {n} points x 600 edges ({dt:.1f} s), C float32 crossing test, formulation 2"}
+    s = SgemmProblem()
     inp = s.host_inputs()
     t0 = time.perf_counter()
     O.sgemm(inp["a"], inp["b"], inp["c0"], s.alpha, s.beta)
     dt = time.perf_counter() - t0
     out["sgemm"] = {"value": round(s.total_flops / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
-                    "sample": f"2048^3 ({dt:.1f} s), numpy float64 matmul oracle (OpenBLAS threads)"}
+                    "sample": f"4096^3 ({dt:.1f} s), numpy float64 matmul oracle (OpenBLAS threads)"}
     return out
 
 
