@@ -306,7 +306,7 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: 
 #: the sharded tuning leg: a fixed slice of the conv2d space (strong scaling over ranks)
 #: (64 points: an equal share for 1, 2, 4 and 8 ranks)
 TUNE_SPACE = {"block_size_x": [32, 64], "block_size_y": [2, 4, 8], "tile_size_x": [4, 8], "tile_size_y": [1, 2, 4],
-              "use_shmem": [0, 1], "use_padding": [0], "fma2": [0]}
+              "use_shmem": [0, 1], "use_padding": [0], "fma2": [0], "min_blocks": [0]}
 TUNE_WINDOW_S = 0.2  # launch loop per point: >= 2 energy-counter updates (~100 ms cadence)
 
 

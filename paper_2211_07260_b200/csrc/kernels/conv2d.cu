@@ -22,7 +22,8 @@
 // packed FFMA2 (filter coefficient as the broadcast operand, held in a uniform
 // register) does two FMAs; odd columns stay scalar. Half the issue slots of
 // the even-column FMAs, the same fma.rn per output in the same order: the
-// result is bit-identical to FMA2 = 0. Needs an even TILE_X.
+// result is bit-identical to FMA2 = 0. Needs an even TILE_X. MIN_BLOCKS
+// (optional): the __launch_bounds__ minimum-blocks hint.
 #ifndef BLOCK_X
 #define BLOCK_X 32
 #endif
@@ -123,7 +124,12 @@ __device__ __forceinline__ void fma_split(unsigned long long &acc, float f, floa
 }
 #endif
 
+#ifdef MIN_BLOCKS  // minimum resident blocks: with 2, ptxas may use up to 64 registers (more loads in
+                   // flight) while two 512-thread blocks still fit (scripts/time_conv_minb.py)
+extern "C" __global__ void __launch_bounds__(BLOCK_X *BLOCK_Y, MIN_BLOCKS)
+#else
 extern "C" __global__ void __launch_bounds__(BLOCK_X *BLOCK_Y)
+#endif
 conv2d(float *__restrict__ out, const float *__restrict__ in) {
     const int x0 = blockIdx.x * OUT_TW;
     const int y0 = blockIdx.y * OUT_TH;

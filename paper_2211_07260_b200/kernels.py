@@ -646,6 +646,7 @@ class Conv2DProblem(KernelProblem):
             "use_shmem": [0, 1],
             "use_padding": [0, 1],
             "fma2": [0, 1],
+            "min_blocks": [0, 2],
         }
 
     def restrictions(self):
@@ -656,13 +657,14 @@ class Conv2DProblem(KernelProblem):
             f"{self.height} % (block_size_y * tile_size_y) == 0",
             "use_shmem == 1 or use_padding == 0",
             "fma2 == 0 or tile_size_x % 2 == 0",
+            "min_blocks * block_size_x * block_size_y <= 2048",
             f"use_shmem == 0 or (block_size_y * tile_size_y + {self.fh - 1}) * "
             f"(block_size_x * tile_size_x + {self.fw - 1} + 4 * use_padding) * 4 <= 48000",
         ]
 
     def default_config(self):
         return {"block_size_x": 32, "block_size_y": 4, "tile_size_x": 4, "tile_size_y": 4, "use_shmem": 1,
-                "use_padding": 0, "fma2": 0}
+                "use_padding": 0, "fma2": 0, "min_blocks": 0}
 
     def defines(self, config):
         c = _as_dict(config)
@@ -674,6 +676,7 @@ class Conv2DProblem(KernelProblem):
             "USE_SMEM": c["use_shmem"],
             "PAD": 4 * c["use_padding"],
             "FMA2": c.get("fma2", 0),
+            **({"MIN_BLOCKS": c["min_blocks"]} if c.get("min_blocks", 0) else {}),
             "IMAGE_W": self.width,
             "IMAGE_H": self.height,
             "FW": self.fw,

@@ -132,6 +132,9 @@ CONV_CONFIGS = [
     dict(block_size_x=16, block_size_y=2, tile_size_x=2, tile_size_y=8, use_shmem=0, use_padding=0),
     dict(block_size_x=64, block_size_y=1, tile_size_x=2, tile_size_y=4, use_shmem=1, use_padding=1),
     dict(block_size_x=32, block_size_y=16, tile_size_x=1, tile_size_y=8, use_shmem=1, use_padding=0),
+    dict(block_size_x=64, block_size_y=8, tile_size_x=8, tile_size_y=2, use_shmem=0, use_padding=0, fma2=1,
+         min_blocks=2),
+    dict(block_size_x=32, block_size_y=4, tile_size_x=4, tile_size_y=4, use_shmem=1, use_padding=0, min_blocks=2),
 ]
 
 
