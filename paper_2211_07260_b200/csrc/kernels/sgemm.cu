@@ -166,7 +166,11 @@ __device__ __forceinline__ void fma2(unsigned long long &acc2, float a, float b0
 }
 #endif
 
+#ifdef MIN_BLOCKS  // (optional) __launch_bounds__ minimum resident blocks (register cap)
+extern "C" __global__ void __launch_bounds__(THREADS, MIN_BLOCKS)
+#else
 extern "C" __global__ void __launch_bounds__(THREADS)
+#endif
 sgemm(const int M, const int N, const int K, const float alpha, const float beta,
       const float *__restrict__ at, const float *__restrict__ b, float *__restrict__ c) {
     const int tid = threadIdx.x;
