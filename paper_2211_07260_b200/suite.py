@@ -20,7 +20,7 @@ from . import tuned
 from .gpu import GPU
 from .kernels import KernelProblem, make_problem
 
-__all__ = ["Runner", "conv2d", "pnpoly", "sgemm", "sgemm_tf32", "pinned", "device"]
+__all__ = ["Runner", "conv2d", "conv2d_many", "pnpoly", "sgemm", "sgemm_tf32", "pinned", "device"]
 
 _lock = threading.Lock()
 _gpus: dict[int, GPU] = {}
@@ -99,6 +99,63 @@ class Runner:
             gpu.synchronize()
         return out
 
+    def run_many(self, partner: "Runner", uploads: list, outs: list, *, strips: int) -> list:
+        """A sequence of calls pipelined across calls as well as within them.
+
+        Call j runs on ``self`` (even j) or ``partner`` (odd j), two prepared
+        copies of the same problem with their own device buffers, so the H2D of
+        call j+1 and the D2H of call j-1 overlap the launches of call j. Call j
+        reuses the buffers of call j-2 only after that call's kernels (input
+        buffer) and D2H copies (output buffer) are done (stream events).
+        """
+        runners = (self, partner)
+        plans = []
+        for j, up in enumerate(uploads):
+            r = runners[j % 2]
+            up = {k: np.ascontiguousarray(v) for k, v in up.items()}
+            plan = r.problem.strips(r.config, up, outs[j], max(1, strips))
+            if not plan:
+                raise ValueError(f"{r.problem.name} does not split into strips")
+            plans.append(plan)
+        gpu, base = self.gpu, self.EVENT_BASE
+        n_strips = sum(len(p) for p in plans)
+        gpu.reserve_streams(3)
+        gpu.reserve_events(base + 2 * n_strips + 2 * len(plans))
+        for r in runners:
+            r.problem.bind(r.kernel, r.config)
+        done_k, done_d2h = {}, {}  # call -> event index
+        ev = base
+        try:
+            for j, plan in enumerate(plans):
+                r = runners[j % 2]
+                for i, strip in enumerate(plan):
+                    gpu.use_stream(self.H2D)
+                    if i == 0 and j >= 2:
+                        gpu.wait_event(done_k[j - 2])  # call j-2 no longer reads these inputs
+                    for dev, host in strip.h2d:
+                        gpu.h2d_async(dev, host)
+                    gpu.record(ev)
+                    gpu.use_stream(self.COMPUTE)
+                    gpu.wait_event(ev)
+                    if i == 0 and j >= 2:
+                        gpu.wait_event(done_d2h[j - 2])  # call j-2's output has left the device
+                    gpu.launch(r.kernel, strip.launch, strip.args)
+                    gpu.record(ev + 1)
+                    gpu.use_stream(self.D2H)
+                    gpu.wait_event(ev + 1)
+                    for host, dev in strip.d2h:
+                        gpu.d2h_async(host, dev)
+                    ev += 2
+                done_k[j] = ev - 1
+                gpu.use_stream(self.D2H)
+                gpu.record(ev)
+                done_d2h[j] = ev
+                ev += 1
+        finally:
+            gpu.use_stream(self.COMPUTE)
+            gpu.synchronize()
+        return outs
+
     def _single(self, uploads: Mapping[str, np.ndarray], out: np.ndarray) -> np.ndarray:
         gpu = self.gpu
         for name, host in uploads.items():
@@ -146,6 +203,28 @@ def conv2d(image: np.ndarray, filt: np.ndarray, *, config=None, out=None, ordina
                 {"image": image, "filter": filt}, ordinal)
     r.problem.inputs["filter"] = filt
     return r.run({"image": image}, out, strips=strips)
+
+
+def conv2d_many(images: list, filt: np.ndarray, *, config=None, outs: list | None = None, ordinal: int = 0,
+                strips: int = CONV2D_STRIPS) -> list:
+    """``conv2d`` over a sequence of same-shape images, pipelined across images too: the
+    upload of image j+1 and the download of result j-1 overlap the convolution of image
+    j (two device buffer sets). Every image is still copied in and its result copied out."""
+    filt = np.asarray(filt, dtype=np.float32)
+    if not images:
+        return []
+    image = np.asarray(images[0], dtype=np.float32)
+    fh, fw = filt.shape
+    h, w = image.shape[0] - fh + 1, image.shape[1] - fw + 1
+    key = (h, w, fh, fw)
+    kwargs = {"width": w, "height": h, "fw": fw, "fh": fh}
+    a = _runner("conv2d", key, config, kwargs, {"image": image, "filter": filt}, ordinal)
+    b = _runner("conv2d", key + ("partner",), a.config, kwargs, {"image": image, "filter": filt}, ordinal)
+    for r in (a, b):
+        r.problem.inputs["filter"] = filt
+    if outs is None:
+        outs = [np.empty((h, w), np.float32) for _ in images]
+    return a.run_many(b, [{"image": np.asarray(im, dtype=np.float32)} for im in images], outs, strips=strips)
 
 
 def pnpoly(points: np.ndarray, vx: np.ndarray, vy: np.ndarray, *, config=None, out=None, ordinal: int = 0,

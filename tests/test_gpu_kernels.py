@@ -288,6 +288,30 @@ def test_suite_pipelined_strips_match_single_launch():
         np.testing.assert_array_equal(suite.pnpoly(pi["points"], pi["vx"], pi["vy"], strips=n), want)
 
 
+def test_suite_conv2d_many_matches_single_calls():
+    """conv2d_many (pipelined across images over two device buffer sets) gives, image for
+    image, the bits of separate single-launch calls; odd counts and repeated output
+    buffers included."""
+    from paper_2211_07260_b200 import suite
+    from paper_2211_07260_b200.kernels import Conv2DProblem
+
+    rng = np.random.default_rng(5)
+    filt = rng.uniform(0, 1, (17, 17)).astype(np.float32)
+    images = [rng.uniform(0, 1, (496 + 16, 512 + 16)).astype(np.float32) for _ in range(5)]
+    want = [suite.conv2d(im, filt, strips=1).copy() for im in images]
+    for strips in (1, 4):
+        got = suite.conv2d_many(images, filt, strips=strips)
+        for g, w in zip(got, want):
+            np.testing.assert_array_equal(g, w)
+    pinned = [suite.pinned(want[0].shape) for _ in range(2)]
+    suite.conv2d_many(images[:4], filt, outs=[pinned[0], pinned[1], pinned[0], pinned[1]], strips=3)
+    np.testing.assert_array_equal(pinned[0], want[2])
+    np.testing.assert_array_equal(pinned[1], want[3])
+    p = Conv2DProblem(width=512, height=496)
+    assert O.conv2d_error(want[0], O.conv2d(images[0], filt), images[0], filt) <= O.CONV_TOL
+    assert p.width == 512
+
+
 # -- SGEMM on tcgen05 (TF32, its own tolerance) -------------------------------------------------
 
 
