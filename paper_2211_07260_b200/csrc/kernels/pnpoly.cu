@@ -53,6 +53,11 @@
 //                 structure-of-arrays table {vy0..3, sl0..3, ic0..3} per 4
 //                 edges, so no register shuffling: 3 issue slots per
 //                 edge-point (1.5 FMA-pipe + 1.5 ALU). Same formulation 3.
+//                 9: ASM 7 over a table whose 128-bit loads put each slope pair
+//                 and intercept pair in opposite halves of a register quad (no
+//                 register-bank overlap between the two FFMA2 pair operands).
+//                 Measured identical to ASM 7 (1.775 ms): bank conflicts on the
+//                 FFMA2 are not what holds ASM 7 back.
 //                 8: ASM 7's arithmetic written in C++ over the same table
 //                 held in __constant__ memory (POLY_SMEM=0): the edge pairs
 //                 are warp-uniform loads, so ptxas can feed them to FADD2 /
@@ -106,7 +111,7 @@
 #if ASM == 5 && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
 #error "ASM=5 needs POLY_SMEM=1, METHOD=2 and TILE in {2,4,6,8}"
 #endif
-#if ASM == 7 && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
+#if (ASM == 7 || ASM == 9) && !(POLY_SMEM == 1 && METHOD == 2 && (TILE == 2 || TILE == 4 || TILE == 6 || TILE == 8))
 #error "ASM=7 needs POLY_SMEM=1, METHOD=2 and TILE in {2,4,6,8}"
 #endif
 #if ASM == 8 && !(POLY_SMEM == 0 && METHOD == 2)
@@ -118,7 +123,7 @@
 // ASM 7 table: edges padded to a multiple of 8 (two 4-edge groups per loop
 // trip), 12 floats per 4-edge group
 #define NPAIR8 (((VERTICES) + 7) / 8 * 8)
-#if ASM == 7 || ASM == 8
+#if ASM == 7 || ASM == 8 || ASM == 9
 #define TAB_VEC4 (NPAIR8 * 3 / 4)
 #else
 #define TAB_VEC4 NPACK
@@ -653,7 +658,7 @@
     "mov.u32 ptr, %" S4_BASE ";\nadd.u32 end, ptr, %" S4_SPAN ";\n" "PNPOLY_S4_LOOP:\n" \
     S4_BODY "add.u32 ptr, ptr, 64;\nsetp.lt.u32 s, ptr, end;\n@s bra PNPOLY_S4_LOOP;\n}\n"
 #endif
-#if ASM == 7
+#if ASM == 7 || ASM == 9
 // One 4-edge group for one point. vyA = {vy0, vy1}, vyB = {vy2, vy3} (same
 // for sl / ic) come from LDS.64, so every f32x2 operand is an aligned pair;
 // the point's px / py enter as broadcast scalars. PREV holds py - vy of the
@@ -682,10 +687,21 @@
 #define S7_STEP(NS, NPX, NPY, NLAST, CS, CACC, CPREV, CLAST)                                         \
     S7_F1(NS, NPX, NPY) S7_L1(CS, CPREV) S7_F2(NS) S7_L2(CS) S7_F3(NS) S7_L3(CS, CACC)               \
     S7_F4(NS) S7_L4(CS) S7_F5(NS) S7_L5(CS, CLAST) S7_F6(NS, NLAST) S7_L3(CS, CACC)
+#if ASM == 9
+// register-bank-friendly table: {vy0..3}{sl0,sl1,ic2,ic3}{sl2,sl3,ic0,ic1}. A 128-bit load
+// fills an aligned register quad, so slope and intercept pairs land in opposite halves of
+// two quads and each FFMA2 (slope pair x py + intercept pair) reads its two pair operands
+// from different register banks (ASM 7: both from the same half of their quads)
+#define S7_LOAD(OFF)                                            \
+    "ld.shared.v2.b64 {vyA, vyB}, [ptr+" OFF "];\n"             \
+    "ld.shared.v2.b64 {slA, icB}, [ptr+" OFF "+16];\n"          \
+    "ld.shared.v2.b64 {slB, icA}, [ptr+" OFF "+32];\n"
+#else
 #define S7_LOAD(OFF)                                            \
     "ld.shared.v2.b64 {vyA, vyB}, [ptr+" OFF "];\n"             \
     "ld.shared.v2.b64 {slA, slB}, [ptr+" OFF "+16];\n"          \
     "ld.shared.v2.b64 {icA, icB}, [ptr+" OFF "+32];\n"
+#endif
 #define S7_INIT1(I, PY, VL) "sub.rn.f32 dp" #I ", %" PY ", %" VL ";\n"
 #if TILE == 2
 #define S7_GROUP_P \
@@ -1677,7 +1693,7 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
         for (int t = 0; t < TILE; ++t) inside[t] = acc[t] >> 31;
     }
-#elif ASM == 3 || ASM == 5 || ASM == 7
+#elif ASM == 3 || ASM == 5 || ASM == 7 || ASM == 9
 #if ASM == 3
 #define SS_ASM S3_ASM
 #elif ASM == 5
@@ -1691,7 +1707,7 @@ pnpoly(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
         for (int t = 0; t < TILE; ++t) acc[t] = 0u;
         const unsigned sbase = (unsigned)__cvta_generic_to_shared(s_packed);
-#if ASM == 7
+#if ASM == 7 || ASM == 9
         const unsigned span = NPAIR8 * 12u;  // 4-edge groups of 12 floats
         const float vy_last = reinterpret_cast<const float *>(s_packed)[(VERTICES - 1) / 4 * 12 + (VERTICES - 1) % 4];
 #else

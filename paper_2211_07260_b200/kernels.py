@@ -201,7 +201,7 @@ class PnPolyProblem(KernelProblem):
             "method": [0, 1, 2],
             "between": [0, 1],
             "poly_smem": [0, 1],
-            "asm": [0, 1, 2, 3, 4, 5, 6, 7, 8],
+            "asm": [0, 1, 2, 3, 4, 5, 6, 7, 8, 9],
             "persist": [0, 1],
         }
 
@@ -273,6 +273,7 @@ class PnPolyProblem(KernelProblem):
         self.buffers["packed"] = gpu.array(self.packed_table())
         self.buffers["packed3"] = gpu.array(self.chain_table())
         self.buffers["packed7"] = gpu.array(self.pair_table())
+        self.buffers["packed9"] = gpu.array(self.pair_table(bank_split=True))
 
     def chain_table(self) -> np.ndarray:
         """{vy_k, slope, icpt, 0} per edge for the sign-bit chain (ASM=3),
@@ -288,11 +289,15 @@ class PnPolyProblem(KernelProblem):
         table[:n, 2] = edges[:, 1]
         return table
 
-    def pair_table(self) -> np.ndarray:
+    def pair_table(self, bank_split: bool = False) -> np.ndarray:
         """ASM=7 structure-of-arrays chain table: per group of 4 edges the 12
         floats {vy0..3, slope0..3, icpt0..3}, edges padded to a multiple of 8
         with the chain's zero-length continuation (vy of the last vertex,
-        slope = icpt = 0). Pure repacking of chain_table()."""
+        slope = icpt = 0). Pure repacking of chain_table().
+
+        ``bank_split`` (ASM=9): {vy0..3, sl0, sl1, ic2, ic3, sl2, sl3, ic0, ic1},
+        so each 128-bit load puts a slope pair and an intercept pair in opposite
+        halves of its register quad (different register banks for FFMA2)."""
         edges, _ = self._tables[2]
         n = edges.shape[0]
         n8 = (n + 7) // 8 * 8
@@ -301,7 +306,11 @@ class PnPolyProblem(KernelProblem):
         chain[:n, 0] = edges[:, 0]
         chain[:n, 1] = edges[:, 2]
         chain[:n, 2] = edges[:, 1]
-        return np.ascontiguousarray(chain.reshape(n8 // 4, 4, 3).transpose(0, 2, 1)).reshape(-1)
+        groups = np.ascontiguousarray(chain.reshape(n8 // 4, 4, 3).transpose(0, 2, 1))  # [g][vy|sl|ic][4]
+        if bank_split:
+            vy, sl, ic = groups[:, 0], groups[:, 1], groups[:, 2]
+            groups = np.concatenate([vy, sl[:, :2], ic[:, 2:], sl[:, 2:], ic[:, :2]], axis=1)
+        return np.ascontiguousarray(groups).reshape(-1)
 
     def packed_table(self) -> np.ndarray:
         """{ymin, ymax, slope, icpt} per edge (METHOD 2), padded to a multiple
@@ -323,7 +332,8 @@ class PnPolyProblem(KernelProblem):
         m = _as_dict(config)["method"]
         b = self.buffers
         asm = _as_dict(config).get("asm", 0)
-        packed = b["packed7"] if asm == 7 else b["packed3"] if asm >= 3 else b["packed"]
+        packed = (b["packed9"] if asm == 9 else b["packed7"] if asm == 7 else b["packed3"] if asm >= 3
+                  else b["packed"])
         return [b["out"], b["points"], i32(self.n_points), b[f"edges{m}"], b[f"ybounds{m}"], packed]
 
     def strips(self, config, uploads, out, n):

@@ -37,7 +37,7 @@ def run_once(gpu, problem, cfg):
 
 PNPOLY_CONFIGS = (
     [dict(block_size_x=b, tile=t, vec=2, method=2, between=0, poly_smem=1, asm=a, persist=ps)
-     for a, b, t, ps in itertools.product((3, 5, 7), (96, 256, 1024), (2, 4, 6, 8), (0, 1))]
+     for a, b, t, ps in itertools.product((3, 5, 7, 9), (96, 256, 1024), (2, 4, 6, 8), (0, 1))]
     + [dict(block_size_x=b, tile=t, vec=2, method=2, between=0, poly_smem=1, asm=a, persist=ps)
        for a, b, t, ps in itertools.product((4, 6), (128, 512), (4, 8), (0, 1))]
     + [dict(block_size_x=b, tile=t, vec=v, method=2, between=0, poly_smem=0, asm=8, persist=ps)
@@ -93,8 +93,8 @@ def test_pnpoly_degenerate_points_and_polygon(gpu):
     pts = np.array([[x, y] for x in xs for y in ys], np.float32)
     p = PnPolyProblem(n_points=len(pts), n_vertices=vx.size)
     p.prepare(gpu, {"points": pts, "vx": vx, "vy": vy})
-    pairs = [dict(block_size_x=128, tile=t, vec=2, method=2, between=0, poly_smem=int(a == 7), asm=a, persist=1)
-             for t in (2, 8) for a in (7, 8)]
+    pairs = [dict(block_size_x=128, tile=t, vec=2, method=2, between=0, poly_smem=int(a != 8), asm=a, persist=1)
+             for t in (2, 8) for a in (7, 8, 9)]
     for cfg in PNPOLY_CONFIGS[::5] + pairs:  # 7 vertices: ASM 7/8 pad their 8-edge groups
         got = run_once(gpu, p, cfg)
         np.testing.assert_array_equal(got, O.pnpoly(pts, vx, vy, p.formula(cfg)), err_msg=str(cfg))
