@@ -1,8 +1,8 @@
 """Issue-rate microbenchmarks behind the PnPoly brute-force ceiling.
 
 Each probe is a loop of independent chains of one instruction form (inline
-PTX, so ptxas emits exactly that SASS op), run by 148 x 4 blocks of 256
-threads (16 warps per SMSP). Every warp times its loop with clock64; the
+PTX, so ptxas emits exactly that SASS op), run by as many 256-thread
+blocks per SM as are resident at once (up to 4, register-limited). Every warp times its loop with clock64; the
 issue rate per SMSP is warps_per_smsp x instructions_per_iteration x iters /
 cycles. Forms:
 
@@ -17,6 +17,8 @@ cycles. Forms:
   mix_f_lop  one FADD + one 3-register LOP3 per chain step
   asm7_edge2 the ASM 7 step for one point and two edges: FADD2, FFMA2, FADD2
              (broadcast scalar operands) and three 3-register LOP3s
+  asm7_dep   the same, with the LOP3s reading the halves of the FADD2 results
+             (the kernel's data flow)
 
 The SASS op counts of each probe's loop (cuobjdump) are printed with it, so a
 rate can be read per SASS instruction actually issued.
@@ -49,6 +51,12 @@ FORMS = {
     "lop3_rri": ("lop3.b32 u{k}, u{k}, v{k}, 0x5A5A5A5A, 0x96;", 1),
     "mix_f2_lop": ("mov.b64 t{k}, {{s, s}};\nsub.rn.f32x2 p{k}, t{k}, p{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x96;", 2),
     "mix_f_lop": ("add.rn.f32 c{k}, c{k}, x{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x96;", 2),
+    # the same mix, but the LOP3s consume the halves of the f32x2 results (as in the kernel)
+    "asm7_dep": ("{{\n.reg .b32 dl, dh, el, eh;\nmov.b64 t{k}, {{s, s}};\nsub.rn.f32x2 p{k}, t{k}, p{k};\n"
+                 "fma.rn.f32x2 q{k}, q{k}, t{k}, p{k};\nsub.rn.f32x2 q{k}, t{k}, q{k};\n"
+                 "mov.b64 {{dl, dh}}, p{k};\nmov.b64 {{el, eh}}, q{k};\n"
+                 "lop3.b32 u{k}, dl, w{k}, el, 0x28;\nlop3.b32 v{k}, dh, dl, eh, 0x28;\n"
+                 "lop3.b32 w{k}, w{k}, u{k}, v{k}, 0x96;\n}}", 6),
     "asm7_edge2": ("mov.b64 t{k}, {{s, s}};\nsub.rn.f32x2 p{k}, t{k}, p{k};\nfma.rn.f32x2 q{k}, p{k}, t{k}, q{k};\n"
                    "sub.rn.f32x2 p{k}, t{k}, q{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x28;\n"
                    "lop3.b32 v{k}, u{k}, v{k}, w{k}, 0x28;\nlop3.b32 w{k}, u{k}, v{k}, w{k}, 0x96;", 6),
@@ -75,7 +83,11 @@ extern "C" __global__ void __launch_bounds__(256) probe(unsigned long long *cycl
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     unsigned smid;
     asm volatile("mov.u32 %%0, %%%%smid;" : "=r"(smid));
-    if ((threadIdx.x & 31) == 0) cycles[gw] = ((unsigned long long)smid << 48) | (t1 - t0);
+    if ((threadIdx.x & 31) == 0) {  // per warp: SM id, start and end of the timed loop (SM clock)
+        cycles[3 * gw] = smid;
+        cycles[3 * gw + 1] = t0;
+        cycles[3 * gw + 2] = t1;
+    }
     if (out == 12345.f) sink[threadIdx.x] = out;
 }
 """
@@ -134,36 +146,44 @@ def loop_ops(cubin: bytes) -> dict:
 def main():
     gpu = GPU(0)
     sms = gpu.sm_count
-    blocks, threads, iters = sms * 4, 256, 4096
-    warps_per_smsp = blocks * threads // 32 / (sms * 4)
-    cycles = gpu.empty((blocks * threads // 32,), np.uint64)
+    threads, iters = 256, 4096
+    cycles = gpu.empty((3 * sms * 8 * threads // 32,), np.uint64)
     sink = gpu.empty((threads,), np.float32)
     for name, (body, per_chain) in FORMS.items():
         src = kernel_source(body)
         cubin = native.compile_cubin(src, f"probe_{name}", native._nvrtc_options({}))
         k = gpu.load(cubin, "probe")
+        # launch only as many blocks as are resident at once (register-limited), so every
+        # warp's clock64 window overlaps the others' and per-SM rates are not inflated
+        resident = max(1, min(4, 65536 // (max(k.regs, 1) * threads)))
+        blocks = sms * resident
         launch = Launch((blocks, 1, 1), (threads, 1, 1))
         args = [cycles, sink, i32(iters), f32(1.5)]
         gpu.launch(k, launch, args)
         gpu.synchronize()
         gpu.launch(k, launch, args)
         gpu.synchronize()
-        raw = cycles.download()
-        sm = (raw >> np.uint64(48)).astype(np.int64)
-        cyc = (raw & np.uint64((1 << 48) - 1)).astype(np.float64)
-        # per SM: warps resident there / 4 SMSPs, over the slowest warp's cycles on that SM
-        # (the block scheduler need not spread blocks evenly)
+        raw = cycles.download()[: 3 * blocks * threads // 32].reshape(-1, 3)
+        sm, t0, t1 = raw[:, 0].astype(np.int64), raw[:, 1].astype(np.float64), raw[:, 2].astype(np.float64)
+        # per SM: all of its warps' instructions over the SM's busy window (first start to last
+        # end on that SM's clock), per SMSP; blocks that ran in a second wave are then counted
+        # against the time they really took
         instrs = per_chain * CHAINS * UNROLL * iters
         ops = loop_ops(cubin)
-        rates, issued_rates = [], []
+        rates, issued_rates, spans = [], [], []
         for s_id in np.unique(sm):
             w = sm == s_id
-            rates.append(w.sum() / 4.0 * instrs / cyc[w].max())
-            issued_rates.append(w.sum() / 4.0 * sum(ops.values()) * iters / cyc[w].max())
+            window = t1[w].max() - t0[w].min()
+            rates.append(w.sum() / 4.0 * instrs / window)
+            issued_rates.append(w.sum() / 4.0 * sum(ops.values()) * iters / window)
+            spans.append(window / np.median(t1[w] - t0[w]))
         per_smsp = float(np.median(rates))
         issued = float(np.median(issued_rates))
         warps_per_smsp = float(np.median(np.bincount(sm)[np.unique(sm)])) / 4.0
-        print(json.dumps({"form": name, "instrs_per_trip_per_warp": per_chain * CHAINS * UNROLL,
+        span = float(np.median(spans))  # 1 = the SM's warps all ran concurrently, 2 = two waves
+        cyc = t1 - t0
+        print(json.dumps({"form": name, "regs": k.regs, "blocks_per_sm": resident, "span": round(float(span), 3),
+                          "instrs_per_trip_per_warp": per_chain * CHAINS * UNROLL,
                           "sass_loop_ops": ops, "sass_issue_per_smsp_per_cycle": round(issued, 3),
                           "warp_instr_per_smsp_per_cycle": round(per_smsp, 3),
                           "median_cycles": float(np.median(cyc)), "warps_per_smsp": warps_per_smsp}), flush=True)
