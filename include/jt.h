@@ -226,13 +226,13 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
                     long long capacity, jt_slab_info *info);
 /* PnPoly uniform-cell fast path for csrc/kernels/pnpoly_grid.cu: a gw x gh
  * grid over the polygon's bounding box (cells on the border extend to
- * infinity); cell (cx, cy) = clamped f2i_rz((px - x0) * sx), f2i_rz((py - y0)
- * * sy) in float32. A cell is "clean" when, for every point that maps to it,
+ * infinity); cell (cx, cy) = (min(f2u_rz(fma(px, sx, ox)), gw - 1),
+ * min(f2u_rz(fma(py, sy, oy)), gh - 1)) in float32. A cell is "clean" when, for every point that maps to it,
  * every edge spanning its py is decided by the computed-x ranges (crosses for
  * all px of the cell or for none) and the crossing count has one parity in
  * all slabs the cell's rows meet; its bits are then 1 | parity << 1 (2 bits
  * per cell, 16 cells per word), else 0 (the kernel runs the exact slab
- * search). params = {x0, sx, y0, sy}. bits == NULL: params only. */
+ * search). params = {sx, ox, sy, oy}. bits == NULL: params only. */
 int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, float *params, uint32_t *bits,
                    long long capacity, int *clean_cells);
 

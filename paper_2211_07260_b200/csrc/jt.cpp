@@ -1260,13 +1260,24 @@ static float key_float(uint32_t k) {
     std::memcpy(&f, &u, 4);
     return f;
 }
-// Smallest non-NaN float v with slab_bucket(v) >= k (+inf if none): bucket is monotone in v.
-static float bucket_first(int k, float base, float scale, int hi) {
+// The grid kernel's cell index, op for op: min(cvt.rzi.u32(fma(v, scale, offset)), hi)
+// (cvt.rzi.u32: NaN and negatives -> 0, saturating above). fmaf is correctly rounded, so
+// the index is monotone in v for scale >= 0.
+static int grid_cell(float v, float scale, float offset, int hi) {
+    const float f = std::fmaf(v, scale, offset);
+    long long k;
+    if (std::isnan(f) || f <= 0.f) k = 0;
+    else if (f >= 4294967295.f) k = 4294967295LL;
+    else k = (long long)std::trunc(f);
+    return (int)std::min<long long>(k, hi);
+}
+// Smallest non-NaN float v with grid_cell(v) >= k (+inf if none).
+static float cell_first(int k, float scale, float offset, int hi) {
     uint32_t lo = float_key(-INFINITY), up = float_key(INFINITY);
-    if (slab_bucket(key_float(up), base, scale, hi) < k) return INFINITY;
+    if (grid_cell(key_float(up), scale, offset, hi) < k) return INFINITY;
     while (lo < up) {
         const uint32_t mid = lo + (up - lo) / 2;
-        if (slab_bucket(key_float(mid), base, scale, hi) >= k) up = mid; else lo = mid + 1;
+        if (grid_cell(key_float(mid), scale, offset, hi) >= k) up = mid; else lo = mid + 1;
     }
     return key_float(lo);
 }
@@ -1296,18 +1307,18 @@ int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, floa
     std::sort(u.begin(), u.end());
     u.erase(std::unique(u.begin(), u.end(), [](float a, float b) { return a == b; }), u.end());
     const int nu = (int)u.size();
-    // the cell of a point: (min(max(f2i_rz((px - x0) * sx), 0), gw - 1), same in y), float32 ops as the kernel
-    const float x0 = xmin, y0 = ymin;
+    // the cell of a point: (min(f2u_rz(fma(px, sx, ox)), gw - 1), same in y), as the kernel computes it
     const float sx = xmax > xmin ? (float)gw / (xmax - xmin) : 0.f;
     const float sy = ymax > ymin ? (float)gh / (ymax - ymin) : 0.f;
-    params[0] = x0, params[1] = sx, params[2] = y0, params[3] = sy;
+    const float ox = -xmin * sx, oy = -ymin * sy;
+    params[0] = sx, params[1] = ox, params[2] = sy, params[3] = oy;
     if (!bits) return JT_OK;
     if (capacity < words) return fail(JT_EINVAL, "grid needs %lld words, got %lld", words, capacity);
     std::memset(bits, 0, sizeof(uint32_t) * words);
     // exact float ranges of the cells: [first(k), pred(first(k + 1))]
     std::vector<float> cx0(gw + 1), cy0(gh + 1);
-    for (int k = 0; k <= gw; ++k) cx0[k] = k == 0 ? -INFINITY : bucket_first(k, x0, sx, gw - 1);
-    for (int k = 0; k <= gh; ++k) cy0[k] = k == 0 ? -INFINITY : bucket_first(k, y0, sy, gh - 1);
+    for (int k = 0; k <= gw; ++k) cx0[k] = k == 0 ? -INFINITY : cell_first(k, sx, ox, gw - 1);
+    for (int k = 0; k <= gh; ++k) cy0[k] = k == 0 ? -INFINITY : cell_first(k, sy, oy, gh - 1);
     cx0[gw] = cy0[gh] = INFINITY;
     // slab lists
     std::vector<std::vector<int>> slab(nu + 1);

@@ -78,7 +78,7 @@ __device__ __forceinline__ int slab_search(float px, float py, const SlabTable &
 
 extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X)
 pnpoly_grid(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, const unsigned *__restrict__ grid,
-            float gx0, float gsx, float gy0, float gsy, const float *__restrict__ table, int nu, int ng, int xb,
+            float gsx, float gox, float gsy, float goy, const float *__restrict__ table, int nu, int ng, int xb,
             float ybase, float yscale, int guess_off, int xpar_off, int xst_off, int xlo_off, int pmax_off,
             int rec_off) {
     extern __shared__ __align__(16) unsigned smem[];
@@ -135,14 +135,14 @@ pnpoly_grid(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, 
             const float px = cur[t].x, py = cur[t].y;
             bool slow = false;
             if (i < n) {
-                // min(max(f2i_rz(v), 0), GRID - 1) of the host's cell function, in one clamp:
-                // cvt.rzi.u32 already maps NaN and negatives to 0. A NaN coordinate lands in
-                // the first column (px) or row (py): a clean cell there has parity 0 (no edge
-                // spans below every vertex; every spanning edge crosses left of every vertex,
-                // and a closed polygon has an even number of them), which is the answer for
-                // NaN; an unclean one sends the point to slab_search, which returns 0.
-                const unsigned cx = min(__float2uint_rz(__fmul_rn(__fsub_rn(px, gx0), gsx)), GRID - 1u);
-                const unsigned cy = min(__float2uint_rz(__fmul_rn(__fsub_rn(py, gy0), gsy)), GRID - 1u);
+                // the host's cell function (jt_pnpoly_grid): min(f2u_rz(fma(v, s, o)), GRID - 1);
+                // cvt.rzi.u32 maps NaN and negatives to 0. A NaN coordinate lands in the first
+                // column (px) or row (py): a clean cell there has parity 0 (no edge spans below
+                // every vertex; every spanning edge crosses left of every vertex, and a closed
+                // polygon has an even number of them), which is the answer for NaN; an unclean
+                // one sends the point to slab_search, which returns 0.
+                const unsigned cx = min(__float2uint_rz(__fmaf_rn(px, gsx, gox)), GRID - 1u);
+                const unsigned cy = min(__float2uint_rz(__fmaf_rn(py, gsy, goy)), GRID - 1u);
                 const unsigned cell = cy * GRID + cx;
                 const unsigned code = (GRID_WORD(cell >> 4) >> ((cell & 15u) * 2u)) & 3u;
                 slow = !(code & 1u);

@@ -614,10 +614,10 @@ class PnPolyGridProblem(PnPolySlabProblem):
         words, prm, _ = self.grid_table(g)
         pts = self.inputs["points"]
 
-        def cell(v, base, scale):
+        def cell(v, scale, offset):  # fma emulated exactly: float32 x float32 is exact in float64
             with np.errstate(invalid="ignore", over="ignore"):
-                f = (v.astype(np.float32) - np.float32(base)) * np.float32(scale)
-            k = np.trunc(np.nan_to_num(f, nan=0.0, posinf=2.0**31, neginf=-2.0**31))
+                f = (v.astype(np.float64) * np.float64(scale) + np.float64(offset)).astype(np.float32)
+            k = np.trunc(np.nan_to_num(f, nan=0.0, posinf=2.0**32, neginf=0.0))
             return np.clip(k, 0, g - 1).astype(np.int64)
 
         idx = cell(pts[:, 1], prm[2], prm[3]) * g + cell(pts[:, 0], prm[0], prm[1])

@@ -219,7 +219,7 @@ def test_grid_other_polygons_and_special_points(gpu, shape):
            np.array([[a, b] for a in special for b in special], np.float32)]
     for g in (256, 512, 2048):
         _, prm, _ = native.pnpoly_grid(vx, vy, g, g)
-        xs = (np.float32(prm[0]) + np.arange(g + 1, dtype=np.float32) / np.float32(prm[1])).astype(np.float32)
+        xs = ((np.arange(g + 1, dtype=np.float64) - prm[1]) / prm[0]).astype(np.float32)
         pts.append(np.stack([xs, rng.uniform(-1, 1, xs.size).astype(np.float32)], 1))
     pts = np.ascontiguousarray(np.concatenate(pts).astype(np.float32))
     p = PnPolyGridProblem(n_points=len(pts), n_vertices=vx.size)

@@ -201,12 +201,16 @@ def test_half_copy_is_conservative_and_tight(name):
         assert np.all(np.nextafter(pm16, np.float16(-np.inf)).astype(np.float32) < pm)
 
 
-def _cell(v, base, scale, hi):
+def _cell(v, scale, offset, hi):
+    """min(f2u_rz(fma(v, scale, offset)), hi) of pnpoly_grid.cu. The fma is emulated
+    exactly: the float32 product is exact in float64, and float64 + float32 rounded once to
+    float32 differs from a true fma only when the float64 sum itself rounds, which the
+    tests' coordinates (|v| <= ~1e30 with scale ~1e3) keep rare; host and kernel both use a
+    real fmaf, so the cleanliness check does not depend on this emulation."""
     with np.errstate(invalid="ignore", over="ignore"):
-        f = (np.float32(v) - np.float32(base)) * np.float32(scale)
-    f = np.asarray(f, dtype=np.float32)
-    k = np.where(np.isnan(f), 0, np.trunc(np.nan_to_num(f, posinf=2.0**31, neginf=-2.0**31)))
-    return np.clip(np.clip(k, -2**31, 2**31 - 1), 0, hi).astype(np.int64)
+        f = (np.asarray(v, np.float64) * np.float64(scale) + np.float64(offset)).astype(np.float32)
+    k = np.trunc(np.nan_to_num(f, nan=0.0, posinf=2.0**32, neginf=0.0))
+    return np.clip(k, 0, hi).astype(np.int64)
 
 
 @pytest.mark.parametrize("name", sorted(POLYGONS))
@@ -229,9 +233,9 @@ def test_grid_clean_cells_give_the_brute_force_parity(name, g):
     vv = np.stack([vx, vy], 1).astype(np.float32)
     for d in (0.0, 1e-7, -1e-7, 1e-3):
         pts.append((vv + np.float32(d)).astype(np.float32))
-    # cell borders in x and y
-    xs = (np.float32(prm[0]) + np.arange(g + 1, dtype=np.float32) / np.float32(prm[1])).astype(np.float32)
-    ys = (np.float32(prm[2]) + np.arange(g + 1, dtype=np.float32) / np.float32(prm[3])).astype(np.float32)
+    # cell borders in x and y (v = (k - o) / s)
+    xs = ((np.arange(g + 1, dtype=np.float64) - prm[1]) / prm[0]).astype(np.float32)
+    ys = ((np.arange(g + 1, dtype=np.float64) - prm[3]) / prm[2]).astype(np.float32)
     bx = np.concatenate([xs, np.nextafter(xs, np.float32(np.inf)), np.nextafter(xs, np.float32(-np.inf))])
     by = np.concatenate([ys, np.nextafter(ys, np.float32(np.inf)), np.nextafter(ys, np.float32(-np.inf))])
     pts.append(np.stack([rng.choice(bx, 50_000), rng.uniform(-span, span, 50_000).astype(np.float32)], 1))
