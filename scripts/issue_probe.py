@@ -57,6 +57,11 @@ FORMS = {
                  "mov.b64 {{dl, dh}}, p{k};\nmov.b64 {{el, eh}}, q{k};\n"
                  "lop3.b32 u{k}, dl, w{k}, el, 0x28;\nlop3.b32 v{k}, dh, dl, eh, 0x28;\n"
                  "lop3.b32 w{k}, w{k}, u{k}, v{k}, 0x96;\n}}", 6),
+    # predicate forms (PnPoly ASM 1/2 style): FSETP chains and a predicated-toggle crossing step
+    # (third field: chains, so the predicates fit the 7 hardware predicate registers)
+    "fsetp_and": ("setp.lt.and.f32 P{k}, c{k}, x{k}, P{k};", 1, 6),
+    "asm1_step": ("setp.ge.f32 S{k}, c{k}, x{k};\nsetp.lt.and.f32 S{k}, c{k}, y{k}, S{k};\n"
+                  "fma.rn.f32 y{k}, y{k}, s, x{k};\n@S{k} setp.lt.xor.f32 P{k}, s, y{k}, P{k};", 4, 3),
     "asm7_edge2": ("mov.b64 t{k}, {{s, s}};\nsub.rn.f32x2 p{k}, t{k}, p{k};\nfma.rn.f32x2 q{k}, p{k}, t{k}, q{k};\n"
                    "sub.rn.f32x2 p{k}, t{k}, q{k};\nlop3.b32 u{k}, u{k}, v{k}, w{k}, 0x28;\n"
                    "lop3.b32 v{k}, u{k}, v{k}, w{k}, 0x28;\nlop3.b32 w{k}, u{k}, v{k}, w{k}, 0x96;", 6),
@@ -67,7 +72,7 @@ extern "C" __global__ void __launch_bounds__(256) probe(unsigned long long *cycl
     unsigned long long t0, t1;
     float out;
     asm volatile("{\n"
-        ".reg .f32 s, %s;\n.reg .b32 %s;\n.reg .b64 %s;\n.reg .pred lp;\n.reg .s32 it;\n"
+        ".reg .f32 s, %s;\n.reg .b32 %s;\n.reg .b64 %s;\n.reg .pred lp, %s;\n.reg .s32 it;\n"
         "mov.f32 s, %%3;\n"
         %s
         "mov.u64 %%0, %%clock64;\n"
@@ -93,24 +98,27 @@ extern "C" __global__ void __launch_bounds__(256) probe(unsigned long long *cycl
 """
 
 
-def kernel_source(body: str) -> str:
+def kernel_source(body: str, chains: int = CHAINS) -> str:
     f32 = ", ".join(f"c{k}, x{k}, y{k}" for k in range(CHAINS))
     b32 = ", ".join(f"u{k}, v{k}, w{k}" for k in range(CHAINS))
     b64 = ", ".join(f"p{k}, q{k}, t{k}" for k in range(CHAINS))
+    preds = ", ".join(f"P{k}, S{k}" for k in range(CHAINS))
     init = ""
     for k in range(CHAINS):
         init += (f"add.f32 c{k}, s, 0f3F8{k}0000;\nadd.f32 x{k}, s, 0f3F9{k}0000;\nadd.f32 y{k}, s, 0f3FA{k}0000;\n"
                  f"mov.b32 u{k}, c{k};\nmov.b32 v{k}, x{k};\nmov.b32 w{k}, y{k};\n"
-                 f"mov.b64 p{k}, {{x{k}, y{k}}};\nmov.b64 q{k}, {{y{k}, c{k}}};\nmov.b64 t{k}, {{s, s}};\n")
-    loop = "".join(body.format(k=k) + "\n" for _ in range(UNROLL) for k in range(CHAINS))
+                 f"mov.b64 p{k}, {{x{k}, y{k}}};\nmov.b64 q{k}, {{y{k}, c{k}}};\nmov.b64 t{k}, {{s, s}};\n"
+                 f"setp.lt.f32 P{k}, c{k}, x{k};\nsetp.lt.f32 S{k}, x{k}, c{k};\n")
+    loop = "".join(body.format(k=k) + "\n" for _ in range(UNROLL) for k in range(chains))
     fold = "mov.f32 %2, c0;\n"
     for k in range(CHAINS):
         fold += (f"add.f32 %2, %2, c{k};\nadd.f32 %2, %2, x{k};\nadd.f32 %2, %2, y{k};\n"
                  f"{{ .reg .f32 a, b; mov.b64 {{a, b}}, p{k}; add.f32 %2, %2, a; add.f32 %2, %2, b; "
                  f"mov.b64 {{a, b}}, q{k}; add.f32 %2, %2, a; }}\n"
                  f"{{ .reg .b32 z; xor.b32 z, u{k}, v{k}; xor.b32 z, z, w{k}; cvt.rn.f32.u32 x{k}, z; "
-                 f"add.f32 %2, %2, x{k}; }}\n")
-    return TEMPLATE % (f32, b32, b64, cstr(init), cstr(loop), cstr(fold))
+                 f"add.f32 %2, %2, x{k}; }}\n"
+                 f"{{ .reg .f32 z; selp.f32 z, 1.0, 0.0, P{k}; add.f32 %2, %2, z; }}\n")
+    return TEMPLATE % (f32, b32, b64, preds, cstr(init), cstr(loop), cstr(fold))
 
 
 def cstr(ptx: str) -> str:
@@ -149,8 +157,9 @@ def main():
     threads, iters = 256, 4096
     cycles = gpu.empty((3 * sms * 8 * threads // 32,), np.uint64)
     sink = gpu.empty((threads,), np.float32)
-    for name, (body, per_chain) in FORMS.items():
-        src = kernel_source(body)
+    for name, (body, per_chain, *rest) in FORMS.items():
+        chains = rest[0] if rest else CHAINS
+        src = kernel_source(body, chains)
         cubin = native.compile_cubin(src, f"probe_{name}", native._nvrtc_options({}))
         k = gpu.load(cubin, "probe")
         # launch only as many blocks as are resident at once (register-limited), so every
@@ -168,7 +177,7 @@ def main():
         # per SM: all of its warps' instructions over the SM's busy window (first start to last
         # end on that SM's clock), per SMSP; blocks that ran in a second wave are then counted
         # against the time they really took
-        instrs = per_chain * CHAINS * UNROLL * iters
+        instrs = per_chain * chains * UNROLL * iters
         ops = loop_ops(cubin)
         rates, issued_rates, spans = [], [], []
         for s_id in np.unique(sm):
@@ -183,7 +192,7 @@ def main():
         span = float(np.median(spans))  # 1 = the SM's warps all ran concurrently, 2 = two waves
         cyc = t1 - t0
         print(json.dumps({"form": name, "regs": k.regs, "blocks_per_sm": resident, "span": round(float(span), 3),
-                          "instrs_per_trip_per_warp": per_chain * CHAINS * UNROLL,
+                          "instrs_per_trip_per_warp": per_chain * chains * UNROLL,
                           "sass_loop_ops": ops, "sass_issue_per_smsp_per_cycle": round(issued, 3),
                           "warp_instr_per_smsp_per_cycle": round(per_smsp, 3),
                           "median_cycles": float(np.median(cyc)), "warps_per_smsp": warps_per_smsp}), flush=True)
