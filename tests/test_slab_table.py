@@ -56,6 +56,9 @@ POLYGONS = {
     "signed-zeros": (np.array([-1.0, 1.0, 1.0, -1.0], np.float32), np.array([-0.0, 0.0, 1.0, 1.0], np.float32)),
     "comb": (np.array([0, 4, 4, 3, 3, 2, 2, 1, 1, 0], np.float32),
              np.array([0, 0, 3, 3, 1, 1, 3, 3, 1, 1], np.float32)),
+    "flat": (np.array([0.0, 1.0, 2.0, 0.5], np.float32), np.array([0.25, 0.25, 0.25, 0.25], np.float32)),
+    "tiny": (np.array([0.0, 3e-30, 1e-30], np.float32), np.array([0.0, 1e-30, 4e-30], np.float32)),
+    "huge": (np.array([-1e30, 2e30, 0.0, 5e29], np.float32), np.array([-1e30, 0.0, 3e30, 1e29], np.float32)),
 }
 
 
@@ -234,8 +237,9 @@ def test_grid_clean_cells_give_the_brute_force_parity(name, g):
     for d in (0.0, 1e-7, -1e-7, 1e-3):
         pts.append((vv + np.float32(d)).astype(np.float32))
     # cell borders in x and y (v = (k - o) / s)
-    xs = ((np.arange(g + 1, dtype=np.float64) - prm[1]) / prm[0]).astype(np.float32)
-    ys = ((np.arange(g + 1, dtype=np.float64) - prm[3]) / prm[2]).astype(np.float32)
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):  # flat polygons: scale 0
+        xs = ((np.arange(g + 1, dtype=np.float64) - prm[1]) / prm[0]).astype(np.float32)
+        ys = ((np.arange(g + 1, dtype=np.float64) - prm[3]) / prm[2]).astype(np.float32)
     bx = np.concatenate([xs, np.nextafter(xs, np.float32(np.inf)), np.nextafter(xs, np.float32(-np.inf))])
     by = np.concatenate([ys, np.nextafter(ys, np.float32(np.inf)), np.nextafter(ys, np.float32(-np.inf))])
     pts.append(np.stack([rng.choice(bx, 50_000), rng.uniform(-span, span, 50_000).astype(np.float32)], 1))
