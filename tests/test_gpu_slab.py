@@ -117,6 +117,29 @@ def test_slab_host_api_matches_brute_force(gpu, strips):
     np.testing.assert_array_equal(slab, O.pnpoly(inp["points"], inp["vx"], inp["vy"], 2))
 
 
+EXTREME = {
+    "flat": (np.array([0.0, 1.0, 2.0, 0.5], np.float32), np.array([0.25, 0.25, 0.25, 0.25], np.float32), 1.0),
+    "tiny": (np.array([0.0, 3e-30, 1e-30], np.float32), np.array([0.0, 1e-30, 4e-30], np.float32), 5e-30),
+    "huge": (np.array([-1e30, 2e30, 0.0, 5e29], np.float32), np.array([-1e30, 0.0, 3e30, 1e29], np.float32), 4e30),
+}
+
+
+@pytest.mark.parametrize("shape", sorted(EXTREME))
+def test_slab_and_grid_extreme_polygons(gpu, shape):
+    """Zero-height, 1e-30-sized and 1e30-sized polygons through the slab and grid kernels."""
+    from paper_2211_07260_b200.kernels import PnPolyGridProblem, PnPolySlabProblem
+
+    vx, vy, span = EXTREME[shape]
+    rng = np.random.default_rng(21)
+    pts = np.concatenate([rng.uniform(-span, span, (100_003, 2)), np.stack([vx, vy], 1)]).astype(np.float32)
+    want = O.pnpoly(pts, vx, vy, 2)
+    for cls, cfgs in ((PnPolySlabProblem, SLAB_CONFIGS[::6]), (PnPolyGridProblem, GRID_CONFIGS[::4])):
+        p = cls(n_points=len(pts), n_vertices=vx.size)
+        p.prepare(gpu, {"points": pts, "vx": vx, "vy": vy})
+        for cfg in [c for c in cfgs if p.is_valid(c)] + [p.default_config()]:
+            np.testing.assert_array_equal(run_once(gpu, p, cfg), want, err_msg=f"{shape} {cls.__name__} {cfg}")
+
+
 @pytest.mark.parametrize("shape", ["star3000", "convex50", "comb"])
 def test_slab_other_polygons(gpu, shape):
     """Slab kernel on polygons unlike the benchmark one: a 3000-vertex star (long slab
