@@ -235,6 +235,19 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
  * search). params = {sx, ox, sy, oy}. bits == NULL: params only. */
 int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, float *params, uint32_t *bits,
                    long long capacity, int *clean_cells);
+/* Per-cell edge lists over the same gw x gh raster and cell function as
+ * jt_pnpoly_grid, for csrc/kernels/pnpoly_cells.cu. Per cell, 2 bits: 0 / 1 =
+ * every edge's METHOD 2 test is constant over the cell and the answer is that
+ * parity; 2 = the undecided edges are listed (heads[2 cell] = first entry,
+ * heads[2 cell + 1] = count << 1 | parity of the always-true edges; entries are
+ * float4 {slope, icpt, ylo, yhi} in `edges`); 3 = more than `lmax` undecided
+ * edges (the kernel runs the exact slab search). Border cells (row 0, column 0,
+ * where NaN coordinates land) with parity 1 are always listed. stats = {entries,
+ * clean cells, listed cells, fallback cells}. bits or heads NULL: params and
+ * stats only; edges NULL or too small: sizes only (JT_EINVAL if too small). */
+int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int lmax, float *params, uint32_t *bits,
+                    long long bits_capacity, uint32_t *heads, long long heads_capacity, float *edges,
+                    long long edge_capacity, long long *stats);
 
 /* TMA descriptor (CUtensorMap, 128 bytes written to out128) for a row-major
  * fp32 matrix [rows][cols] at dptr, tiles of box_rows x box_cols elements.

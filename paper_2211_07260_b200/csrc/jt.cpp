@@ -1382,6 +1382,134 @@ int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, floa
     return JT_OK;
 }
 
+// Per-cell edge lists for csrc/kernels/pnpoly_cells.cu. The METHOD 2 test of edge k,
+// spans(py) && px < fma(slope, py, icpt) with spans = ylo <= py < yhi, is decided for a
+// whole cell [X0, X1] x [Y0, Y1] when it is false for every point (no py of the cell's
+// rows in the span, or X0 >= every computed x over the spanned py) or true for every
+// point (the span covers the rows and X1 < every computed x); computed x is monotone in
+// py, so its range over a py interval comes from the interval's ends. The always-true
+// edges give the cell's base parity, the undecided ones are listed; a point's answer is
+// base ^ the XOR of its listed edges' tests, which is the brute-force XOR over all edges.
+int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int lmax, float *params, uint32_t *bits,
+                    long long bits_capacity, uint32_t *heads, long long heads_capacity, float *edges,
+                    long long edge_capacity, long long *stats) {
+    if (!vx || !vy || !params || n < 3) return fail(JT_EINVAL, "polygon needs >= 3 vertices");
+    if (gw < 1 || gh < 1 || (long long)gw * gh > (1LL << 24)) return fail(JT_EINVAL, "bad grid %d x %d", gw, gh);
+    if (lmax < 0 || lmax > (1 << 20)) return fail(JT_EINVAL, "bad list limit %d", lmax);
+    const long long cells = (long long)gw * gh, words = (cells + 15) / 16;
+    std::vector<float> slope(n), icpt(n), ylo(n), yhi(n);
+    float xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+    for (int k = 0; k < n; ++k) {
+        if (std::isnan(vy[k]) || std::isnan(vx[k])) return fail(JT_EINVAL, "vertex %d is NaN", k);
+        const int p = (k + n - 1) % n;
+        volatile float s = (vx[p] - vx[k]) / (vy[p] - vy[k]);
+        slope[k] = s;
+        icpt[k] = std::fmaf(-slope[k], vy[k], vx[k]);
+        ylo[k] = std::min(vy[k], vy[p]);
+        yhi[k] = std::max(vy[k], vy[p]);
+        xmin = std::min(xmin, vx[k]), xmax = std::max(xmax, vx[k]);
+        ymin = std::min(ymin, vy[k]), ymax = std::max(ymax, vy[k]);
+    }
+    // the cell function of jt_pnpoly_grid: min(f2u_rz(fma(v, s, o)), g - 1)
+    const float sx = xmax > xmin ? (float)gw / (xmax - xmin) : 0.f;
+    const float sy = ymax > ymin ? (float)gh / (ymax - ymin) : 0.f;
+    const float ox = -xmin * sx, oy = -ymin * sy;
+    params[0] = sx, params[1] = ox, params[2] = sy, params[3] = oy;
+    const bool fill = bits && heads;
+    if (fill && (bits_capacity < words || heads_capacity < 2 * cells))
+        return fail(JT_EINVAL, "cell tables need %lld words and %lld heads", words, 2 * cells);
+    if (fill) {
+        std::memset(bits, 0, sizeof(uint32_t) * words);
+        std::memset(heads, 0, sizeof(uint32_t) * 2 * cells);
+    }
+    std::vector<float> cx0(gw + 1), cy0(gh + 1);
+    for (int k = 0; k <= gw; ++k) cx0[k] = k == 0 ? -INFINITY : cell_first(k, sx, ox, gw - 1);
+    for (int k = 0; k <= gh; ++k) cy0[k] = k == 0 ? -INFINITY : cell_first(k, sy, oy, gh - 1);
+    cx0[gw] = cy0[gh] = INFINITY;
+    long long entries = 0, n_clean = 0, n_listed = 0, n_fallback = 0;
+    struct Row { int k; bool full, exact; float xl, xh; };
+    std::vector<Row> row;
+    std::vector<int> list, part;
+    std::vector<float> steps;
+    for (int cy = 0; cy < gh; ++cy) {
+        const float Y0 = cy0[cy], Y1 = cy0[cy + 1] == INFINITY ? INFINITY : std::nextafter(cy0[cy + 1], -INFINITY);
+        if (!(Y0 <= Y1)) continue;  // no float maps to this row
+        row.clear();
+        for (int k = 0; k < n; ++k) {
+            if (!(ylo[k] < yhi[k])) continue;  // horizontal: never spans
+            const float a = std::max(Y0, ylo[k]), b = std::min(Y1, std::nextafter(yhi[k], -INFINITY));
+            if (!(a <= b)) continue;  // spans no py of the row
+            Row r{k, ylo[k] <= Y0 && Y1 < yhi[k], false, 0.f, 0.f};
+            if (std::isfinite(slope[k]) && std::isfinite(icpt[k])) {
+                const float xa = std::fmaf(slope[k], a, icpt[k]), xb = std::fmaf(slope[k], b, icpt[k]);
+                if (!std::isnan(xa) && !std::isnan(xb)) r.exact = true, r.xl = std::min(xa, xb), r.xh = std::max(xa, xb);
+            }
+            row.push_back(r);
+        }
+        for (int cx = 0; cx < gw; ++cx) {
+            const float X0 = cx0[cx], X1 = cx0[cx + 1] == INFINITY ? INFINITY : std::nextafter(cx0[cx + 1], -INFINITY);
+            if (!(X0 <= X1)) continue;
+            int base = 0;
+            list.clear();
+            part.clear();
+            for (const Row &r : row) {
+                if (r.exact && X0 >= r.xh) continue;  // false for every point
+                if (r.exact && X1 < r.xl) {           // true wherever the edge spans py
+                    if (r.full) base ^= 1;
+                    else part.push_back(r.k);
+                    continue;
+                }
+                list.push_back(r.k);
+            }
+            // the partly spanning always-right edges contribute the parity of #{k: ylo <= py < yhi},
+            // a step function of py: constant over the row when every step y inside (Y0, Y1]
+            // toggles it an even number of times (e.g. the two edges at a vertex)
+            if (!part.empty()) {
+                steps.clear();
+                int at_y0 = 0;
+                for (int k : part) {
+                    at_y0 ^= (ylo[k] <= Y0 && Y0 < yhi[k]) ? 1 : 0;
+                    if (Y0 < ylo[k] && ylo[k] <= Y1) steps.push_back(ylo[k]);
+                    if (Y0 < yhi[k] && yhi[k] <= Y1) steps.push_back(yhi[k]);
+                }
+                std::sort(steps.begin(), steps.end());
+                bool constant = true;
+                for (size_t i = 0; i < steps.size() && constant;) {
+                    size_t j = i;
+                    while (j < steps.size() && steps[j] == steps[i]) ++j;
+                    constant = ((j - i) & 1) == 0;
+                    i = j;
+                }
+                if (constant) base ^= at_y0;
+                else list.insert(list.end(), part.begin(), part.end());
+            }
+            const long long cell = (long long)cy * gw + cx;
+            // NaN coordinates land in row 0 / column 0 and are never inside: a clean cell
+            // there with base parity 1 is listed (with no edges) so the exact path answers
+            const bool border = cx == 0 || cy == 0;
+            uint32_t code;
+            if (list.empty() && !(border && base)) code = (uint32_t)base, ++n_clean;
+            else if ((int)list.size() <= lmax) {
+                code = 2, ++n_listed;
+                if (fill) heads[2 * cell] = (uint32_t)entries, heads[2 * cell + 1] = ((uint32_t)list.size() << 1) | base;
+                if (fill && edges && entries + (long long)list.size() <= edge_capacity)
+                    for (size_t i = 0; i < list.size(); ++i) {
+                        float *e = edges + 4 * (entries + (long long)i);
+                        const int k = list[i];
+                        e[0] = slope[k], e[1] = icpt[k], e[2] = ylo[k], e[3] = yhi[k];
+                    }
+                entries += (long long)list.size();
+            } else code = 3, ++n_fallback;  // too many edges: the exact slab search
+            if (fill) bits[cell >> 4] |= code << ((cell & 15) * 2);
+        }
+    }
+    if (entries > (1LL << 31)) return fail(JT_EINVAL, "cell lists need %lld entries", entries);
+    if (stats) stats[0] = entries, stats[1] = n_clean, stats[2] = n_listed, stats[3] = n_fallback;
+    if (fill && edges && entries > edge_capacity)
+        return fail(JT_EINVAL, "cell lists need %lld entries, got %lld", entries, edge_capacity);
+    return JT_OK;
+}
+
 int jt_tensor_map_2d(jt_ctx *c, unsigned long long dptr, unsigned long long rows, unsigned long long cols,
                      unsigned box_rows, unsigned box_cols, int swizzle, void *out128) {
     if (int e = bind(c)) return e;

@@ -624,6 +624,98 @@ class PnPolyGridProblem(PnPolySlabProblem):
         return float(((words[idx >> 4] >> ((idx & 15) * 2).astype(np.uint32)) & 1).mean())
 
 
+@dataclass
+class PnPolyCellsProblem(PnPolyGridProblem):
+    """PnPoly with per-cell edge lists (csrc/kernels/pnpoly_cells.cu).
+
+    The same bitmap as :class:`PnPolyProblem` at METHOD 2, bit for bit: libjt
+    ``jt_pnpoly_cells`` decides every edge's test per cell of a GRID x GRID
+    raster; decided cells answer with one shared-memory lookup, undecided ones
+    list their few undecided edges (base parity ^ their tests), cells with more
+    than ``lmax`` fall back to the slab search. Two points per 16-byte load.
+    Reported as its own kernel against the HBM roofline.
+    """
+
+    name: str = "pnpoly_cells"
+    source: str = "pnpoly_cells.cu"
+    symbol: str = "pnpoly_cells"
+
+    def tune_params(self):
+        return {
+            "block_size_x": [256, 512, 1024],
+            "tile": [1, 2, 4],
+            "grid": [256, 512, 1024],
+            "grid_smem": [0, 1],
+            "lmax": [4, 16],
+            "stream": [0, 1],
+        }
+
+    def restrictions(self):
+        # ring: 128 x tile int slots per warp (tile in 1, 2, 4; QCAP in pnpoly_cells.cu)
+        return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * 512 * tile) <= {227 * 1024}"]
+
+    def default_config(self):
+        return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0}
+
+    def defines(self, config):
+        c = _as_dict(config)
+        return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"],
+                "GRID_SMEM": c.get("grid_smem", 1), "STREAM": c.get("stream", 0)}
+
+    def cell_table(self, g: int, lmax: int):
+        cache = self.__dict__.setdefault("_cell_tables", {})
+        if (g, lmax) not in cache:
+            vx, vy = self._polygon()
+            cache[(g, lmax)] = native.pnpoly_cells(vx, vy, g, g, lmax)
+        return cache[(g, lmax)]
+
+    def smem_bytes(self, config) -> int:
+        c = _as_dict(config)
+        words = (c["grid"] * c["grid"] + 15) // 16 if c.get("grid_smem", 1) else 0
+        ring = 128 if c["tile"] <= 1 else 256 if c["tile"] <= 2 else 512
+        return ((words + 3) // 4 * 4) * 4 + c["block_size_x"] // 32 * ring * 4
+
+    def launch(self, config, n_points: int | None = None):
+        c = _as_dict(config)
+        chunk = 2 * c["block_size_x"] * c["tile"]
+        chunks = max(1, math.ceil((self.n_points if n_points is None else n_points) / chunk))
+        smem = self.smem_bytes(c)
+        sms = self.gpu.sm_count if self.gpu is not None else 148
+        resident = max(1, min(2048 // c["block_size_x"], (228 * 1024) // (smem + 1024)))
+        return Launch((min(chunks, sms * resident), 1, 1), (c["block_size_x"], 1, 1), smem)
+
+    def prepare(self, gpu, inputs=None):
+        super().prepare(gpu, inputs)
+        self.__dict__.pop("_cell_tables", None)
+
+    def _tail(self, c):
+        g, lmax = c["grid"], c["lmax"]
+        key = f"cells{g}x{lmax}"
+        words, params, heads, edges, _ = self.cell_table(g, lmax)
+        if key not in self.buffers:
+            self.buffers[key] = (self.gpu.array(words), self.gpu.array(heads), self.gpu.array(edges))
+        bw, bh, be = self.buffers[key]
+        info = self.slab_info(1024, 16)
+        return [bw, bh, be, f32(params[0]), f32(params[1]), f32(params[2]), f32(params[3]),
+                self._table_buffer(1024, 16), i32(info.nu), i32(info.ng), i32(info.xb),
+                f32(info.ybase), f32(info.yscale), i32(info.guess_off), i32(info.xpar_off), i32(info.xst_off),
+                i32(info.xlo_off), i32(info.pmax_off), i32(info.pair_off)]
+
+    def clean_fraction(self, g: int, lmax: int = 16) -> float:
+        """Fraction of this input's points answered by the cell lookup alone (codes 0 / 1)."""
+        words, prm, _, _, _ = self.cell_table(g, lmax)
+        pts = self.inputs["points"]
+
+        def cell(v, scale, offset):
+            with np.errstate(invalid="ignore", over="ignore"):
+                f = (v.astype(np.float64) * np.float64(scale) + np.float64(offset)).astype(np.float32)
+            k = np.trunc(np.nan_to_num(f, nan=0.0, posinf=2.0**32, neginf=0.0))
+            return np.clip(k, 0, g - 1).astype(np.int64)
+
+        idx = cell(pts[:, 1], prm[2], prm[3]) * g + cell(pts[:, 0], prm[0], prm[1])
+        return float((((words[idx >> 4] >> ((idx & 15) * 2).astype(np.uint32)) & 3) < 2).mean())
+
+
 # -- Conv2D -------------------------------------------------------------------------------
 
 
@@ -990,6 +1082,7 @@ class BurnerProblem(KernelProblem):
 
 
 PROBLEMS = {"pnpoly": PnPolyProblem, "pnpoly_slab": PnPolySlabProblem, "pnpoly_grid": PnPolyGridProblem,
+            "pnpoly_cells": PnPolyCellsProblem,
             "conv2d": Conv2DProblem, "sgemm": SgemmProblem, "sgemm_tf32": SgemmTF32Problem,
             "burner": BurnerProblem}
 

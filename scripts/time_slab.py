@@ -13,10 +13,11 @@ from paper_2211_07260_b200.gpu import GPU  # noqa: E402
 from paper_2211_07260_b200.kernels import make_problem  # noqa: E402
 
 gpu = GPU(0)
-# usage: time_slab.py [--grid] [key=value ...]  (--grid: the cell fast-path kernel, pnpoly_grid.cu)
+# usage: time_slab.py [--grid | --cells] [key=value ...]  (--grid: pnpoly_grid.cu, --cells: pnpoly_cells.cu)
 grid_mode = "--grid" in sys.argv
-sys.argv = [a for a in sys.argv if a != "--grid"]
-p = make_problem("pnpoly_grid" if grid_mode else "pnpoly_slab")
+cells_mode = "--cells" in sys.argv
+sys.argv = [a for a in sys.argv if a not in ("--grid", "--cells")]
+p = make_problem("pnpoly_cells" if cells_mode else "pnpoly_grid" if grid_mode else "pnpoly_slab")
 p.prepare(gpu)
 want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
 configs = [c.as_dict() for c in p.space().enumerate()]
@@ -39,5 +40,5 @@ for cfg in configs:
 rows.sort(key=lambda r: r[0])
 print("BEST", [(round(t * 1e6, 1), c, ok) for t, c, ok in rows[:8]])
 print("useful edge tests per point", p.useful_edge_tests() / p.n_points)
-if grid_mode:
+if grid_mode or cells_mode:
     print("clean fraction", {g: round(p.clean_fraction(g), 4) for g in (256, 512)})

@@ -127,13 +127,14 @@ EXTREME = {
 @pytest.mark.parametrize("shape", sorted(EXTREME))
 def test_slab_and_grid_extreme_polygons(gpu, shape):
     """Zero-height, 1e-30-sized and 1e30-sized polygons through the slab and grid kernels."""
-    from paper_2211_07260_b200.kernels import PnPolyGridProblem, PnPolySlabProblem
+    from paper_2211_07260_b200.kernels import PnPolyCellsProblem, PnPolyGridProblem, PnPolySlabProblem
 
     vx, vy, span = EXTREME[shape]
     rng = np.random.default_rng(21)
     pts = np.concatenate([rng.uniform(-span, span, (100_003, 2)), np.stack([vx, vy], 1)]).astype(np.float32)
     want = O.pnpoly(pts, vx, vy, 2)
-    for cls, cfgs in ((PnPolySlabProblem, SLAB_CONFIGS[::6]), (PnPolyGridProblem, GRID_CONFIGS[::4])):
+    for cls, cfgs in ((PnPolySlabProblem, SLAB_CONFIGS[::6]), (PnPolyGridProblem, GRID_CONFIGS[::4]),
+                      (PnPolyCellsProblem, CELLS_CONFIGS[::5])):
         p = cls(n_points=len(pts), n_vertices=vx.size)
         p.prepare(gpu, {"points": pts, "vx": vx, "vy": vy})
         for cfg in [c for c in cfgs if p.is_valid(c)] + [p.default_config()]:
@@ -218,12 +219,13 @@ def test_grid_tiny_and_ragged_inputs(gpu, n):
                                       O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2))
 
 
+@pytest.mark.parametrize("kind", ["grid", "cells"])
 @pytest.mark.parametrize("shape", ["degenerate", "star3000", "convex50", "comb"])
-def test_grid_other_polygons_and_special_points(gpu, shape):
+def test_grid_other_polygons_and_special_points(gpu, shape, kind):
     """Degenerate polygon with +-0, +-inf and NaN coordinates; the slab tests' other polygons;
-    points exactly on vertices and on cell borders."""
+    points exactly on vertices and on cell borders (grid and cell-list kernels)."""
     from paper_2211_07260_b200 import native
-    from paper_2211_07260_b200.kernels import PnPolyGridProblem
+    from paper_2211_07260_b200.kernels import PnPolyCellsProblem, PnPolyGridProblem
 
     rng = np.random.default_rng(12)
     if shape == "degenerate":
@@ -245,10 +247,13 @@ def test_grid_other_polygons_and_special_points(gpu, shape):
         xs = ((np.arange(g + 1, dtype=np.float64) - prm[1]) / prm[0]).astype(np.float32)
         pts.append(np.stack([xs, rng.uniform(-1, 1, xs.size).astype(np.float32)], 1))
     pts = np.ascontiguousarray(np.concatenate(pts).astype(np.float32))
-    p = PnPolyGridProblem(n_points=len(pts), n_vertices=vx.size)
+    cls, configs = (PnPolyGridProblem, GRID_CONFIGS[::3]) if kind == "grid" else (PnPolyCellsProblem, CELLS_CONFIGS[::3])
+    p = cls(n_points=len(pts), n_vertices=vx.size)
     p.prepare(gpu, {"points": pts, "vx": vx, "vy": vy})
     want = O.pnpoly(pts, vx, vy, 2)
-    cfgs = [c for c in GRID_CONFIGS[::3] if p.is_valid(c)] + [p.default_config()]
+    cfgs = [c for c in configs if p.is_valid(c)] + [p.default_config()]
+    if kind == "cells":
+        cfgs.append(dict(p.default_config(), lmax=0))  # every undecided cell -> slab search
     for cfg in cfgs:
         np.testing.assert_array_equal(run_once(gpu, p, cfg), want, err_msg=f"{shape} {cfg}")
 
@@ -262,6 +267,59 @@ def test_grid_full_size_matches_brute_force(gpu):
     want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
     for cfg in {str(c): c for c in [p.default_config(), tuned.best_config("pnpoly_grid"),
                                     tuned.best_config("pnpoly_grid", "energy_optimal")] if c}.values():
+        got = run_once(gpu, p, cfg)
+        assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ ({cfg})"
+    assert p.clean_fraction(512) > 0.9
+
+
+# -- per-cell edge lists (csrc/kernels/pnpoly_cells.cu) --------------------------------------
+
+CELLS_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stream=st)
+                  for b, t, g, l, st in itertools.product((256, 1024), (1, 2, 4), (256, 512), (4, 16), (0, 1))
+                  if not (b == 1024 and t == 4)]
+                 + [dict(block_size_x=b, tile=2, grid=g, grid_smem=0, lmax=16, stream=0)
+                    for b, g in itertools.product((256, 1024), (512, 1024))])
+
+
+@pytest.fixture(scope="module")
+def cells_small(gpu):
+    from paper_2211_07260_b200.kernels import PnPolyCellsProblem
+
+    p = PnPolyCellsProblem(n_points=1_000_003)
+    p.prepare(gpu)
+    return p, O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
+
+
+@pytest.mark.parametrize("cfg", CELLS_CONFIGS, ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
+def test_cells_bit_exact_across_configs(gpu, cells_small, cfg):
+    p, want = cells_small
+    assert p.is_valid(cfg)
+    got = run_once(gpu, p, cfg)
+    assert np.array_equal(got, want), f"{int((got != want).sum())} points differ"
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 33, 4097, 65537])
+def test_cells_tiny_and_ragged_inputs(gpu, n):
+    from paper_2211_07260_b200.kernels import PnPolyCellsProblem
+
+    p = PnPolyCellsProblem(n_points=n)
+    p.prepare(gpu)
+    for cfg in (p.default_config(), dict(p.default_config(), block_size_x=256, tile=1, grid=256),
+                dict(p.default_config(), tile=4, block_size_x=512), dict(p.default_config(), grid=1024, grid_smem=0),
+                dict(p.default_config(), lmax=0)):
+        np.testing.assert_array_equal(run_once(gpu, p, cfg),
+                                      O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2), err_msg=str(cfg))
+
+
+def test_cells_full_size_matches_brute_force(gpu):
+    from paper_2211_07260_b200 import tuned
+    from paper_2211_07260_b200.kernels import PnPolyCellsProblem
+
+    p = PnPolyCellsProblem()
+    p.prepare(gpu)
+    want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
+    for cfg in {str(c): c for c in [p.default_config(), tuned.best_config("pnpoly_cells"),
+                                    tuned.best_config("pnpoly_cells", "energy_optimal")] if c}.values():
         got = run_once(gpu, p, cfg)
         assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ ({cfg})"
     assert p.clean_fraction(512) > 0.9

@@ -6,6 +6,8 @@ y-test ``(vy_k > py) != (vy_j > py)`` holds, with the same slope / intercept
 bits. Both are checked here on the benchmark polygon and on degenerate ones.
 """
 
+import ctypes
+import ctypes.util
 import math
 
 import numpy as np
@@ -230,6 +232,21 @@ def test_grid_clean_cells_give_the_brute_force_parity(name, g):
         vx, vy = POLYGONS[name]
     words, prm, clean = native.pnpoly_grid(vx, vy, g, g)
     assert 0 <= clean <= g * g
+    pts = _grid_points(vx, vy, prm, g)
+    cx = _cell(pts[:, 0], prm[0], prm[1], g - 1)
+    cy = _cell(pts[:, 1], prm[2], prm[3], g - 1)
+    cell = cy * g + cx
+    code = (words[cell >> 4] >> ((cell & 15) * 2).astype(np.uint32)) & 3
+    want = O.pnpoly(pts, vx, vy, 2)
+    is_clean = (code & 1) == 1
+    assert np.array_equal((code[is_clean] >> 1).astype(np.int32), want[is_clean]), name
+    if name == "benchmark" and g == 512:
+        assert is_clean.mean() > 0.8  # the fast path is the common path
+
+
+def _grid_points(vx, vy, prm, g):
+    """Random points, points on / next to the vertices and on / next to the cell borders of a
+    g x g raster with params prm, and far-away points."""
     rng = np.random.default_rng(3)
     span = float(max(abs(vx).max(), abs(vy).max())) * 1.3
     pts = [rng.uniform(-span, span, (200_000, 2)).astype(np.float32)]
@@ -245,16 +262,7 @@ def test_grid_clean_cells_give_the_brute_force_parity(name, g):
     pts.append(np.stack([rng.choice(bx, 50_000), rng.uniform(-span, span, 50_000).astype(np.float32)], 1))
     pts.append(np.stack([rng.uniform(-span, span, 50_000).astype(np.float32), rng.choice(by, 50_000)], 1))
     pts.append(np.array([[1e30, 0], [-1e30, 0], [0, 1e30], [0, -1e30], [np.inf, 0], [-np.inf, 0]], np.float32))
-    pts = np.ascontiguousarray(np.concatenate(pts).astype(np.float32))
-    cx = _cell(pts[:, 0], prm[0], prm[1], g - 1)
-    cy = _cell(pts[:, 1], prm[2], prm[3], g - 1)
-    cell = cy * g + cx
-    code = (words[cell >> 4] >> ((cell & 15) * 2).astype(np.uint32)) & 3
-    want = O.pnpoly(pts, vx, vy, 2)
-    is_clean = (code & 1) == 1
-    assert np.array_equal((code[is_clean] >> 1).astype(np.int32), want[is_clean]), name
-    if name == "benchmark" and g == 512:
-        assert is_clean.mean() > 0.8  # the fast path is the common path
+    return np.ascontiguousarray(np.concatenate(pts).astype(np.float32))
 
 
 @pytest.mark.parametrize("name", sorted(POLYGONS))
@@ -272,3 +280,62 @@ def test_grid_border_cells_are_zero_when_clean(name):
             for c in (k * g, k):  # first column of row k, first row's cell k
                 if code(c) & 1:
                     assert code(c) >> 1 == 0, (name, g, k)
+
+
+_libm = ctypes.CDLL(ctypes.util.find_library("m"))
+_libm.fmaf.restype = ctypes.c_float
+_libm.fmaf.argtypes = [ctypes.c_float] * 3
+
+
+def _polygon(name):
+    return PnPolySlabProblem(n_points=4096)._polygon() if POLYGONS[name] is None else POLYGONS[name]
+
+
+@pytest.mark.parametrize("name", sorted(POLYGONS))
+@pytest.mark.parametrize("g,lmax", [(7, 8), (64, 2), (512, 8)])
+def test_cell_lists_give_the_brute_force_answer(name, g, lmax):
+    """jt_pnpoly_cells: the pnpoly_cells.cu decision, emulated - code 0 / 1 is the answer,
+    code 2 is the base parity XOR the listed edges' METHOD 2 tests (libm fmaf, NaN -> 0) -
+    equals the brute-force bit for every point outside the code-3 (slab search) cells."""
+    from oracle import kernels_oracle as O
+
+    vx, vy = _polygon(name)
+    words, prm, heads, edges, st = native.pnpoly_cells(vx, vy, g, g, lmax)
+    assert st[1] + st[2] + st[3] <= g * g and st[0] <= max(1, st[2] * lmax)
+    pts = _grid_points(vx, vy, prm, g)
+    cell = _cell(pts[:, 1], prm[2], prm[3], g - 1) * g + _cell(pts[:, 0], prm[0], prm[1], g - 1)
+    code = (words[cell >> 4] >> ((cell & 15) * 2).astype(np.uint32)) & 3
+    want = O.pnpoly(pts, vx, vy, 2)
+    got = np.where(code < 2, code, 0).astype(np.int32)
+    for i in np.nonzero(code == 2)[0]:
+        px, py = float(pts[i, 0]), float(pts[i, 1])
+        if px != px or py != py:
+            continue
+        c = int(cell[i])
+        r = int(heads[2 * c + 1]) & 1
+        for e in edges[heads[2 * c]: heads[2 * c] + (int(heads[2 * c + 1]) >> 1)]:
+            if e[2] <= py < e[3] and px < _libm.fmaf(float(e[0]), py, float(e[1])):
+                r ^= 1
+        got[i] = r
+    keep = code != 3
+    assert np.array_equal(got[keep], want[keep]), (name, int((got[keep] != want[keep]).sum()))
+    if name == "benchmark" and g == 512:
+        assert (code < 2).mean() > 0.8 and (code == 3).mean() < 0.01
+
+
+@pytest.mark.parametrize("name", sorted(POLYGONS))
+def test_cell_lists_border_and_limits(name):
+    """NaN lands in row 0 / column 0: clean cells there hold 0. lmax 0 sends every undecided
+    cell to the slab search (code 3) and lists nothing; the clean cells equal jt_pnpoly_grid's."""
+    vx, vy = _polygon(name)
+    for g in (7, 256):
+        words, _, _, _, st = native.pnpoly_cells(vx, vy, g, g, 8)
+        code = lambda c: (int(words[c >> 4]) >> ((c & 15) * 2)) & 3  # noqa: E731
+        for k in range(g):
+            for c in (k * g, k):
+                assert code(c) != 1, (name, g, k)
+        w0, _, _, e0, s0 = native.pnpoly_cells(vx, vy, g, g, 0)
+        assert s0[0] == 0 and s0[2] == 0 and s0[1] == st[1]
+        assert s0[1] + s0[3] == st[1] + st[2] + st[3]
+    with pytest.raises(Exception):
+        native.pnpoly_cells(vx, vy, 0, 4, 8)
