@@ -236,7 +236,9 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
 int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, float *params, uint32_t *bits,
                    long long capacity, int *clean_cells);
 /* Per-cell edge lists over the same gw x gh raster and cell function as
- * jt_pnpoly_grid, for csrc/kernels/pnpoly_cells.cu. Per cell, 2 bits: 0 / 1 =
+ * jt_pnpoly_grid, for csrc/kernels/pnpoly_cells.cu (gw a multiple of 32). Per
+ * cell a 2-bit code, stored as two bit planes per 32 cells of a row (word 2j:
+ * code & 1 of cells 32j.., word 2j + 1: code >> 1; gw * gh / 16 words): 0 / 1 =
  * every edge's METHOD 2 test is constant over the cell and the answer is that
  * parity; 2 = the undecided edges are listed (heads[2 cell] = first entry,
  * heads[2 cell + 1] = count << 1 | parity of the always-true edges; entries are

@@ -1396,7 +1396,8 @@ int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int
     if (!vx || !vy || !params || n < 3) return fail(JT_EINVAL, "polygon needs >= 3 vertices");
     if (gw < 1 || gh < 1 || (long long)gw * gh > (1LL << 24)) return fail(JT_EINVAL, "bad grid %d x %d", gw, gh);
     if (lmax < 0 || lmax > (1 << 20)) return fail(JT_EINVAL, "bad list limit %d", lmax);
-    const long long cells = (long long)gw * gh, words = (cells + 15) / 16;
+    if (gw % 32) return fail(JT_EINVAL, "grid width %d is not a multiple of 32", gw);
+    const long long cells = (long long)gw * gh, words = cells / 16;
     std::vector<float> slope(n), icpt(n), ylo(n), yhi(n);
     float xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
     for (int k = 0; k < n; ++k) {
@@ -1500,7 +1501,10 @@ int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int
                     }
                 entries += (long long)list.size();
             } else code = 3, ++n_fallback;  // too many edges: the exact slab search
-            if (fill) bits[cell >> 4] |= code << ((cell & 15) * 2);
+            if (fill) {  // two bit planes per 32 cells of a row: answer / fallback, then undecided
+                bits[(cell >> 5) * 2] |= (code & 1u) << (cell & 31);
+                bits[(cell >> 5) * 2 + 1] |= (code >> 1) << (cell & 31);
+            }
         }
     }
     if (entries > (1LL << 31)) return fail(JT_EINVAL, "cell lists need %lld entries", entries);

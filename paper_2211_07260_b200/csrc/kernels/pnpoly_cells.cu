@@ -36,9 +36,8 @@
 #define STREAM 0
 #endif
 #define CHUNK (BLOCK_SIZE_X * TILE)
-// ring slots per warp (a power of two): < 32 left after a drain + 2 x 32 pushed per pair
-#define QCAP (TILE <= 1 ? 128 : TILE <= 2 ? 256 : TILE <= 6 ? 512 : 1024)
-#define GRID_WORDS ((GRID * GRID + 15) / 16)
+// ring slots per warp (a power of two): < 32 left after a drain + 32 pushed per pair step
+#define QCAP (TILE <= 3 ? 128 : 256)
 
 #if STREAM
 #define LOAD_PAIR(p) __ldcs(p)
@@ -98,60 +97,62 @@ __device__ __forceinline__ int cell_search(float px, float py, unsigned cell, un
     return in;
 }
 
-// the host's cell function (jt_pnpoly_cells): min(f2u_rz(fma(v, s, o)), GRID - 1); cvt.rzi.u32
-// maps NaN and negatives to 0, so NaN lands in row / column 0 (whose clean cells hold 0)
-__device__ __forceinline__ unsigned cell_of(float px, float py, float gsx, float gox, float gsy, float goy) {
-    const unsigned cx = min(__float2uint_rz(__fmaf_rn(px, gsx, gox)), GRID - 1u);
-    const unsigned cy = min(__float2uint_rz(__fmaf_rn(py, gsy, goy)), GRID - 1u);
-    return cy * GRID + cx;
-}
-
-// one undecided point of the drain: reload it (L1 / L2: its line was read moments ago),
-// redo its cell and code, answer it
-#define DRAIN_ONE(idx)                                                                      \
-    do {                                                                                    \
-        const float2 p_ = points[idx];                                                      \
-        const unsigned cell_ = cell_of(p_.x, p_.y, gsx, gox, gsy, goy);                     \
-        const unsigned w_ = GRID_WORD(cell_ >> 4);                                          \
-        const unsigned code_ = __funnelshift_r(w_, w_, cell_ * 2u) & 3u;                    \
-        bitmap[idx] = cell_search(p_.x, p_.y, cell_, code_, heads, edges, SLAB_ARGS);       \
+// The host's cell function (jt_pnpoly_cells): min(f2u_rz(fma(v, s, o)), GRID - 1); cvt.rzi.u32
+// maps NaN and negatives to 0, so NaN lands in row / column 0 (whose decided cells hold 0).
+// The raster holds two bit planes per 32 cells of a row ({code & 1, code >> 1} words), so a
+// point's code is one 8-byte lookup and two rotates by cx (mod 32).
+struct Code {
+    unsigned lo, hi;  // bit 0: code & 1 (the answer, or the fallback flag), code >> 1 (undecided)
+};
+#if GRID_SMEM
+#define GRID_PAIR(i) s_grid[i]
+#else
+#define GRID_PAIR(i) __ldg(grid + (i))
+#endif
+#define CODE_OF(px, py, out)                                                                 \
+    do {                                                                                     \
+        const unsigned cx_ = min(__float2uint_rz(__fmaf_rn(px, gsx, gox)), GRID - 1u);        \
+        const unsigned cy_ = min(__float2uint_rz(__fmaf_rn(py, gsy, goy)), GRID - 1u);        \
+        const uint2 w_ = GRID_PAIR(cy_ * (GRID / 32) + (cx_ >> 5));                           \
+        (out).lo = __funnelshift_r(w_.x, w_.x, cx_);                                          \
+        (out).hi = __funnelshift_r(w_.y, w_.y, cx_);                                          \
+        cell_ = cy_ * GRID + cx_;                                                            \
     } while (0)
 
 // full occupancy (2048 threads per SM) needs <= 32 registers per thread
 extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X, 2048 / BLOCK_SIZE_X)
-pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, const unsigned *__restrict__ grid,
+pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, const uint2 *__restrict__ grid,
              const uint2 *__restrict__ heads, const float4 *__restrict__ edges, float gsx, float gox, float gsy,
              float goy, SLAB_PARAMS) {
     extern __shared__ __align__(16) unsigned smem[];
 #if GRID_SMEM
-    unsigned *s_grid = smem;
-    int *ring = reinterpret_cast<int *>(smem + ((GRID_WORDS + 3) & ~3)) + (threadIdx.x >> 5) * QCAP;
-    for (int i = threadIdx.x; i < GRID_WORDS / 4; i += BLOCK_SIZE_X)
+    constexpr int GRID_PAIRS = GRID * GRID / 32;
+    uint2 *s_grid = reinterpret_cast<uint2 *>(smem);
+    int *ring = reinterpret_cast<int *>(smem + 2 * GRID_PAIRS) + (threadIdx.x >> 5) * QCAP;
+    for (int i = threadIdx.x; i < GRID_PAIRS / 2; i += BLOCK_SIZE_X)
         reinterpret_cast<uint4 *>(s_grid)[i] = __ldg(reinterpret_cast<const uint4 *>(grid) + i);
-    for (int i = GRID_WORDS / 4 * 4 + threadIdx.x; i < GRID_WORDS; i += BLOCK_SIZE_X) s_grid[i] = __ldg(grid + i);
     __syncthreads();
-#define GRID_WORD(w) s_grid[w]
 #else
     int *ring = reinterpret_cast<int *>(smem) + (threadIdx.x >> 5) * QCAP;
-#define GRID_WORD(w) __ldg(grid + (w))
 #endif
     const float4 *pairs = reinterpret_cast<const float4 *>(points);
     int2 *out = reinterpret_cast<int2 *>(bitmap);
     const int full = n >> 1, npairs = (n + 1) >> 1;  // pair q = points 2q, 2q + 1; an odd tail pair
     const int lane = threadIdx.x & 31;
-    const unsigned lanes_below = (1u << lane) - 1u;
-    // per-warp ring of undecided point indices: pushed at tail during a chunk, drained 32 at
-    // a time from head at its end (warp-uniform counters; < 32 left after a drain, so a
-    // chunk's <= 64 TILE pushes never reach the slots the last drain read). Nothing but
+    unsigned lanes_below;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_below));
+    // Per-warp ring of pairs with an undecided point: pushed at tail during a chunk, drained
+    // 32 at a time from head at its end (warp-uniform counters; < 32 left after a drain, so
+    // a chunk's <= 32 TILE pushes never reach the slots the last drain read). Nothing but
     // loop counters is live across the drain: the chunk's loads are issued after it.
     unsigned head = 0, tail = 0;
     const int n_chunks = (npairs + CHUNK - 1) / CHUNK;
-    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    auto chunk = [&](int c, const bool FULL) {  // inlined twice with FULL constant
         float4 cur[TILE];
 #pragma unroll
         for (int t = 0; t < TILE; ++t) {
             const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
-            if (q < full) cur[t] = LOAD_PAIR(pairs + q);
+            if (FULL || q < full) cur[t] = LOAD_PAIR(pairs + q);
             else if (q < npairs) {
                 const float2 p = points[2 * q];
                 cur[t] = make_float4(p.x, p.y, 0.f, 0.f);
@@ -160,32 +161,46 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
         for (int t = 0; t < TILE; ++t) {
             const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
-            const unsigned c0 = cell_of(cur[t].x, cur[t].y, gsx, gox, gsy, goy);
-            const unsigned c1 = cell_of(cur[t].z, cur[t].w, gsx, gox, gsy, goy);
-            const unsigned w0 = GRID_WORD(c0 >> 4), w1 = GRID_WORD(c1 >> 4);
-            const unsigned k0 = __funnelshift_r(w0, w0, c0 * 2u) & 3u, k1 = __funnelshift_r(w1, w1, c1 * 2u) & 3u;
-            // codes 0 / 1: the answer; 2: listed edges; 3: slab search. Undecided points get a
-            // placeholder here and their answer from a later drain of the same warp.
-            if (q < full) STORE_PAIR(out + q, make_int2((int)(k0 & 1u), (int)(k1 & 1u)));
-            else if (q < npairs) bitmap[2 * q] = (int)(k0 & 1u);
-            const bool s0 = q < npairs && (k0 & 2u), s1 = q < full && (k1 & 2u);
-            const unsigned need0 = __ballot_sync(0xffffffffu, s0), need1 = __ballot_sync(0xffffffffu, s1);
-            if (need0 | need1) {
-                if (s0) ring[(tail + __popc(need0 & lanes_below)) % QCAP] = 2 * q;
-                tail += __popc(need0);
-                if (s1) ring[(tail + __popc(need1 & lanes_below)) % QCAP] = 2 * q + 1;
-                tail += __popc(need1);
-            }
+            Code k0, k1;
+            unsigned cell_;
+            CODE_OF(cur[t].x, cur[t].y, k0);
+            CODE_OF(cur[t].z, cur[t].w, k1);
+            // decided points get their answer here; a pair with an undecided point is queued
+            // and both its points are rewritten by a later drain of the same warp
+            if (FULL || q < full) STORE_PAIR(out + q, make_int2((int)(k0.lo & 1u), (int)(k1.lo & 1u)));
+            else if (q < npairs) bitmap[2 * q] = (int)(k0.lo & 1u);
+            const bool slow = (FULL || q < npairs) && ((k0.hi | k1.hi) & 1u);
+            const unsigned need = __ballot_sync(0xffffffffu, slow);
+            if (slow) ring[(tail + __popc(need & lanes_below)) % QCAP] = q;
+            tail += __popc(need);
         }
+    };
+    // one queued pair: both points redone, the undecided ones searched
+    auto drain = [&](int q) {
+        float4 v;
+        if (q < full) v = __ldg(pairs + q);
+        else { const float2 p = points[2 * q]; v = make_float4(p.x, p.y, 0.f, 0.f); }
+        Code k;
+        unsigned cell_;
+        CODE_OF(v.x, v.y, k);
+        const int r0 = (k.hi & 1u) ? cell_search(v.x, v.y, cell_, 2u | (k.lo & 1u), heads, edges, SLAB_ARGS)
+                                   : (int)(k.lo & 1u);
+        if (q < full) {
+            CODE_OF(v.z, v.w, k);
+            const int r1 = (k.hi & 1u) ? cell_search(v.z, v.w, cell_, 2u | (k.lo & 1u), heads, edges, SLAB_ARGS)
+                                       : (int)(k.lo & 1u);
+            out[q] = make_int2(r0, r1);
+        } else bitmap[2 * q] = r0;
+    };
+    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        if ((c + 1) * CHUNK <= full) chunk(c, true);
+        else chunk(c, false);
         __syncwarp();
         while (tail - head >= 32u) {
-            const int idx = ring[(head + lane) % QCAP];
+            const int q = ring[(head + lane) % QCAP];
             head += 32;
-            DRAIN_ONE(idx);
+            drain(q);
         }
     }
-    if (lane < tail - head) {  // the warp's leftovers
-        const int idx = ring[(head + lane) % QCAP];
-        DRAIN_ONE(idx);
-    }
+    if (lane < tail - head) drain(ring[(head + lane) % QCAP]);  // the warp's leftovers
 }

@@ -651,8 +651,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         }
 
     def restrictions(self):
-        # ring: 128 x tile int slots per warp (tile in 1, 2, 4; QCAP in pnpoly_cells.cu)
-        return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * 512 * tile) <= {227 * 1024}"]
+        # ring: 128 int slots per warp for tile <= 3, 256 for tile 4 (QCAP in pnpoly_cells.cu)
+        return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * 512 * (1 + tile // 4)) <= {227 * 1024}"]
 
     def default_config(self):
         return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0}
@@ -671,9 +671,9 @@ class PnPolyCellsProblem(PnPolyGridProblem):
 
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
-        words = (c["grid"] * c["grid"] + 15) // 16 if c.get("grid_smem", 1) else 0
-        ring = 128 if c["tile"] <= 1 else 256 if c["tile"] <= 2 else 512
-        return ((words + 3) // 4 * 4) * 4 + c["block_size_x"] // 32 * ring * 4
+        words = c["grid"] * c["grid"] // 16 if c.get("grid_smem", 1) else 0
+        ring = 128 if c["tile"] <= 3 else 256
+        return words * 4 + c["block_size_x"] // 32 * ring * 4
 
     def launch(self, config, n_points: int | None = None):
         c = _as_dict(config)
@@ -713,7 +713,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
             return np.clip(k, 0, g - 1).astype(np.int64)
 
         idx = cell(pts[:, 1], prm[2], prm[3]) * g + cell(pts[:, 0], prm[0], prm[1])
-        return float((((words[idx >> 4] >> ((idx & 15) * 2).astype(np.uint32)) & 3) < 2).mean())
+        undecided = (words[(idx >> 5) * 2 + 1] >> (idx & 31).astype(np.uint32)) & 1
+        return float((undecided == 0).mean())
 
 
 # -- Conv2D -------------------------------------------------------------------------------

@@ -292,7 +292,7 @@ def _polygon(name):
 
 
 @pytest.mark.parametrize("name", sorted(POLYGONS))
-@pytest.mark.parametrize("g,lmax", [(7, 8), (64, 2), (512, 8)])
+@pytest.mark.parametrize("g,lmax", [(32, 8), (64, 2), (512, 8)])
 def test_cell_lists_give_the_brute_force_answer(name, g, lmax):
     """jt_pnpoly_cells: the pnpoly_cells.cu decision, emulated - code 0 / 1 is the answer,
     code 2 is the base parity XOR the listed edges' METHOD 2 tests (libm fmaf, NaN -> 0) -
@@ -304,7 +304,7 @@ def test_cell_lists_give_the_brute_force_answer(name, g, lmax):
     assert st[1] + st[2] + st[3] <= g * g and st[0] <= max(1, st[2] * lmax)
     pts = _grid_points(vx, vy, prm, g)
     cell = _cell(pts[:, 1], prm[2], prm[3], g - 1) * g + _cell(pts[:, 0], prm[0], prm[1], g - 1)
-    code = (words[cell >> 4] >> ((cell & 15) * 2).astype(np.uint32)) & 3
+    code = _cells_code(words, cell)
     want = O.pnpoly(pts, vx, vy, 2)
     got = np.where(code < 2, code, 0).astype(np.int32)
     for i in np.nonzero(code == 2)[0]:
@@ -328,14 +328,24 @@ def test_cell_lists_border_and_limits(name):
     """NaN lands in row 0 / column 0: clean cells there hold 0. lmax 0 sends every undecided
     cell to the slab search (code 3) and lists nothing; the clean cells equal jt_pnpoly_grid's."""
     vx, vy = _polygon(name)
-    for g in (7, 256):
+    for g in (32, 256):
         words, _, _, _, st = native.pnpoly_cells(vx, vy, g, g, 8)
-        code = lambda c: (int(words[c >> 4]) >> ((c & 15) * 2)) & 3  # noqa: E731
         for k in range(g):
             for c in (k * g, k):
-                assert code(c) != 1, (name, g, k)
+                assert _cells_code(words, np.array([c]))[0] != 1, (name, g, k)
         w0, _, _, e0, s0 = native.pnpoly_cells(vx, vy, g, g, 0)
         assert s0[0] == 0 and s0[2] == 0 and s0[1] == st[1]
         assert s0[1] + s0[3] == st[1] + st[2] + st[3]
     with pytest.raises(Exception):
         native.pnpoly_cells(vx, vy, 0, 4, 8)
+    with pytest.raises(Exception):
+        native.pnpoly_cells(vx, vy, 48, 48, 8)  # width not a multiple of 32
+
+
+def _cells_code(words, cell):
+    """2-bit codes from jt_pnpoly_cells' bit planes (word 2j: bit 0 of cells 32j.., 2j + 1: bit 1)."""
+    cell = np.asarray(cell, dtype=np.int64)
+    sh = (cell & 31).astype(np.uint32)
+    lo = (words[(cell >> 5) * 2] >> sh) & 1
+    hi = (words[(cell >> 5) * 2 + 1] >> sh) & 1
+    return (lo | (hi << 1)).astype(np.int64)
