@@ -294,10 +294,12 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: 
         if prob.roofline_kind == "issue":
             peak /= 2.0  # 1 lane-instruction slot per lane per clock, not 2 flop/FFMA
         out["roofline_frac"] = round(rate / peak, 4)
-    if name in ("pnpoly", "pnpoly_slab", "pnpoly_grid"):
+    if name in ("pnpoly", "pnpoly_slab", "pnpoly_grid", "pnpoly_cells"):
         out["edge_tests_per_s"] = round(prob.edge_tests / run.per_launch_s, 1)  # brute-force-equivalent
     if name == "pnpoly_grid":
         out["clean_cell_fraction"] = round(prob.clean_fraction(cfg["grid"]), 4)
+    if name == "pnpoly_cells":
+        out["decided_cell_fraction"] = round(prob.clean_fraction(cfg["grid"], cfg["lmax"]), 4)
     for b in prob.buffers.values():
         b.free()
     return out
@@ -456,7 +458,7 @@ def run_ours(args, dist: Dist) -> int:
     # per-kernel tuned summaries (time- and energy-optimal) on this rank's GPU
     per_kernel = {}
     if dist.rank == 0 and not args.quick:
-        for name in ("conv2d", "pnpoly", "pnpoly_slab", "pnpoly_grid", "sgemm", "sgemm_tf32"):
+        for name in ("conv2d", "pnpoly", "pnpoly_slab", "pnpoly_grid", "pnpoly_cells", "sgemm", "sgemm_tf32"):
             per_kernel[name] = {obj: measure_tuned(gpu, name, obj) for obj in ("time_optimal", "energy_optimal")}
 
     cpu = None

@@ -236,17 +236,18 @@ int jt_pnpoly_slabs(const float *vx, const float *vy, int n, int buckets, int pa
 int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, float *params, uint32_t *bits,
                    long long capacity, int *clean_cells);
 /* Per-cell edge lists over the same gw x gh raster and cell function as
- * jt_pnpoly_grid, for csrc/kernels/pnpoly_cells.cu (gw a multiple of 32). Per
- * cell a 2-bit code, stored as two bit planes per 32 cells of a row (word 2j:
- * code & 1 of cells 32j.., word 2j + 1: code >> 1; gw * gh / 16 words): 0 / 1 =
- * every edge's METHOD 2 test is constant over the cell and the answer is that
- * parity; 2 = the undecided edges are listed (heads[2 cell] = first entry,
- * heads[2 cell + 1] = count << 1 | parity of the always-true edges; entries are
- * float4 {slope, icpt, ylo, yhi} in `edges`); 3 = more than `lmax` undecided
- * edges (the kernel runs the exact slab search). Border cells (row 0, column 0,
- * where NaN coordinates land) with parity 1 are always listed. stats = {entries,
- * clean cells, listed cells, fallback cells}. bits or heads NULL: params and
- * stats only; edges NULL or too small: sizes only (JT_EINVAL if too small). */
+ * jt_pnpoly_grid, for csrc/kernels/pnpoly_cells.cu. Per cell a 2-bit code
+ * (16 cells per word, cell c at bits 2 (c % 16)): 0 / 1 = every edge's METHOD 2
+ * test is constant over the cell and the answer is that parity; 2 | base = some
+ * tests are undecided, base = the parity of the always-true ones, and the
+ * cell's 16-byte head (4 words at heads + 4 cell) holds the one undecided edge
+ * as float {slope, icpt, ylo, yhi}, or {first entry, count, NaN, 0} with the
+ * count undecided edges as float4 entries in `edges` from that entry on (count
+ * 0xffffffff: more than `lmax`, the kernel runs the exact slab search). Border
+ * cells (row 0, column 0, where NaN coordinates land) with base 1 are always
+ * undecided. stats = {entries, decided cells, listed cells, fallback cells}.
+ * bits or heads NULL: params and stats only; edges NULL or too small: sizes
+ * only (JT_EINVAL if too small). */
 int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int lmax, float *params, uint32_t *bits,
                     long long bits_capacity, uint32_t *heads, long long heads_capacity, float *edges,
                     long long edge_capacity, long long *stats);

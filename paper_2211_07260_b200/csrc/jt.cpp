@@ -15,6 +15,7 @@
 #include <time.h>
 
 #include <algorithm>
+#include <limits>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -1396,8 +1397,7 @@ int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int
     if (!vx || !vy || !params || n < 3) return fail(JT_EINVAL, "polygon needs >= 3 vertices");
     if (gw < 1 || gh < 1 || (long long)gw * gh > (1LL << 24)) return fail(JT_EINVAL, "bad grid %d x %d", gw, gh);
     if (lmax < 0 || lmax > (1 << 20)) return fail(JT_EINVAL, "bad list limit %d", lmax);
-    if (gw % 32) return fail(JT_EINVAL, "grid width %d is not a multiple of 32", gw);
-    const long long cells = (long long)gw * gh, words = cells / 16;
+    const long long cells = (long long)gw * gh, words = (cells + 15) / 16;
     std::vector<float> slope(n), icpt(n), ylo(n), yhi(n);
     float xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
     for (int k = 0; k < n; ++k) {
@@ -1417,11 +1417,11 @@ int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int
     const float ox = -xmin * sx, oy = -ymin * sy;
     params[0] = sx, params[1] = ox, params[2] = sy, params[3] = oy;
     const bool fill = bits && heads;
-    if (fill && (bits_capacity < words || heads_capacity < 2 * cells))
-        return fail(JT_EINVAL, "cell tables need %lld words and %lld heads", words, 2 * cells);
+    if (fill && (bits_capacity < words || heads_capacity < 4 * cells))
+        return fail(JT_EINVAL, "cell tables need %lld words and %lld head words", words, 4 * cells);
     if (fill) {
         std::memset(bits, 0, sizeof(uint32_t) * words);
-        std::memset(heads, 0, sizeof(uint32_t) * 2 * cells);
+        std::memset(heads, 0, sizeof(uint32_t) * 4 * cells);
     }
     std::vector<float> cx0(gw + 1), cy0(gh + 1);
     for (int k = 0; k <= gw; ++k) cx0[k] = k == 0 ? -INFINITY : cell_first(k, sx, ox, gw - 1);
@@ -1488,23 +1488,39 @@ int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int
             // NaN coordinates land in row 0 / column 0 and are never inside: a clean cell
             // there with base parity 1 is listed (with no edges) so the exact path answers
             const bool border = cx == 0 || cy == 0;
+            // codes: 0 / 1 decided (the answer); 2 | base undecided, with a 16-byte head: the
+            // one listed edge {slope, icpt, ylo, yhi}, or {first entry, count, NaN, 0} for 0 or
+            // >= 2 listed edges in `edges` (count 0xffffffff: over lmax, the slab search).
+            // No real edge has ylo NaN (NaN vertices are rejected).
             uint32_t code;
             if (list.empty() && !(border && base)) code = (uint32_t)base, ++n_clean;
-            else if ((int)list.size() <= lmax) {
-                code = 2, ++n_listed;
-                if (fill) heads[2 * cell] = (uint32_t)entries, heads[2 * cell + 1] = ((uint32_t)list.size() << 1) | base;
-                if (fill && edges && entries + (long long)list.size() <= edge_capacity)
-                    for (size_t i = 0; i < list.size(); ++i) {
-                        float *e = edges + 4 * (entries + (long long)i);
-                        const int k = list[i];
-                        e[0] = slope[k], e[1] = icpt[k], e[2] = ylo[k], e[3] = yhi[k];
+            else {
+                code = 2u | (uint32_t)base;
+                const bool over = (int)list.size() > lmax;
+                over ? ++n_fallback : ++n_listed;
+                uint32_t *h = fill ? heads + 4 * cell : nullptr;
+                if (!over && list.size() == 1) {
+                    const int k = list[0];
+                    const float e0[4] = {slope[k], icpt[k], ylo[k], yhi[k]};
+                    if (h) std::memcpy(h, e0, sizeof e0);
+                } else {
+                    const float nan = std::numeric_limits<float>::quiet_NaN();
+                    if (h) {
+                        h[0] = over ? 0u : (uint32_t)entries, h[1] = over ? 0xffffffffu : (uint32_t)list.size();
+                        std::memcpy(h + 2, &nan, 4), h[3] = 0;
                     }
-                entries += (long long)list.size();
-            } else code = 3, ++n_fallback;  // too many edges: the exact slab search
-            if (fill) {  // two bit planes per 32 cells of a row: answer / fallback, then undecided
-                bits[(cell >> 5) * 2] |= (code & 1u) << (cell & 31);
-                bits[(cell >> 5) * 2 + 1] |= (code >> 1) << (cell & 31);
+                    if (!over) {
+                        if (fill && edges && entries + (long long)list.size() <= edge_capacity)
+                            for (size_t i = 0; i < list.size(); ++i) {
+                                float *e = edges + 4 * (entries + (long long)i);
+                                const int k = list[i];
+                                e[0] = slope[k], e[1] = icpt[k], e[2] = ylo[k], e[3] = yhi[k];
+                            }
+                        entries += (long long)list.size();
+                    }
+                }
             }
+            if (fill) bits[cell >> 4] |= code << ((cell & 15) * 2);  // 16 cells per word
         }
     }
     if (entries > (1LL << 31)) return fail(JT_EINVAL, "cell lists need %lld entries", entries);

@@ -5,21 +5,27 @@
 // GRID x GRID raster over the polygon's bounding box: its METHOD 2 test is
 // false for every point of the cell, true for every point, or undecided. A
 // cell whose edges are all decided stores its parity (2 bits per cell, staged
-// in shared memory): on the benchmark polygon 92% of the points are answered
+// in shared memory): on the benchmark polygon 95% of the points are answered
 // by that one lookup. An undecided cell lists its undecided edges (1.3 on
-// average at GRID = 512) with the parity of the always-true ones; its points
-// are queued per warp and answered by base ^ their listed tests (two dependent
-// L2 reads: the cell head, then its edges). Cells with more than `lmax`
-// undecided edges fall back to the exact slab search of pnpoly_slab.cu.
+// average at GRID = 512); its points are queued per warp with their
+// coordinates and answered 32 at a time by base ^ their listed tests: one
+// 16-byte head read per point (the edge itself when there is one), more only
+// for cells with several. Cells with more than `lmax` undecided edges fall back
+// to the exact slab search of pnpoly_slab.cu.
 //
 // Memory side: two points per 16-byte load and two results per 8-byte store,
-// TILE pairs per thread in flight per chunk. The kernel is HBM bound
-// when the lookup path issues few enough instructions; 8 bytes read and 4
-// written per point are its algorithmic traffic.
+// TILE pairs per thread per chunk. The L1 pipe is the shared resource: the
+// random raster lookups' bank conflicts and the scattered reads / writes of
+// the queued points are what it spends its wavefronts on, so the queue carries
+// the points (no re-read) and a head answers most of them in one read.
 //
 // Tunables (-D): BLOCK_SIZE_X, TILE (point pairs per thread per chunk), GRID
 // (cells per side), GRID_SMEM (1: raster in shared memory; 0: read through L1),
-// STREAM (1: points loaded / results stored with the evict-first hints).
+// STREAM (1: points loaded / results stored with the evict-first hints), PREFETCH (chunks
+// ahead that one thread of the block pulls into L2 with cp.async.bulk.prefetch: the
+// block's points are one contiguous span per chunk, so the next chunk's HBM latency
+// overlaps this chunk's work without holding registers), REGPF (1: the next chunk's pairs
+// are loaded into registers before this chunk is classified).
 #ifndef BLOCK_SIZE_X
 #define BLOCK_SIZE_X 1024
 #endif
@@ -35,9 +41,15 @@
 #ifndef STREAM
 #define STREAM 0
 #endif
+#ifndef PREFETCH
+#define PREFETCH 1
+#endif
+#ifndef REGPF
+#define REGPF 0
+#endif
 #define CHUNK (BLOCK_SIZE_X * TILE)
-// ring slots per warp (a power of two): < 32 left after a drain + 32 pushed per pair step
-#define QCAP (TILE <= 3 ? 128 : 256)
+// ring slots per warp (a power of two): < 32 left after a drain + 64 pushed per pair step
+#define QCAP 128
 
 #if STREAM
 #define LOAD_PAIR(p) __ldcs(p)
@@ -53,7 +65,7 @@
 #define SLAB_PARAMS const float *__restrict__ table, int nu, int ng, int xb, float ybase, float yscale, \
     int guess_off, int xpar_off, int xst_off, int xlo_off, int pmax_off, int rec_off
 #define SLAB_ARGS table, nu, ng, xb, ybase, yscale, guess_off, xpar_off, xst_off, xlo_off, pmax_off, rec_off
-__device__ __forceinline__ int slab_search(float px, float py, SLAB_PARAMS) {
+__device__ __noinline__ int slab_search(float px, float py, SLAB_PARAMS) {  // rare: out of line
     if (!(px == px) || !(py == py)) return 0;  // NaN: every compare is false, never inside
     const float *u = table;
     int g = __float2int_rz(__fmul_rn(__fsub_rn(py, ybase), yscale));
@@ -80,127 +92,165 @@ __device__ __forceinline__ int slab_search(float px, float py, SLAB_PARAMS) {
     return in;
 }
 
-// A queued point: base parity ^ the listed edges' METHOD 2 tests (ylo <= py < yhi is the
-// y-test (vy_k > py) != (vy_j > py)), or the slab search for a code-3 cell.
-__device__ __forceinline__ int cell_search(float px, float py, unsigned cell, unsigned code,
-                                           const uint2 *__restrict__ heads, const float4 *__restrict__ edges,
+// A queued undecided point: base parity ^ the METHOD 2 tests of its cell's listed edges
+// (ylo <= py < yhi is the y-test (vy_k > py) != (vy_j > py)). The cell's 16-byte head is
+// its one listed edge, or {first entry, count, NaN, 0} (count ~0: the slab search).
+__device__ __forceinline__ int edge_test(float4 e, float px, float py) {
+    return (e.z <= py && py < e.w && px < __fmaf_rn(e.x, py, e.y)) ? 1 : 0;
+}
+__device__ __forceinline__ int cell_search(float px, float py, unsigned cell, int base,
+                                           const float4 *__restrict__ heads, const float4 *__restrict__ edges,
                                            SLAB_PARAMS) {
-    if (code == 3u) return slab_search(px, py, SLAB_ARGS);
     if (!(px == px) || !(py == py)) return 0;
-    const uint2 h = __ldg(heads + cell);
-    int in = h.y & 1;
-    const int cnt = h.y >> 1;
-    for (int k = 0; k < cnt; ++k) {
-        const float4 q = __ldg(edges + h.x + k);
-        in ^= (q.z <= py && py < q.w && px < __fmaf_rn(q.x, py, q.y)) ? 1 : 0;
-    }
+    const float4 h = __ldg(heads + cell);
+    if (h.z == h.z) return base ^ edge_test(h, px, py);
+    const unsigned first = __float_as_uint(h.x), cnt = __float_as_uint(h.y);
+    if (cnt == 0xffffffffu) return slab_search(px, py, SLAB_ARGS);
+    int in = base;
+#pragma unroll 1
+    for (unsigned k = 0; k < cnt; ++k) in ^= edge_test(__ldg(edges + first + k), px, py);
     return in;
 }
 
 // The host's cell function (jt_pnpoly_cells): min(f2u_rz(fma(v, s, o)), GRID - 1); cvt.rzi.u32
 // maps NaN and negatives to 0, so NaN lands in row / column 0 (whose decided cells hold 0).
-// The raster holds two bit planes per 32 cells of a row ({code & 1, code >> 1} words), so a
-// point's code is one 8-byte lookup and two rotates by cx (mod 32).
-struct Code {
-    unsigned lo, hi;  // bit 0: code & 1 (the answer, or the fallback flag), code >> 1 (undecided)
-};
+// The raster packs 16 cells per 32-bit word: one 4-byte shared load per point (random
+// cells: these lookups' bank conflicts are what the L1 pipe spends its wavefronts on, so a
+// single 32-bit load beats an 8-byte one) and a rotate by 2 cell (mod 32): bit 0 = code & 1
+// (the answer, or the fallback flag), bit 1 = undecided.
 #if GRID_SMEM
-#define GRID_PAIR(i) s_grid[i]
+#define GRID_WORD(i) s_grid[i]
 #else
-#define GRID_PAIR(i) __ldg(grid + (i))
+#define GRID_WORD(i) __ldg(grid + (i))
 #endif
-#define CODE_OF(px, py, out)                                                                 \
+#define CELL_OF(px, py)                                                                      \
     do {                                                                                     \
         const unsigned cx_ = min(__float2uint_rz(__fmaf_rn(px, gsx, gox)), GRID - 1u);        \
         const unsigned cy_ = min(__float2uint_rz(__fmaf_rn(py, gsy, goy)), GRID - 1u);        \
-        const uint2 w_ = GRID_PAIR(cy_ * (GRID / 32) + (cx_ >> 5));                           \
-        (out).lo = __funnelshift_r(w_.x, w_.x, cx_);                                          \
-        (out).hi = __funnelshift_r(w_.y, w_.y, cx_);                                          \
         cell_ = cy_ * GRID + cx_;                                                            \
     } while (0)
+#if PROBE_FLOOR  // measurement probe only (scripts/cells_floor.py): same loop, no lookup
+#define CODE_OF(px, py, out) ((out) = (px) < (py) ? 1u : 0u, cell_ = 0u)
+#else
+#define CODE_OF(px, py, out)                                                                 \
+    do {                                                                                     \
+        CELL_OF(px, py);                                                                     \
+        const unsigned w_ = GRID_WORD(cell_ >> 4);                                           \
+        (out) = __funnelshift_r(w_, w_, cell_ * 2u);                                         \
+    } while (0)
+#endif
+
+// pull chunk c's pairs (one contiguous span) into L2
+__device__ __forceinline__ void prefetch_chunk(const float4 *pairs, int c, int full) {
+    const long long q0 = (long long)c * CHUNK;
+    if (q0 >= full) return;
+    const long long q1 = min((long long)full, q0 + CHUNK);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pairs + q0), "r"((unsigned)((q1 - q0) * 16))
+                 : "memory");
+}
 
 // full occupancy (2048 threads per SM) needs <= 32 registers per thread
 extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X, 2048 / BLOCK_SIZE_X)
-pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, const uint2 *__restrict__ grid,
-             const uint2 *__restrict__ heads, const float4 *__restrict__ edges, float gsx, float gox, float gsy,
+pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, const unsigned *__restrict__ grid,
+             const float4 *__restrict__ heads, const float4 *__restrict__ edges, float gsx, float gox, float gsy,
              float goy, SLAB_PARAMS) {
     extern __shared__ __align__(16) unsigned smem[];
 #if GRID_SMEM
-    constexpr int GRID_PAIRS = GRID * GRID / 32;
-    uint2 *s_grid = reinterpret_cast<uint2 *>(smem);
-    int *ring = reinterpret_cast<int *>(smem + 2 * GRID_PAIRS) + (threadIdx.x >> 5) * QCAP;
-    for (int i = threadIdx.x; i < GRID_PAIRS / 2; i += BLOCK_SIZE_X)
+    constexpr int GRID_WORDS = (GRID * GRID + 15) / 16;
+    unsigned *s_grid = smem;
+    unsigned *rings = smem + ((GRID_WORDS + 3) & ~3);
+    for (int i = threadIdx.x; i < GRID_WORDS / 4; i += BLOCK_SIZE_X)
         reinterpret_cast<uint4 *>(s_grid)[i] = __ldg(reinterpret_cast<const uint4 *>(grid) + i);
+    for (int i = GRID_WORDS / 4 * 4 + threadIdx.x; i < GRID_WORDS; i += BLOCK_SIZE_X) s_grid[i] = __ldg(grid + i);
     __syncthreads();
 #else
-    int *ring = reinterpret_cast<int *>(smem) + (threadIdx.x >> 5) * QCAP;
+    unsigned *rings = smem;
 #endif
+    // per warp: QCAP undecided points {px, py} and their indices (bit 31: base parity)
+    float2 *ring_p = reinterpret_cast<float2 *>(rings) + (threadIdx.x >> 5) * QCAP;
+    int *ring_i = reinterpret_cast<int *>(rings + 2 * (BLOCK_SIZE_X / 32) * QCAP) + (threadIdx.x >> 5) * QCAP;
     const float4 *pairs = reinterpret_cast<const float4 *>(points);
     int2 *out = reinterpret_cast<int2 *>(bitmap);
     const int full = n >> 1, npairs = (n + 1) >> 1;  // pair q = points 2q, 2q + 1; an odd tail pair
     const int lane = threadIdx.x & 31;
     unsigned lanes_below;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_below));
-    // Per-warp ring of pairs with an undecided point: pushed at tail during a chunk, drained
-    // 32 at a time from head at its end (warp-uniform counters; < 32 left after a drain, so
-    // a chunk's <= 32 TILE pushes never reach the slots the last drain read). Nothing but
-    // loop counters is live across the drain: the chunk's loads are issued after it.
+    // The ring is pushed at tail and drained 32 points at a time from head (warp-uniform
+    // counters) after each pair step: < 32 are left after a drain, so a step's <= 64 pushes
+    // never reach the slots the last drain read.
     unsigned head = 0, tail = 0;
-    const int n_chunks = (npairs + CHUNK - 1) / CHUNK;
-    auto chunk = [&](int c, const bool FULL) {  // inlined twice with FULL constant
-        float4 cur[TILE];
-#pragma unroll
-        for (int t = 0; t < TILE; ++t) {
-            const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
-            if (FULL || q < full) cur[t] = LOAD_PAIR(pairs + q);
-            else if (q < npairs) {
-                const float2 p = points[2 * q];
-                cur[t] = make_float4(p.x, p.y, 0.f, 0.f);
-            } else cur[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int t = 0; t < TILE; ++t) {
-            const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
-            Code k0, k1;
-            unsigned cell_;
-            CODE_OF(cur[t].x, cur[t].y, k0);
-            CODE_OF(cur[t].z, cur[t].w, k1);
-            // decided points get their answer here; a pair with an undecided point is queued
-            // and both its points are rewritten by a later drain of the same warp
-            if (FULL || q < full) STORE_PAIR(out + q, make_int2((int)(k0.lo & 1u), (int)(k1.lo & 1u)));
-            else if (q < npairs) bitmap[2 * q] = (int)(k0.lo & 1u);
-            const bool slow = (FULL || q < npairs) && ((k0.hi | k1.hi) & 1u);
-            const unsigned need = __ballot_sync(0xffffffffu, slow);
-            if (slow) ring[(tail + __popc(need & lanes_below)) % QCAP] = q;
-            tail += __popc(need);
-        }
-    };
-    // one queued pair: both points redone, the undecided ones searched
-    auto drain = [&](int q) {
-        float4 v;
-        if (q < full) v = __ldg(pairs + q);
-        else { const float2 p = points[2 * q]; v = make_float4(p.x, p.y, 0.f, 0.f); }
-        Code k;
-        unsigned cell_;
-        CODE_OF(v.x, v.y, k);
-        const int r0 = (k.hi & 1u) ? cell_search(v.x, v.y, cell_, 2u | (k.lo & 1u), heads, edges, SLAB_ARGS)
-                                   : (int)(k.lo & 1u);
-        if (q < full) {
-            CODE_OF(v.z, v.w, k);
-            const int r1 = (k.hi & 1u) ? cell_search(v.z, v.w, cell_, 2u | (k.lo & 1u), heads, edges, SLAB_ARGS)
-                                       : (int)(k.lo & 1u);
-            out[q] = make_int2(r0, r1);
-        } else bitmap[2 * q] = r0;
-    };
-    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-        if ((c + 1) * CHUNK <= full) chunk(c, true);
-        else chunk(c, false);
+    auto drain = [&]() {
         __syncwarp();
         while (tail - head >= 32u) {
-            const int q = ring[(head + lane) % QCAP];
+            const float2 e = ring_p[(head + lane) % QCAP];
+            const int i = ring_i[(head + lane) % QCAP];
             head += 32;
-            drain(q);
+            unsigned cell_;
+            CELL_OF(e.x, e.y);
+            bitmap[i & 0x7fffffff] = cell_search(e.x, e.y, cell_, (int)((unsigned)i >> 31), heads, edges, SLAB_ARGS);
         }
+    };
+    const int n_chunks = (npairs + CHUNK - 1) / CHUNK;
+    auto load = [&](int c, float4 *v) {
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) {
+            const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
+            if (c < n_chunks && q < full) v[t] = LOAD_PAIR(pairs + q);
+            else if (c < n_chunks && q < npairs) {
+                const float2 p = points[2 * q];
+                v[t] = make_float4(p.x, p.y, 0.f, 0.f);
+            } else v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    auto chunk = [&](int c, const float4 *cur, const bool FULL) {  // inlined twice with FULL constant
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) {
+            const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
+            unsigned k0, k1, cell_;
+            CODE_OF(cur[t].x, cur[t].y, k0);
+            CODE_OF(cur[t].z, cur[t].w, k1);
+            // decided points get their answer here; undecided ones a placeholder, rewritten
+            // by a later drain of the same warp
+            if (FULL || q < full) STORE_PAIR(out + q, make_int2((int)(k0 & 1u), (int)(k1 & 1u)));
+            else if (q < npairs) bitmap[2 * q] = (int)(k0 & 1u);
+            const bool s0 = (FULL || q < npairs) && (k0 & 2u), s1 = (FULL || q < full) && (k1 & 2u);
+            const unsigned need0 = __ballot_sync(0xffffffffu, s0), need1 = __ballot_sync(0xffffffffu, s1);
+            const unsigned p0 = (tail + __popc(need0 & lanes_below)) % QCAP, t1 = tail + __popc(need0);
+            const unsigned p1 = (t1 + __popc(need1 & lanes_below)) % QCAP;
+            if (s0) ring_p[p0] = make_float2(cur[t].x, cur[t].y), ring_i[p0] = (2 * q) | (int)(k0 << 31);
+            if (s1) ring_p[p1] = make_float2(cur[t].z, cur[t].w), ring_i[p1] = (2 * q + 1) | (int)(k1 << 31);
+            tail = t1 + __popc(need1);
+            drain();
+        }
+    };
+#if PREFETCH
+    if (threadIdx.x == 0)
+        for (int a = 1; a <= PREFETCH; ++a) prefetch_chunk(pairs, blockIdx.x + a * gridDim.x, full);
+#endif
+#if REGPF
+    float4 nxt[TILE];  // the next chunk, loaded while this one is classified
+    load(blockIdx.x, nxt);
+#endif
+    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+#if PREFETCH
+        if (threadIdx.x == 0) prefetch_chunk(pairs, c + (PREFETCH + 1) * gridDim.x, full);
+#endif
+        float4 cur[TILE];
+#if REGPF
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) cur[t] = nxt[t];
+        load(c + gridDim.x, nxt);
+#else
+        load(c, cur);
+#endif
+        if ((c + 1) * CHUNK <= full) chunk(c, cur, true);
+        else chunk(c, cur, false);
     }
-    if (lane < tail - head) drain(ring[(head + lane) % QCAP]);  // the warp's leftovers
+    if (lane < tail - head) {  // the warp's leftovers
+        const float2 e = ring_p[(head + lane) % QCAP];
+        const int i = ring_i[(head + lane) % QCAP];
+        unsigned cell_;
+        CELL_OF(e.x, e.y);
+        bitmap[i & 0x7fffffff] = cell_search(e.x, e.y, cell_, (int)((unsigned)i >> 31), heads, edges, SLAB_ARGS);
+    }
 }

@@ -648,19 +648,22 @@ class PnPolyCellsProblem(PnPolyGridProblem):
             "grid_smem": [0, 1],
             "lmax": [4, 16],
             "stream": [0, 1],
+            "prefetch": [0, 1, 2],
+            "regpf": [0, 1],
         }
 
     def restrictions(self):
-        # ring: 128 int slots per warp for tile <= 3, 256 for tile 4 (QCAP in pnpoly_cells.cu)
-        return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * 512 * (1 + tile // 4)) <= {227 * 1024}"]
+        # ring: 128 x 12-byte slots per warp (QCAP in pnpoly_cells.cu)
+        return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * 1536) <= {227 * 1024}"]
 
     def default_config(self):
-        return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0}
+        return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0, "prefetch": 1, "regpf": 0}
 
     def defines(self, config):
         c = _as_dict(config)
         return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"],
-                "GRID_SMEM": c.get("grid_smem", 1), "STREAM": c.get("stream", 0)}
+                "GRID_SMEM": c.get("grid_smem", 1), "STREAM": c.get("stream", 0), "PREFETCH": c.get("prefetch", 0),
+                "REGPF": c.get("regpf", 0)}
 
     def cell_table(self, g: int, lmax: int):
         cache = self.__dict__.setdefault("_cell_tables", {})
@@ -671,9 +674,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
 
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
-        words = c["grid"] * c["grid"] // 16 if c.get("grid_smem", 1) else 0
-        ring = 128 if c["tile"] <= 3 else 256
-        return words * 4 + c["block_size_x"] // 32 * ring * 4
+        words = (c["grid"] * c["grid"] + 15) // 16 if c.get("grid_smem", 1) else 0
+        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * 128 * 12
 
     def launch(self, config, n_points: int | None = None):
         c = _as_dict(config)
@@ -713,8 +715,7 @@ class PnPolyCellsProblem(PnPolyGridProblem):
             return np.clip(k, 0, g - 1).astype(np.int64)
 
         idx = cell(pts[:, 1], prm[2], prm[3]) * g + cell(pts[:, 0], prm[0], prm[1])
-        undecided = (words[(idx >> 5) * 2 + 1] >> (idx & 31).astype(np.uint32)) & 1
-        return float((undecided == 0).mean())
+        return float((((words[idx >> 4] >> ((idx & 15) * 2).astype(np.uint32)) & 3) < 2).mean())
 
 
 # -- Conv2D -------------------------------------------------------------------------------

@@ -400,7 +400,7 @@ def pnpoly_grid(vx, vy, gw: int, gh: int):
 
 def pnpoly_cells(vx, vy, gw: int, gh: int, lmax: int):
     """Per-cell edge lists for csrc/kernels/pnpoly_cells.cu (libjt ``jt_pnpoly_cells``): returns
-    (uint32 words: two bit planes per 32 cells), params {sx, ox, sy, oy}, uint32 heads (2 per cell),
+    (uint32 words, 2-bit codes, 16 cells per word), params {sx, ox, sy, oy}, uint32 heads (4 per cell),
     float32 edge entries (k, 4) and stats {entries, clean, listed, fallback}."""
     import numpy as np
 
@@ -410,8 +410,8 @@ def pnpoly_cells(vx, vy, gw: int, gh: int, lmax: int):
     stats = np.zeros(4, dtype=np.int64)
     args = (vx.ctypes.data, vy.ctypes.data, vx.size, int(gw), int(gh), int(lmax), params.ctypes.data)
     check(lib().jt_pnpoly_cells(*args, None, 0, None, 0, None, 0, stats.ctypes.data), "jt_pnpoly_cells")
-    words = np.zeros(max(1, gw * gh // 16), dtype=np.uint32)
-    heads = np.zeros(2 * gw * gh, dtype=np.uint32)
+    words = np.zeros((gw * gh + 15) // 16, dtype=np.uint32)
+    heads = np.zeros(4 * gw * gh, dtype=np.uint32)
     edges = np.zeros((max(1, int(stats[0])), 4), dtype=np.float32)
     check(lib().jt_pnpoly_cells(*args, words.ctypes.data, words.size, heads.ctypes.data, heads.size,
                                 edges.ctypes.data, edges.shape[0], stats.ctypes.data), "jt_pnpoly_cells")

@@ -235,9 +235,10 @@ def pnpoly(points: np.ndarray, vx: np.ndarray, vy: np.ndarray, *, config=None, o
     ``algorithm``: "brute" tests every edge (pnpoly.cu, the paper's kernel);
     "slab" locates each point's y-slab and x-position first (pnpoly_slab.cu);
     "grid" answers points in provably clean cells with one lookup and runs the
-    slab search for the rest (pnpoly_grid.cu). All three give the brute-force
-    METHOD 2 bitmap bit for bit."""
-    names = {"brute": "pnpoly", "slab": "pnpoly_slab", "grid": "pnpoly_grid"}
+    slab search for the rest (pnpoly_grid.cu); "cells" answers the rest from
+    per-cell lists of the few undecided edges (pnpoly_cells.cu). All four give
+    the brute-force METHOD 2 bitmap bit for bit."""
+    names = {"brute": "pnpoly", "slab": "pnpoly_slab", "grid": "pnpoly_grid", "cells": "pnpoly_cells"}
     if algorithm not in names:
         raise ValueError(f"algorithm must be one of {sorted(names)}, not {algorithm!r}")
     points = np.asarray(points, dtype=np.float32)

@@ -59,7 +59,7 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
             "restrictions": [],
         }
         return doc, "exhaustive", None
-    if name in ("conv2d", "sgemm_tf32", "pnpoly_slab", "pnpoly_grid"):
+    if name in ("conv2d", "sgemm_tf32", "pnpoly_slab", "pnpoly_grid", "pnpoly_cells"):
         return problem.space_document(), "exhaustive", None
     if name == "sgemm":
         doc = {
@@ -88,7 +88,7 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
 def oracle_check(problem, cfg) -> tuple[bool, float]:
     out = problem.fetch_output()
     inp = problem.inputs
-    if problem.name in ("pnpoly", "pnpoly_slab", "pnpoly_grid"):
+    if problem.name in ("pnpoly", "pnpoly_slab", "pnpoly_grid", "pnpoly_cells"):
         want = O.pnpoly(inp["points"], inp["vx"], inp["vy"], problem.formula(cfg))
         bad = int((out != want).sum())
         return bad == 0, float(bad)

@@ -274,11 +274,11 @@ def test_grid_full_size_matches_brute_force(gpu):
 
 # -- per-cell edge lists (csrc/kernels/pnpoly_cells.cu) --------------------------------------
 
-CELLS_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stream=st)
-                  for b, t, g, l, st in itertools.product((256, 1024), (1, 2, 4), (256, 512), (4, 16), (0, 1))
-                  if not (b == 1024 and t == 4)]
-                 + [dict(block_size_x=b, tile=2, grid=g, grid_smem=0, lmax=16, stream=0)
-                    for b, g in itertools.product((256, 1024), (512, 1024))])
+CELLS_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stream=st, prefetch=(b + t + st) % 3,
+                       regpf=(t + l) % 2)
+                  for b, t, g, l, st in itertools.product((256, 1024), (1, 2, 4), (256, 512), (4, 16), (0, 1))]
+                 + [dict(block_size_x=b, tile=2, grid=g, grid_smem=0, lmax=16, stream=0, prefetch=pf, regpf=pf // 2)
+                    for b, g, pf in itertools.product((256, 1024), (512, 1024), (0, 2))])
 
 
 @pytest.fixture(scope="module")

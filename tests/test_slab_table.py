@@ -292,7 +292,7 @@ def _polygon(name):
 
 
 @pytest.mark.parametrize("name", sorted(POLYGONS))
-@pytest.mark.parametrize("g,lmax", [(32, 8), (64, 2), (512, 8)])
+@pytest.mark.parametrize("g,lmax", [(7, 8), (64, 2), (512, 8)])
 def test_cell_lists_give_the_brute_force_answer(name, g, lmax):
     """jt_pnpoly_cells: the pnpoly_cells.cu decision, emulated - code 0 / 1 is the answer,
     code 2 is the base parity XOR the listed edges' METHOD 2 tests (libm fmaf, NaN -> 0) -
@@ -307,20 +307,29 @@ def test_cell_lists_give_the_brute_force_answer(name, g, lmax):
     code = _cells_code(words, cell)
     want = O.pnpoly(pts, vx, vy, 2)
     got = np.where(code < 2, code, 0).astype(np.int32)
-    for i in np.nonzero(code == 2)[0]:
+    fallback = np.zeros(len(pts), dtype=bool)
+    for i in np.nonzero(code >= 2)[0]:
         px, py = float(pts[i, 0]), float(pts[i, 1])
         if px != px or py != py:
             continue
-        c = int(cell[i])
-        r = int(heads[2 * c + 1]) & 1
-        for e in edges[heads[2 * c]: heads[2 * c] + (int(heads[2 * c + 1]) >> 1)]:
+        h = heads[4 * int(cell[i]): 4 * int(cell[i]) + 4]
+        hf = h.view(np.float32)
+        if hf[2] == hf[2]:
+            listed = [hf]
+        elif h[1] == 0xFFFFFFFF:
+            fallback[i] = True
+            continue
+        else:
+            listed = list(edges[h[0]: h[0] + h[1]])
+        r = int(code[i]) & 1
+        for e in listed:
             if e[2] <= py < e[3] and px < _libm.fmaf(float(e[0]), py, float(e[1])):
                 r ^= 1
         got[i] = r
-    keep = code != 3
+    keep = ~fallback
     assert np.array_equal(got[keep], want[keep]), (name, int((got[keep] != want[keep]).sum()))
     if name == "benchmark" and g == 512:
-        assert (code < 2).mean() > 0.8 and (code == 3).mean() < 0.01
+        assert (code < 2).mean() > 0.8 and fallback.mean() < 0.01
 
 
 @pytest.mark.parametrize("name", sorted(POLYGONS))
@@ -328,24 +337,24 @@ def test_cell_lists_border_and_limits(name):
     """NaN lands in row 0 / column 0: clean cells there hold 0. lmax 0 sends every undecided
     cell to the slab search (code 3) and lists nothing; the clean cells equal jt_pnpoly_grid's."""
     vx, vy = _polygon(name)
-    for g in (32, 256):
+    for g in (7, 256):
         words, _, _, _, st = native.pnpoly_cells(vx, vy, g, g, 8)
         for k in range(g):
             for c in (k * g, k):
                 assert _cells_code(words, np.array([c]))[0] != 1, (name, g, k)
-        w0, _, _, e0, s0 = native.pnpoly_cells(vx, vy, g, g, 0)
-        assert s0[0] == 0 and s0[2] == 0 and s0[1] == st[1]
-        assert s0[1] + s0[3] == st[1] + st[2] + st[3]
+        w0, _, h0, e0, s0 = native.pnpoly_cells(vx, vy, g, g, 0)
+        assert s0[0] == 0 and s0[1] == st[1]
+        assert s0[1] + s0[2] + s0[3] == st[1] + st[2] + st[3]
+        # lmax 0: no head holds an edge; only the edge-less (border, base 1) cells are listed
+        und = _cells_code(w0, np.arange(g * g)) >= 2
+        hf = h0.reshape(-1, 4)
+        assert np.all(np.isnan(hf[und].view(np.float32)[:, 2]))
+        assert np.all((hf[und, 1] == 0xFFFFFFFF) | (hf[und, 1] == 0))
     with pytest.raises(Exception):
         native.pnpoly_cells(vx, vy, 0, 4, 8)
-    with pytest.raises(Exception):
-        native.pnpoly_cells(vx, vy, 48, 48, 8)  # width not a multiple of 32
 
 
 def _cells_code(words, cell):
-    """2-bit codes from jt_pnpoly_cells' bit planes (word 2j: bit 0 of cells 32j.., 2j + 1: bit 1)."""
+    """2-bit codes from jt_pnpoly_cells' raster (16 cells per word)."""
     cell = np.asarray(cell, dtype=np.int64)
-    sh = (cell & 31).astype(np.uint32)
-    lo = (words[(cell >> 5) * 2] >> sh) & 1
-    hi = (words[(cell >> 5) * 2 + 1] >> sh) & 1
-    return (lo | (hi << 1)).astype(np.int64)
+    return ((words[cell >> 4] >> ((cell & 15) * 2).astype(np.uint32)) & 3).astype(np.int64)
