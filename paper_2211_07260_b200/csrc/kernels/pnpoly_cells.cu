@@ -25,7 +25,9 @@
 // ahead that one thread of the block pulls into L2 with cp.async.bulk.prefetch: the
 // block's points are one contiguous span per chunk, so the next chunk's HBM latency
 // overlaps this chunk's work without holding registers), REGPF (1: the next chunk's pairs
-// are loaded into registers before this chunk is classified).
+// are loaded into registers before this chunk is classified). Tried and dropped: a
+// 2-4 stage shared-memory ring filled by cp.async.bulk from one producer thread (67 us
+// and up: the producer waits for every warp to free a stage, which couples the warps).
 #ifndef BLOCK_SIZE_X
 #define BLOCK_SIZE_X 1024
 #endif
@@ -155,6 +157,13 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
              const float4 *__restrict__ heads, const float4 *__restrict__ edges, float gsx, float gox, float gsy,
              float goy, SLAB_PARAMS) {
     extern __shared__ __align__(16) unsigned smem[];
+    const float4 *pairs = reinterpret_cast<const float4 *>(points);
+    const int full = n >> 1, npairs = (n + 1) >> 1;  // pair q = points 2q, 2q + 1; an odd tail pair
+#if PREFETCH
+    // this block's first chunks head for L2 while the raster is staged
+    if (threadIdx.x == 0)
+        for (int a = 0; a <= PREFETCH; ++a) prefetch_chunk(pairs, blockIdx.x + a * gridDim.x, full);
+#endif
 #if GRID_SMEM
     constexpr int GRID_WORDS = (GRID * GRID + 15) / 16;
     unsigned *s_grid = smem;
@@ -169,9 +178,7 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
     // per warp: QCAP undecided points {px, py} and their indices (bit 31: base parity)
     float2 *ring_p = reinterpret_cast<float2 *>(rings) + (threadIdx.x >> 5) * QCAP;
     int *ring_i = reinterpret_cast<int *>(rings + 2 * (BLOCK_SIZE_X / 32) * QCAP) + (threadIdx.x >> 5) * QCAP;
-    const float4 *pairs = reinterpret_cast<const float4 *>(points);
     int2 *out = reinterpret_cast<int2 *>(bitmap);
-    const int full = n >> 1, npairs = (n + 1) >> 1;  // pair q = points 2q, 2q + 1; an odd tail pair
     const int lane = threadIdx.x & 31;
     unsigned lanes_below;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_below));
@@ -223,10 +230,6 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
             drain();
         }
     };
-#if PREFETCH
-    if (threadIdx.x == 0)
-        for (int a = 1; a <= PREFETCH; ++a) prefetch_chunk(pairs, blockIdx.x + a * gridDim.x, full);
-#endif
 #if REGPF
     float4 nxt[TILE];  // the next chunk, loaded while this one is classified
     load(blockIdx.x, nxt);
