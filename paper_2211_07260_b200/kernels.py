@@ -694,9 +694,11 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         g, lmax = c["grid"], c["lmax"]
         key = f"cells{g}x{lmax}"
         words, params, heads, edges, _ = self.cell_table(g, lmax)
-        if key not in self.buffers:
-            self.buffers[key] = (self.gpu.array(words), self.gpu.array(heads), self.gpu.array(edges))
-        bw, bh, be = self.buffers[key]
+        if key + "w" not in self.buffers:  # one entry per device buffer (buffers are freed one by one)
+            self.buffers[key + "w"] = self.gpu.array(words)
+            self.buffers[key + "h"] = self.gpu.array(heads)
+            self.buffers[key + "e"] = self.gpu.array(edges)
+        bw, bh, be = (self.buffers[key + x] for x in "whe")
         info = self.slab_info(1024, 16)
         return [bw, bh, be, f32(params[0]), f32(params[1]), f32(params[2]), f32(params[3]),
                 self._table_buffer(1024, 16), i32(info.nu), i32(info.ng), i32(info.xb),
