@@ -51,7 +51,14 @@
 #endif
 #define CHUNK (BLOCK_SIZE_X * TILE)
 // ring slots per warp (a power of two): < 32 left after a drain + 64 pushed per pair step
+#ifndef ADRAIN
+#define ADRAIN 1
+#endif
+#if ADRAIN
+#define QCAP 64  // drained after each point push: < 32 + 32
+#else
 #define QCAP 128
+#endif
 
 #if STREAM
 #define LOAD_PAIR(p) __ldcs(p)
@@ -100,6 +107,17 @@ __device__ __noinline__ int slab_search(float px, float py, SLAB_PARAMS) {  // r
 __device__ __forceinline__ int edge_test(float4 e, float px, float py) {
     return (e.z <= py && py < e.w && px < __fmaf_rn(e.x, py, e.y)) ? 1 : 0;
 }
+__device__ __forceinline__ int resolve(float px, float py, int base, float4 h, const float4 *__restrict__ edges,
+                                       SLAB_PARAMS) {
+    if (!(px == px) || !(py == py)) return 0;
+    if (h.z == h.z) return base ^ edge_test(h, px, py);
+    const unsigned first = __float_as_uint(h.x), cnt = __float_as_uint(h.y);
+    if (cnt == 0xffffffffu) return slab_search(px, py, SLAB_ARGS);
+    int in = base;
+#pragma unroll 1
+    for (unsigned k = 0; k < cnt; ++k) in ^= edge_test(__ldg(edges + first + k), px, py);
+    return in;
+}
 __device__ __forceinline__ int cell_search(float px, float py, unsigned cell, int base,
                                            const float4 *__restrict__ heads, const float4 *__restrict__ edges,
                                            SLAB_PARAMS) {
@@ -131,7 +149,7 @@ __device__ __forceinline__ int cell_search(float px, float py, unsigned cell, in
         const unsigned cy_ = min(__float2uint_rz(__fmaf_rn(py, gsy, goy)), GRID - 1u);        \
         cell_ = cy_ * GRID + cx_;                                                            \
     } while (0)
-#if PROBE_FLOOR  // measurement probe only (scripts/cells_floor.py): same loop, no lookup
+#if PROBE_FLOOR == 1  // measurement probes only (scripts/cells_floor.py): 1 = same loop, no lookup
 #define CODE_OF(px, py, out) ((out) = (px) < (py) ? 1u : 0u, cell_ = 0u)
 #else
 #define CODE_OF(px, py, out)                                                                 \
@@ -149,6 +167,24 @@ __device__ __forceinline__ void prefetch_chunk(const float4 *pairs, int c, int f
     const long long q1 = min((long long)full, q0 + CHUNK);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pairs + q0), "r"((unsigned)((q1 - q0) * 16))
                  : "memory");
+}
+// the same from one thread without a branch: predicated on `issue` (and on the chunk
+// holding full pairs); the size is clamped to the pairs left
+__device__ __forceinline__ void prefetch_chunk_if(bool issue, const float4 *pairs, int c, int full) {
+    const int q0 = c * CHUNK;
+    const int left = max(min(full - q0, CHUNK), 0);
+    const unsigned go = (issue && left > 0) ? 1u : 0u;
+    asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %2, 0;\n"
+                 "@p cp.async.bulk.prefetch.L2.global [%0], %1;\n}" ::"l"(pairs + q0), "r"(left * 16), "r"(go)
+                 : "memory");
+}
+
+// warp ballot of (v != 0)
+__device__ __forceinline__ unsigned ballot_nz(unsigned v) {
+    unsigned m;
+    asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %1, 0;\nvote.sync.ballot.b32 %0, p, 0xffffffff;\n}"
+                 : "=r"(m) : "r"(v));
+    return m;
 }
 
 // full occupancy (2048 threads per SM) needs <= 32 registers per thread
@@ -186,6 +222,37 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
     // counters) after each pair step: < 32 are left after a drain, so a step's <= 64 pushes
     // never reach the slots the last drain read.
     unsigned head = 0, tail = 0;
+#if ADRAIN
+    // Drains are split in two so the head read's L2 latency overlaps the next chunks: a
+    // batch of 32 takes its points into registers and starts a 16-byte cp.async of each
+    // point's cell head into a per-lane slot; the batch is finished (test, store) when the
+    // next one starts, or at the end. One batch is pending once any has started (head > 0).
+    float4 *hslot = reinterpret_cast<float4 *>(rings + 3 * (BLOCK_SIZE_X / 32) * QCAP) + threadIdx.x;
+    float apx = 0.f, apy = 0.f;
+    int aidx = 0;
+    auto finish = [&]() {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        bitmap[aidx & 0x7fffffff] = resolve(apx, apy, (int)((unsigned)aidx >> 31), *hslot, edges, SLAB_ARGS);
+    };
+    auto drain = [&]() {
+        __syncwarp();
+#if PROBE_FLOOR == 3  // 3 = pushes, the drained points dropped
+        while (tail - head >= 32u) head += 32;
+        return;
+#endif
+        while (tail - head >= 32u) {
+            if (head) finish();
+            const float2 e = ring_p[(head + lane) % QCAP];
+            aidx = ring_i[(head + lane) % QCAP];
+            apx = e.x, apy = e.y;
+            head += 32;
+            unsigned cell_;
+            CELL_OF(apx, apy);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\ncp.async.commit_group;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(hslot)), "l"(heads + cell_) : "memory");
+        }
+    };
+#else
     auto drain = [&]() {
         __syncwarp();
         while (tail - head >= 32u) {
@@ -197,6 +264,7 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
             bitmap[i & 0x7fffffff] = cell_search(e.x, e.y, cell_, (int)((unsigned)i >> 31), heads, edges, SLAB_ARGS);
         }
     };
+#endif
     const int n_chunks = (npairs + CHUNK - 1) / CHUNK;
     auto load = [&](int c, float4 *v) {
 #pragma unroll
@@ -220,14 +288,30 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
             // by a later drain of the same warp
             if (FULL || q < full) STORE_PAIR(out + q, make_int2((int)(k0 & 1u), (int)(k1 & 1u)));
             else if (q < npairs) bitmap[2 * q] = (int)(k0 & 1u);
-            const bool s0 = (FULL || q < npairs) && (k0 & 2u), s1 = (FULL || q < full) && (k1 & 2u);
-            const unsigned need0 = __ballot_sync(0xffffffffu, s0), need1 = __ballot_sync(0xffffffffu, s1);
+#if PROBE_FLOOR == 2  // 2 = lookups, nothing queued
+            const unsigned u0 = 0u, u1 = 0u;
+#else
+            const unsigned u0 = (FULL || q < npairs) ? (k0 & 2u) : 0u, u1 = (FULL || q < full) ? (k1 & 2u) : 0u;
+#endif
+            const bool s0 = u0 != 0u, s1 = u1 != 0u;
+            const unsigned need0 = ballot_nz(u0), need1 = ballot_nz(u1);
+#if ADRAIN  // drain after each point's push: the ring holds < 32 + 32
+            const unsigned p0 = (tail + __popc(need0 & lanes_below)) % QCAP;
+            if (s0) ring_p[p0] = make_float2(cur[t].x, cur[t].y), ring_i[p0] = (2 * q) | (int)(k0 << 31);
+            tail += __popc(need0);
+            drain();
+            const unsigned p1 = (tail + __popc(need1 & lanes_below)) % QCAP;
+            if (s1) ring_p[p1] = make_float2(cur[t].z, cur[t].w), ring_i[p1] = (2 * q + 1) | (int)(k1 << 31);
+            tail += __popc(need1);
+            drain();
+#else
             const unsigned p0 = (tail + __popc(need0 & lanes_below)) % QCAP, t1 = tail + __popc(need0);
             const unsigned p1 = (t1 + __popc(need1 & lanes_below)) % QCAP;
             if (s0) ring_p[p0] = make_float2(cur[t].x, cur[t].y), ring_i[p0] = (2 * q) | (int)(k0 << 31);
             if (s1) ring_p[p1] = make_float2(cur[t].z, cur[t].w), ring_i[p1] = (2 * q + 1) | (int)(k1 << 31);
             tail = t1 + __popc(need1);
             drain();
+#endif
         }
     };
 #if REGPF
@@ -236,7 +320,7 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #endif
     for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
 #if PREFETCH
-        if (threadIdx.x == 0) prefetch_chunk(pairs, c + (PREFETCH + 1) * gridDim.x, full);
+        prefetch_chunk_if(threadIdx.x == 0, pairs, c + (PREFETCH + 1) * gridDim.x, full);
 #endif
         float4 cur[TILE];
 #if REGPF
@@ -249,6 +333,11 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
         if ((c + 1) * CHUNK <= full) chunk(c, cur, true);
         else chunk(c, cur, false);
     }
+#if ADRAIN
+#if PROBE_FLOOR != 3
+    if (head) finish();
+#endif
+#endif
     if (lane < tail - head) {  // the warp's leftovers
         const float2 e = ring_p[(head + lane) % QCAP];
         const int i = ring_i[(head + lane) % QCAP];

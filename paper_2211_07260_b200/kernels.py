@@ -650,20 +650,24 @@ class PnPolyCellsProblem(PnPolyGridProblem):
             "stream": [0, 1],
             "prefetch": [0, 1, 2],
             "regpf": [0, 1],
+            "adrain": [0, 1],
         }
 
     def restrictions(self):
-        # ring: 128 x 12-byte slots per warp (QCAP in pnpoly_cells.cu)
-        return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * 1536) <= {227 * 1024}"]
+        # ring: 128 x 12-byte slots per warp, or 64 + a 16-byte head slot per thread with
+        # the split drain (QCAP in pnpoly_cells.cu)
+        return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * (1536 - 768 * adrain) + "
+                f"16 * block_size_x * adrain) <= {227 * 1024}"]
 
     def default_config(self):
-        return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0, "prefetch": 1, "regpf": 0}
+        return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0, "prefetch": 1, "regpf": 0,
+                "adrain": 1}
 
     def defines(self, config):
         c = _as_dict(config)
         return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"],
                 "GRID_SMEM": c.get("grid_smem", 1), "STREAM": c.get("stream", 0), "PREFETCH": c.get("prefetch", 0),
-                "REGPF": c.get("regpf", 0)}
+                "REGPF": c.get("regpf", 0), "ADRAIN": c.get("adrain", 0)}
 
     def cell_table(self, g: int, lmax: int):
         cache = self.__dict__.setdefault("_cell_tables", {})
@@ -675,7 +679,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
         words = (c["grid"] * c["grid"] + 15) // 16 if c.get("grid_smem", 1) else 0
-        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * 128 * 12
+        ad = c.get("adrain", 0)
+        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * (64 if ad else 128) * 12 + 16 * c["block_size_x"] * ad
 
     def launch(self, config, n_points: int | None = None):
         c = _as_dict(config)
