@@ -240,16 +240,17 @@ int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, floa
  * (16 cells per word, cell c at bits 2 (c % 16)): 0 / 1 = every edge's METHOD 2
  * test is constant over the cell and the answer is that parity; 2 | base = some
  * tests are undecided, base = the parity of the always-true ones, and the
- * cell's 16-byte head (4 words at heads + 4 cell) holds the one undecided edge
- * as float {slope, icpt, ylo, yhi}, or {first entry, count, NaN, 0} with the
- * count undecided edges as float4 entries in `edges` from that entry on (count
- * 0xffffffff: more than `lmax`, the kernel runs the exact slab search). Border
- * cells (row 0, column 0, where NaN coordinates land) with base 1 are always
- * undecided. stats = {entries, decided cells, listed cells, fallback cells}.
- * bits or heads NULL: params and stats only; edges NULL or too small: sizes
- * only (JT_EINVAL if too small). */
-int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int lmax, float *params, uint32_t *bits,
-                    long long bits_capacity, uint32_t *heads, long long heads_capacity, float *edges,
+ * cell's head (head_words = 4 or 8 words at heads + head_words cell) holds the
+ * undecided edges in place when there are 1 .. head_words / 4 of them (float
+ * {slope, icpt, ylo, yhi} each; an unused slot is {0, 0, NaN, 0}, never true),
+ * else {first entry, count, NaN, 0} with the count undecided edges as float4
+ * entries in `edges` from that entry on (count 0xffffffff: more than `lmax`,
+ * the kernel runs the exact slab search). Border cells (row 0, column 0, where
+ * NaN coordinates land) with base 1 are always undecided. stats = {entries,
+ * decided cells, listed cells, fallback cells}. bits or heads NULL: params and
+ * stats only; edges NULL or too small: sizes only (JT_EINVAL if too small). */
+int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int lmax, int head_words, float *params,
+                    uint32_t *bits, long long bits_capacity, uint32_t *heads, long long heads_capacity, float *edges,
                     long long edge_capacity, long long *stats);
 
 /* TMA descriptor (CUtensorMap, 128 bytes written to out128) for a row-major

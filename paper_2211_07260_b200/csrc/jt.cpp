@@ -1391,12 +1391,14 @@ int jt_pnpoly_grid(const float *vx, const float *vy, int n, int gw, int gh, floa
 // py, so its range over a py interval comes from the interval's ends. The always-true
 // edges give the cell's base parity, the undecided ones are listed; a point's answer is
 // base ^ the XOR of its listed edges' tests, which is the brute-force XOR over all edges.
-int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int lmax, float *params, uint32_t *bits,
-                    long long bits_capacity, uint32_t *heads, long long heads_capacity, float *edges,
+int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int lmax, int head_words, float *params,
+                    uint32_t *bits, long long bits_capacity, uint32_t *heads, long long heads_capacity, float *edges,
                     long long edge_capacity, long long *stats) {
     if (!vx || !vy || !params || n < 3) return fail(JT_EINVAL, "polygon needs >= 3 vertices");
     if (gw < 1 || gh < 1 || (long long)gw * gh > (1LL << 24)) return fail(JT_EINVAL, "bad grid %d x %d", gw, gh);
     if (lmax < 0 || lmax > (1 << 20)) return fail(JT_EINVAL, "bad list limit %d", lmax);
+    if (head_words != 4 && head_words != 8) return fail(JT_EINVAL, "head_words must be 4 or 8, not %d", head_words);
+    const int inline_edges = head_words / 4;  // edges a head holds in place
     const long long cells = (long long)gw * gh, words = (cells + 15) / 16;
     std::vector<float> slope(n), icpt(n), ylo(n), yhi(n);
     float xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
@@ -1417,11 +1419,11 @@ int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int
     const float ox = -xmin * sx, oy = -ymin * sy;
     params[0] = sx, params[1] = ox, params[2] = sy, params[3] = oy;
     const bool fill = bits && heads;
-    if (fill && (bits_capacity < words || heads_capacity < 4 * cells))
-        return fail(JT_EINVAL, "cell tables need %lld words and %lld head words", words, 4 * cells);
+    if (fill && (bits_capacity < words || heads_capacity < head_words * cells))
+        return fail(JT_EINVAL, "cell tables need %lld words and %lld head words", words, head_words * cells);
     if (fill) {
         std::memset(bits, 0, sizeof(uint32_t) * words);
-        std::memset(heads, 0, sizeof(uint32_t) * 4 * cells);
+        std::memset(heads, 0, sizeof(uint32_t) * head_words * cells);
     }
     std::vector<float> cx0(gw + 1), cy0(gh + 1);
     for (int k = 0; k <= gw; ++k) cx0[k] = k == 0 ? -INFINITY : cell_first(k, sx, ox, gw - 1);
@@ -1498,13 +1500,20 @@ int jt_pnpoly_cells(const float *vx, const float *vy, int n, int gw, int gh, int
                 code = 2u | (uint32_t)base;
                 const bool over = (int)list.size() > lmax;
                 over ? ++n_fallback : ++n_listed;
-                uint32_t *h = fill ? heads + 4 * cell : nullptr;
-                if (!over && list.size() == 1) {
-                    const int k = list[0];
-                    const float e0[4] = {slope[k], icpt[k], ylo[k], yhi[k]};
-                    if (h) std::memcpy(h, e0, sizeof e0);
+                uint32_t *h = fill ? heads + (long long)head_words * cell : nullptr;
+                const float nan = std::numeric_limits<float>::quiet_NaN();
+                if (!over && list.size() >= 1 && (int)list.size() <= inline_edges) {
+                    // the edges in place; an unused second slot is a never-true {0, 0, NaN, 0}
+                    for (int j = 0; j < inline_edges && h; ++j) {
+                        if (j < (int)list.size()) {
+                            const int k = list[(size_t)j];
+                            const float e[4] = {slope[k], icpt[k], ylo[k], yhi[k]};
+                            std::memcpy(h + 4 * j, e, sizeof e);
+                        } else {
+                            h[4 * j] = h[4 * j + 1] = h[4 * j + 3] = 0, std::memcpy(h + 4 * j + 2, &nan, 4);
+                        }
+                    }
                 } else {
-                    const float nan = std::numeric_limits<float>::quiet_NaN();
                     if (h) {
                         h[0] = over ? 0u : (uint32_t)entries, h[1] = over ? 0xffffffffu : (uint32_t)list.size();
                         std::memcpy(h + 2, &nan, 4), h[3] = 0;

@@ -54,6 +54,10 @@
 #ifndef ADRAIN
 #define ADRAIN 1
 #endif
+#ifndef HEAD32
+#define HEAD32 0  // 1: 32-byte heads holding up to two undecided edges in place
+#endif
+#define HW (1 + HEAD32)  // float4s per head
 #if ADRAIN
 #define QCAP 64  // drained after each point push: < 32 + 32
 #else
@@ -107,10 +111,10 @@ __device__ __noinline__ int slab_search(float px, float py, SLAB_PARAMS) {  // r
 __device__ __forceinline__ int edge_test(float4 e, float px, float py) {
     return (e.z <= py && py < e.w && px < __fmaf_rn(e.x, py, e.y)) ? 1 : 0;
 }
-__device__ __forceinline__ int resolve(float px, float py, int base, float4 h, const float4 *__restrict__ edges,
-                                       SLAB_PARAMS) {
+__device__ __forceinline__ int resolve(float px, float py, int base, float4 h, float4 h1,
+                                       const float4 *__restrict__ edges, SLAB_PARAMS) {
     if (!(px == px) || !(py == py)) return 0;
-    if (h.z == h.z) return base ^ edge_test(h, px, py);
+    if (h.z == h.z) return base ^ edge_test(h, px, py) ^ (HEAD32 ? edge_test(h1, px, py) : 0);
     const unsigned first = __float_as_uint(h.x), cnt = __float_as_uint(h.y);
     if (cnt == 0xffffffffu) return slab_search(px, py, SLAB_ARGS);
     int in = base;
@@ -122,14 +126,8 @@ __device__ __forceinline__ int cell_search(float px, float py, unsigned cell, in
                                            const float4 *__restrict__ heads, const float4 *__restrict__ edges,
                                            SLAB_PARAMS) {
     if (!(px == px) || !(py == py)) return 0;
-    const float4 h = __ldg(heads + cell);
-    if (h.z == h.z) return base ^ edge_test(h, px, py);
-    const unsigned first = __float_as_uint(h.x), cnt = __float_as_uint(h.y);
-    if (cnt == 0xffffffffu) return slab_search(px, py, SLAB_ARGS);
-    int in = base;
-#pragma unroll 1
-    for (unsigned k = 0; k < cnt; ++k) in ^= edge_test(__ldg(edges + first + k), px, py);
-    return in;
+    return resolve(px, py, base, __ldg(heads + HW * cell), HEAD32 ? __ldg(heads + HW * cell + 1) : make_float4(0.f, 0.f, 0.f, 0.f),
+                   edges, SLAB_ARGS);
 }
 
 // The host's cell function (jt_pnpoly_cells): min(f2u_rz(fma(v, s, o)), GRID - 1); cvt.rzi.u32
@@ -227,12 +225,13 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
     // batch of 32 takes its points into registers and starts a 16-byte cp.async of each
     // point's cell head into a per-lane slot; the batch is finished (test, store) when the
     // next one starts, or at the end. One batch is pending once any has started (head > 0).
-    float4 *hslot = reinterpret_cast<float4 *>(rings + 3 * (BLOCK_SIZE_X / 32) * QCAP) + threadIdx.x;
+    float4 *hslot = reinterpret_cast<float4 *>(rings + 3 * (BLOCK_SIZE_X / 32) * QCAP) + HW * threadIdx.x;
     float apx = 0.f, apy = 0.f;
     int aidx = 0;
     auto finish = [&]() {
         asm volatile("cp.async.wait_all;" ::: "memory");
-        bitmap[aidx & 0x7fffffff] = resolve(apx, apy, (int)((unsigned)aidx >> 31), *hslot, edges, SLAB_ARGS);
+        bitmap[aidx & 0x7fffffff] = resolve(apx, apy, (int)((unsigned)aidx >> 31), hslot[0], hslot[HW - 1], edges,
+                                            SLAB_ARGS);
     };
     auto drain = [&]() {
         __syncwarp();
@@ -248,8 +247,12 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
             head += 32;
             unsigned cell_;
             CELL_OF(apx, apy);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\ncp.async.commit_group;" ::"r"(
-                             (unsigned)__cvta_generic_to_shared(hslot)), "l"(heads + cell_) : "memory");
+            const unsigned slot = (unsigned)__cvta_generic_to_shared(hslot);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot), "l"(heads + HW * cell_) : "memory");
+            if (HEAD32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot + 16), "l"(heads + HW * cell_ + 1)
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
     };
 #else

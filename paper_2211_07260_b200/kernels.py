@@ -644,43 +644,44 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         return {
             "block_size_x": [256, 512, 1024],
             "tile": [1, 2, 4],
-            "grid": [256, 512, 1024],
+            "grid": [256, 448, 512, 1024],
             "grid_smem": [0, 1],
             "lmax": [4, 16],
-            "stream": [0, 1],
             "prefetch": [0, 1, 2],
-            "regpf": [0, 1],
             "adrain": [0, 1],
+            "head32": [0, 1],
         }
+    # STREAM (evict-first hints) and REGPF (register double buffering) stay kernel options
+    # (tests/test_gpu_slab.py runs them); measured slower everywhere, so not tuned
 
     def restrictions(self):
         # ring: 128 x 12-byte slots per warp, or 64 + a 16-byte head slot per thread with
         # the split drain (QCAP in pnpoly_cells.cu)
         return [f"(grid_smem * grid * grid / 4 + block_size_x / 32 * (1536 - 768 * adrain) + "
-                f"16 * block_size_x * adrain) <= {227 * 1024}"]
+                f"16 * (1 + head32) * block_size_x * adrain) <= {227 * 1024}"]
 
     def default_config(self):
         return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0, "prefetch": 1, "regpf": 0,
-                "adrain": 1}
+                "adrain": 1, "head32": 0}
 
     def defines(self, config):
         c = _as_dict(config)
         return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"],
                 "GRID_SMEM": c.get("grid_smem", 1), "STREAM": c.get("stream", 0), "PREFETCH": c.get("prefetch", 0),
-                "REGPF": c.get("regpf", 0), "ADRAIN": c.get("adrain", 0)}
+                "REGPF": c.get("regpf", 0), "ADRAIN": c.get("adrain", 0), "HEAD32": c.get("head32", 0)}
 
-    def cell_table(self, g: int, lmax: int):
+    def cell_table(self, g: int, lmax: int, head_words: int = 4):
         cache = self.__dict__.setdefault("_cell_tables", {})
-        if (g, lmax) not in cache:
+        if (g, lmax, head_words) not in cache:
             vx, vy = self._polygon()
-            cache[(g, lmax)] = native.pnpoly_cells(vx, vy, g, g, lmax)
-        return cache[(g, lmax)]
+            cache[(g, lmax, head_words)] = native.pnpoly_cells(vx, vy, g, g, lmax, head_words)
+        return cache[(g, lmax, head_words)]
 
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
         words = (c["grid"] * c["grid"] + 15) // 16 if c.get("grid_smem", 1) else 0
-        ad = c.get("adrain", 0)
-        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * (64 if ad else 128) * 12 + 16 * c["block_size_x"] * ad
+        ad, hw = c.get("adrain", 0), 1 + c.get("head32", 0)
+        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * (64 if ad else 128) * 12 + 16 * hw * c["block_size_x"] * ad
 
     def launch(self, config, n_points: int | None = None):
         c = _as_dict(config)
@@ -696,9 +697,9 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         self.__dict__.pop("_cell_tables", None)
 
     def _tail(self, c):
-        g, lmax = c["grid"], c["lmax"]
-        key = f"cells{g}x{lmax}"
-        words, params, heads, edges, _ = self.cell_table(g, lmax)
+        g, lmax, hw = c["grid"], c["lmax"], 4 + 4 * c.get("head32", 0)
+        key = f"cells{g}x{lmax}h{hw}"
+        words, params, heads, edges, _ = self.cell_table(g, lmax, hw)
         if key + "w" not in self.buffers:  # one entry per device buffer (buffers are freed one by one)
             self.buffers[key + "w"] = self.gpu.array(words)
             self.buffers[key + "h"] = self.gpu.array(heads)

@@ -239,8 +239,8 @@ def _declare(lib) -> None:
         "jt_pnpoly_slabs": (c.c_int, [P, P, c.c_int, c.c_int, c.c_int, c.c_int, P, c.c_longlong,
                                       c.POINTER(JTSlabInfo)]),
         "jt_pnpoly_grid": (c.c_int, [P, P, c.c_int, c.c_int, c.c_int, P, P, c.c_longlong, c.POINTER(c.c_int)]),
-        "jt_pnpoly_cells": (c.c_int, [P, P, c.c_int, c.c_int, c.c_int, c.c_int, P, P, c.c_longlong, P, c.c_longlong,
-                                      P, c.c_longlong, P]),
+        "jt_pnpoly_cells": (c.c_int, [P, P, c.c_int, c.c_int, c.c_int, c.c_int, c.c_int, P, P, c.c_longlong, P,
+                                      c.c_longlong, P, c.c_longlong, P]),
         "jt_module_set_global": (c.c_int, [P, P, c.c_char_p, P, c.c_size_t]),
     }
     for name, (res, args) in sig.items():
@@ -398,20 +398,21 @@ def pnpoly_grid(vx, vy, gw: int, gh: int):
     return words, params, clean.value
 
 
-def pnpoly_cells(vx, vy, gw: int, gh: int, lmax: int):
+def pnpoly_cells(vx, vy, gw: int, gh: int, lmax: int, head_words: int = 4):
     """Per-cell edge lists for csrc/kernels/pnpoly_cells.cu (libjt ``jt_pnpoly_cells``): returns
-    (uint32 words, 2-bit codes, 16 cells per word), params {sx, ox, sy, oy}, uint32 heads (4 per cell),
-    float32 edge entries (k, 4) and stats {entries, clean, listed, fallback}."""
+    (uint32 words, 2-bit codes, 16 cells per word), params {sx, ox, sy, oy}, uint32 heads
+    (head_words per cell), float32 edge entries (k, 4) and stats {entries, decided, listed,
+    fallback}."""
     import numpy as np
 
     vx = np.ascontiguousarray(vx, dtype=np.float32)
     vy = np.ascontiguousarray(vy, dtype=np.float32)
     params = np.zeros(4, dtype=np.float32)
     stats = np.zeros(4, dtype=np.int64)
-    args = (vx.ctypes.data, vy.ctypes.data, vx.size, int(gw), int(gh), int(lmax), params.ctypes.data)
+    args = (vx.ctypes.data, vy.ctypes.data, vx.size, int(gw), int(gh), int(lmax), int(head_words), params.ctypes.data)
     check(lib().jt_pnpoly_cells(*args, None, 0, None, 0, None, 0, stats.ctypes.data), "jt_pnpoly_cells")
     words = np.zeros((gw * gh + 15) // 16, dtype=np.uint32)
-    heads = np.zeros(4 * gw * gh, dtype=np.uint32)
+    heads = np.zeros(int(head_words) * gw * gh, dtype=np.uint32)
     edges = np.zeros((max(1, int(stats[0])), 4), dtype=np.float32)
     check(lib().jt_pnpoly_cells(*args, words.ctypes.data, words.size, heads.ctypes.data, heads.size,
                                 edges.ctypes.data, edges.shape[0], stats.ctypes.data), "jt_pnpoly_cells")

@@ -292,15 +292,16 @@ def _polygon(name):
 
 
 @pytest.mark.parametrize("name", sorted(POLYGONS))
-@pytest.mark.parametrize("g,lmax", [(7, 8), (64, 2), (512, 8)])
-def test_cell_lists_give_the_brute_force_answer(name, g, lmax):
+@pytest.mark.parametrize("g,lmax,hw", [(7, 8, 4), (64, 2, 8), (512, 8, 4), (512, 16, 8)])
+def test_cell_lists_give_the_brute_force_answer(name, g, lmax, hw):
     """jt_pnpoly_cells: the pnpoly_cells.cu decision, emulated - code 0 / 1 is the answer,
-    code 2 is the base parity XOR the listed edges' METHOD 2 tests (libm fmaf, NaN -> 0) -
-    equals the brute-force bit for every point outside the code-3 (slab search) cells."""
+    code 2 | base is base XOR the listed edges' METHOD 2 tests (libm fmaf, NaN -> 0), the
+    edges in the head (4- or 8-word heads) or in the edge array - equals the brute-force bit
+    for every point outside the fallback (slab search) cells."""
     from oracle import kernels_oracle as O
 
     vx, vy = _polygon(name)
-    words, prm, heads, edges, st = native.pnpoly_cells(vx, vy, g, g, lmax)
+    words, prm, heads, edges, st = native.pnpoly_cells(vx, vy, g, g, lmax, hw)
     assert st[1] + st[2] + st[3] <= g * g and st[0] <= max(1, st[2] * lmax)
     pts = _grid_points(vx, vy, prm, g)
     cell = _cell(pts[:, 1], prm[2], prm[3], g - 1) * g + _cell(pts[:, 0], prm[0], prm[1], g - 1)
@@ -312,10 +313,10 @@ def test_cell_lists_give_the_brute_force_answer(name, g, lmax):
         px, py = float(pts[i, 0]), float(pts[i, 1])
         if px != px or py != py:
             continue
-        h = heads[4 * int(cell[i]): 4 * int(cell[i]) + 4]
-        hf = h.view(np.float32)
-        if hf[2] == hf[2]:
-            listed = [hf]
+        h = heads[hw * int(cell[i]): hw * int(cell[i]) + hw]
+        hf = h.view(np.float32).reshape(-1, 4)
+        if hf[0, 2] == hf[0, 2]:
+            listed = list(hf)  # in place (an unused slot never tests true)
         elif h[1] == 0xFFFFFFFF:
             fallback[i] = True
             continue
@@ -352,6 +353,8 @@ def test_cell_lists_border_and_limits(name):
         assert np.all((hf[und, 1] == 0xFFFFFFFF) | (hf[und, 1] == 0))
     with pytest.raises(Exception):
         native.pnpoly_cells(vx, vy, 0, 4, 8)
+    with pytest.raises(Exception):
+        native.pnpoly_cells(vx, vy, 8, 8, 8, 6)  # head_words 4 or 8
 
 
 def _cells_code(words, cell):
