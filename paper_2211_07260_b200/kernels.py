@@ -647,12 +647,13 @@ class PnPolyCellsProblem(PnPolyGridProblem):
             "grid": [256, 448, 512, 1024],
             "grid_smem": [0, 1],
             "lmax": [4, 16],
+            "stream": [0, 1],
             "prefetch": [0, 1, 2],
             "adrain": [0, 1],
             "head32": [0, 1],
         }
-    # STREAM (evict-first hints) and REGPF (register double buffering) stay kernel options
-    # (tests/test_gpu_slab.py runs them); measured slower everywhere, so not tuned
+    # REGPF (register double buffering) stays a kernel option (tests/test_gpu_slab.py runs
+    # it); it measured slower everywhere, so it is not tuned
 
     def restrictions(self):
         # ring: 128 x 12-byte slots per warp, or 64 + a 16-byte head slot per thread with

@@ -22,7 +22,7 @@ p.prepare(gpu)
 want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2)
 configs = [c.as_dict() for c in p.space().enumerate()]
 if len(sys.argv) > 1:
-    configs = [c for c in configs if all(str(c[k]) == v for k, v in (a.split("=") for a in sys.argv[1:]))]
+    configs = [c for c in configs if all(str(c.get(k)) == v for k, v in (a.split("=") for a in sys.argv[1:]))]
 with ThreadPoolExecutor(16) as pool:
     list(pool.map(p.cubin, configs))
 hbm = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]

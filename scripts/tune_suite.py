@@ -59,6 +59,11 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
             "restrictions": [],
         }
         return doc, "exhaustive", None
+    if name == "pnpoly_cells_focus":  # the neighbourhood of the full sweep's winners
+        doc = {"parameters": {"block_size_x": [1024], "tile": [1, 2], "grid": [448, 512], "grid_smem": [1],
+                              "lmax": [16], "stream": [0, 1], "prefetch": [1, 2], "adrain": [0, 1], "head32": [0, 1]},
+               "restrictions": problem.restrictions()}
+        return doc, "exhaustive", None
     if name in ("conv2d", "sgemm_tf32", "pnpoly_slab", "pnpoly_grid", "pnpoly_cells"):
         return problem.space_document(), "exhaustive", None
     if name == "sgemm":
@@ -158,7 +163,7 @@ def confirm(dev, problem, leaders) -> list[dict]:
 
 
 def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | None) -> dict:
-    problem = make_problem("sgemm" if name == "sgemm_wide" else name)
+    problem = make_problem({"sgemm_wide": "sgemm", "pnpoly_cells_focus": "pnpoly_cells"}.get(name, name))
     doc, strategy, budget = curated_space(name, problem)
     space = SearchSpace.from_dict(doc)
     if clocks:
@@ -273,12 +278,14 @@ def main():
     data = json.loads(TUNED_PATH.read_text()) if TUNED_PATH.exists() else {}
     for name in args.kernels.split(","):
         entry = tune(gpu, name, args.duration, args.seed, clocks)
-        if name == "sgemm_wide":  # a follow-up sweep of the sgemm space: keep whichever wins
-            old = data.get("sgemm")
+        if name in ("sgemm_wide", "pnpoly_cells_focus"):  # follow-up sweeps: keep whichever wins
+            base = {"sgemm_wide": "sgemm", "pnpoly_cells_focus": "pnpoly_cells"}[name]
+            old = data.get(base)
             if old and old["time_optimal"]["time_s"] <= entry["time_optimal"]["time_s"]:
-                data["sgemm_wide_sweep"] = entry
+                data[name + "_sweep"] = entry
                 continue
-            name = "sgemm"
+            data[name + "_sweep"] = entry
+            name = base
         data[name] = entry
         TUNED_PATH.write_text(json.dumps(data, indent=1) + "\n")
     Path("gpurun_out").mkdir(exist_ok=True)
