@@ -5,29 +5,31 @@
 // GRID x GRID raster over the polygon's bounding box: its METHOD 2 test is
 // false for every point of the cell, true for every point, or undecided. A
 // cell whose edges are all decided stores its parity (2 bits per cell, staged
-// in shared memory): on the benchmark polygon 95% of the points are answered
-// by that one lookup. An undecided cell lists its undecided edges (1.3 on
-// average at GRID = 512); its points are queued per warp with their
-// coordinates and answered 32 at a time by base ^ their listed tests: one
-// 16-byte head read per point (the edge itself when there is one), more only
-// for cells with several. Cells with more than `lmax` undecided edges fall back
-// to the exact slab search of pnpoly_slab.cu.
+// in shared memory): on the benchmark polygon 94-95% of the points are
+// answered by that one lookup. An undecided cell lists its undecided edges
+// (1.3 on average at GRID = 512); its points are queued per warp with their
+// coordinates and answered 32 at a time by base ^ their listed tests: one head
+// read per point (16 bytes holding one edge in place, or 32 bytes holding two
+// with HEAD32), more only for cells with more edges. Cells with more than
+// `lmax` undecided edges fall back to the exact slab search of pnpoly_slab.cu.
 //
 // Memory side: two points per 16-byte load and two results per 8-byte store,
-// TILE pairs per thread per chunk. The L1 pipe is the shared resource: the
-// random raster lookups' bank conflicts and the scattered reads / writes of
-// the queued points are what it spends its wavefronts on, so the queue carries
-// the points (no re-read) and a head answers most of them in one read.
+// TILE pairs per thread per chunk. The raster lookups cost nothing measurable
+// (scripts/cells_floor.py); the queued points' dependent head reads are the
+// cost above the loop's own floor, hence in-place edges and the split drain.
 //
 // Tunables (-D): BLOCK_SIZE_X, TILE (point pairs per thread per chunk), GRID
 // (cells per side), GRID_SMEM (1: raster in shared memory; 0: read through L1),
-// STREAM (1: points loaded / results stored with the evict-first hints), PREFETCH (chunks
-// ahead that one thread of the block pulls into L2 with cp.async.bulk.prefetch: the
-// block's points are one contiguous span per chunk, so the next chunk's HBM latency
-// overlaps this chunk's work without holding registers), REGPF (1: the next chunk's pairs
-// are loaded into registers before this chunk is classified). Tried and dropped: a
-// 2-4 stage shared-memory ring filled by cp.async.bulk from one producer thread (67 us
-// and up: the producer waits for every warp to free a stage, which couples the warps).
+// STREAM (1: points loaded / results stored with the evict-first hints), PREFETCH
+// (chunks ahead that one thread of the block pulls into L2 with
+// cp.async.bulk.prefetch: the block's points are one contiguous span per chunk,
+// so the next chunk's HBM latency overlaps this chunk's work without holding
+// registers), REGPF (1: the next chunk's pairs are loaded into registers before
+// this chunk is classified), ADRAIN (1: split drains, the heads fetched by
+// cp.async and tested at the next drain), HEAD32 (32-byte heads). Tried and
+// dropped: a 2-4 stage shared-memory ring filled by cp.async.bulk from one
+// producer thread (67 us and up: the producer waits for every warp to free a
+// stage, which couples the warps).
 #ifndef BLOCK_SIZE_X
 #define BLOCK_SIZE_X 1024
 #endif
@@ -50,7 +52,6 @@
 #define REGPF 0
 #endif
 #define CHUNK (BLOCK_SIZE_X * TILE)
-// ring slots per warp (a power of two): < 32 left after a drain + 64 pushed per pair step
 #ifndef ADRAIN
 #define ADRAIN 1
 #endif
@@ -58,8 +59,10 @@
 #define HEAD32 0  // 1: 32-byte heads holding up to two undecided edges in place
 #endif
 #define HW (1 + HEAD32)  // float4s per head
+// ring slots per warp (a power of two): < 32 left after a drain, + 32 per point push (split
+// drains run after each push) or + 64 per pair step
 #if ADRAIN
-#define QCAP 64  // drained after each point push: < 32 + 32
+#define QCAP 64
 #else
 #define QCAP 128
 #endif

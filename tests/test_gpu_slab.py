@@ -101,7 +101,8 @@ def test_slab_matches_brute_force_kernel_full_size(gpu):
 
 @pytest.mark.parametrize("strips", [1, 5])
 def test_slab_host_api_matches_brute_force(gpu, strips):
-    """suite.pnpoly(algorithm="slab") through pinned host buffers equals the brute-force call."""
+    """suite.pnpoly(algorithm="slab" / "grid" / "cells") through pinned host buffers equals the
+    brute-force call."""
     from paper_2211_07260_b200 import suite
     from paper_2211_07260_b200.kernels import PnPolyProblem
 
@@ -111,6 +112,8 @@ def test_slab_host_api_matches_brute_force(gpu, strips):
     slab = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips, algorithm="slab").copy()
     grid = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips, algorithm="grid").copy()
     np.testing.assert_array_equal(grid, slab)
+    cells = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips, algorithm="cells").copy()
+    np.testing.assert_array_equal(cells, slab)
     brute = suite.pnpoly(pts, inp["vx"], inp["vy"], strips=strips,
                          config=dict(PnPolyProblem().default_config(), asm=0, method=2)).copy()
     np.testing.assert_array_equal(slab, brute)
