@@ -12,7 +12,7 @@ the round's B200 measurements:
   measured for the tuned config (tuned_b200.json), and the reference runtime
   law t(f) = t_ref * (kappa * f_ref / f + 1 - kappa) (device.py:169-172) with
   t_ref the measured time, kappa = 1 for the FP32-pipe-bound kernels and 0.5
-  for the memory/latency-bound PnPoly slab / grid kernels;
+  for the memory/latency-bound PnPoly slab / grid / cells kernels;
 * steered: a noisy (1%) full-load burner sweep -> prepare_sweep (drops the
   power-capped samples) -> fit -> optimal_frequency -> frequency_band(+-10%);
   each kernel is then swept only over the band (powermodel.py:387-431).
@@ -42,7 +42,7 @@ from paper_2211_07260_b200.tuned import TUNED_PATH  # noqa: E402
 GRID = [float(f) for f in np.arange(195.0, 1966.0, 15.0)]
 F_REF = 1965.0
 P_IDLE, P_MAX, TAU, BETA = 180.0, 1000.0, 1200.0, 0.0012
-KAPPA = {"conv2d": 1.0, "sgemm": 1.0, "pnpoly": 1.0, "pnpoly_slab": 0.5, "pnpoly_grid": 0.5}
+KAPPA = {"conv2d": 1.0, "sgemm": 1.0, "pnpoly": 1.0, "pnpoly_slab": 0.5, "pnpoly_grid": 0.5, "pnpoly_cells": 0.5}
 
 
 def board(alpha_u: float) -> GroundTruth:
