@@ -60,8 +60,8 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
         }
         return doc, "exhaustive", None
     if name == "pnpoly_cells_focus":  # the neighbourhood of the full sweep's winners
-        doc = {"parameters": {"block_size_x": [1024], "tile": [1, 2], "grid": [448, 512], "grid_smem": [1],
-                              "lmax": [16], "stream": [0, 1], "prefetch": [1, 2], "adrain": [0, 1], "head32": [0, 1]},
+        doc = {"parameters": {"block_size_x": [1024], "tile": [1, 2], "grid": [320, 384, 416, 448], "grid_smem": [1],
+                              "lmax": [16], "stream": [0, 1], "prefetch": [0, 1], "adrain": [0, 1], "head32": [0, 1]},
                "restrictions": problem.restrictions()}
         return doc, "exhaustive", None
     if name in ("conv2d", "sgemm_tf32", "pnpoly_slab", "pnpoly_grid", "pnpoly_cells"):
