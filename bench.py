@@ -95,6 +95,8 @@ class Dist:
 
 
 E2E_STRIPS = 4  # row bands of the pipelined host-buffer call (suite.CONV2D_STRIPS)
+ENERGY_LOOP_S = 1.5  # the headline's dedicated energy loop (>= 10 energy-counter updates)
+ENERGY_SETTLE_S = 0.25  # skipped at its start: power ramp after the timed region
 
 
 def torch_sync():
@@ -221,6 +223,7 @@ def summarize_samples(samples, t0, t1):
         reasons |= int(s[8])
     inst = [s[1] for s in inside if math.isfinite(s[1])]
     return {
+        "n": len(inside),
         "counter_w": watts,
         "instant_w": statistics.median(inst) if inst else None,
         "sm_mhz": statistics.median(clocks) if clocks else None,
@@ -251,7 +254,10 @@ def tf32_peak_gflops(sustained: bool = False) -> float:
     return bf16 / 2.0 * 1e3
 
 
-def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: float = 0.25):
+def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: float = 0.25, sets: int = 2):
+    """One tuned config in a >= 1 s device-timed loop over ``sets`` rotating input/output sets (each larger
+    than L2 or alone in it, so no launch reads an L2-warm input), energy from the NVML counter slope taken
+    ``settle`` s into the loop (past the power ramp)."""
     from paper_2211_07260_b200 import tuned
     from paper_2211_07260_b200.gpu import fp32_peak_tflops
     from paper_2211_07260_b200.kernels import make_problem
@@ -261,55 +267,58 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: 
     cfg = tuned.best_config(name, objective) or prob.default_config()
     k = prob.kernel(cfg)
     prob.bind(k, cfg)
-    run = gpu.bench(k, prob.launch(cfg), prob.args(cfg), min_seconds=seconds)
-    summ = summarize_samples(run.samples, run.loop_t0 + settle, run.loop_t1)  # past the power ramp
-    rate = prob.total_flops / run.per_launch_s / 1e9
-    out = {
-        "config": cfg,
-        "ms": round(run.per_launch_s * 1e3, 4),
-        "gflops": round(rate, 1),
-        "gflops_per_w": round(prob.total_flops / (summ["counter_w"] * run.per_launch_s) / 1e9, 2)
-        if summ["counter_w"] else None,
-        "power_w": round(summ["counter_w"], 1) if summ["counter_w"] else None,
-        "sm_mhz": summ["sm_mhz"],
-    }
-    if prob.roofline_kind == "tensor":
-        # a >= 1 s back-to-back loop runs at the power cap: the sustained measured peak is the
-        # denominator (the burst one is reported beside it)
-        peak = tf32_peak_gflops(sustained=True)
-        out["roofline_frac"] = round(rate / peak, 4)
-        out["roofline_peak_gflops"] = peak
-        out["roofline_frac_vs_burst"] = round(rate / tf32_peak_gflops(), 4)
-        out["roofline_basis"] = ("MEASURED_PEAKS bf16_tflops_sustained / 2 (tcgen05 kind::tf32 issues K=8 per MMA vs "
-                                 "K=16; loop runs power-capped like the sustained bf16 measurement)")
-    elif prob.roofline_kind == "hbm":
+    run = gpu.bench(k, prob.launch(cfg), prob.args(cfg), min_seconds=seconds, rotate=prob.rotation_sets(cfg, sets))
+    summ = summarize_samples(run.samples, run.loop_t0 + settle, run.loop_t1)
+    watts = summ["counter_w"]
+    out = {"config": cfg, "ms": round(run.per_launch_s * 1e3, 4), "rotating_sets": sets,
+           "power_w": round(watts, 1) if watts else None, "sm_mhz": summ["sm_mhz"], "reasons": summ["reasons"]}
+    if prob.roofline_kind == "hbm":
+        # work-skipping PnPoly kernels: no flop credit for the edge tests they do not run
         peaks = ROOT / "MEASURED_PEAKS.json"
         hbm = (json.loads(peaks.read_text()) if peaks.exists() else {}).get("hbm_gbs") or 7700.0
         gbs = prob.algorithmic_bytes / run.per_launch_s / 1e9
-        out["roofline_frac"] = round(gbs / hbm, 4)
-        out["roofline_basis"] = (f"HBM: {prob.algorithmic_bytes / 1e6:.1f} MB algorithmic (points + bitmap) per launch "
-                                 f"= {gbs:.0f} GB/s vs {hbm} GB/s (MEASURED_PEAKS hbm_gbs)")
-    elif summ["sm_mhz"]:
-        peak = fp32_peak_tflops(gpu.sm_count, summ["sm_mhz"]) * 1e3
-        if prob.roofline_kind == "issue":
-            peak /= 2.0  # 1 lane-instruction slot per lane per clock, not 2 flop/FFMA
-        out["roofline_frac"] = round(rate / peak, 4)
-    if name in ("pnpoly", "pnpoly_slab", "pnpoly_grid", "pnpoly_cells"):
-        out["edge_tests_per_s"] = round(prob.edge_tests / run.per_launch_s, 1)  # brute-force-equivalent
-    if name == "pnpoly_grid":
-        out["clean_cell_fraction"] = round(prob.clean_fraction(cfg["grid"]), 4)
-    if name == "pnpoly_cells":
-        out["decided_cell_fraction"] = round(prob.clean_fraction(cfg["grid"], cfg["lmax"]), 4)
+        out.update({
+            "points_per_s": round(prob.n_points / run.per_launch_s, 1),
+            "gb_per_s": round(gbs, 1),
+            "j_per_bitmap": round(watts * run.per_launch_s, 6) if watts else None,
+            "roofline_frac": round(gbs / hbm, 4),
+            "roofline_basis": (f"HBM: {prob.algorithmic_bytes / 1e6:.1f} MB algorithmic (points + bitmap) per "
+                               f"launch = {gbs:.0f} GB/s vs {hbm} GB/s (MEASURED_PEAKS hbm_gbs)"),
+        })
+        if name == "pnpoly_grid":
+            out["clean_cell_fraction"] = round(prob.clean_fraction(cfg["grid"]), 4)
+        if name == "pnpoly_cells":
+            out["decided_cell_fraction"] = round(prob.clean_fraction(cfg["grid"], cfg["lmax"]), 4)
+    else:
+        rate = prob.total_flops / run.per_launch_s / 1e9
+        out["gflops"] = round(rate, 1)
+        out["gflops_per_w"] = round(prob.total_flops / (watts * run.per_launch_s) / 1e9, 2) if watts else None
+        if prob.roofline_kind == "tensor":
+            # a >= 1 s back-to-back loop runs at the power cap: the sustained measured peak is the
+            # denominator (the burst one is reported beside it)
+            peak = tf32_peak_gflops(sustained=True)
+            out["roofline_frac"] = round(rate / peak, 4)
+            out["roofline_peak_gflops"] = peak
+            out["roofline_frac_vs_burst"] = round(rate / tf32_peak_gflops(), 4)
+            out["roofline_basis"] = ("MEASURED_PEAKS bf16_tflops_sustained / 2 (tcgen05 kind::tf32 issues K=8 per "
+                                     "MMA vs K=16; loop runs power-capped like the sustained bf16 measurement)")
+        elif summ["sm_mhz"]:
+            peak = fp32_peak_tflops(gpu.sm_count, summ["sm_mhz"]) * 1e3
+            if prob.roofline_kind == "issue":
+                peak /= 2.0  # 1 lane-instruction slot per lane per clock, not 2 flop/FFMA
+                out["edge_tests_per_s"] = round(prob.edge_tests / run.per_launch_s, 1)
+                out["j_per_bitmap"] = round(watts * run.per_launch_s, 6) if watts else None
+            out["roofline_frac"] = round(rate / peak, 4)
     for b in prob.buffers.values():
         b.free()
     return out
 
 
-#: the sharded tuning leg: a fixed slice of the conv2d space (strong scaling over ranks)
-#: (64 points: an equal share for 1, 2, 4 and 8 ranks)
-TUNE_SPACE = {"block_size_x": [32, 64], "block_size_y": [2, 4, 8], "tile_size_x": [4, 8], "tile_size_y": [1, 2, 4],
-              "use_shmem": [0, 1], "use_padding": [0], "fma2": [0], "min_blocks": [0]}
-TUNE_WINDOW_S = 0.2  # launch loop per point: >= 2 energy-counter updates (~100 ms cadence)
+#: the sharded tuning leg: a fixed slice of the conv2d space (strong scaling over ranks), 516 points so that
+#: each of 8 ranks measures >= 64 of them
+TUNE_SPACE = {"block_size_x": [32, 64], "block_size_y": [2, 4, 8, 16], "tile_size_x": [2, 4, 8],
+              "tile_size_y": [1, 2, 4], "use_shmem": [0, 1], "use_padding": [0], "fma2": [0, 1], "min_blocks": [0, 2]}
+TUNE_WINDOW_S = 0.15  # launch loop per point: >= 1 energy-counter update (~100 ms cadence)
 
 
 def tuning_leg(gpu, dist: Dist) -> dict:
@@ -318,12 +327,13 @@ def tuning_leg(gpu, dist: Dist) -> dict:
     ``partition.plan`` deals the configs over the ranks (LPT); each
     rank measures its shard on its own GPU with the NVML observer
     (``run_strategy``'s evaluator, energy objective), writes a JSONL shard, and
-    rank 0 merges them on the filesystem after a barrier. Compilation happens
-    before the timed region. points/s = all points / slowest shard's seconds.
+    rank 0 merges them on the filesystem after a barrier. Per-rank fixed costs
+    (input upload + device setup, compilation) are timed apart from the shard
+    loop; points/s = all points / slowest shard loop.
     """
     import tempfile
 
-    from paper_2211_07260_b200 import NVMLObserver, Objective, SearchSpace, default_metrics, partition
+    from paper_2211_07260_b200 import NVMLObserver, Objective, SearchSpace, partition
     from paper_2211_07260_b200.b200 import B200Device
     from paper_2211_07260_b200.kernels import make_problem
 
@@ -331,8 +341,10 @@ def tuning_leg(gpu, dist: Dist) -> dict:
     space = SearchSpace.from_dict({"parameters": TUNE_SPACE, "restrictions": problem.restrictions()})
     shards = partition.plan(space, dist.world)
     mine = shards[dist.rank]
+    t0 = time.perf_counter()
     with ThreadPoolExecutor(8) as pool:
         list(pool.map(lambda c: problem.cubin({**problem.default_config(), **c.as_dict()}), mine.configs))
+    compile_s = time.perf_counter() - t0
     base = os.environ.get("BENCH_TUNE_DIR") or os.path.join(tempfile.gettempdir(),
                                                             f"bench_tune_{os.environ.get('MASTER_PORT', 'solo')}")
     workdir = Path(base)
@@ -341,18 +353,26 @@ def tuning_leg(gpu, dist: Dist) -> dict:
         for f in workdir.iterdir():
             f.unlink()
     dist.barrier()
-    device = B200Device(problem, gpu=gpu, min_window=TUNE_WINDOW_S)
+    t0 = time.perf_counter()
+    device = B200Device(problem, gpu=gpu, min_window=TUNE_WINDOW_S)  # uploads this rank's inputs
+    setup_s = time.perf_counter() - t0
+    metrics, consts = problem.user_metrics()
     stats = partition.run_shard(mine, device, [NVMLObserver(TUNE_WINDOW_S)], out=workdir / f"shard{dist.rank}.jsonl",
-                                user_metrics=default_metrics(problem.total_flops),
-                                constants={"total_flops": problem.total_flops})
+                                user_metrics=metrics, constants=consts)
     dist.barrier()
     slowest = dist.max(stats["seconds"])
     points = len(space.enumerate())
+    per_point_ms = 1e3 * stats["seconds"] / max(1, mine.points())
     out = {"space": "conv2d slice " + json.dumps(TUNE_SPACE, separators=(",", ":")), "points": points,
            "window_s": TUNE_WINDOW_S, "points_per_s": round(points / slowest, 3), "slowest_shard_s": round(slowest, 2),
            "shard_points": [s.points() for s in shards],
-           "timing": "wall clock of each rank's shard loop (compile excluded), max over ranks",
-           "note": "0.2 s windows see ~2 energy-counter updates: the optima below are screening values "
+           "per_point_ms_max": round(dist.max(per_point_ms), 1),
+           "fixed_cost_s": {"setup_max": round(dist.max(setup_s), 3), "compile_max": round(dist.max(compile_s), 2),
+                            "note": "per rank, outside the shard loop: input upload + device probe; NVRTC compile "
+                                    "of the shard's configs (8 host threads, cubin cache cold or warm)"},
+           "points_per_s_incl_fixed": round(points / dist.max(stats["seconds"] + setup_s + compile_s), 3),
+           "timing": "wall clock of each rank's shard loop, max over ranks",
+           "note": "0.15 s windows see 1-2 energy-counter updates: the optima below are screening values "
                    "(tune_suite.py re-measures leaders in 1 s windows; per_kernel holds the confirmed ones)"}
     if dist.rank == 0:
         merged = partition.merge(space, [workdir / f"shard{r}.jsonl" for r in range(dist.world)],
@@ -414,11 +434,22 @@ def run_ours(args, dist: Dist) -> int:
     elapsed_max = dist.max(elapsed)
     ranks_flops = dist.sum(prob.total_flops * args.steps)
     # the loop occupied the last `elapsed` seconds before t_host1; skip 0.1 s of ramp
-    summ = summarize_samples(samples, max(t_host0, t_host1 - elapsed) + 0.1, t_host1)
+    loop_t0 = max(t_host0, t_host1 - elapsed)
+    summ = summarize_samples(samples, loop_t0 + min(0.1, 0.5 * elapsed), t_host1)
+
+    # energy: a dedicated loop of the same kernel and config over the same 4 rotating sets, independent
+    # of --steps (a 20-step timed region lasts ~3 ms, far below the ~100 ms energy-counter cadence)
+    erun = gpu.bench(kernel, launch, sets[0], rotate=sets[1:], min_seconds=ENERGY_LOOP_S)
+    esumm = summarize_samples(erun.samples, erun.loop_t0 + ENERGY_SETTLE_S, erun.loop_t1)
 
     per_step = elapsed / args.steps
     value = ranks_flops / elapsed_max / 1e9
-    sm = summ["sm_mhz"] or 1965.0
+    if summ["sm_mhz"]:
+        sm, sm_basis, clock_src = summ["sm_mhz"], "observed median in the timed region", summ
+    elif esumm["sm_mhz"]:
+        sm, sm_basis, clock_src = esumm["sm_mhz"], "observed median in the energy loop (timed region unsampled)", esumm
+    else:
+        sm, sm_basis, clock_src = 1965.0, "assumed 1965 MHz max clock (no NVML clock sample)", esumm
     achieved_tf = prob.total_flops / per_step / 1e12
     peak_tf = fp32_peak_tflops(gpu.sm_count, sm)
     traffic = kernel_profile("conv2d", cfg)
@@ -472,7 +503,8 @@ def run_ours(args, dist: Dist) -> int:
                          f"{threads} threads over 32-row bands"}
 
     if dist.rank == 0:
-        gflops_per_w = prob.total_flops / (summ["counter_w"] * per_step) / 1e9 if summ["counter_w"] else None
+        ew = esumm["counter_w"]
+        gflops_per_w = prob.total_flops / (ew * erun.per_launch_s) / 1e9 if ew else None
         line = {
             "metric": METRIC,
             "value": round(value, 1),
@@ -497,9 +529,15 @@ def run_ours(args, dist: Dist) -> int:
             },
             "energy": {
                 "gflops_per_w": round(gflops_per_w, 2) if gflops_per_w else None,
-                "power_w_counter": round(summ["counter_w"], 1) if summ["counter_w"] else None,
-                "power_w_instant_median": summ["instant_w"],
-                "source": "NVML total-energy counter slope over the timed region (libjt sampler)",
+                "power_w_counter": round(ew, 1) if ew else None,
+                "power_w_instant_median": esumm["instant_w"],
+                "gflops": round(prob.total_flops / erun.per_launch_s / 1e9, 1),
+                "ms_per_launch": round(erun.per_launch_s * 1e3, 5),
+                "sm_mhz": esumm["sm_mhz"],
+                "reasons": esumm["reasons"],
+                "source": (f"NVML total-energy counter slope (libjt sampler) over a dedicated {erun.total_s:.2f} s "
+                           f"loop of {erun.reps} launches of the same kernel/config over the same 4 rotating sets, "
+                           f"from {ENERGY_SETTLE_S} s in (past the power ramp); GFLOPS/W = flop / (W x s per launch)"),
             },
             "roofline": {
                 "bound": "fp32",
@@ -508,13 +546,14 @@ def run_ours(args, dist: Dist) -> int:
                 "unit": "TFLOP/s",
                 "frac": round(achieved_tf / peak_tf, 4),
                 "traffic": traffic,
-                "peak_basis": f"FP32 FFMA peak 2 x {gpu.sm_count} SMs x 128 lanes x {sm:.0f} MHz (observed median); "
+                "peak_basis": f"FP32 FFMA peak 2 x {gpu.sm_count} SMs x 128 lanes x {sm:.0f} MHz ({sm_basis}); "
                               "MEASURED_PEAKS.json has no FP32 figure",
                 "frac_at_1965mhz": round(achieved_tf / fp32_peak_tflops(gpu.sm_count, 1965.0), 4),
                 "algorithmic_flops_per_launch": prob.total_flops,
             },
-            "clocks": {"sm_mhz": summ["sm_mhz"], "sm_max_mhz": gpu.info.max_sm_clock_mhz,
-                       "reasons": summ["reasons"], "temp_c": summ["temp_c"]},
+            "clocks": {"sm_mhz": clock_src["sm_mhz"], "sm_max_mhz": gpu.info.max_sm_clock_mhz,
+                       "reasons": sorted(set(summ["reasons"]) | set(esumm["reasons"])), "temp_c": clock_src["temp_c"],
+                       "source": sm_basis, "timed_region_samples": summ["n"]},
             "e2e": {"value": round(e2e_value, 1), "unit": "GFLOP/s",
                     "h2d_bytes_per_step": int(prob.inputs["image"].nbytes),
                     "d2h_bytes_per_step": int(prob.width * prob.height * 4),

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define JT_ABI_VERSION 2
+#define JT_ABI_VERSION 3
 
 /* Status codes and the Python exception each maps to (native.py):         */
 typedef enum {
@@ -152,6 +152,13 @@ int jt_time(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const 
 int jt_bench(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args,
              double min_seconds, int min_reps, int max_reps, int sample_period_us, jt_bench_result *out,
              jt_sample *samples, int cap);
+/* jt_bench over `n_sets` argument sets (args holds n_sets x n_args entries):
+ * launch i uses set i % n_sets, so a loop can rotate inputs/outputs larger
+ * than L2 between launches (bench.py per-kernel loops). n_sets = 1 is
+ * jt_bench. */
+int jt_bench_sets(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args,
+                  int n_sets, double min_seconds, int min_reps, int max_reps, int sample_period_us,
+                  jt_bench_result *out, jt_sample *samples, int cap);
 /* CUDA events on the context's stream: an indexed pool of `n` events for
  * timing arbitrary launch/copy sequences (bench.py). */
 int jt_events_reserve(jt_ctx *ctx, int n);

@@ -6,11 +6,14 @@ one bound :class:`~.kernels.KernelProblem` — the way Kernel Tuner's
 ``tune_kernel`` binds one kernel source to a device:
 
 * ``set_core_clock(MHz)`` — ``DomainError`` if not an NVML-supported clock;
-  otherwise locks the SM clock with ``nvmlDeviceSetGpuLockedClocks`` (no-op if
-  unchanged, settle wait only on a real change). If NVML refuses
-  (NO_PERMISSION) nothing is raised: ``clock_locked`` turns False, the
-  observed clock becomes the truth and results carry ``nvml_clock_locked=0``.
-* ``set_power_limit(W)`` — range-checked ``nvmlDeviceSetPowerManagementLimit``.
+  otherwise locks the SM clock with ``nvmlDeviceSetGpuLockedClocks`` (else
+  applications clocks; no-op if unchanged, settle wait only on a real
+  change). If NVML refuses, :class:`ControlRefusedError` is raised — the
+  tuner records a failed result with NVML's reason — except for the default
+  clock with no lock active, which is the driver-managed state itself
+  (results carry ``nvml_clock_locked=0`` and the observed clock).
+* ``set_power_limit(W)`` — range-checked ``nvmlDeviceSetPowerManagementLimit``,
+  read back; refused → :class:`ControlRefusedError`.
 * ``execute(config, duration_hint)`` — compile (NVRTC, cached) and load the
   config's module, run one probe launch and then a CUDA-event-timed
   back-to-back loop of >= max(duration_hint, min_window) seconds while the
@@ -36,12 +39,15 @@ from typing import Any, Callable, Mapping
 import numpy as np
 
 from .hardware import EXECUTION_PARAMS, DeviceSpec, DeviceState, Execution, PowerSample
-from .errors import CapabilityError, DomainError
-from .gpu import ENERGY, E_STAMP, GPU, MEM_MHZ, P_INST, REASONS, SM_MHZ, SW_POWER_CAP, TEMP, T
+from .errors import CapabilityError, ControlRefusedError, DomainError
+from .gpu import ENERGY, E_STAMP, GPU, MEM_MHZ, P_AVG, P_INST, REASONS, SM_MHZ, SW_POWER_CAP, TEMP, T
 from .kernels import KernelProblem, make_problem
 from .spaces import KernelConfig, normalize_value
 
-__all__ = ["B200Device", "counter_slope", "steady_window"]
+__all__ = ["B200Device", "counter_slope", "steady_window", "NVML_AVERAGE_WINDOW_S"]
+
+#: nvmlDeviceGetPowerUsage on Ampere and newer (incl. B200) reports power averaged over 1 s
+NVML_AVERAGE_WINDOW_S = 1.0
 
 
 def steady_window(total: float, settle: float) -> tuple[float, float]:
@@ -114,6 +120,10 @@ class B200Device:
         self.state = DeviceState(self.spec.base_clock, self.spec.power_limit_range[1])
         self._requested_clock: float | None = None
         self._requested_limit: float | None = None
+        #: which knob holds a clock lock right now ("locked" / "application" / None)
+        self._lock_kind: str | None = None
+        #: every refused controller request: {"knob", "requested", "reason", ...}
+        self.refusals: list[dict] = []
         if self.problem.gpu is not self.gpu:
             self.problem.prepare(self.gpu)
 
@@ -150,8 +160,7 @@ class B200Device:
 
     def close(self) -> None:
         try:
-            if self._requested_clock is not None:
-                self._reset_clock()
+            self._reset_clock()
             if self._requested_limit is not None:
                 self.gpu.reset_power_limit()
         finally:
@@ -168,53 +177,96 @@ class B200Device:
 
     # -- controller -----------------------------------------------------------
     def set_core_clock(self, clock: float) -> DeviceState:
+        """Lock the SM clock (reference ``device.py:277-284``).
+
+        A refused lock raises :class:`ControlRefusedError` (a failed result in
+        ``benchmark``), except for a request for the default clock while no
+        lock is active: that is the driver-managed state the board is already
+        in, measured with ``nvml_clock_locked = 0`` and the observed clock.
+        Every refusal is kept in ``refusals`` with NVML's own text.
+        """
         if clock not in self.spec.supported_core_clocks:
             raise DomainError(
                 f"{clock} MHz is not supported on {self.spec.name}; supported: {list(self.spec.supported_core_clocks)}"
             )
-        if self._requested_clock != float(clock):
-            self.clock_locked = self._apply_clock(int(clock))
-            self._requested_clock = float(clock)
-            time.sleep(self.clock_settle)
-        self.state = replace(self.state, core_clock=float(clock))
+        clock = float(clock)
+        if self._requested_clock != clock:
+            if self._apply_clock(int(clock)):
+                self.clock_locked = True
+                self._requested_clock = clock
+                time.sleep(self.clock_settle)
+            elif clock == self.spec.base_clock and self._lock_kind is None:
+                self.clock_locked = False
+                self._requested_clock = clock
+            else:
+                reason = self.gpu.last_refusal or "refused"
+                self.refusals.append({"knob": "core_clock", "requested": clock, "reason": reason,
+                                      "active_lock_mhz": self._requested_clock if self._lock_kind else None})
+                raise ControlRefusedError("core_clock", clock, reason)
+        self.state = replace(self.state, core_clock=clock)
         return self.state
 
     def _apply_clock(self, mhz: int) -> bool:
-        """Locked clocks, else applications clocks; False if NVML refuses both."""
-        if self.clock_mode in (None, "locked"):
+        """Locked clocks, else applications clocks; False if NVML refuses both.
+
+        ``_lock_kind`` remembers which knob holds the board now, independently
+        of later refusals, so :meth:`release_clock` / :meth:`close` always
+        undo a lock that is still active."""
+        if self.clock_mode in (None, "locked", "refused") and self._lock_kind in (None, "locked"):
             if self.gpu.lock_clocks(mhz, mhz):
-                self.clock_mode = "locked"
+                self.clock_mode = self._lock_kind = "locked"
                 return True
-        if self.clock_mode in (None, "application"):
+        if self.clock_mode in (None, "application", "refused") and self._lock_kind in (None, "application"):
             if self.gpu.set_app_clocks(int(self.gpu.info.mem_clock_mhz), mhz):
-                self.clock_mode = "application"
+                self.clock_mode = self._lock_kind = "application"
                 return True
-        self.clock_mode = "refused"
+        if self._lock_kind is None:
+            self.clock_mode = "refused"
         return False
 
     def release_clock(self) -> None:
         """Back to driver-managed clocks (e.g. before an untuned measurement)."""
         if self._requested_clock is not None:
+            locked = self._lock_kind is not None
             self._reset_clock()
             self._requested_clock = None
             self.clock_locked = None
-            time.sleep(self.clock_settle)
+            if locked:
+                time.sleep(self.clock_settle)
 
     def _reset_clock(self) -> None:
-        if self.clock_mode == "locked":
+        if self._lock_kind == "locked":
             self.gpu.reset_clocks()
-        elif self.clock_mode == "application":
+        elif self._lock_kind == "application":
             self.gpu.reset_app_clocks()
+        self._lock_kind = None
 
     def set_power_limit(self, watts: float) -> DeviceState:
+        """Board power limit (reference ``device.py:286-293``).
+
+        NVML refusing the change raises :class:`ControlRefusedError` unless the
+        limit already in force equals the request; an accepted change is read
+        back and must be the enforced limit."""
         lo, hi = self.spec.power_limit_range
         if not lo <= watts <= hi:
             raise DomainError(f"power limit {watts} W outside [{lo}, {hi}] W on {self.spec.name}")
-        if self._requested_limit != float(watts):
-            self.gpu.set_power_limit(float(watts))
-            self._requested_limit = float(watts)
-            time.sleep(self.clock_settle)
-        self.state = replace(self.state, power_limit=float(watts))
+        watts = float(watts)
+        if self._requested_limit != watts:
+            if self.gpu.set_power_limit(watts):
+                self._requested_limit = watts
+                time.sleep(self.clock_settle)
+                enforced = self.gpu.enforced_power_limit_w()
+                if abs(enforced - watts) > 1.0:
+                    reason = f"NVML accepted the limit but enforces {enforced:g} W"
+                    self.refusals.append({"knob": "power_limit", "requested": watts, "reason": reason})
+                    raise ControlRefusedError("power_limit", watts, reason)
+            elif abs(self.gpu.enforced_power_limit_w() - watts) <= 1.0:
+                pass  # already the limit in force: nothing to change
+            else:
+                reason = self.gpu.last_refusal or "refused"
+                self.refusals.append({"knob": "power_limit", "requested": watts, "reason": reason})
+                raise ControlRefusedError("power_limit", watts, reason)
+        self.state = replace(self.state, power_limit=watts)
         return self.state
 
     def effective_clock(self, requested: float | None = None, *, utilization: float = 1.0) -> float:
@@ -315,6 +367,8 @@ class B200Device:
             "reps": float(run.reps),
             "energy_source": source,
         }
+        # NVML's own 1 s average as the board reported it during the loop (averaged-sensor mode)
+        sensor = tuple(PowerSample(s[T] - t0, s[P_AVG]) for s in during if math.isfinite(s[P_AVG]))
         return Execution(
             runtime=run.per_launch_s,
             samples=tuple(trace),
@@ -325,6 +379,8 @@ class B200Device:
             counter_energy=None if slope is None else slope * total,
             counter_power=slope,
             telemetry=telemetry,
+            sensor_samples=sensor or None,
+            sensor_window=NVML_AVERAGE_WINDOW_S,
         )
 
     # -- helpers for workflows ---------------------------------------------------

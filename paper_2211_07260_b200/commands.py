@@ -37,7 +37,7 @@ from typing import Any
 import numpy as np
 
 from . import __version__, landscape, pmodel, recipes, records, search, steering
-from .errors import ConfigurationError, JouleTuneError
+from .errors import CapabilityError, ConfigurationError, ControlRefusedError, JouleTuneError
 from .hardware import CLOCK_PARAM
 from .observer_hooks import AveragedPowerObserver, InstantPowerObserver, NVMLObserver
 from .sensors import AveragedSensorConfig, averaged_reading, instant_energy
@@ -154,9 +154,13 @@ def cmd_simulate_sweep(args) -> int:
     if hasattr(device, "surface"):  # simulator: a full-load kernel scaling with the clock
         device.surface = ConstantSurface(reference_clock=device.spec.peak_clock, base_time=1e-3, kappa=1.0, load=1.0)
     cfg = AveragedSensorConfig(continuous_duration=args.duration)
-    samples, raw = [], []
+    samples, raw, refused = [], [], []
     for clock in _sweep_clocks(device, args.points):
-        device.set_core_clock(clock)
+        try:
+            device.set_core_clock(clock)
+        except ControlRefusedError as exc:  # real device only: no sample under a label the board never ran at
+            refused.append({"requested_mhz": clock, "reason": exc.reason})
+            continue
         run = device.execute(KernelConfig(()), duration_hint=args.duration)
         watts = _sweep_power(run, args.observer, cfg)
         volts = device.read_voltage(clock) if device.spec.voltage_readable else None
@@ -168,8 +172,15 @@ def cmd_simulate_sweep(args) -> int:
     if hasattr(device, "release_clock"):  # real device: observed clocks, capped samples out
         device.release_clock()
         samples, dropped = steering.prepare_sweep(raw, power_limit=device.spec.tdp)
-        sidecar = {"records": raw, "dropped": dropped, "clock_mode": device.clock_mode}
+        sidecar = {"records": raw, "dropped": dropped, "refused": refused, "clock_mode": device.clock_mode}
         Path(str(args.out) + ".meta.json").write_text(json.dumps(sidecar, indent=1) + "\n")
+        distinct = {round(s.frequency) for s in samples}
+        if refused and len(distinct) < 4:
+            # too few clocks the board actually ran at for a P(f) fit: no CSV, the refusal is the result
+            raise CapabilityError(
+                f"clock control refused for {len(refused)} of {len(refused) + len(raw)} sweep clocks "
+                f"({refused[0]['reason']}); {len(distinct)} usable sample(s), no sweep written "
+                f"(records in {args.out}.meta.json)")
     steering.write_samples_csv(samples, args.out)
     print(f"wrote {len(samples)} sweep samples to {args.out}")
     return 0

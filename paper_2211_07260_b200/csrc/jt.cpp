@@ -815,12 +815,21 @@ int jt_time(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *arg
 
 int jt_bench(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *args, int n_args, double min_seconds,
              int min_reps, int max_reps, int sample_period_us, jt_bench_result *out, jt_sample *samples, int cap) {
+    return jt_bench_sets(c, k, s, args, n_args, 1, min_seconds, min_reps, max_reps, sample_period_us, out, samples,
+                         cap);
+}
+
+int jt_bench_sets(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *args, int n_args, int n_sets,
+                  double min_seconds, int min_reps, int max_reps, int sample_period_us, jt_bench_result *out,
+                  jt_sample *samples, int cap) {
     if (int e = bind(c)) return e;
-    if (!k || !out) return fail(JT_EINVAL, "bad jt_bench arguments");
+    if (!k || !out || n_sets < 1) return fail(JT_EINVAL, "bad jt_bench arguments");
     if (int e = check_shape(s)) return e;
     std::memset(out, 0, sizeof *out);
-    std::vector<void *> params;
-    if (int e = pack_args(args, n_args, params)) return e;
+    // launch i uses argument set i % n_sets (inputs rotate so no launch reads an L2-warm set)
+    std::vector<std::vector<void *>> params(n_sets);
+    for (int j = 0; j < n_sets; ++j)
+        if (int e = pack_args(args + (size_t)j * n_args, n_args, params[j])) return e;
     min_reps = std::max(min_reps, 1);
     max_reps = std::max(max_reps, min_reps);
     const bool sampling = samples && cap > 0;
@@ -837,7 +846,7 @@ int jt_bench(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *ar
     // probe launch (also the warm-up): untimed by the loop, timed by events
     CUresult r;
     if ((r = D.p_cuEventRecord(c->ev_a, active(c))) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
-    if (int e = launch_on(c, k, s, params.data())) return finish(e);
+    if (int e = launch_on(c, k, s, params[0].data())) return finish(e);
     if ((r = D.p_cuEventRecord(c->ev_b, active(c))) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
     if ((r = D.p_cuEventSynchronize(c->ev_b)) != CUDA_SUCCESS) return finish(cu_fail(r, "kernel execution"));
     float ms = 0.f;
@@ -850,7 +859,7 @@ int jt_bench(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_arg *ar
     out->host_t_enqueue = mono_now();
     if ((r = D.p_cuEventRecord(c->ev_a, active(c))) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
     for (int i = 0; i < reps; ++i)
-        if (int e = launch_on(c, k, s, params.data())) return finish(e);
+        if (int e = launch_on(c, k, s, params[i % n_sets].data())) return finish(e);
     if ((r = D.p_cuEventRecord(c->ev_b, active(c))) != CUDA_SUCCESS) return finish(cu_fail(r, "cuEventRecord"));
     if ((r = D.p_cuEventSynchronize(c->ev_b)) != CUDA_SUCCESS) return finish(cu_fail(r, "kernel execution"));
     out->host_t_done = mono_now();

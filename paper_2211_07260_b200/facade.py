@@ -39,7 +39,7 @@ from .gpu import DeviceArray, Launch, f32, f64, i32, i64
 from .kernels import KernelProblem, make_problem
 from .observer_hooks import BenchmarkObserver, NVMLObserver
 from .spaces import SearchSpace
-from .records import Objective, ResultCache, UserMetric
+from .records import Objective, ResultCache, UserMetric, default_metrics
 from .search import StrategyOutcome, TuningRun, run_strategy
 
 __all__ = ["tune_kernel", "SourceProblem", "CallableMetric"]
@@ -222,16 +222,18 @@ def tune_kernel(
             checker = lambda got, ans, cfg: _verify_list(got, ans, cfg, atol)  # noqa: E731
         device = B200Device(problem, ordinal, answer=answer, verify=checker, min_window=duration)
     observers = list(observers) if observers is not None else [NVMLObserver(duration)]
-    flops = total_flops if total_flops is not None else problem.total_flops
+    if total_flops is not None:
+        defaults, consts = default_metrics(total_flops), {"total_flops": float(total_flops)}
+    else:
+        defaults, consts = problem.user_metrics()
     if metrics is None:
-        user_metrics: list[UserMetric] = [UserMetric("gflops", "total_flops / time / 1e9"),
-                                          UserMetric("gflops_per_w", "total_flops / energy / 1e9")]
+        user_metrics: list[UserMetric] = list(defaults)
     elif isinstance(metrics, Mapping):
         user_metrics = [CallableMetric(name.replace("/", "_per_").replace(" ", "_"), "0", fn=fn)
                         if callable(fn) else UserMetric(name, fn) for name, fn in metrics.items()]
     else:
         user_metrics = list(metrics)
-    consts = {"total_flops": flops, **(constants or {})}
+    consts = {**consts, **(constants or {})}
     if isinstance(cache, str):
         cache = ResultCache(cache)
     outcome = run_strategy(TuningRun(space, strategy, Objective.parse(objective), budget, seed), device, observers,

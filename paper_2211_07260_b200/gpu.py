@@ -80,6 +80,14 @@ class DeviceArray:
         check(native.lib().jt_d2h(self.gpu.handle, out.ctypes.data, self.ptr, out.nbytes), "jt_d2h")
         return out
 
+    def clone(self) -> "DeviceArray":
+        """A new allocation holding the same bytes (slack included), staged through the host."""
+        raw = np.empty(self.nbytes, np.uint8)
+        check(native.lib().jt_d2h(self.gpu.handle, raw.ctypes.data, self.ptr, self.nbytes), "jt_d2h")
+        copy = DeviceArray(self.gpu, self.nbytes, self.shape, self.dtype)
+        check(native.lib().jt_h2d(self.gpu.handle, copy.ptr, raw.ctypes.data, self.nbytes), "jt_h2d")
+        return copy
+
     def fill(self, byte: int = 0) -> None:
         check(native.lib().jt_memset_d8(self.gpu.handle, self.ptr, byte, self.nbytes), "jt_memset_d8")
         self.gpu.synchronize()
@@ -358,15 +366,21 @@ class GPU:
         max_reps: int = 1 << 20,
         sample_period_us: int = 1000,
         sample: bool = True,
+        rotate: Sequence[Sequence] = (),
     ) -> BenchRun:
-        packed = _pack(args)
+        """``jt_bench``: device-timed loop + NVML trace. ``rotate``: further argument
+        sets; launch i then uses set i % (1 + len(rotate)) (``jt_bench_sets``)."""
+        sets = [list(args), *[list(r) for r in rotate]]
+        if any(len(s) != len(args) for s in sets):
+            raise ValueError("every rotated argument set needs the same arity")
+        packed = _pack([a for s in sets for a in s])
         shape = launch.shape()
         res = JTBenchResult()
         cap = int(max(64, min(1 << 20, (min_seconds + 2.0) * 1e6 / max(sample_period_us, 100) + 64))) if sample else 0
         buf = (JTSample * max(cap, 1))()
         check(
-            native.lib().jt_bench(
-                self.handle, kernel.handle, ctypes.byref(shape), packed, len(args), float(min_seconds),
+            native.lib().jt_bench_sets(
+                self.handle, kernel.handle, ctypes.byref(shape), packed, len(args), len(sets), float(min_seconds),
                 int(min_reps), int(max_reps), int(sample_period_us), ctypes.byref(res),
                 buf if sample else None, cap,
             ),
@@ -399,35 +413,40 @@ class GPU:
         ]
 
     _REFUSED = (native.JT_ENOPERM, native.JT_ENOTSUP)
+    #: NVML's text for the last refused controller call (e.g. "nvmlDeviceSetGpuLockedClocks: Not Supported")
+    last_refusal: str | None = None
+
+    def _control(self, status: int, what: str, tolerate: tuple[int, ...] = _REFUSED) -> bool:
+        st = check(status, what, tolerate=tolerate)
+        if st != native.JT_OK:
+            self.last_refusal = native.last_error()
+        return st == native.JT_OK
 
     def lock_clocks(self, mhz_min: int, mhz_max: int) -> bool:
         """True if NVML accepted the lock; False if it refused (NO_PERMISSION or
-        NOT_SUPPORTED): recorded by the caller, never raised."""
-        st = check(native.lib().jt_clock_lock(self.handle, int(mhz_min), int(mhz_max)), "jt_clock_lock",
-                   tolerate=self._REFUSED)
-        return st == native.JT_OK
+        NOT_SUPPORTED, text in ``last_refusal``): the caller decides, never raised here."""
+        return self._control(native.lib().jt_clock_lock(self.handle, int(mhz_min), int(mhz_max)), "jt_clock_lock")
 
     def reset_clocks(self) -> bool:
-        st = check(native.lib().jt_clock_reset(self.handle), "jt_clock_reset", tolerate=self._REFUSED)
-        return st == native.JT_OK
+        return self._control(native.lib().jt_clock_reset(self.handle), "jt_clock_reset")
 
     def set_app_clocks(self, mem_mhz: int, sm_mhz: int) -> bool:
-        st = check(native.lib().jt_app_clocks_set(self.handle, int(mem_mhz), int(sm_mhz)), "jt_app_clocks_set",
-                   tolerate=self._REFUSED + (native.JT_EINVAL,))
-        return st == native.JT_OK
+        return self._control(native.lib().jt_app_clocks_set(self.handle, int(mem_mhz), int(sm_mhz)),
+                             "jt_app_clocks_set", self._REFUSED + (native.JT_EINVAL,))
 
     def reset_app_clocks(self) -> bool:
-        st = check(native.lib().jt_app_clocks_reset(self.handle), "jt_app_clocks_reset", tolerate=self._REFUSED)
-        return st == native.JT_OK
+        return self._control(native.lib().jt_app_clocks_reset(self.handle), "jt_app_clocks_reset")
 
     def set_power_limit(self, watts: float) -> bool:
-        st = check(native.lib().jt_power_limit_set(self.handle, int(round(watts * 1000))), "jt_power_limit_set",
-                   tolerate=self._REFUSED)
-        return st == native.JT_OK
+        return self._control(native.lib().jt_power_limit_set(self.handle, int(round(watts * 1000))),
+                             "jt_power_limit_set")
 
     def reset_power_limit(self) -> bool:
-        st = check(native.lib().jt_power_limit_reset(self.handle), "jt_power_limit_reset", tolerate=self._REFUSED)
-        return st == native.JT_OK
+        return self._control(native.lib().jt_power_limit_reset(self.handle), "jt_power_limit_reset")
+
+    def enforced_power_limit_w(self) -> float:
+        """The limit NVML reports now (read back after a set)."""
+        return self.refresh_info().power_limit_mw / 1000.0
 
 
 # sample tuple field indices

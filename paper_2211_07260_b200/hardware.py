@@ -85,7 +85,12 @@ class Execution:
     * ``counter_energy`` / ``counter_power`` — NVML energy-counter delta over
       the loop (J) and its slope over the steady window (W);
     * ``telemetry`` — medians of SM / memory clock, temperature and the
-      controller / throttle status over the window.
+      controller / throttle status over the window;
+    * ``sensor_samples`` / ``sensor_window`` — the board's own averaged
+      power sensor as it reported during the loop (NVML's 1 s average on
+      B200) and its averaging window (s). When present, the averaged-sensor
+      rules read this sensor instead of re-averaging the instant trace
+      (``sensors.sensor_reading``).
     """
 
     runtime: float
@@ -97,3 +102,5 @@ class Execution:
     counter_energy: float | None = None
     counter_power: float | None = None
     telemetry: Mapping[str, float] | None = None
+    sensor_samples: tuple[PowerSample, ...] | None = None
+    sensor_window: float | None = None

@@ -31,6 +31,7 @@ import numpy as np
 
 from . import native
 from .gpu import GPU, Kernel, Launch, f32, i32, rows
+from .records import UserMetric, default_metrics
 from .spaces import KernelConfig, SearchSpace
 
 __all__ = [
@@ -84,6 +85,11 @@ class KernelProblem:
 
     #: "fp32" (FFMA-pipe roofline) or "issue" (lane-instruction roofline)
     roofline_kind = "fp32"
+
+    def user_metrics(self) -> tuple[tuple, dict[str, float]]:
+        """(tuner user metrics, their constants): ``gflops`` / ``gflops_per_w`` over
+        the algorithmic flop count (``tuner.default_metrics``)."""
+        return default_metrics(self.total_flops), {"total_flops": self.total_flops}
 
     def tune_params(self) -> dict[str, list]:
         raise NotImplementedError
@@ -148,6 +154,25 @@ class KernelProblem:
         """Split one host-buffer call into ~n independent strips (None: not splittable)."""
         return None
 
+    #: buffers a rotated argument set replaces: the streamed inputs and the output
+    rotating = ("out",)
+
+    def rotation_sets(self, config: Mapping[str, Any], n: int) -> list[list]:
+        """``n - 1`` argument sets besides :meth:`args`, each over its own copies of the
+        ``rotating`` buffers (kept in ``buffers`` as ``key@j``), for loops that must not
+        re-read an L2-warm input (``GPU.bench(..., rotate=...)``). Tables stay shared."""
+        base = self.args(config)
+        sets = []
+        for j in range(1, n):
+            swap = {}
+            for key in self.rotating:
+                name = f"{key}@{j}"
+                if name not in self.buffers:
+                    self.buffers[name] = self.buffers[key].clone()
+                swap[id(self.buffers[key])] = self.buffers[name]
+            sets.append([swap.get(id(a), a) for a in base])
+        return sets
+
     # -- compilation ------------------------------------------------------------
     def options(self, config: Mapping[str, Any]) -> list[str]:
         return native._nvrtc_options(self.defines(config))
@@ -180,6 +205,7 @@ class PnPolyProblem(KernelProblem):
     roofline_kind = "issue"
     #: lane-instruction slots credited per edge test (SURVEY §8(d) convention)
     ops_per_edge = 3
+    rotating = ("points", "out")
 
     @property
     def edge_tests(self) -> float:
@@ -369,9 +395,10 @@ class PnPolySlabProblem(PnPolyProblem):
     Same inputs and the same bitmap as :class:`PnPolyProblem` at METHOD 2
     (bit for bit: the skipped edges are exactly those whose y-test fails), but
     a different amount of work, so it is reported as its own kernel: its
-    roofline is HBM (the 240 MB of points and bitmap), and ``total_flops``
-    keeps the brute-force edge-test count so GFLOP/s compares 1:1 with the
-    brute-force kernel on the same output.
+    roofline is HBM (the 240 MB of points and bitmap). It is not credited with
+    the brute-force edge tests it skips: ``total_flops`` raises, and its
+    metrics are points/s, GB/s and joules per bitmap (:meth:`user_metrics`).
+    ``edge_tests`` stays the brute-force-equivalent count, for reference only.
     """
 
     name: str = "pnpoly_slab"
@@ -381,6 +408,18 @@ class PnPolySlabProblem(PnPolyProblem):
     roofline_kind = "hbm"
     #: slab lists are padded to a multiple of this (4 edges per trip of the edge loop)
     pad = 4
+
+    @property
+    def total_flops(self) -> float:
+        from .errors import ConfigurationError
+
+        raise ConfigurationError(f"{self.name} skips most edge tests and is not flop-counted; "
+                                 "use user_metrics() (points/s, GB/s, J per bitmap)")
+
+    def user_metrics(self):
+        return ((UserMetric("points_per_s", "n_points / time"), UserMetric("gb_per_s", "hbm_bytes / time / 1e9"),
+                 UserMetric("j_per_bitmap", "energy"), UserMetric("points_per_j", "n_points / energy")),
+                {"n_points": float(self.n_points), "hbm_bytes": float(self.algorithmic_bytes)})
 
     def tune_params(self):
         return {
@@ -736,6 +775,7 @@ class Conv2DProblem(KernelProblem):
     source: str = "conv2d.cu"
     symbol: str = "conv2d"
     seed: int = 3
+    rotating = ("image", "out")
     width: int = 4096
     height: int = 4096
     fw: int = 17
@@ -858,6 +898,7 @@ class SgemmProblem(KernelProblem):
     beta: float = 0.5
     #: "paper": Kernel Tuner's CLBlast value lists; "b200": widened for 227 KB smem / 255 regs
     value_set: str = "paper"
+    rotating = ("at", "b", "out")
 
     @property
     def total_flops(self) -> float:
@@ -1039,6 +1080,15 @@ class SgemmTF32Problem(SgemmProblem):
         counters.fill(0)
         self.buffers["counters"] = counters
 
+    def rotation_sets(self, config, n):
+        """As the base class, plus TMA descriptors of each set's own A and B copies."""
+        sets = super().rotation_sets(config, n)
+        sw = self.gpu.SWIZZLE_128B_ATOM_32B
+        for j, args in enumerate(sets, start=1):
+            args[0] = self.gpu.tensor_map_2d(self.buffers[f"at@{j}"], self.k, self.m, 32, 32, sw)
+            args[1] = self.gpu.tensor_map_2d(self.buffers[f"b@{j}"], self.k, self.n, 32, 32, sw)
+        return sets
+
     def args(self, config):
         c = _as_dict(config)
         b = self.buffers
@@ -1056,6 +1106,7 @@ class BurnerProblem(KernelProblem):
     name: str = "burner"
     source: str = "burner.cu"
     symbol: str = "burner"
+    rotating = ()
     iters: int = 4096
     blocks_per_sm: int = 8
 

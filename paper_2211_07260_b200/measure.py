@@ -27,7 +27,7 @@ from .hardware import CLOCK_PARAM, POWER_LIMIT_PARAM
 from .errors import ConfigurationError, JouleTuneError, MeasurementError
 from .observer_hooks import AveragedPowerObserver, BenchmarkObserver, InstantPowerObserver, NVMLObserver
 from .records import CORE_FIELDS, BenchmarkResult, UserMetric
-from .sensors import AveragedSensorConfig, TracePlayback, averaged_reading, instant_energy
+from .sensors import AveragedSensorConfig, TracePlayback, instant_energy, sensor_reading
 from .spaces import KernelConfig
 
 __all__ = ["MeasurementSetup", "benchmark"]
@@ -124,7 +124,7 @@ def _measure(device, config, setup: MeasurementSetup, user_metrics, constants) -
 
     runtime = run.runtime
     if mode == "averaged":
-        watts = averaged_reading(run.samples, run.total_duration, setup.averaged)
+        watts = sensor_reading(run, run.total_duration, setup.averaged)
     elif mode == "counter":
         if run.counter_power is None:
             raise MeasurementError("device reported no energy-counter reading")

@@ -48,7 +48,7 @@ EXPORTS = (
     "jt_abi_version", "jt_now", "jt_last_error", "jt_device_count", "jt_open", "jt_close",
     "jt_device_info_get", "jt_alloc", "jt_free", "jt_host_alloc", "jt_host_free", "jt_h2d", "jt_d2h",
     "jt_memset_d8", "jt_synchronize", "jt_compile", "jt_free_image", "jt_module_load", "jt_module_unload",
-    "jt_kernel_get", "jt_kernel_attributes", "jt_launch", "jt_time", "jt_bench", "jt_l2_flush",
+    "jt_kernel_get", "jt_kernel_attributes", "jt_launch", "jt_time", "jt_bench", "jt_bench_sets", "jt_l2_flush",
     "jt_sample_now", "jt_sampler_start", "jt_sampler_stop", "jt_clock_lock", "jt_clock_reset",
     "jt_app_clocks_set", "jt_app_clocks_reset", "jt_power_limit_set", "jt_power_limit_reset",
     "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
@@ -215,6 +215,11 @@ def _declare(lib) -> None:
             c.c_int,
             [P, P, c.POINTER(JTLaunchShape), c.POINTER(JTArg), c.c_int, c.c_double, c.c_int, c.c_int, c.c_int,
              c.POINTER(JTBenchResult), c.POINTER(JTSample), c.c_int],
+        ),
+        "jt_bench_sets": (
+            c.c_int,
+            [P, P, c.POINTER(JTLaunchShape), c.POINTER(JTArg), c.c_int, c.c_int, c.c_double, c.c_int, c.c_int,
+             c.c_int, c.POINTER(JTBenchResult), c.POINTER(JTSample), c.c_int],
         ),
         "jt_l2_flush": (c.c_int, [P]),
         "jt_events_reserve": (c.c_int, [P, c.c_int]),

@@ -23,8 +23,8 @@ from .errors import ConfigurationError, MeasurementError, SensorNotReadyError
 from .hardware import Execution, PowerSample
 from .spaces import KernelConfig
 
-__all__ = ["AveragedSensorConfig", "InstantSensorConfig", "averaged_reading", "instant_energy", "ContinuousResult",
-           "continuous_benchmark", "TracePlayback"]
+__all__ = ["AveragedSensorConfig", "InstantSensorConfig", "averaged_reading", "sensor_reading", "instant_energy",
+           "ContinuousResult", "continuous_benchmark", "TracePlayback"]
 
 
 @dataclass(frozen=True)
@@ -94,6 +94,34 @@ def averaged_reading(
     return area / width
 
 
+def sensor_reading(execution: Execution, t: float, cfg: AveragedSensorConfig | None = None) -> float:
+    """What the averaged sensor reports at ``t`` for one execution.
+
+    Simulated traces: :func:`averaged_reading` over the instant trace (the
+    reference rule, ``observers.py:81-107``). A real board with its own
+    averaging sensor (``execution.sensor_samples``, NVML's 1 s average on
+    B200): the value that sensor reported at or before ``t``. Its window is
+    fixed by the hardware, so ``cfg.refresh_rate`` must be its inverse (1 Hz
+    on B200) — anything else is a configuration error, not a silently
+    different measurement — and nothing is ready before one full window.
+    """
+    cfg = cfg or AveragedSensorConfig()
+    if execution.sensor_samples is None:
+        return averaged_reading(execution.samples, t, cfg)
+    width = float(execution.sensor_window or 1.0)
+    if abs(1.0 / cfg.refresh_rate - width) > 1e-6 * width:
+        raise ConfigurationError(
+            f"this device's averaged sensor reports {width:g} s averages: refresh_rate must be {1.0 / width:g} Hz "
+            f"(got {cfg.refresh_rate:g} Hz)")
+    if t < width - 1e-9:
+        raise SensorNotReadyError(f"no completed {width:.3g}s window at t={t:.6g}s")
+    # the board's average covers (t_s - width, t_s]: only readings whose window lies inside the trace
+    ready = [s for s in execution.sensor_samples if width - 1e-9 <= s.timestamp <= t + 1e-12 and math.isfinite(s.power)]
+    if not ready:
+        raise MeasurementError(f"the averaged sensor reported nothing in [{width:.3g}, {t:.6g}] s")
+    return ready[-1].power
+
+
 def instant_energy(samples: Sequence[PowerSample], t0: float, t1: float) -> float:
     """Median sample power inside [t0, t1] times the elapsed time."""
     if t0 >= t1:
@@ -139,7 +167,7 @@ def continuous_benchmark(device, config: KernelConfig, cfg: AveragedSensorConfig
             stacklevel=2,
         )
     run = device.execute(config, duration_hint=0.0 if too_long else cfg.continuous_duration)
-    watts = averaged_reading(run.samples, run.total_duration, cfg)
+    watts = sensor_reading(run, run.total_duration, cfg)
     return ContinuousResult(
         energy=watts * run.total_duration,
         mean_power=watts,
@@ -175,9 +203,9 @@ class TracePlayback:
         return _value_at(self.execution.samples, self._stamps, self.now)
 
     def averaged_power(self, cfg: AveragedSensorConfig) -> float:
-        return averaged_reading(self.execution.samples, self.now, cfg)
+        return sensor_reading(self.execution, self.now, cfg)
 
     def final_averaged_power(self, cfg: AveragedSensorConfig) -> float:
-        return averaged_reading(self.execution.samples, self.total_duration, cfg)
+        return sensor_reading(self.execution, self.total_duration, cfg)
 
 

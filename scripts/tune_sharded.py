@@ -65,8 +65,8 @@ def main():
         lambda ordinal: B200Device(problem, ordinal, min_window=args.duration),
         lambda: [NVMLObserver(args.duration)],
         workdir=args.workdir, rank=rank, world=world, local_rank=local, barrier=barrier,
-        objective=Objective("energy"), user_metrics=default_metrics(problem.total_flops),
-        constants={"total_flops": problem.total_flops},
+        objective=Objective("energy"), user_metrics=problem.user_metrics()[0],
+        constants=problem.user_metrics()[1],
     )
     if rank == 0:
         best_t = min((r for r in out.history if not r.failed), key=lambda r: r.time)

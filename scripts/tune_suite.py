@@ -150,8 +150,7 @@ def confirm(dev, problem, leaders) -> list[dict]:
             "config": r.config.as_dict(),
             "time_s": t,
             "energy_j": t * w,
-            "gflops": problem.total_flops / t / 1e9,
-            "gflops_per_w": problem.total_flops / (t * w) / 1e9,
+            **rates(problem, t, w),
             "power_w": w,
             "sm_clock_mhz": tel.get("sm_clock"),
             "temperature_c": tel.get("temperature"),
@@ -160,6 +159,15 @@ def confirm(dev, problem, leaders) -> list[dict]:
             "n": len(got),
         })
     return out
+
+
+def rates(problem, t: float, w: float) -> dict:
+    """Per-config figures: GFLOP/s and GFLOPS/W for flop-counted kernels; points/s, GB/s and
+    joules per bitmap for the PnPoly kernels that skip edge tests (no brute-force flop credit)."""
+    if problem.roofline_kind == "hbm":
+        return {"points_per_s": problem.n_points / t, "gb_per_s": problem.algorithmic_bytes / t / 1e9,
+                "j_per_bitmap": t * w}
+    return {"gflops": problem.total_flops / t / 1e9, "gflops_per_w": problem.total_flops / (t * w) / 1e9}
 
 
 def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | None) -> dict:
@@ -181,14 +189,14 @@ def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | No
     dev = B200Device(problem, gpu=gpu, min_window=duration)
     RESULTS.mkdir(exist_ok=True)
     cache = ResultCache(RESULTS / f"cache_{name}.jsonl")
-    metrics = default_metrics(problem.total_flops)
+    metrics, consts = problem.user_metrics()
     t0 = time.time()
     outcome = run_strategy(
         TuningRun(space, strategy, Objective("energy"), budget=budget, seed=seed),
         dev,
         [NVMLObserver(duration)],
         user_metrics=metrics,
-        constants={"total_flops": problem.total_flops},
+        constants=consts,
         cache=cache,
     )
     # known-good seeds (hand-explored, scripts/time_sgemm.py) join the sampled configs
@@ -197,7 +205,7 @@ def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | No
             {**c, "FMA2": 1} for c in [tuned_entry_config("sgemm")] if c]):
         one = SearchSpace.from_dict({"parameters": {k: [v] for k, v in seed_cfg.items()}})
         seeded += run_strategy(TuningRun(one, "exhaustive", Objective("energy")), dev, [NVMLObserver(duration)],
-                               user_metrics=metrics, constants={"total_flops": problem.total_flops},
+                               user_metrics=metrics, constants=consts,
                                cache=cache).history
     tune_s = time.time() - t0
     ok = [r for r in outcome.history + seeded if not r.failed]

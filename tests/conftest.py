@@ -50,3 +50,22 @@ def reference():
     import jouletune
 
     return jouletune
+
+
+FULL_PIN = ROOT / "tests" / "golden" / "pnpoly_full_pin.json"
+
+
+def assert_full_size_pin(bitmap) -> None:
+    """A full-size (BASELINE) PnPoly bitmap against tests/golden/pnpoly_full_pin.json: it must be the
+    formula-2 bitmap bit for bit, which differs from the paper's Kernel-Tuner op order (formula 0)
+    at exactly the recorded points."""
+    import hashlib
+
+    import numpy as np
+
+    pin = json.loads(FULL_PIN.read_text())
+    got = np.ascontiguousarray(bitmap, dtype=np.int32)
+    assert got.size == pin["n_points"]
+    assert hashlib.sha256(got.tobytes()).hexdigest() == pin["sha256"]["formula2"]
+    for d in pin["formula0_vs_formula2_differ"]:
+        assert got[d["index"]] == d["formula2"] != d["formula0"]

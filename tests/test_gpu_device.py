@@ -66,15 +66,72 @@ def test_instant_observer_window_rule(conv_device):
 
 def test_clock_request_recorded_and_unsupported_clock_fails(conv_device):
     cfg = B.KernelConfig.from_dict({**conv_device.problem.default_config(),
-                                    "nvml_gr_clock": conv_device.spec.peak_clock})
+                                    "nvml_gr_clock": conv_device.spec.base_clock})
     res = B.benchmark(conv_device, cfg, [B.NVMLObserver(0.2)])
-    assert not res.failed
+    assert not res.failed, res.failure_reason  # locked, or the driver-managed default clock
     assert conv_device.clock_mode in ("locked", "application", "refused")
+    lower = [c for c in conv_device.spec.supported_core_clocks if c < 0.8 * conv_device.spec.base_clock][-1]
+    low = B.benchmark(conv_device, B.KernelConfig.from_dict({**cfg.as_dict(), "nvml_gr_clock": lower}),
+                      [B.NVMLObserver(0.2)])
     if conv_device.clock_mode == "refused":
         assert res.observer_results["nvml_clock_locked"] == 0.0
+        # a refused clock is a failed result carrying NVML's reason, never a mislabelled measurement
+        assert low.failed and "ControlRefusedError" in low.failure_reason
+        assert conv_device.refusals and conv_device.refusals[-1]["requested"] == lower
+    else:
+        assert not low.failed and low.observer_results["nvml_sm_clock"] <= lower + 15
     bad = B.KernelConfig.from_dict({**conv_device.problem.default_config(), "nvml_gr_clock": 1234.5})
     res = B.benchmark(conv_device, bad, [B.NVMLObserver(0.2)])
     assert res.failed and "DomainError" in res.failure_reason
+    conv_device.release_clock()
+
+
+def test_power_limit_request_is_applied_or_failed(conv_device):
+    cfg = B.KernelConfig.from_dict({**conv_device.problem.default_config(), "nvml_pwr_limit": 600})
+    res = B.benchmark(conv_device, cfg, [B.NVMLObserver(0.2)])
+    if res.failed:
+        assert "ControlRefusedError" in res.failure_reason and "power_limit" in res.failure_reason
+    else:  # accepted: the limit was read back as enforced
+        assert conv_device.gpu.enforced_power_limit_w() == pytest.approx(600.0, abs=1.0)
+    conv_device.gpu.reset_power_limit()
+
+
+def test_continuous_benchmark_through_probe_runtime(conv_device):
+    """Averaged-sensor mode on B200 (reference observers.py:136-172): the runtime probe is a CUDA-event
+    launch (probe_runtime, not the simulator's surface) and the reading is NVML's own 1 s average."""
+    cfg = B.KernelConfig.from_dict(conv_device.problem.default_config())
+    probe = conv_device.probe_runtime(cfg)
+    assert 1e-6 < probe < 0.1
+    sensor = B.AveragedSensorConfig(refresh_rate=1.0, continuous_duration=2.0)
+    out = B.continuous_benchmark(conv_device, cfg, sensor)
+    assert not out.long_kernel and out.repetitions > 100 and out.duration >= 2.0
+    assert 150.0 < out.mean_power < 1200.0 and out.energy == pytest.approx(out.mean_power * out.duration)
+    # same loop through the energy counter: the board's 1 s average agrees within 15 %
+    res = B.benchmark(conv_device, cfg, [B.NVMLObserver(2.0)])
+    assert abs(out.mean_power - res.observer_results["nvml_power"]) < 0.15 * res.observer_results["nvml_power"]
+    with pytest.raises(B.ConfigurationError):  # NVML's window is 1 s: a 10 Hz sensor config is a caller mistake
+        B.continuous_benchmark(conv_device, cfg, B.AveragedSensorConfig(refresh_rate=10.0, continuous_duration=1.0))
+    # the averaged observer through benchmark() reads the same sensor
+    avg = B.benchmark(conv_device, cfg, [B.AveragedPowerObserver(sensor)], averaged_cfg=sensor)
+    assert not avg.failed and 150.0 < avg.observer_results["nvml_power"] < 1200.0
+
+
+def test_simulate_sweep_cli_on_b200(tmp_path):
+    """``simulate-sweep --device b200`` (reference cli.py:132-176) end to end on the real board: a P(f)
+    sweep when clock control works, else exit 1 with every refusal recorded and no sweep written."""
+    from paper_2211_07260_b200 import commands
+    import json
+
+    out = tmp_path / "sweep.csv"
+    rc = commands.main(["simulate-sweep", "--device", "b200:burner", "--out", str(out), "--points", "5",
+                        "--observer", "nvml", "--duration", "0.3"])
+    meta = json.loads((tmp_path / "sweep.csv.meta.json").read_text())
+    if meta["clock_mode"] == "refused":
+        assert rc == 1 and not out.exists()
+        assert len(meta["refused"]) == 4 and all(r["reason"] for r in meta["refused"])
+        assert len(meta["records"]) == 1 and meta["records"][0]["clock_locked"] == 0.0
+    else:
+        assert rc == 0 and out.exists() and len(meta["records"]) == 5
 
 
 def test_invalid_launch_is_a_failed_result_not_a_crash(gpu):

@@ -9,6 +9,7 @@ import itertools
 
 import numpy as np
 import pytest
+from conftest import assert_full_size_pin
 
 from oracle import kernels_oracle as O
 
@@ -118,8 +119,29 @@ def test_pnpoly_full_size_tuned_bit_exact(gpu):
         got = run_once(gpu, p, cfg)
         want = O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], p.formula(cfg))
         assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ"
+        assert_full_size_pin(got)  # == formula 2; differs from the paper op order exactly where pinned
         # formula 3 (sign-bit) and the IEEE-compare formula 2 agree on this input
         assert np.array_equal(want, O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2))
+
+
+def test_pnpoly_full_size_paper_op_order(gpu):
+    """The brute-force kernel in the paper's Kernel-Tuner op order (METHOD 0: (dx*(py-vy))/dy + vx with IEEE
+    rounding per op) over the whole BASELINE input reproduces the formula-0 oracle bitmap bit for bit
+    (pinned by SHA-256 in tests/golden/pnpoly_full_pin.json)."""
+    import hashlib
+    import json
+
+    from conftest import FULL_PIN
+    from paper_2211_07260_b200.kernels import PnPolyProblem
+
+    pin = json.loads(FULL_PIN.read_text())
+    p = PnPolyProblem()
+    p.prepare(gpu)
+    for cfg in (dict(p.default_config(), method=0, asm=0), dict(p.default_config(), method=0, asm=0, poly_smem=0)):
+        got = np.ascontiguousarray(run_once(gpu, p, cfg), dtype=np.int32)
+        assert hashlib.sha256(got.tobytes()).hexdigest() == pin["sha256"]["formula0"], cfg
+        for d in pin["formula0_vs_formula2_differ"]:
+            assert got[d["index"]] == d["formula0"]
 
 
 # -- Conv2D ------------------------------------------------------------------------------

@@ -5,6 +5,7 @@ import itertools
 
 import numpy as np
 import pytest
+from conftest import assert_full_size_pin
 
 from oracle import kernels_oracle as O
 
@@ -97,6 +98,7 @@ def test_slab_matches_brute_force_kernel_full_size(gpu):
                                     tuned.best_config("pnpoly_slab", "energy_optimal")] if c}.values():
         got = run_once(gpu, p, cfg)
         assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ ({cfg})"
+        assert_full_size_pin(got)  # == formula 2; differs from the paper op order exactly where pinned
 
 
 @pytest.mark.parametrize("strips", [1, 5])
@@ -272,6 +274,7 @@ def test_grid_full_size_matches_brute_force(gpu):
                                     tuned.best_config("pnpoly_grid", "energy_optimal")] if c}.values():
         got = run_once(gpu, p, cfg)
         assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ ({cfg})"
+        assert_full_size_pin(got)  # == formula 2; differs from the paper op order exactly where pinned
     assert p.clean_fraction(512) > 0.9
 
 
@@ -327,4 +330,5 @@ def test_cells_full_size_matches_brute_force(gpu):
                                     tuned.best_config("pnpoly_cells", "energy_optimal")] if c}.values():
         got = run_once(gpu, p, cfg)
         assert np.array_equal(got, want), f"{int((got != want).sum())} of 20M points differ ({cfg})"
+        assert_full_size_pin(got)  # == formula 2; differs from the paper op order exactly where pinned
     assert p.clean_fraction(512) > 0.9

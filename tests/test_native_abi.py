@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing
     assert set(names) == set(native.EXPORTS)
-    assert native.lib().jt_abi_version() == 2
+    assert native.lib().jt_abi_version() == 3
 
 
 def test_no_gpu_means_capability_error_not_fallback():
