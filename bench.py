@@ -318,7 +318,7 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: 
 #: each of 8 ranks measures >= 64 of them
 TUNE_SPACE = {"block_size_x": [32, 64], "block_size_y": [2, 4, 8, 16], "tile_size_x": [2, 4, 8],
               "tile_size_y": [1, 2, 4], "use_shmem": [0, 1], "use_padding": [0], "fma2": [0, 1], "min_blocks": [0, 2]}
-TUNE_WINDOW_S = 0.15  # launch loop per point: >= 1 energy-counter update (~100 ms cadence)
+TUNE_WINDOW_S = 0.25  # launch loop per point: >= 2 energy-counter updates (~100 ms cadence)
 
 
 def tuning_leg(gpu, dist: Dist) -> dict:
@@ -372,7 +372,7 @@ def tuning_leg(gpu, dist: Dist) -> dict:
                                     "of the shard's configs (8 host threads, cubin cache cold or warm)"},
            "points_per_s_incl_fixed": round(points / dist.max(stats["seconds"] + setup_s + compile_s), 3),
            "timing": "wall clock of each rank's shard loop, max over ranks",
-           "note": "0.15 s windows see 1-2 energy-counter updates: the optima below are screening values "
+           "note": "0.25 s windows see 2-3 energy-counter updates: the optima below are screening values "
                    "(tune_suite.py re-measures leaders in 1 s windows; per_kernel holds the confirmed ones)"}
     if dist.rank == 0:
         merged = partition.merge(space, [workdir / f"shard{r}.jsonl" for r in range(dist.world)],

@@ -145,10 +145,12 @@ int jt_launch(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, cons
 /* Event-timed loop of exactly `reps` launches; *seconds = total device time. */
 int jt_time(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args,
             int reps, double *seconds);
-/* The benchmark primitive: one probe launch, then reps = clamp(ceil(min_seconds
- * / probe), min_reps, max_reps) back-to-back launches between two CUDA events
- * while the NVML sampler records every `sample_period_us` into `samples`
- * (capacity `cap`; may be NULL to skip sampling). */
+/* The benchmark primitive: one probe launch, then back-to-back launches
+ * between two CUDA events while the NVML sampler records every
+ * `sample_period_us` into `samples` (capacity `cap`; may be NULL to skip
+ * sampling). The loop lasts >= min_seconds: its first quarter (sized from the
+ * probe) is timed on its own and the remaining launch count recomputed from it
+ * while a second quarter keeps the GPU busy; reps stays in [min_reps, max_reps]. */
 int jt_bench(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args,
              double min_seconds, int min_reps, int max_reps, int sample_period_us, jt_bench_result *out,
              jt_sample *samples, int cap);
@@ -174,6 +176,15 @@ int jt_stream_wait_event(jt_ctx *ctx, int event_index);   /* selected stream wai
 /* Async copies on the selected stream (host memory should be pinned). */
 int jt_h2d_async(jt_ctx *ctx, unsigned long long dst, const void *src, size_t bytes);
 int jt_d2h_async(jt_ctx *ctx, void *dst, unsigned long long src, size_t bytes);
+/* Pitched (2D) async copies on the selected stream: `rows` rows of
+ * `width_bytes`, row starts `*_pitch` bytes apart. The host-buffer API uses
+ * them to place an arbitrary M x N operand inside a buffer padded to the
+ * kernel's tile multiples (CLBlast's "indirect" GEMM padding, done by the
+ * copy engines) and to read the valid region back. */
+int jt_h2d_2d_async(jt_ctx *ctx, unsigned long long dst, size_t dst_pitch, const void *src, size_t src_pitch,
+                    size_t width_bytes, size_t rows);
+int jt_d2h_2d_async(jt_ctx *ctx, void *dst, size_t dst_pitch, unsigned long long src, size_t src_pitch,
+                    size_t width_bytes, size_t rows);
 /* Overwrite a scratch buffer larger than L2 (126 MB on B200). */
 int jt_l2_flush(jt_ctx *ctx);
 

@@ -291,6 +291,21 @@ class GPU:
     def d2h_async(self, host: np.ndarray, src: "DeviceArray") -> None:
         check(native.lib().jt_d2h_async(self.handle, host.ctypes.data, src.ptr, host.nbytes), "jt_d2h_async")
 
+    def h2d_2d_async(self, dst: "DeviceArray", dst_pitch: int, host: np.ndarray) -> None:
+        """A row-major 2D host array into the top-left of a pitched device buffer (``dst_pitch`` bytes/row)."""
+        host = np.ascontiguousarray(host)
+        rows, row_bytes = host.shape[0], host.strides[0]
+        check(native.lib().jt_h2d_2d_async(self.handle, dst.ptr, int(dst_pitch), host.ctypes.data, row_bytes,
+                                            row_bytes, rows), "jt_h2d_2d_async")
+
+    def d2h_2d_async(self, host: np.ndarray, src: "DeviceArray", src_pitch: int) -> None:
+        """The top-left ``host.shape`` block of a pitched device buffer into a C-contiguous host array."""
+        if not host.flags.c_contiguous:
+            raise ValueError("destination must be C-contiguous")
+        rows, row_bytes = host.shape[0], host.strides[0]
+        check(native.lib().jt_d2h_2d_async(self.handle, host.ctypes.data, row_bytes, src.ptr, int(src_pitch),
+                                            row_bytes, rows), "jt_d2h_2d_async")
+
     SWIZZLE_128B = 3
     SWIZZLE_128B_ATOM_32B = 4
 

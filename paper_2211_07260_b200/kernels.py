@@ -113,17 +113,35 @@ class KernelProblem:
         return space.is_valid(KernelConfig.from_dict({k: merged[k] for k in space.names}))
 
     def fitting_config(self, preferred: list) -> dict[str, Any]:
-        """First valid config among ``preferred`` (None entries skipped), else the
-        valid config closest (Hamming) to the default."""
-        for cfg in preferred:
-            if cfg and self.is_valid(cfg):
+        """First valid config among ``preferred`` (None entries skipped).
+
+        Raises ``ConfigurationError`` naming the restrictions the first candidate
+        breaks when none fits this problem's shape (no search over the space)."""
+        from .errors import ConfigurationError
+
+        candidates = [c for c in preferred if c]
+        for cfg in candidates:
+            if self.is_valid(cfg):
                 return {**self.default_config(), **cfg}
-        default = self.default_config()
-        best = min(self.space().enumerate(), key=lambda c: sum(c[k] != default.get(k) for k in c))
-        return best.as_dict()
+        first = {**self.default_config(), **(candidates[0] if candidates else {})}
+        broken = self.broken_restrictions(first)
+        raise ConfigurationError(f"{self.name}: no tuned or default config fits this shape; {first} breaks "
+                                 f"{broken or 'the value lists'}")
+
+    def broken_restrictions(self, config: Mapping[str, Any]) -> list[str]:
+        """The restriction expressions ``config`` violates on this problem's shape."""
+        from .expressions import Expression
+
+        env = {**self.default_config(), **_as_dict(config)}
+        return [r for r in self.restrictions() if not Expression(r)(env)]
 
     def defines(self, config: Mapping[str, Any]) -> dict[str, Any]:
         return {k.upper(): v for k, v in config.items()}
+
+    def tile_multiples(self, config: Mapping[str, Any]) -> dict[str, int]:
+        """Problem-size fields and the multiple ``config`` needs each of them to be
+        (the host API pads other shapes up to these, ``suite``); {} = any size."""
+        return {}
 
     def launch(self, config: Mapping[str, Any]) -> Launch:
         raise NotImplementedError
@@ -836,6 +854,10 @@ class Conv2DProblem(KernelProblem):
             "FH": self.fh,
         }
 
+    def tile_multiples(self, config):
+        c = _as_dict(config)
+        return {"width": c["block_size_x"] * c["tile_size_x"], "height": c["block_size_y"] * c["tile_size_y"]}
+
     def launch(self, config):
         c = _as_dict(config)
         gx = self.width // (c["block_size_x"] * c["tile_size_x"])
@@ -953,6 +975,10 @@ class SgemmProblem(KernelProblem):
     def defines(self, config):
         return dict(_as_dict(config))
 
+    def tile_multiples(self, config):
+        c = _as_dict(config)
+        return {"m": c["MWG"], "n": c["NWG"], "k": c["KWG"]}
+
     def launch(self, config):
         c = _as_dict(config)
         stages = c.get("ASYNC", 0)
@@ -1021,6 +1047,10 @@ class SgemmTF32Problem(SgemmProblem):
         if c.get("PERSIST", 0):
             d["SPLIT_TAIL"] = c.get("SPLIT_TAIL", 0)
         return d
+
+    def tile_multiples(self, config):
+        c = _as_dict(config)
+        return {"m": 128 * (1 + c.get("PAIR", 0)), "n": c["BN"], "k": 32}
 
     def _variant(self, config) -> tuple[str, str]:
         """(source file, kernel symbol): CTA-pair (cta_group::2), persistent warp-specialised, or one

@@ -53,7 +53,8 @@ EXPORTS = (
     "jt_app_clocks_set", "jt_app_clocks_reset", "jt_power_limit_set", "jt_power_limit_reset",
     "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
     "jt_h2d_async", "jt_d2h_async", "jt_tensor_map_2d", "jt_streams_reserve", "jt_stream_select",
-    "jt_stream_wait_event", "jt_pnpoly_slabs", "jt_pnpoly_grid", "jt_pnpoly_cells",
+    "jt_stream_wait_event", "jt_pnpoly_slabs", "jt_pnpoly_grid", "jt_pnpoly_cells", "jt_h2d_2d_async",
+    "jt_d2h_2d_async",
 )
 
 
@@ -231,6 +232,8 @@ def _declare(lib) -> None:
         "jt_stream_wait_event": (c.c_int, [P, c.c_int]),
         "jt_tensor_map_2d": (c.c_int, [P, c.c_ulonglong, c.c_ulonglong, c.c_ulonglong, c.c_uint, c.c_uint, c.c_int, P]),
         "jt_d2h_async": (c.c_int, [P, P, c.c_ulonglong, c.c_size_t]),
+        "jt_h2d_2d_async": (c.c_int, [P, c.c_ulonglong, c.c_size_t, P, c.c_size_t, c.c_size_t, c.c_size_t]),
+        "jt_d2h_2d_async": (c.c_int, [P, P, c.c_size_t, c.c_ulonglong, c.c_size_t, c.c_size_t, c.c_size_t]),
         "jt_sample_now": (c.c_int, [P, c.POINTER(JTSample)]),
         "jt_sampler_start": (c.c_int, [P, c.c_int, c.c_int]),
         "jt_sampler_stop": (c.c_int, [P, c.POINTER(JTSample), c.c_int, c.POINTER(c.c_int)]),

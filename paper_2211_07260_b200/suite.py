@@ -17,6 +17,7 @@ from typing import Any, Mapping
 import numpy as np
 
 from . import tuned
+from .errors import ConfigurationError
 from .gpu import GPU
 from .kernels import KernelProblem, make_problem
 
@@ -167,18 +168,106 @@ class Runner:
         return out
 
 
-def _runner(name: str, key: tuple, config, problem_kwargs: dict, inputs: dict, ordinal: int) -> Runner:
-    problem = make_problem(name, **problem_kwargs)
+class PaddedRunner(Runner):
+    """A problem prepared at its tile-padded size; calls copy the valid region in and out.
+
+    Shapes the tuned kernels cannot tile exactly (conv2d 4095^2, SGEMM 1000^3) run
+    on buffers padded up to the config's tile multiples, CLBlast's "indirect"
+    approach: operands go in with pitched copies (the padding stays zero, so the
+    extra K terms of a GEMM are 0 * 0 and conv2d outputs only read their own
+    window), a row-major A is transposed and padded on the device
+    (``csrc/kernels/layout.cu``) instead of on the host, and only the valid block
+    of the result comes back.
+    """
+
+    def __init__(self, problem: KernelProblem, config, gpu: GPU, inputs, shape: dict[str, int]):
+        super().__init__(problem, config, gpu, inputs)
+        self.shape = shape  # the caller's (unpadded) sizes
+        out = problem.buffers.get("out")
+        if out is not None:  # inputs were prepared from zeros; padding regions start (and stay) zero
+            out.fill(0)
+        self._transpose = None
+        self._staging = None
+
+    def transpose_kernel(self):
+        if self._transpose is None:
+            from . import native
+
+            cubin = native.compile_cubin(native.kernel_source("layout.cu"), "layout", native._nvrtc_options({}))
+            self._transpose = self.gpu.load(cubin, "transpose_pad")
+        return self._transpose
+
+    def run_gemm(self, a: np.ndarray, b: np.ndarray, c: np.ndarray) -> np.ndarray:
+        from .gpu import Launch, i32
+
+        gpu, p = self.gpu, self.problem
+        m, n, k = self.shape["m"], self.shape["n"], self.shape["k"]
+        bufs = p.buffers
+        if a.flags.f_contiguous and not a.flags.c_contiguous:  # column-major A: already the kernel's layout
+            gpu.h2d_2d_async(bufs["at"], p.m * 4, a.T)
+        else:
+            if self._staging is None:
+                self._staging = gpu.empty((m, k), np.float32)
+            gpu.h2d_async(self._staging, np.ascontiguousarray(a))
+            gpu.launch(self.transpose_kernel(), Launch((-(-p.k // 32), -(-p.m // 32), 1), (32, 8, 1)),
+                       [bufs["at"], self._staging, i32(m), i32(k), i32(p.k), i32(p.m)])
+        gpu.h2d_2d_async(bufs["b"], p.n * 4, b)
+        gpu.h2d_2d_async(bufs["out"], p.n * 4, c)
+        p.bind(self.kernel, self.config)
+        gpu.launch(self.kernel, self.launch_shape, self.args)
+        out = np.empty((m, n), np.float32)
+        gpu.d2h_2d_async(out, bufs["out"], p.n * 4)
+        gpu.synchronize()
+        return out
+
+    def run_conv(self, image: np.ndarray, out: np.ndarray | None) -> np.ndarray:
+        gpu, p = self.gpu, self.problem
+        h, w = self.shape["height"], self.shape["width"]
+        gpu.h2d_2d_async(p.buffers["image"], (p.width + p.fw - 1) * 4, np.ascontiguousarray(image))
+        p.bind(self.kernel, self.config)
+        gpu.launch(self.kernel, self.launch_shape, self.args)
+        if out is None:
+            out = np.empty((h, w), np.float32)
+        gpu.d2h_2d_async(out, p.buffers["out"], p.width * 4)
+        gpu.synchronize()
+        return out
+
+
+def _choose_config(name: str, config, problem_kwargs: dict, pad: bool) -> dict:
+    probe = make_problem(name, **problem_kwargs)
     if config:
-        cfg = dict(config)
-    else:  # tuned configs were tuned at the BASELINE size; keep the first that fits this shape
-        cfg = problem.fitting_config([tuned.best_config(name), tuned.best_config(name, "energy_optimal"),
-                                      problem.default_config()])
+        return {**probe.default_config(), **dict(config)}
+    # tuned configs were tuned at the BASELINE size: padded calls take the tuned one as is, the
+    # others the first that divides this shape
+    candidates = [tuned.best_config(name), tuned.best_config(name, "energy_optimal"), probe.default_config()]
+    if pad:
+        return {**probe.default_config(), **next(c for c in candidates if c)}
+    return probe.fitting_config(candidates)
+
+
+def _runner(name: str, key: tuple, config, problem_kwargs: dict, inputs, ordinal: int, pad: bool = False,
+            staged: bool = False) -> Runner:
+    """A cached runner. ``pad``: sizes in ``problem_kwargs`` that the config cannot tile are padded up
+    (``inputs`` is then a callable building zero inputs for the padded kwargs); ``staged``: always a
+    :class:`PaddedRunner` (the GEMM entry points stage A through the device transpose)."""
+    cfg = _choose_config(name, config, problem_kwargs, pad)
+    kwargs = dict(problem_kwargs)
+    if pad:
+        for field_name, multiple in make_problem(name, **kwargs).tile_multiples(cfg).items():
+            kwargs[field_name] = -(-kwargs[field_name] // multiple) * multiple
+    padded = kwargs != problem_kwargs
     cache_key = (name, key, tuple(sorted(cfg.items())), ordinal)
     with _lock:
         hit = _runners.get(cache_key)
     if hit is None:
-        hit = Runner(problem, cfg, device(ordinal), inputs)
+        problem = make_problem(name, **kwargs)
+        broken = problem.broken_restrictions(cfg)
+        if broken or not problem.is_valid(cfg):
+            raise ConfigurationError(f"{name} config {cfg} is not valid for {kwargs}: breaks {broken or 'value lists'}")
+        if padded or staged:
+            hit = PaddedRunner(problem, cfg, device(ordinal), inputs(kwargs), problem_kwargs)
+        else:
+            hit = Runner(problem, cfg, device(ordinal), inputs(kwargs) if callable(inputs) else inputs)
         with _lock:
             _runners[cache_key] = hit
     return hit
@@ -194,14 +283,25 @@ PNPOLY_STRIPS = 6
 def conv2d(image: np.ndarray, filt: np.ndarray, *, config=None, out=None, ordinal: int = 0,
            strips: int = CONV2D_STRIPS) -> np.ndarray:
     """Valid-mode 2D correlation of a pre-padded float32 image with a 17x17-style filter
-    (``strips`` row bands pipelined over copy/compute streams; 1 = one launch)."""
+    (``strips`` row bands pipelined over copy/compute streams; 1 = one launch). Output
+    sizes the config's tile does not divide run on a padded problem (:class:`PaddedRunner`)."""
     image = np.asarray(image, dtype=np.float32)
     filt = np.asarray(filt, dtype=np.float32)
+    if image.ndim != 2 or filt.ndim != 2:
+        raise ConfigurationError("conv2d takes a 2D image and a 2D filter")
     fh, fw = filt.shape
     h, w = image.shape[0] - fh + 1, image.shape[1] - fw + 1
-    r = _runner("conv2d", (h, w, fh, fw), config, {"width": w, "height": h, "fw": fw, "fh": fh},
-                {"image": image, "filter": filt}, ordinal)
+    if h < 1 or w < 1:
+        raise ConfigurationError(f"image {image.shape} is smaller than the filter {filt.shape}")
+
+    def zero_inputs(kw):
+        return {"image": np.zeros((kw["height"] + fh - 1, kw["width"] + fw - 1), np.float32), "filter": filt}
+
+    r = _runner("conv2d", (h, w, fh, fw), config, {"width": w, "height": h, "fw": fw, "fh": fh}, zero_inputs,
+                ordinal, pad=True)
     r.problem.inputs["filter"] = filt
+    if isinstance(r, PaddedRunner):
+        return r.run_conv(image, out)
     return r.run({"image": image}, out, strips=strips)
 
 
@@ -218,6 +318,11 @@ def conv2d_many(images: list, filt: np.ndarray, *, config=None, outs: list | Non
     h, w = image.shape[0] - fh + 1, image.shape[1] - fw + 1
     key = (h, w, fh, fw)
     kwargs = {"width": w, "height": h, "fw": fw, "fh": fh}
+    try:
+        _choose_config("conv2d", config, kwargs, pad=False)
+    except ConfigurationError:  # the tiles do not divide this shape: padded calls, one after the other
+        outs = outs or [None] * len(images)
+        return [conv2d(im, filt, config=config, out=o, ordinal=ordinal) for im, o in zip(images, outs)]
     a = _runner("conv2d", key, config, kwargs, {"image": image, "filter": filt}, ordinal)
     b = _runner("conv2d", key + ("partner",), a.config, kwargs, {"image": image, "filter": filt}, ordinal)
     for r in (a, b):
@@ -240,7 +345,7 @@ def pnpoly(points: np.ndarray, vx: np.ndarray, vy: np.ndarray, *, config=None, o
     the brute-force METHOD 2 bitmap bit for bit."""
     names = {"brute": "pnpoly", "slab": "pnpoly_slab", "grid": "pnpoly_grid", "cells": "pnpoly_cells"}
     if algorithm not in names:
-        raise ValueError(f"algorithm must be one of {sorted(names)}, not {algorithm!r}")
+        raise ConfigurationError(f"algorithm must be one of {sorted(names)}, not {algorithm!r}")
     points = np.asarray(points, dtype=np.float32)
     vx = np.asarray(vx, dtype=np.float32)
     vy = np.asarray(vy, dtype=np.float32)
@@ -269,10 +374,16 @@ def _gemm(name, a, b, c, alpha, beta, config, ordinal) -> np.ndarray:
     a = np.asarray(a, dtype=np.float32)
     b = np.asarray(b, dtype=np.float32)
     c = np.asarray(c, dtype=np.float32)
+    if a.ndim != 2 or b.ndim != 2 or c.ndim != 2 or a.shape[1] != b.shape[0] or c.shape != (a.shape[0], b.shape[1]):
+        raise ConfigurationError(f"{name}: shapes {a.shape} x {b.shape} + {c.shape} do not form a GEMM")
     m, k = a.shape
     n = b.shape[1]
+
+    def zero_inputs(kw):
+        return {"a": np.zeros((kw["m"], kw["k"]), np.float32), "b": np.zeros((kw["k"], kw["n"]), np.float32),
+                "c0": np.zeros((kw["m"], kw["n"]), np.float32)}
+
     r = _runner(name, (m, n, k, float(alpha), float(beta)), config,
-                {"m": m, "n": n, "k": k, "alpha": float(alpha), "beta": float(beta)}, {"a": a, "b": b, "c0": c},
-                ordinal)
-    at = a.T if a.flags.f_contiguous else np.ascontiguousarray(a.T)
-    return r.run({"at": at, "b": b, "out": c})
+                {"m": m, "n": n, "k": k, "alpha": float(alpha), "beta": float(beta)}, zero_inputs, ordinal, pad=True,
+                staged=True)
+    return r.run_gemm(a, b, c)

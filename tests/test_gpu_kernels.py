@@ -289,6 +289,45 @@ def test_suite_host_api_matches_oracles():
     assert 1e-6 < err <= O.SGEMM_TF32_TOL
 
 
+@pytest.mark.parametrize("m,n,k", [(1000, 1000, 1000), (1023, 777, 513), (4096, 4096, 4096)])
+def test_suite_sgemm_any_shape(m, n, k):
+    """Shapes the tuned tiles do not divide run padded (CLBlast's indirect GEMM): A is uploaded row-major and
+    transposed + zero-padded on the device (no host transpose), B / C go in with pitched copies."""
+    from paper_2211_07260_b200 import suite
+
+    rng = np.random.default_rng(m + n + k)
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    c = rng.uniform(-1, 1, (m, n)).astype(np.float32)
+    ref = O.sgemm(a, b, c, 1.0, 0.5)
+    assert O.sgemm_error(suite.sgemm(a, b, c, 1.0, 0.5), ref) <= O.SGEMM_TOL
+    # column-major A (a Fortran-ordered view) is already the kernel's layout: pitched copy, same result
+    np.testing.assert_array_equal(suite.sgemm(np.asfortranarray(a), b, c, 1.0, 0.5), suite.sgemm(a, b, c, 1.0, 0.5))
+    err = O.sgemm_error(suite.sgemm_tf32(a, b, c, 1.0, 0.5), ref)
+    assert 1e-6 < err <= O.SGEMM_TF32_TOL
+
+
+def test_suite_conv2d_untileable_width_and_bad_shapes():
+    from paper_2211_07260_b200 import suite
+    from paper_2211_07260_b200.kernels import Conv2DProblem
+
+    ci = Conv2DProblem(width=4095, height=4095).host_inputs()  # 4111^2 image -> 4095^2 output
+    out = suite.conv2d(ci["image"], ci["filter"])
+    assert out.shape == (4095, 4095)
+    for rows in (slice(0, 24), slice(2000, 2008), slice(4071, 4095)):  # bounded oracle bands incl. the edges
+        ref = O.conv2d_rows(ci["image"], ci["filter"], rows)
+        assert O.conv2d_error(out[rows], ref, ci["image"], ci["filter"]) <= O.CONV_TOL
+    small = Conv2DProblem(width=37, height=29).host_inputs()
+    got = suite.conv2d(small["image"], small["filter"])
+    assert O.conv2d_error(got, O.conv2d(small["image"], small["filter"]), small["image"], small["filter"]) <= O.CONV_TOL
+    import paper_2211_07260_b200 as B
+
+    with pytest.raises(B.ConfigurationError):
+        suite.conv2d(np.zeros((8, 8), np.float32), ci["filter"])  # image smaller than the filter
+    with pytest.raises(B.ConfigurationError):
+        suite.sgemm(np.zeros((4, 5), np.float32), np.zeros((6, 4), np.float32), np.zeros((4, 4), np.float32))
+
+
 def test_suite_pipelined_strips_match_single_launch():
     """Pipelined host calls (bands / chunks over 3 streams) give the single-launch bits."""
     from paper_2211_07260_b200 import suite
