@@ -31,6 +31,10 @@
 //                   for the same FMA-pipe work, leaving issue bandwidth for
 //                   the fragment loads. Per element the same fma.rn sequence,
 //                   so the result is bit-identical to FMA2 = 0. Needs VWN even.
+//   GROUP_M         (B200 addition) CTA rasterisation: 1 = launch order (all of
+//                   A streams past every B column panel), g = groups of g M-tiles
+//                   sweep the N-tiles together, so the resident CTAs' A and B
+//                   panels stay in L2 (fewer DRAM re-reads; same result bits).
 //
 // Requirements (the tuning-space restrictions, kernels.py):
 //   MWG % (MDIMC*VWM) == 0, NWG % (NDIMC*VWN) == 0,
@@ -92,6 +96,9 @@
 #ifndef FMA2
 #define FMA2 0
 #endif
+#ifndef GROUP_M  // (B200 addition) CTA rasterisation group along M; 1 = CLBlast's launch order
+#define GROUP_M 1
+#endif
 #if FMA2 && (VWN % 2)
 #error "FMA2 needs an even VWN (accumulator pairs inside one B vector)"
 #endif
@@ -118,12 +125,28 @@ template <>
 struct vec<2> { typedef float2 t; };
 template <>
 struct vec<4> { typedef float4 t; };
+// CLBlast's float8 (OpenCL has it, CUDA does not): two float4 halves, 32-byte aligned
+struct __align__(32) float8 {
+    float4 lo, hi;
+};
+template <>
+struct vec<8> { typedef float8 t; };
 typedef typename vec<VWM>::t vm_t;
 typedef typename vec<VWN>::t vn_t;
 
 __device__ __forceinline__ float lane(const float &v, int) { return v; }
 __device__ __forceinline__ float lane(const float2 &v, int i) { return i == 0 ? v.x : v.y; }
 __device__ __forceinline__ float lane(const float4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+__device__ __forceinline__ float lane(const float8 &v, int i) { return i < 4 ? lane(v.lo, i) : lane(v.hi, i - 4); }
+
+// read-only global loads of one vector (__ldg has no float8 overload)
+template <typename T>
+__device__ __forceinline__ T ldg(const T *p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ float8 ldg(const float8 *p) {
+    const float4 *q = reinterpret_cast<const float4 *>(p);
+    return float8{__ldg(q), __ldg(q + 1)};
+}
 
 // Offset (in vectors of VWM) of this thread's w-th A fragment vector inside the MWG tile.
 __device__ __forceinline__ int frag_m(int tm, int w) {
@@ -146,7 +169,10 @@ __device__ __forceinline__ int frag_n(int tn, int w) {
 template <typename T>
 __device__ __forceinline__ void cp_async(T *dst, const T *src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    if constexpr (sizeof(T) == 16)
+    if constexpr (sizeof(T) == 32) {  // float8: two 16-byte copies
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16), "l"((const char *)src + 16) : "memory");
+    } else if constexpr (sizeof(T) == 16)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"((int)sizeof(T)) : "memory");
@@ -175,11 +201,26 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
       const float *__restrict__ at, const float *__restrict__ b, float *__restrict__ c) {
     const int tid = threadIdx.x;
     const int tm = tid % MDIMC, tn = tid / MDIMC;
-    const int m0 = blockIdx.x * MWG, n0 = blockIdx.y * NWG;
+    // CTA rasterisation: GROUP_M = 1 is CLBlast's launch order (blockIdx.x walks M with one B
+    // column panel); GROUP_M = g walks g M-tiles across all N-tiles before moving on, so the CTAs
+    // resident at once share g A panels and a run of B panels in L2 instead of all of A.
+    int m_tile = blockIdx.x, n_tile = blockIdx.y;
+#if GROUP_M > 1
+    {
+        const int tiles_m = gridDim.x, tiles_n = gridDim.y;
+        const int pid = blockIdx.x + blockIdx.y * tiles_m;
+        const int per_group = GROUP_M * tiles_n;
+        const int first = (pid / per_group) * GROUP_M;
+        const int rows = min(tiles_m - first, GROUP_M);
+        m_tile = first + (pid % per_group) % rows;
+        n_tile = (pid % per_group) / rows;
+    }
+#endif
+    const int m0 = m_tile * MWG, n0 = n_tile * NWG;
 
 #if ASYNC
     // ASYNC stages of {A tile, B tile} in dynamic shared memory
-    extern __shared__ __align__(16) unsigned char smem_dyn[];
+    extern __shared__ __align__(128) unsigned char smem_dyn[];
     typedef vm_t a_tile_t[KWG][MWG / VWM];
     typedef vn_t b_tile_t[KWG][NWG / VWN];
     a_tile_t *a_sm = reinterpret_cast<a_tile_t *>(smem_dyn);
@@ -187,13 +228,18 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
     const int ma = tid % MDIMA, ka = tid / MDIMA;
     const int nb = tid % NDIMB, kb = tid / NDIMB;
 #else
+    // CLBlast's two shared-memory buffers, in dynamic shared memory: the paper's space has
+    // configs (KWG 32, 128 x 128, SA = SB = 1: 64 KB double-buffered) above the 48 KB static cap
+    extern __shared__ __align__(128) unsigned char smem_dyn[];
 #if SA
-    __shared__ __align__(16) vm_t a_sm[2][KWG][MWG / VWM];
+    typedef vm_t a_tile_t[KWG][MWG / VWM];
+    a_tile_t *a_sm = reinterpret_cast<a_tile_t *>(smem_dyn);
     const int ma = tid % MDIMA, ka = tid / MDIMA;
     vm_t a_reg[KWA][MWA / VWM];
 #endif
 #if SB
-    __shared__ __align__(16) vn_t b_sm[2][KWG][NWG / VWN];
+    typedef vn_t b_tile_t[KWG][NWG / VWN];
+    b_tile_t *b_sm = reinterpret_cast<b_tile_t *>(smem_dyn + (SA ? 2 * KWG * MWG * 4 : 0));
     const int nb = tid % NDIMB, kb = tid / NDIMB;
     vn_t b_reg[KWB][NWB / VWN];
 #endif
@@ -232,7 +278,7 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
 #if SA
                     af[w] = a_sm[buf][k][frag_m(tm, w)];
 #else
-                    af[w] = __ldg(at_v + (size_t)(k0 + k) * lda_v + m0 / VWM + frag_m(tm, w));
+                    af[w] = ldg(at_v + (size_t)(k0 + k) * lda_v + m0 / VWM + frag_m(tm, w));
 #endif
                 }
 #pragma unroll
@@ -240,7 +286,7 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
 #if SB
                     bf[w] = b_sm[buf][k][frag_n(tn, w)];
 #else
-                    bf[w] = __ldg(b_v + (size_t)(k0 + k) * ldb_v + n0 / VWN + frag_n(tn, w));
+                    bf[w] = ldg(b_v + (size_t)(k0 + k) * ldb_v + n0 / VWN + frag_n(tn, w));
 #endif
                 }
 #pragma unroll
@@ -296,14 +342,14 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
         for (int kk = 0; kk < KWA; ++kk)
 #pragma unroll
             for (int mv = 0; mv < MWA / VWM; ++mv)
-                a_reg[kk][mv] = __ldg(at_v + (size_t)(k0 + ka + kk * KDIMA) * lda_v + m0 / VWM + ma + mv * MDIMA);
+                a_reg[kk][mv] = ldg(at_v + (size_t)(k0 + ka + kk * KDIMA) * lda_v + m0 / VWM + ma + mv * MDIMA);
 #endif
 #if SB
 #pragma unroll
         for (int kk = 0; kk < KWB; ++kk)
 #pragma unroll
             for (int nv = 0; nv < NWB / VWN; ++nv)
-                b_reg[kk][nv] = __ldg(b_v + (size_t)(k0 + kb + kk * KDIMB) * ldb_v + n0 / VWN + nb + nv * NDIMB);
+                b_reg[kk][nv] = ldg(b_v + (size_t)(k0 + kb + kk * KDIMB) * ldb_v + n0 / VWN + nb + nv * NDIMB);
 #endif
     };
     auto stash = [&](int buf) {

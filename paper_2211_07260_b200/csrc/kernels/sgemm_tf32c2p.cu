@@ -114,6 +114,25 @@ __host__ __device__ constexpr unsigned instr_desc() {
            ((unsigned)(256 >> 4) << 24);
 }
 
+#ifndef GROUP_M  // tile walk: GROUP_M M-tiles sweep every N-tile before the next group (1 = M fastest, all of A per B panel)
+#define GROUP_M 1
+#endif
+// Persistent tile order -> (M tile, N tile). GROUP_M = 1: consecutive tiles share the B column
+// panel and walk all of A. GROUP_M = g: g M-tiles x all N-tiles per group, so the tiles in flight
+// at once (one per CTA / pair) touch g A panels and a run of B panels that stay in L2.
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int &mt, int &nt) {
+#if GROUP_M > 1
+    const int per_group = GROUP_M * tiles_n;
+    const int first = (tile / per_group) * GROUP_M;
+    const int rows = min(tiles_m - first, GROUP_M);
+    mt = first + (tile % per_group) % rows;
+    nt = (tile % per_group) / rows;
+#else
+    mt = tile % tiles_m;
+    nt = tile / tiles_m;
+#endif
+}
+
 // A work unit: a tile and a K range; part 0 = whole tile, 1/2 = split halves.
 struct Unit {
     int tile, k_begin, k_end, part;
@@ -195,7 +214,9 @@ sgemm_tf32c2p(const __grid_constant__ TensorMap map_a, const __grid_constant__ T
             int g = 0;
             for (int u = 0; u < n_units; ++u) {
                 const Unit unit = sched.at(u, pairs);
-                const int m0 = (unit.tile % tiles_m) * 256, n0 = (unit.tile / tiles_m) * BN;
+                int mt, nt;
+                tile_coords(unit.tile, tiles_m, N / BN, mt, nt);
+                const int m0 = mt * 256, n0 = nt * BN;
                 const int m_own = m0 + (int)rank * BM, n_own = n0 + (int)rank * BN_HALF;
                 for (int kt = unit.k_begin; kt < unit.k_end; ++kt, ++g) {
                     const int s = g % STAGES;
@@ -257,7 +278,9 @@ sgemm_tf32c2p(const __grid_constant__ TensorMap map_a, const __grid_constant__ T
         for (int u = 0; u < n_units; ++u) {
             const Unit unit = sched.at(u, pairs);
             const int acc = u & 1;
-            const int m0 = (unit.tile % tiles_m) * 256, n0 = (unit.tile / tiles_m) * BN;
+            int mt, nt;
+            tile_coords(unit.tile, tiles_m, N / BN, mt, nt);
+            const int m0 = mt * 256, n0 = nt * BN;
             mbar_wait(smem_u32(&tmem_full[acc]), (u >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int local_row = (int)rank * BM + quarter * 32 + lane;  // row within the 256-row tile

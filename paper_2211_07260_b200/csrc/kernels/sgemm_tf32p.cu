@@ -111,9 +111,30 @@ struct Schedule {
     }
 };
 
-__device__ __forceinline__ void tile_origin(int tile, int tiles_m, int &m0, int &n0) {
-    m0 = (tile % tiles_m) * BM;  // consecutive units share the B column panel
-    n0 = (tile / tiles_m) * BN;
+#ifndef GROUP_M  // tile walk: GROUP_M M-tiles sweep every N-tile before the next group (1 = M fastest, all of A per B panel)
+#define GROUP_M 1
+#endif
+// Persistent tile order -> (M tile, N tile). GROUP_M = 1: consecutive tiles share the B column
+// panel and walk all of A. GROUP_M = g: g M-tiles x all N-tiles per group, so the tiles in flight
+// at once (one per CTA / pair) touch g A panels and a run of B panels that stay in L2.
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int &mt, int &nt) {
+#if GROUP_M > 1
+    const int per_group = GROUP_M * tiles_n;
+    const int first = (tile / per_group) * GROUP_M;
+    const int rows = min(tiles_m - first, GROUP_M);
+    mt = first + (tile % per_group) % rows;
+    nt = (tile % per_group) / rows;
+#else
+    mt = tile % tiles_m;
+    nt = tile / tiles_m;
+#endif
+}
+
+__device__ __forceinline__ void tile_origin(int tile, int tiles_m, int tiles_n, int &m0, int &n0) {
+    int mt, nt;
+    tile_coords(tile, tiles_m, tiles_n, mt, nt);
+    m0 = mt * BM;
+    n0 = nt * BN;
 }
 
 #define TMEM_LD32(taddr, v)                                                                                        \
@@ -173,7 +194,7 @@ sgemm_tf32p(const __grid_constant__ TensorMap map_a, const __grid_constant__ Ten
             for (int u = 0; u < n_units; ++u) {
                 const Unit unit = sched.at(u, gridDim.x);
                 int m0, n0;
-                tile_origin(unit.tile, tiles_m, m0, n0);
+                tile_origin(unit.tile, tiles_m, N / BN, m0, n0);
                 for (int kt = unit.k_begin; kt < unit.k_end; ++kt, ++g) {
                     const int s = g % STAGES;
                     mbar_wait(smem_u32(&empty[s]), ((g / STAGES) & 1) ^ 1);
@@ -228,7 +249,7 @@ sgemm_tf32p(const __grid_constant__ TensorMap map_a, const __grid_constant__ Ten
             const Unit unit = sched.at(u, gridDim.x);
             const int acc = u & 1;
             int m0, n0;
-            tile_origin(unit.tile, tiles_m, m0, n0);
+            tile_origin(unit.tile, tiles_m, N / BN, m0, n0);
             mbar_wait(smem_u32(&tmem_full[acc]), (u >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int row = quarter * 32 + lane;

@@ -930,13 +930,33 @@ class SgemmProblem(KernelProblem):
     def algorithmic_bytes(self) -> float:
         return 4.0 * (self.m * self.k + self.k * self.n + 2 * self.m * self.n)
 
+    #: the paper's space: Kernel Tuner's CLBlast xgemm lists and restrictions,
+    #: 17,472 valid configs
+    CLBLAST_PARAMS = {
+        "MWG": [16, 32, 64, 128], "NWG": [16, 32, 64, 128], "KWG": [32], "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32],
+        "MDIMA": [8, 16, 32], "NDIMB": [8, 16, 32], "KWI": [2], "VWM": [1, 2, 4, 8], "VWN": [1, 2, 4, 8],
+        "STRM": [0], "STRN": [0], "SA": [0, 1], "SB": [0, 1],
+    }
+    CLBLAST_RESTRICTIONS = [
+        "KWG % KWI == 0",
+        "MWG % (MDIMC * VWM) == 0",
+        "NWG % (NDIMC * VWN) == 0",
+        "MWG % (MDIMA * VWM) == 0",
+        "NWG % (NDIMB * VWN) == 0",
+        "KWG % ((MDIMC * NDIMC) / MDIMA) == 0",
+        "KWG % ((MDIMC * NDIMC) / NDIMB) == 0",
+        "not (MWG == 128 and NWG == 128 and MDIMC == 8 and NDIMC == 8)",
+    ]
+
     def tune_params(self):
+        if self.value_set == "clblast":
+            return dict(self.CLBLAST_PARAMS)
         if self.value_set == "b200":
             return {
                 "MWG": [64, 128, 256], "NWG": [64, 128, 256], "KWG": [8, 16, 32],
                 "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32, 64], "NDIMB": [8, 16, 32, 64],
                 "KWI": [1, 2, 4, 8], "VWM": [1, 2, 4], "VWN": [1, 2, 4], "STRM": [0, 1], "STRN": [0, 1],
-                "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3, 4], "FMA2": [0, 1],
+                "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3, 4], "FMA2": [0, 1], "GROUP_M": [1, 4, 8, 16],
             }
         return {
             "MWG": [16, 32, 64, 128], "NWG": [16, 32, 64, 128], "KWG": [16, 32],
@@ -946,8 +966,12 @@ class SgemmProblem(KernelProblem):
         }
 
     def restrictions(self):
-        # CLBlast's xgemm constraints (KWG % KWI, tile divisibility, load shapes)
-        # plus the B200 static-smem budget (double buffered) and vector widths <= 4.
+        shape = f"{self.m} % MWG == 0 and {self.n} % NWG == 0 and {self.k} % KWG == 0"
+        if self.value_set == "clblast":
+            # every one of the 17,472 fits the B200 kernel (dynamic shared memory, float8 vectors)
+            return [*self.CLBLAST_RESTRICTIONS, shape]
+        # CLBlast's xgemm constraints (KWG % KWI, tile divisibility, load shapes) plus the B200
+        # shared-memory budget (two buffers, or ASYNC cp.async stages) and the register cap.
         return [
             "KWG % KWI == 0",
             "MWG % (MDIMC * VWM) == 0",
@@ -958,19 +982,18 @@ class SgemmProblem(KernelProblem):
             "KWG % ((MDIMC * NDIMC) / NDIMB) == 0",
             "(MDIMC * NDIMC) % MDIMA == 0",
             "(MDIMC * NDIMC) % NDIMB == 0",
-            "VWM <= 4 and VWN <= 4",
-            # ASYNC = 0: CLBlast's two static buffers (48 KB); ASYNC = S: S cp.async stages (dynamic, 227 KB)
             "ASYNC == 0 or (SA == 1 and SB == 1)",
-            "(ASYNC == 0 and (SA * KWG * MWG + SB * KWG * NWG) * 2 * 4 <= 48 * 1024)"
+            "(ASYNC == 0 and (SA * KWG * MWG + SB * KWG * NWG) * 2 * 4 <= 227 * 1024)"
             " or (ASYNC > 0 and KWG * (MWG + NWG) * 4 * ASYNC <= 227 * 1024)",
             "(MWG / MDIMC) * (NWG / NDIMC) <= 128",
-            f"{self.m} % MWG == 0 and {self.n} % NWG == 0 and {self.k} % KWG == 0",
+            shape,
             "FMA2 == 0 or VWN % 2 == 0",
         ]
 
     def default_config(self):
         return {"MWG": 128, "NWG": 128, "KWG": 16, "MDIMC": 16, "NDIMC": 16, "MDIMA": 32, "NDIMB": 32,
-                "KWI": 2, "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 0, "FMA2": 0}
+                "KWI": 2, "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 0, "FMA2": 0,
+                "GROUP_M": 1}
 
     def defines(self, config):
         return dict(_as_dict(config))
@@ -982,7 +1005,10 @@ class SgemmProblem(KernelProblem):
     def launch(self, config):
         c = _as_dict(config)
         stages = c.get("ASYNC", 0)
-        smem = c["KWG"] * (c["MWG"] + c["NWG"]) * 4 * stages  # dynamic cp.async stages (0: static buffers)
+        if stages:  # cp.async stages
+            smem = c["KWG"] * (c["MWG"] + c["NWG"]) * 4 * stages
+        else:  # CLBlast's two buffers of the staged operands
+            smem = 2 * 4 * c["KWG"] * (c["SA"] * c["MWG"] + c["SB"] * c["NWG"])
         return Launch((self.m // c["MWG"], self.n // c["NWG"], 1), (c["MDIMC"] * c["NDIMC"], 1, 1), smem=smem)
 
     def host_inputs(self):
@@ -1026,7 +1052,7 @@ class SgemmTF32Problem(SgemmProblem):
 
     def tune_params(self):
         return {"BN": [64, 128, 256], "STAGES": [2, 3, 4, 5, 6, 7], "PERSIST": [0, 1], "SPLIT_TAIL": [0, 1],
-                "PAIR": [0, 1]}
+                "PAIR": [0, 1], "GROUP_M": [1, 4, 8]}
 
     def restrictions(self):
         return [
@@ -1035,17 +1061,20 @@ class SgemmTF32Problem(SgemmProblem):
             "PERSIST == 1 or SPLIT_TAIL == 0",
             "PAIR == 0 or BN >= 128",
             "PAIR == 0 or PERSIST == 1 or SPLIT_TAIL == 0",
+            "PERSIST == 1 or GROUP_M == 1",  # the tile walk of the persistent variants
             f"{self.m} % (128 * (1 + PAIR)) == 0 and {self.n} % BN == 0 and {self.k} % 32 == 0",
         ]
 
     def default_config(self):
-        return {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1, "PAIR": 0}
+        return {"BN": 256, "STAGES": 4, "PERSIST": 1, "SPLIT_TAIL": 1, "PAIR": 0, "GROUP_M": 1}
 
     def defines(self, config):
         c = _as_dict(config)
         d = {"BN": c["BN"], "STAGES": c["STAGES"]}
         if c.get("PERSIST", 0):
             d["SPLIT_TAIL"] = c.get("SPLIT_TAIL", 0)
+            if c.get("GROUP_M", 1) > 1:
+                d["GROUP_M"] = c["GROUP_M"]
         return d
 
     def tile_multiples(self, config):

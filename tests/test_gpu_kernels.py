@@ -250,6 +250,63 @@ def test_sgemm_fma2_bit_identical_to_scalar(gpu, overrides):
     assert O.sgemm_error(packed, ref) <= O.SGEMM_TOL
 
 
+def _clblast_sample(n=16, seed=7):
+    import random
+
+    from paper_2211_07260_b200.kernels import SgemmProblem
+
+    cfgs = [c.as_dict() for c in SgemmProblem(value_set="clblast").space().enumerate()]
+    rng = random.Random(seed)
+    extremes = [c for c in cfgs if c["VWM"] == 8 and c["VWN"] == 8][:2] + \
+        [c for c in cfgs if c["MWG"] == c["NWG"] == 128 and c["SA"] == c["SB"] == 1][:2] + \
+        [c for c in cfgs if c["SA"] == c["SB"] == 0][:1]
+    return extremes + rng.sample(cfgs, n)
+
+
+@pytest.mark.parametrize("overrides", _clblast_sample(), ids=lambda c: "-".join(str(v) for v in c.values()))
+def test_sgemm_paper_clblast_space(gpu, overrides):
+    """Configs of the paper's 17,472-config CLBlast space (float8 vectors, > 48 KB of double-buffered
+    shared memory, global-memory fragments) within the FP32 bar."""
+    from paper_2211_07260_b200.kernels import SgemmProblem
+
+    p = SgemmProblem(m=256, n=256, k=128, value_set="clblast")
+    p.prepare(gpu)
+    cfg = {**p.default_config(), **overrides}
+    assert p.is_valid(cfg)
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    assert O.sgemm_error(run_once(gpu, p, cfg), ref) <= O.SGEMM_TOL
+
+
+def test_sgemm_group_m_rasterisation_bit_identical(gpu):
+    """GROUP_M only reorders CTAs: the same bits as launch order."""
+    from paper_2211_07260_b200 import tuned
+    from paper_2211_07260_b200.kernels import SgemmProblem
+
+    p = SgemmProblem(m=1024, n=768, k=256)
+    p.prepare(gpu)
+    base = {**p.default_config(), **(tuned.best_config("sgemm") or {})}
+    one = run_once(gpu, p, {**base, "GROUP_M": 1}).copy()
+    for g in (4, 8, 16):
+        np.testing.assert_array_equal(run_once(gpu, p, {**base, "GROUP_M": g}), one)
+
+
+def test_sgemm_tf32_group_m_walk(gpu):
+    """GROUP_M reorders the persistent tile walk only: without split tails the same bits, with them
+    (which tiles get K-split changes) still inside the TF32 bar."""
+    from paper_2211_07260_b200.kernels import SgemmTF32Problem
+
+    p = SgemmTF32Problem(m=1024, n=1024, k=256)
+    p.prepare(gpu)
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    for pair in (0, 1):
+        base = dict(BN=256, STAGES=4, PERSIST=1, SPLIT_TAIL=0, PAIR=pair, GROUP_M=1)
+        one = run_once(gpu, p, base).copy()
+        for g in (4, 8):
+            np.testing.assert_array_equal(run_once(gpu, p, {**base, "GROUP_M": g}), one)
+            err = O.sgemm_error(run_once(gpu, p, {**base, "GROUP_M": g, "SPLIT_TAIL": 1}), ref)
+            assert 1e-6 < err <= O.SGEMM_TF32_TOL
+
+
 def test_sgemm_full_size_tuned(gpu):
     from paper_2211_07260_b200 import tuned
     from paper_2211_07260_b200.kernels import SgemmProblem

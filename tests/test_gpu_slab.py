@@ -184,7 +184,11 @@ def test_slab_through_tune_kernel():
                                                             "pairs_smem": [0], "xbuckets": [16], "exact_flags": [0],
                                                             "half": [0, 1], "buckets": [4096]},
                                 problem_kwargs={"n_points": 1 << 20}, duration=0.05)
-    assert len(rows) == 4 and not any(r["failed"] for r in rows) and outcome.best.metrics["gflops"] > 0
+    assert len(rows) == 4 and not any(r["failed"] for r in rows)
+    # a work-skipping kernel: points/s, GB/s and joules per bitmap, no brute-force flop credit
+    best = outcome.best.metrics
+    assert "gflops" not in best and best["points_per_s"] > 1e9 and best["j_per_bitmap"] == outcome.best.energy
+    assert best["gb_per_s"] == pytest.approx(best["points_per_s"] * 12 / 1e9, rel=1e-3)
 
 
 # -- uniform-cell fast path in front of the slab search (csrc/kernels/pnpoly_grid.cu) ---------

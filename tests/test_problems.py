@@ -22,3 +22,19 @@ def test_tuned_configs_are_valid(name):
     p = make_problem(name, **SMALL.get(name, {}))
     for cfg in tuned.configs_for(name):
         assert p.is_valid(cfg), cfg
+
+
+def test_paper_clblast_space_size():
+    """The paper's GEMM space: Kernel Tuner's CLBlast lists give 17,472 valid configs,
+    all accepted by the B200 kernel at the BASELINE size; x 7 clocks = 122,304 (tests/test_acceptance.py:66-81)."""
+    from paper_2211_07260_b200 import CLOCK_PARAM, TunableParameter
+
+    p = make_problem("sgemm", value_set="clblast")
+    space = p.space()
+    assert len(space.enumerate()) == 17472
+    assert space.augment(TunableParameter(CLOCK_PARAM, tuple(range(7)))).size() == 122304
+    # every config stays inside the B200 limits the kernel needs: <= 1024 threads, <= 227 KB smem
+    for c in space.enumerate():
+        cfg = {**p.default_config(), **c.as_dict()}
+        launch = p.launch(cfg)
+        assert launch.threads <= 1024 and launch.smem <= 227 * 1024
