@@ -56,6 +56,19 @@ def steady_window(total: float, settle: float) -> tuple[float, float]:
     return (skip, total)
 
 
+def counter_updates(samples, t0: float, t1: float) -> int:
+    """Distinct energy-counter readings (change points) stamped inside [t0, t1]."""
+    n, last_e = 0, None
+    for s in samples:
+        e = s[ENERGY]
+        if not math.isfinite(e) or e == last_e:
+            continue
+        last_e = e
+        t = s[E_STAMP] if math.isfinite(s[E_STAMP]) else s[T]
+        n += t0 <= t <= t1
+    return n
+
+
 def counter_slope(samples, t0: float, t1: float) -> float | None:
     """Energy-counter power (W) over [t0, t1] from (time, energy) samples.
 
@@ -342,10 +355,13 @@ class B200Device:
         window = steady_window(total, self.settle)
         steady = [s for s in during if window[0] <= s[T] - t0 <= window[1]] or during or run.samples
         slope = counter_slope(run.samples, t0 + window[0], t0 + window[1])
-        source = 1.0  # energy counter
+        updates = counter_updates(run.samples, t0 + window[0], t0 + window[1])
+        source = 1.0  # energy counter inside the steady window
         if slope is None:
-            # counter cadence (~100 ms on B200) longer than the window: widen to the loop
+            # counter cadence (~100 ms on B200) longer than the window: widen to the loop (the first
+            # reading may then predate the loop, i.e. carry the previous workload's power)
             slope = counter_slope(run.samples, t0 - 0.05, t0 + total + 0.05)
+            source = 0.5
         if slope is None:
             # still < 2 counter updates: median instant power over the steady window
             inst = [s[P_INST] for s in steady if math.isfinite(s[P_INST])]
@@ -366,6 +382,7 @@ class B200Device:
             "power_capped": 1.0 if reasons & SW_POWER_CAP else 0.0,
             "reps": float(run.reps),
             "energy_source": source,
+            "counter_updates": float(updates),
         }
         # NVML's own 1 s average as the board reported it during the loop (averaged-sensor mode)
         sensor = tuple(PowerSample(s[T] - t0, s[P_AVG]) for s in during if math.isfinite(s[P_AVG]))

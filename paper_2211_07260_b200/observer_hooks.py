@@ -116,8 +116,13 @@ class NVMLObserver(BenchmarkObserver):
     * ``nvml_sm_clock`` / ``nvml_temperature`` / ``nvml_mem_clock`` — medians;
     * ``nvml_clock_locked`` — 1.0 if the controller held the requested clock,
       0.0 if NVML refused (the observed clock is then the truth);
-    * ``nvml_energy_source`` — 1.0 energy counter, 0.0 instant-power median
-      (loop too short for two counter updates).
+    * ``nvml_energy_source`` — 1.0 energy counter inside the steady window,
+      0.5 energy counter over the whole loop (fewer than two updates inside
+      the steady window: the slope then reaches back to an update taken
+      before the loop), 0.0 instant-power median (loop too short for two
+      counter updates at all);
+    * ``nvml_counter_updates`` — energy-counter updates inside the steady
+      window (>= 2 for a slope free of the previous workload).
 
     Attaching it switches the benchmark energy rule to ``counter`` mode
     (see ``tuner.MeasurementSetup``).
@@ -146,7 +151,8 @@ class NVMLObserver(BenchmarkObserver):
         inside = [s.power for s in run.samples if window[0] <= s.timestamp <= window[1]]
         if inside:
             out["nvml_power_instant"] = statistics.median(inside)
-        for key in ("sm_clock", "mem_clock", "temperature", "clock_locked", "throttle_reasons", "energy_source"):
+        for key in ("sm_clock", "mem_clock", "temperature", "clock_locked", "throttle_reasons", "energy_source",
+                    "counter_updates"):
             if key in tele:
                 out[f"nvml_{key}"] = float(tele[key])
         self._result = out

@@ -115,7 +115,7 @@ def cmd_sweep(args) -> None:
     metrics, consts = problem.user_metrics()
     done = 0
     with GPU(0) as gpu:
-        dev = B200Device(problem, gpu=gpu, min_window=args.window)
+        dev = B200Device(problem, gpu=gpu, min_window=args.window, settle=args.settle)
         obs = [NVMLObserver(args.window)]
         t1 = time.time()
         for c in batch:
@@ -201,7 +201,9 @@ def main() -> None:
     sub.add_parser("verify")
     s = sub.add_parser("sweep")
     s.add_argument("--seconds", type=float, default=1800.0)
-    s.add_argument("--window", type=float, default=0.2)
+    # >= 0.2 s after the settle: two energy-counter updates (~100 ms cadence) inside the steady window
+    s.add_argument("--window", type=float, default=0.3)
+    s.add_argument("--settle", type=float, default=0.08)
     c = sub.add_parser("confirm")
     c.add_argument("--top", type=int, default=8)
     c.add_argument("--window", type=float, default=0.2)

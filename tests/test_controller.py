@@ -215,3 +215,17 @@ def test_averaged_mode_benchmark_reads_board_sensor():
     with pytest.raises(B.ConfigurationError):
         B.benchmark(SensorDevice(), B.KernelConfig(()), [B.AveragedPowerObserver()],
                     averaged_cfg=B.AveragedSensorConfig(continuous_duration=2.5))
+
+
+def test_counter_updates_and_slope_window():
+    from paper_2211_07260_b200.b200 import counter_slope, counter_updates
+
+    nan = float("nan")
+    # (t, p_inst, p_avg, energy J, energy stamp, sm, mem, temp, reasons): counter steps every 0.1 s at 500 W
+    samples = [(0.01 * i, 500.0, 500.0, 100.0 + 50.0 * (i // 10), 0.1 * (i // 10), 1965, 3996, 50, 0)
+               for i in range(60)]
+    assert counter_updates(samples, 0.05, 0.33) == 3  # stamps 0.1, 0.2, 0.3
+    assert counter_slope(samples, 0.05, 0.33) == pytest.approx(500.0)
+    assert counter_updates(samples, 0.12, 0.19) == 0 and counter_slope(samples, 0.12, 0.19) is None
+    samples.append((0.7, 500.0, 500.0, nan, nan, 1965, 3996, 50, 0))  # a missing reading is ignored
+    assert counter_updates(samples, 0.0, 1.0) == 6
