@@ -13,18 +13,19 @@
 // with HEAD32), more only for cells with more edges. Cells with more than
 // `lmax` undecided edges fall back to the exact slab search of pnpoly_slab.cu.
 //
-// Memory side: two points per 16-byte load and two results per 8-byte store,
-// TILE pairs per thread per chunk. The raster lookups cost nothing measurable
+// Memory side: two points per 16-byte load and two results per 8-byte store
+// (QUAD: four per 32-byte LDG.E.256 load and 16-byte store), TILE vectors per
+// thread per chunk. The raster lookups cost nothing measurable
 // (scripts/cells_floor.py); the queued points' dependent head reads are the
 // cost above the loop's own floor, hence in-place edges and the split drain.
 //
-// Tunables (-D): BLOCK_SIZE_X, TILE (point pairs per thread per chunk), GRID
+// Tunables (-D): BLOCK_SIZE_X, TILE (point vectors per thread per chunk), QUAD, GRID
 // (cells per side), GRID_SMEM (1: raster in shared memory; 0: read through L1),
 // STREAM (1: points loaded / results stored with the evict-first hints), PREFETCH
 // (chunks ahead that one thread of the block pulls into L2 with
 // cp.async.bulk.prefetch: the block's points are one contiguous span per chunk,
 // so the next chunk's HBM latency overlaps this chunk's work without holding
-// registers), REGPF (1: the next chunk's pairs are loaded into registers before
+// registers), REGPF (1: the next chunk's vectors are loaded into registers before
 // this chunk is classified), ADRAIN (1: split drains, the heads fetched by
 // cp.async and tested at the next drain), HEAD32 (32-byte heads). Tried and
 // dropped: a 2-4 stage shared-memory ring filled by cp.async.bulk from one
@@ -51,7 +52,11 @@
 #ifndef REGPF
 #define REGPF 0
 #endif
-#define CHUNK (BLOCK_SIZE_X * TILE)
+#ifndef QUAD
+#define QUAD 0  // 1: four points per 32-byte load (LDG.E.256) and four results per 16-byte store
+#endif
+#define PPV (2 + 2 * QUAD)  // points per vector load
+#define CHUNK (BLOCK_SIZE_X * TILE)  // vectors per block per chunk
 #ifndef ADRAIN
 #define ADRAIN 1
 #endif
@@ -70,10 +75,41 @@
 #if STREAM
 #define LOAD_PAIR(p) __ldcs(p)
 #define STORE_PAIR(p, v) __stcs(p, v)
+#define LDQ "ld.global.cs"
+#define STQ "st.global.cs"
 #else
 #define LOAD_PAIR(p) __ldg(p)
 #define STORE_PAIR(p, v) (*(p) = (v))
+#define LDQ "ld.global.nc"
+#define STQ "st.global"
 #endif
+
+// PPV points {x0, y0, x1, y1, ...} of one vector
+struct pvec {
+    float v[2 * PPV];
+};
+__device__ __forceinline__ pvec load_vec(const float *p) {
+    pvec r;
+#if QUAD
+    asm volatile(LDQ ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                   "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+#else
+    const float4 q = LOAD_PAIR(reinterpret_cast<const float4 *>(p));
+    r.v[0] = q.x, r.v[1] = q.y, r.v[2] = q.z, r.v[3] = q.w;
+#endif
+    return r;
+}
+__device__ __forceinline__ void store_vec(int *o, const unsigned *k) {
+#if QUAD
+    asm volatile(STQ ".v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(o), "r"(k[0] & 1u), "r"(k[1] & 1u), "r"(k[2] & 1u),
+                 "r"(k[3] & 1u)
+                 : "memory");
+#else
+    STORE_PAIR(reinterpret_cast<int2 *>(o), make_int2((int)(k[0] & 1u), (int)(k[1] & 1u)));
+#endif
+}
 
 // The exact search of pnpoly_slab.cu (XSEARCH) over the slab / x-search table of
 // jt_pnpoly_slabs (xbuckets > 0) in global memory, loads through the read-only path. The
@@ -161,22 +197,24 @@ __device__ __forceinline__ int cell_search(float px, float py, unsigned cell, in
     } while (0)
 #endif
 
-// pull chunk c's pairs (one contiguous span) into L2
-__device__ __forceinline__ void prefetch_chunk(const float4 *pairs, int c, int full) {
+// pull chunk c's vectors (one contiguous span) into L2
+__device__ __forceinline__ void prefetch_chunk(const float *pts, int c, int full) {
     const long long q0 = (long long)c * CHUNK;
     if (q0 >= full) return;
     const long long q1 = min((long long)full, q0 + CHUNK);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pairs + q0), "r"((unsigned)((q1 - q0) * 16))
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pts + q0 * 2 * PPV),
+                 "r"((unsigned)((q1 - q0) * 8 * PPV))
                  : "memory");
 }
 // the same from one thread without a branch: predicated on `issue` (and on the chunk
-// holding full pairs); the size is clamped to the pairs left
-__device__ __forceinline__ void prefetch_chunk_if(bool issue, const float4 *pairs, int c, int full) {
+// holding full vectors); the size is clamped to the vectors left
+__device__ __forceinline__ void prefetch_chunk_if(bool issue, const float *pts, int c, int full) {
     const int q0 = c * CHUNK;
     const int left = max(min(full - q0, CHUNK), 0);
     const unsigned go = (issue && left > 0) ? 1u : 0u;
     asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %2, 0;\n"
-                 "@p cp.async.bulk.prefetch.L2.global [%0], %1;\n}" ::"l"(pairs + q0), "r"(left * 16), "r"(go)
+                 "@p cp.async.bulk.prefetch.L2.global [%0], %1;\n}" ::"l"(pts + (long long)q0 * 2 * PPV),
+                 "r"(left * 8 * PPV), "r"(go)
                  : "memory");
 }
 
@@ -194,12 +232,13 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
              const float4 *__restrict__ heads, const float4 *__restrict__ edges, float gsx, float gox, float gsy,
              float goy, SLAB_PARAMS) {
     extern __shared__ __align__(16) unsigned smem[];
-    const float4 *pairs = reinterpret_cast<const float4 *>(points);
-    const int full = n >> 1, npairs = (n + 1) >> 1;  // pair q = points 2q, 2q + 1; an odd tail pair
+    const float *pts = reinterpret_cast<const float *>(points);
+    // vector q = points PPV q .. PPV q + PPV - 1; a partial tail vector when n % PPV != 0
+    const int full = n / PPV, nvec = (n + PPV - 1) / PPV;
 #if PREFETCH
     // this block's first chunks head for L2 while the raster is staged
     if (threadIdx.x == 0)
-        for (int a = 0; a <= PREFETCH; ++a) prefetch_chunk(pairs, blockIdx.x + a * gridDim.x, full);
+        for (int a = 0; a <= PREFETCH; ++a) prefetch_chunk(pts, blockIdx.x + a * gridDim.x, full);
 #endif
 #if GRID_SMEM
     constexpr int GRID_WORDS = (GRID * GRID + 15) / 16;
@@ -215,7 +254,6 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
     // per warp: QCAP undecided points {px, py} and their indices (bit 31: base parity)
     float2 *ring_p = reinterpret_cast<float2 *>(rings) + (threadIdx.x >> 5) * QCAP;
     int *ring_i = reinterpret_cast<int *>(rings + 2 * (BLOCK_SIZE_X / 32) * QCAP) + (threadIdx.x >> 5) * QCAP;
-    int2 *out = reinterpret_cast<int2 *>(bitmap);
     const int lane = threadIdx.x & 31;
     unsigned lanes_below;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_below));
@@ -271,64 +309,69 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
         }
     };
 #endif
-    const int n_chunks = (npairs + CHUNK - 1) / CHUNK;
-    auto load = [&](int c, float4 *v) {
+    const int n_chunks = (nvec + CHUNK - 1) / CHUNK;
+    auto load = [&](int c, pvec *v) {
 #pragma unroll
         for (int t = 0; t < TILE; ++t) {
             const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
-            if (c < n_chunks && q < full) v[t] = LOAD_PAIR(pairs + q);
-            else if (c < n_chunks && q < npairs) {
-                const float2 p = points[2 * q];
-                v[t] = make_float4(p.x, p.y, 0.f, 0.f);
-            } else v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < n_chunks && q < full) v[t] = load_vec(pts + (long long)q * 2 * PPV);
+            else {
+#pragma unroll
+                for (int j = 0; j < 2 * PPV; ++j) v[t].v[j] = 0.f;
+                if (c < n_chunks && q < nvec)  // the partial tail vector: its points one by one
+#pragma unroll
+                    for (int j = 0; j < PPV; ++j)
+                        if (PPV * q + j < n) {
+                            const float2 p = points[PPV * q + j];
+                            v[t].v[2 * j] = p.x, v[t].v[2 * j + 1] = p.y;
+                        }
+            }
         }
     };
-    auto chunk = [&](int c, const float4 *cur, const bool FULL) {  // inlined twice with FULL constant
+    // one point's push into the warp's ring (u != 0: undecided); k carries the base parity in bit 0
+    auto push = [&](float px, float py, int idx, unsigned k, unsigned u) {
+        const unsigned need = ballot_nz(u);
+        const unsigned pos = (tail + __popc(need & lanes_below)) % QCAP;
+        if (u) ring_p[pos] = make_float2(px, py), ring_i[pos] = idx | (int)(k << 31);
+        tail += __popc(need);
+    };
+    auto chunk = [&](int c, const pvec *cur, const bool FULL) {  // inlined twice with FULL constant
 #pragma unroll
         for (int t = 0; t < TILE; ++t) {
             const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
-            unsigned k0, k1, cell_;
-            CODE_OF(cur[t].x, cur[t].y, k0);
-            CODE_OF(cur[t].z, cur[t].w, k1);
+            unsigned k[PPV], cell_;
+#pragma unroll
+            for (int j = 0; j < PPV; ++j) CODE_OF(cur[t].v[2 * j], cur[t].v[2 * j + 1], k[j]);
             // decided points get their answer here; undecided ones a placeholder, rewritten
             // by a later drain of the same warp
-            if (FULL || q < full) STORE_PAIR(out + q, make_int2((int)(k0 & 1u), (int)(k1 & 1u)));
-            else if (q < npairs) bitmap[2 * q] = (int)(k0 & 1u);
+            if (FULL || q < full) store_vec(bitmap + (long long)PPV * q, k);
+            else if (q < nvec)
+#pragma unroll
+                for (int j = 0; j < PPV; ++j)
+                    if (PPV * q + j < n) bitmap[PPV * q + j] = (int)(k[j] & 1u);
+#pragma unroll
+            for (int j = 0; j < PPV; ++j) {
 #if PROBE_FLOOR == 2  // 2 = lookups, nothing queued
-            const unsigned u0 = 0u, u1 = 0u;
+                const unsigned u = 0u;
 #else
-            const unsigned u0 = (FULL || q < npairs) ? (k0 & 2u) : 0u, u1 = (FULL || q < full) ? (k1 & 2u) : 0u;
+                const unsigned u = (FULL || PPV * q + j < n) ? (k[j] & 2u) : 0u;
 #endif
-            const bool s0 = u0 != 0u, s1 = u1 != 0u;
-            const unsigned need0 = ballot_nz(u0), need1 = ballot_nz(u1);
-#if ADRAIN  // drain after each point's push: the ring holds < 32 + 32
-            const unsigned p0 = (tail + __popc(need0 & lanes_below)) % QCAP;
-            if (s0) ring_p[p0] = make_float2(cur[t].x, cur[t].y), ring_i[p0] = (2 * q) | (int)(k0 << 31);
-            tail += __popc(need0);
-            drain();
-            const unsigned p1 = (tail + __popc(need1 & lanes_below)) % QCAP;
-            if (s1) ring_p[p1] = make_float2(cur[t].z, cur[t].w), ring_i[p1] = (2 * q + 1) | (int)(k1 << 31);
-            tail += __popc(need1);
-            drain();
-#else
-            const unsigned p0 = (tail + __popc(need0 & lanes_below)) % QCAP, t1 = tail + __popc(need0);
-            const unsigned p1 = (t1 + __popc(need1 & lanes_below)) % QCAP;
-            if (s0) ring_p[p0] = make_float2(cur[t].x, cur[t].y), ring_i[p0] = (2 * q) | (int)(k0 << 31);
-            if (s1) ring_p[p1] = make_float2(cur[t].z, cur[t].w), ring_i[p1] = (2 * q + 1) | (int)(k1 << 31);
-            tail = t1 + __popc(need1);
-            drain();
-#endif
+                push(cur[t].v[2 * j], cur[t].v[2 * j + 1], PPV * q + j, k[j], u);
+                // ring: < 32 left after a drain; split drains after every push (+32), whole
+                // drains after every second push (+64)
+                if (ADRAIN || (j & 1)) drain();
+            }
         }
     };
 #if REGPF
-    float4 nxt[TILE];  // the next chunk, loaded while this one is classified
+    pvec nxt[TILE];  // the next chunk, loaded while this one is classified
     load(blockIdx.x, nxt);
 #endif
     for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
 #if PREFETCH
-        prefetch_chunk_if(threadIdx.x == 0, pairs, c + (PREFETCH + 1) * gridDim.x, full);
+        prefetch_chunk_if(threadIdx.x == 0, pts, c + (PREFETCH + 1) * gridDim.x, full);
 #endif
-        float4 cur[TILE];
+        pvec cur[TILE];
 #if REGPF
 #pragma unroll
         for (int t = 0; t < TILE; ++t) cur[t] = nxt[t];

@@ -708,6 +708,7 @@ class PnPolyCellsProblem(PnPolyGridProblem):
             "prefetch": [0, 1, 2],
             "adrain": [0, 1],
             "head32": [0, 1],
+            "quad": [0, 1],
         }
     # REGPF (register double buffering) stays a kernel option (tests/test_gpu_slab.py runs
     # it); it measured slower everywhere, so it is not tuned
@@ -720,13 +721,14 @@ class PnPolyCellsProblem(PnPolyGridProblem):
 
     def default_config(self):
         return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0, "prefetch": 1, "regpf": 0,
-                "adrain": 1, "head32": 0}
+                "adrain": 1, "head32": 0, "quad": 0}
 
     def defines(self, config):
         c = _as_dict(config)
         return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"],
                 "GRID_SMEM": c.get("grid_smem", 1), "STREAM": c.get("stream", 0), "PREFETCH": c.get("prefetch", 0),
-                "REGPF": c.get("regpf", 0), "ADRAIN": c.get("adrain", 0), "HEAD32": c.get("head32", 0)}
+                "REGPF": c.get("regpf", 0), "ADRAIN": c.get("adrain", 0), "HEAD32": c.get("head32", 0),
+                **({"QUAD": 1} if c.get("quad", 0) else {})}
 
     def cell_table(self, g: int, lmax: int, head_words: int = 4):
         cache = self.__dict__.setdefault("_cell_tables", {})
@@ -743,7 +745,7 @@ class PnPolyCellsProblem(PnPolyGridProblem):
 
     def launch(self, config, n_points: int | None = None):
         c = _as_dict(config)
-        chunk = 2 * c["block_size_x"] * c["tile"]
+        chunk = (2 + 2 * c.get("quad", 0)) * c["block_size_x"] * c["tile"]
         chunks = max(1, math.ceil((self.n_points if n_points is None else n_points) / chunk))
         smem = self.smem_bytes(c)
         sms = self.gpu.sm_count if self.gpu is not None else 148

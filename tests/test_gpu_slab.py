@@ -288,7 +288,12 @@ CELLS_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stre
                        regpf=(t + l) % 2, adrain=(g // 256 + st) % 2, head32=(b // 256 + l) % 2)
                   for b, t, g, l, st in itertools.product((256, 1024), (1, 2, 4), (256, 512), (4, 16), (0, 1))]
                  + [dict(block_size_x=b, tile=2, grid=g, grid_smem=0, lmax=16, stream=0, prefetch=pf, regpf=pf // 2, adrain=1, head32=pf // 2)
-                    for b, g, pf in itertools.product((256, 1024), (512, 1024), (0, 2))])
+                    for b, g, pf in itertools.product((256, 1024), (512, 1024), (0, 2))]
+                 # QUAD: four points per 32-byte load, four results per 16-byte store
+                 + [dict(block_size_x=b, tile=t, grid=448, grid_smem=1, lmax=16, stream=st, prefetch=pf, regpf=0,
+                         adrain=ad, head32=h, quad=1)
+                    for b, t, st, pf, ad, h in itertools.product((256, 1024), (1, 2), (0, 1), (0, 1), (0, 1), (0, 1))
+                    if (b + t + st + pf + ad + h) % 2 == 0])
 
 
 @pytest.fixture(scope="module")
@@ -318,7 +323,9 @@ def test_cells_tiny_and_ragged_inputs(gpu, n):
                 dict(p.default_config(), tile=4, block_size_x=512), dict(p.default_config(), grid=1024, grid_smem=0),
                 dict(p.default_config(), lmax=0), dict(p.default_config(), adrain=0),
                 dict(p.default_config(), adrain=1, tile=1, block_size_x=256),
-                dict(p.default_config(), head32=1, grid=448), dict(p.default_config(), head32=1, adrain=0)):
+                dict(p.default_config(), head32=1, grid=448), dict(p.default_config(), head32=1, adrain=0),
+                dict(p.default_config(), quad=1, tile=1), dict(p.default_config(), quad=1, adrain=0, regpf=1),
+                dict(p.default_config(), quad=1, block_size_x=256, tile=2, stream=1)):
         np.testing.assert_array_equal(run_once(gpu, p, cfg),
                                       O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2), err_msg=str(cfg))
 
