@@ -134,6 +134,12 @@ int jt_synchronize(jt_ctx *ctx);
 int jt_compile(const char *source, const char *program_name, const char *const *options, int n_options,
                void **image, size_t *image_bytes, char *log, size_t log_capacity);
 void jt_free_image(void *image);
+/* Version and path of the NVRTC jt_compile uses: dlopen'ed by full path from the
+ * toolkit (JT_CUDA_HOME / CUDA_HOME / /usr/local/cuda), never whichever
+ * libnvrtc.so.12 the host process happened to load first. No reference
+ * counterpart (Kernel Tuner reports its compiler through the `compiler`
+ * field of its environment record, core.py get_environment). */
+int jt_nvrtc_version(int *major, int *minor, char *path, size_t path_capacity);
 int jt_module_load(jt_ctx *ctx, const void *image, size_t image_bytes, jt_module **out);
 int jt_module_unload(jt_ctx *ctx, jt_module *module);
 int jt_kernel_get(jt_ctx *ctx, jt_module *module, const char *name, jt_kernel **out);

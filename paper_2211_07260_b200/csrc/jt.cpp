@@ -700,38 +700,109 @@ int jt_stream_wait_event(jt_ctx *c, int event_index) {
 }
 
 // --- compile / load ------------------------------------------------------------
+//
+// NVRTC is dlopen'ed by full path from the toolkit the library was built against
+// (JT_CUDA_HOME, else CUDA_HOME, else /usr/local/cuda), RTLD_LOCAL. Linking it by
+// soname would bind to whichever libnvrtc.so.12 the process loaded first: after
+// `import torch` that is torch's bundled 12.8 copy, whose ptxas rejects PTX 8.8
+// forms the kernels use (ld.global.v8.f32 = LDG.E.256), and whose code generation
+// would silently differ between test processes that did or did not import torch.
+namespace {
+struct Nvrtc {
+    std::once_flag once;
+    void *lib = nullptr;
+    std::string path;
+    decltype(&nvrtcCreateProgram) create = nullptr;
+    decltype(&nvrtcCompileProgram) compile = nullptr;
+    decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+    decltype(&nvrtcGetProgramLog) get_log = nullptr;
+    decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+    decltype(&nvrtcGetCUBIN) get_cubin = nullptr;
+    decltype(&nvrtcDestroyProgram) destroy = nullptr;
+    decltype(&nvrtcGetErrorString) error_string = nullptr;
+    decltype(&nvrtcVersion) version = nullptr;
+} g_nvrtc;
+
+int nvrtc_load() {
+    std::call_once(g_nvrtc.once, [] {
+        std::vector<std::string> tries;
+        for (const char *env : {"JT_CUDA_HOME", "CUDA_HOME"})
+            if (const char *h = std::getenv(env); h && *h) tries.push_back(std::string(h) + "/lib64/libnvrtc.so.12");
+#ifdef JT_CUDA_LIB_DIR
+        tries.push_back(JT_CUDA_LIB_DIR "/libnvrtc.so.12");  // the toolkit libjt was built against
+#endif
+        tries.push_back("/usr/local/cuda/lib64/libnvrtc.so.12");
+        tries.push_back("libnvrtc.so.12");  // last resort: whatever the loader finds
+        for (const auto &p : tries) {
+            if ((g_nvrtc.lib = dlopen(p.c_str(), RTLD_NOW | RTLD_LOCAL))) {
+                g_nvrtc.path = p;
+                break;
+            }
+        }
+        if (!g_nvrtc.lib) return;
+        auto sym = [](auto &fn, const char *name) { fn = reinterpret_cast<std::decay_t<decltype(fn)>>(dlsym(g_nvrtc.lib, name)); };
+        sym(g_nvrtc.create, "nvrtcCreateProgram");
+        sym(g_nvrtc.compile, "nvrtcCompileProgram");
+        sym(g_nvrtc.log_size, "nvrtcGetProgramLogSize");
+        sym(g_nvrtc.get_log, "nvrtcGetProgramLog");
+        sym(g_nvrtc.cubin_size, "nvrtcGetCUBINSize");
+        sym(g_nvrtc.get_cubin, "nvrtcGetCUBIN");
+        sym(g_nvrtc.destroy, "nvrtcDestroyProgram");
+        sym(g_nvrtc.error_string, "nvrtcGetErrorString");
+        sym(g_nvrtc.version, "nvrtcVersion");
+    });
+    if (!g_nvrtc.lib) return fail(JT_ECOMPILE, "libnvrtc.so.12 not found (set JT_CUDA_HOME)");
+    if (!g_nvrtc.create || !g_nvrtc.compile || !g_nvrtc.log_size || !g_nvrtc.get_log || !g_nvrtc.cubin_size ||
+        !g_nvrtc.get_cubin || !g_nvrtc.destroy || !g_nvrtc.error_string || !g_nvrtc.version)
+        return fail(JT_ECOMPILE, "%s lacks an NVRTC entry point", g_nvrtc.path.c_str());
+    return JT_OK;
+}
+}  // namespace
+
+int jt_nvrtc_version(int *major, int *minor, char *path, size_t path_capacity) {
+    if (!major || !minor) return fail(JT_EINVAL, "null version argument");
+    if (int e = nvrtc_load()) return e;
+    g_nvrtc.version(major, minor);
+    if (path && path_capacity) {
+        std::snprintf(path, path_capacity, "%s", g_nvrtc.path.c_str());
+    }
+    return JT_OK;
+}
+
 int jt_compile(const char *source, const char *program_name, const char *const *options, int n_options,
                void **image, size_t *image_bytes, char *log, size_t log_capacity) {
     if (!source || !image || !image_bytes) return fail(JT_EINVAL, "null compile argument");
     *image = nullptr;
     *image_bytes = 0;
     if (log && log_capacity) log[0] = 0;
+    if (int e = nvrtc_load()) return e;
+    const Nvrtc &N = g_nvrtc;
     nvrtcProgram prog;
-    nvrtcResult r = nvrtcCreateProgram(&prog, source, program_name ? program_name : "kernel.cu", 0, nullptr, nullptr);
-    if (r != NVRTC_SUCCESS) return fail(JT_ECOMPILE, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
-    r = nvrtcCompileProgram(prog, n_options, options);
+    nvrtcResult r = N.create(&prog, source, program_name ? program_name : "kernel.cu", 0, nullptr, nullptr);
+    if (r != NVRTC_SUCCESS) return fail(JT_ECOMPILE, "nvrtcCreateProgram: %s", N.error_string(r));
+    r = N.compile(prog, n_options, options);
     size_t log_size = 0;
-    nvrtcGetProgramLogSize(prog, &log_size);
+    N.log_size(prog, &log_size);
     if (log && log_capacity && log_size > 1) {
         std::vector<char> buf(log_size + 1);
-        nvrtcGetProgramLog(prog, buf.data());
+        N.get_log(prog, buf.data());
         size_t k = std::min(log_capacity - 1, log_size);
         std::memcpy(log, buf.data(), k);
         log[k] = 0;
     }
     if (r != NVRTC_SUCCESS) {
-        nvrtcDestroyProgram(&prog);
-        return fail(JT_ECOMPILE, "nvrtcCompileProgram: %s", nvrtcGetErrorString(r));
+        N.destroy(&prog);
+        return fail(JT_ECOMPILE, "nvrtcCompileProgram: %s", N.error_string(r));
     }
     size_t n = 0;
-    r = nvrtcGetCUBINSize(prog, &n);
+    r = N.cubin_size(prog, &n);
     if (r != NVRTC_SUCCESS || n == 0) {
-        nvrtcDestroyProgram(&prog);
-        return fail(JT_ECOMPILE, "no cubin produced (use --gpu-architecture=sm_100a): %s", nvrtcGetErrorString(r));
+        N.destroy(&prog);
+        return fail(JT_ECOMPILE, "no cubin produced (use --gpu-architecture=sm_100a): %s", N.error_string(r));
     }
     void *buf = std::malloc(n);
-    nvrtcGetCUBIN(prog, (char *)buf);
-    nvrtcDestroyProgram(&prog);
+    N.get_cubin(prog, (char *)buf);
+    N.destroy(&prog);
     *image = buf;
     *image_bytes = n;
     return JT_OK;

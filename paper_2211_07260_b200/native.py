@@ -23,6 +23,7 @@ point raises.
 from __future__ import annotations
 
 import ctypes
+import functools
 import hashlib
 import os
 import subprocess
@@ -54,7 +55,7 @@ EXPORTS = (
     "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
     "jt_h2d_async", "jt_d2h_async", "jt_tensor_map_2d", "jt_streams_reserve", "jt_stream_select",
     "jt_stream_wait_event", "jt_pnpoly_slabs", "jt_pnpoly_grid", "jt_pnpoly_cells", "jt_h2d_2d_async",
-    "jt_d2h_2d_async",
+    "jt_d2h_2d_async", "jt_nvrtc_version",
 )
 
 
@@ -162,7 +163,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
         "g++", "-std=c++17", "-O2", "-g", "-ffp-contract=off", "-fPIC", "-shared", "-Wall", "-Wextra",
         "-Wno-unused-parameter", f"-I{INCLUDE_DIR}", f"-I{CUDA_HOME / 'include'}", str(src),
         "-o", str(LIB_PATH) + ".tmp", f"-L{CUDA_HOME / 'lib64'}", f"-Wl,-rpath,{CUDA_HOME / 'lib64'}",
-        "-lnvrtc", "-ldl", "-lpthread",
+        f'-DJT_CUDA_LIB_DIR="{CUDA_HOME / "lib64"}"',
+        "-ldl", "-lpthread",  # NVRTC is dlopen'ed by full path (jt.cpp nvrtc_load)
     ]
     if verbose:
         print(" ".join(cmd))
@@ -202,6 +204,7 @@ def _declare(lib) -> None:
              c.c_char_p, c.c_size_t],
         ),
         "jt_free_image": (None, [P]),
+        "jt_nvrtc_version": (c.c_int, [c.POINTER(c.c_int), c.POINTER(c.c_int), c.c_char_p, c.c_size_t]),
         "jt_module_load": (c.c_int, [P, P, c.c_size_t, c.POINTER(P)]),
         "jt_module_unload": (c.c_int, [P, P]),
         "jt_kernel_get": (c.c_int, [P, P, c.c_char_p, c.POINTER(P)]),
@@ -323,8 +326,18 @@ def kernel_source(filename: str) -> str:
     return (KERNEL_DIR / filename).read_text()
 
 
+@functools.lru_cache(maxsize=1)
+def nvrtc_version() -> tuple[int, int, str]:
+    """(major, minor, library path) of the NVRTC behind jt_compile."""
+    major, minor = ctypes.c_int(), ctypes.c_int()
+    path = ctypes.create_string_buffer(4096)
+    check(lib().jt_nvrtc_version(ctypes.byref(major), ctypes.byref(minor), path, len(path)), "jt_nvrtc_version")
+    return major.value, minor.value, path.value.decode()
+
+
 def cubin_key(source: str, options: list[str]) -> str:
     h = hashlib.sha256()
+    h.update("nvrtc {}.{}\0".format(*nvrtc_version()[:2]).encode())  # a cubin belongs to its compiler
     h.update(source.encode())
     for o in options:
         h.update(b"\0" + o.encode())

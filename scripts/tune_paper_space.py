@@ -1,21 +1,27 @@
-"""Exhaustive tuning of the paper's GEMM space on B200 (17,472 CLBlast configs).
+"""Exhaustive tuning of whole kernel spaces on B200.
 
 The paper benchmarks every config of Kernel Tuner's CLBlast xgemm space
-(``SgemmProblem(value_set="clblast")``) at 4096^3. This script does the same
-through the reference API (``benchmark`` + ``NVMLObserver``, energy from the
-NVML counter), resumable across GPU calls through the reference-format JSONL
-cache ``results/cache_sgemm_clblast.jsonl``:
+(17,472 configs, ``SgemmProblem(value_set="clblast")``) at
+4096^3. This script does the same through the reference API (``benchmark`` +
+``NVMLObserver``, energy from the NVML counter), resumable across GPU calls
+through a reference-format JSONL cache per space, for:
 
-    python scripts/tune_paper_space.py verify              # all 17,472 at 256x256x128 vs the oracle
-    python scripts/tune_paper_space.py sweep --seconds 1800  # measure uncached configs (resumable)
-    python scripts/tune_paper_space.py confirm             # leaders in 3 x 1 s loops -> tuned_b200.json
+* ``--space sgemm_clblast``: the paper's 17,472-config GEMM space (default);
+* ``--space pnpoly``: the whole brute-force PnPoly space (10,624 configs,
+  20 M points x 600 vertices), bit-exact verification against the oracle
+  formulation each config computes;
+* ``--space sgemm_tf32``: the tcgen05 TF32 space (153 configs).
+
+    python scripts/tune_paper_space.py [--space S] verify       # every config at a small shape vs the oracle
+    python scripts/tune_paper_space.py [--space S] sweep --seconds 1800   # measure uncached configs (resumable)
+    python scripts/tune_paper_space.py [--space S] confirm      # leaders in 3 x 1 s loops -> tuned_b200.json
 
 Clock control is refused on this pool (profiles/r2_knob_probe.json), so the
 (config x clock) product of the paper is config-only here; the space runs at
 the driver-managed clock and every result records the observed clock.
 Outputs (also mirrored under gpurun_out/ so they come back from the box):
-results/cache_sgemm_clblast.jsonl, results/paper_space_verify.json,
-results/paper_space_report.json.
+results/cache_<space>.jsonl, results/<space>_verify.json,
+results/<space>_report.json.
 """
 
 from __future__ import annotations
@@ -41,8 +47,40 @@ from paper_2211_07260_b200.gpu import GPU, fp32_peak_tflops  # noqa: E402
 from paper_2211_07260_b200.kernels import make_problem  # noqa: E402
 
 RESULTS = ROOT / "results"
-CACHE = RESULTS / "cache_sgemm_clblast.jsonl"
 MIRROR = ROOT / "gpurun_out" / "results"
+
+#: space -> (problem factory at full size, factory at the verification size, description)
+SPACES = {
+    "sgemm_clblast": (lambda: make_problem("sgemm", value_set="clblast"),
+                      lambda: make_problem("sgemm", value_set="clblast", m=256, n=256, k=128),
+                      "Kernel Tuner CLBlast xgemm, 17,472 configs (PAPER.md:318), 4096^3 FP32, alpha 1 beta 0.5"),
+    "pnpoly": (lambda: make_problem("pnpoly"), lambda: make_problem("pnpoly", n_points=100_003),
+               "brute-force PnPoly, whole space (10,624 configs), 20 M points x 600 vertices"),
+    "sgemm_tf32": (lambda: make_problem("sgemm_tf32"), lambda: make_problem("sgemm_tf32", m=512, n=512, k=256),
+                   "tcgen05 TF32 SGEMM, whole space, 4096^3, alpha 1 beta 0.5"),
+}
+
+
+def cache_path(space: str) -> Path:
+    return RESULTS / f"cache_{space}.jsonl"
+
+
+def check_output(problem, cfg, ref) -> tuple[bool, str, float]:
+    """(ok, message, error) of the problem's current output against the oracle ``ref``."""
+    got = problem.fetch_output()
+    if problem.name.startswith("pnpoly"):
+        bad = int((got != ref[problem.formula(cfg)]).sum())
+        return bad == 0, f"{bad} points differ", float(bad)
+    err = O.sgemm_error(got, ref)
+    tol = O.SGEMM_TF32_TOL if problem.name == "sgemm_tf32" else O.SGEMM_TOL
+    return err <= tol, f"normalised error {err:.3g}", err
+
+
+def oracle_refs(problem):
+    inp = problem.inputs
+    if problem.name.startswith("pnpoly"):
+        return {f: O.pnpoly(inp["points"], inp["vx"], inp["vy"], f) for f in (0, 1, 2, 3)}
+    return O.sgemm(inp["a"], inp["b"], inp["c0"], problem.alpha, problem.beta)
 
 
 def mirror(*paths: Path) -> None:
@@ -68,8 +106,8 @@ def compile_all(problem, configs) -> dict:
 
 
 def cmd_verify(args) -> None:
-    """Every config of the space, once, at a small shape, against the fp64 oracle."""
-    problem = make_problem("sgemm", value_set="clblast", m=256, n=256, k=128)
+    """Every config of the space, once, at a small shape, against the oracle."""
+    problem = SPACES[args.space][1]()
     configs = problem.space().enumerate()
     t0 = time.time()
     errors = compile_all(problem, configs)
@@ -77,32 +115,39 @@ def cmd_verify(args) -> None:
     worst, failed = 0.0, []
     with GPU(0) as gpu:
         problem.prepare(gpu)
-        ref = O.sgemm(problem.inputs["a"], problem.inputs["b"], problem.inputs["c0"], problem.alpha, problem.beta)
+        ref = oracle_refs(problem)
         for c in configs:
             cfg = {**problem.default_config(), **c.as_dict()}
             try:
                 k = problem.kernel(cfg)
                 problem.reset_output()
                 gpu.launch(k, problem.launch(cfg), problem.args(cfg))
-                err = O.sgemm_error(problem.fetch_output(), ref)
+                gpu.synchronize()
+                ok, msg, err = check_output(problem, cfg, ref)
             except Exception as exc:  # noqa: BLE001
                 failed.append({"config": c.as_dict(), "error": str(exc)[:200]})
                 continue
             worst = max(worst, err)
-            if not err <= O.SGEMM_TOL:
-                failed.append({"config": c.as_dict(), "error": f"normalised error {err:.3g}"})
-    doc = {"space": "Kernel Tuner CLBlast xgemm (PAPER.md:318)", "configs": len(configs), "shape": [256, 256, 128],
-           "compile_errors": len(errors), "failed": failed, "worst_normalised_error": worst,
-           "bar": O.SGEMM_TOL, "compile_s": round(compile_s, 1), "run_s": round(time.time() - t0 - compile_s, 1)}
-    out = RESULTS / "paper_space_verify.json"
+            if not ok:
+                failed.append({"config": c.as_dict(), "error": msg})
+    pn = problem.name.startswith("pnpoly")
+    doc = {"space": SPACES[args.space][2], "configs": len(configs),
+           "shape": [problem.n_points, problem.n_vertices] if pn else [problem.m, problem.n, problem.k],
+           "compile_errors": len(errors), "failed": failed,
+           ("worst_points_differing" if pn else "worst_normalised_error"): worst,
+           "bar": "bit-exact vs the oracle formulation each config computes" if pn else
+           (O.SGEMM_TF32_TOL if problem.name == "sgemm_tf32" else O.SGEMM_TOL),
+           "compile_s": round(compile_s, 1), "run_s": round(time.time() - t0 - compile_s, 1)}
+    out = RESULTS / f"{args.space}_verify.json"
     out.write_text(json.dumps(doc, indent=1) + "\n")
     mirror(out)
     print(json.dumps({k: v for k, v in doc.items() if k != "failed"}), "failed:", len(failed), flush=True)
 
 
 def cmd_sweep(args) -> None:
-    problem = make_problem("sgemm", value_set="clblast")
+    problem = SPACES[args.space][0]()
     configs = problem.space().enumerate()
+    CACHE = cache_path(args.space)
     cache = ResultCache(CACHE)
     todo = [c for c in configs if c not in cache]
     print(f"{len(configs)} configs, {len(configs) - len(todo)} cached, {len(todo)} to measure", flush=True)
@@ -135,10 +180,10 @@ def cmd_confirm(args) -> None:
     sys.path.insert(0, str(ROOT / "scripts"))
     from tune_suite import TUNED_PATH, confirm, oracle_check  # noqa: E402
 
-    problem = make_problem("sgemm", value_set="clblast")
+    problem = SPACES[args.space][0]()
     space = problem.space()
     configs = space.enumerate()
-    cache = ResultCache(CACHE)
+    cache = ResultCache(cache_path(args.space))
     results = [cache.get(c) for c in configs]
     have = [r for r in results if r is not None]
     ok = [r for r in have if not r.failed]
@@ -165,7 +210,7 @@ def cmd_confirm(args) -> None:
     best_t = min(ok, key=lambda r: r.time)
     best_e = min(ok, key=lambda r: r.energy)
     report = {
-        "space": "Kernel Tuner CLBlast xgemm, 17,472 configs (PAPER.md:318), 4096^3 FP32, alpha 1 beta 0.5",
+        "space": SPACES[args.space][2],
         "measured": len(have), "failed": len(have) - len(ok), "space_size": len(configs),
         "window_s": args.window, "observer": "NVMLObserver (energy-counter slope x per-launch runtime)",
         "clock": "driver-managed (clock control refused: profiles/r2_knob_probe.json); observed clock per result",
@@ -182,10 +227,10 @@ def cmd_confirm(args) -> None:
         "fp32_peak_tflops_at_1965": fp32_peak_tflops(sm, 1965.0),
         "confirmed": {"time_optimal": by_time, "energy_optimal": by_energy, "candidates": confirmed},
     }
-    out = RESULTS / "paper_space_report.json"
+    out = RESULTS / f"{args.space}_report.json"
     out.write_text(json.dumps(report, indent=1) + "\n")
     data = json.loads(TUNED_PATH.read_text()) if TUNED_PATH.exists() else {}
-    data["sgemm_clblast"] = {"space_size": len(configs), "strategy": "exhaustive", "evaluations": len(have),
+    data[args.space if args.space != "pnpoly" else "pnpoly_space"] = {"space_size": len(configs), "strategy": "exhaustive", "evaluations": len(have),
                              "failed": len(have) - len(ok), "time_optimal": by_time, "energy_optimal": by_energy,
                              "confirm": {"rounds": 3, "window_s": 1.0, "candidates": confirmed}}
     TUNED_PATH.write_text(json.dumps(data, indent=1) + "\n")
@@ -197,6 +242,7 @@ def cmd_confirm(args) -> None:
 
 def main() -> None:
     ap = argparse.ArgumentParser()
+    ap.add_argument("--space", choices=sorted(SPACES), default="sgemm_clblast")
     sub = ap.add_subparsers(dest="cmd", required=True)
     sub.add_parser("verify")
     s = sub.add_parser("sweep")
