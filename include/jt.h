@@ -145,6 +145,10 @@ int jt_module_unload(jt_ctx *ctx, jt_module *module);
 int jt_kernel_get(jt_ctx *ctx, jt_module *module, const char *name, jt_kernel **out);
 int jt_kernel_attributes(jt_ctx *ctx, jt_kernel *kernel, int *regs, int *static_smem, int *local_bytes,
                          int *max_threads);
+/* Resident CTAs per SM for `block_threads` threads and `dynamic_smem` bytes
+ * (cuOccupancyMaxActiveBlocksPerMultiprocessor; raises the kernel's dynamic
+ * shared-memory limit first). Used to size split-tail grids to whole waves. */
+int jt_kernel_occupancy(jt_ctx *ctx, jt_kernel *kernel, int block_threads, size_t dynamic_smem, int *blocks_per_sm);
 
 /* --- execution (SimulatedDevice.execute, device.py:349-382) ------------------ */
 int jt_launch(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, const jt_arg *args, int n_args);

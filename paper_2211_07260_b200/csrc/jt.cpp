@@ -94,6 +94,7 @@ double real_now() {
     X(cuModuleGetGlobal) \
     X(cuModuleLoadData) \
     X(cuModuleUnload) \
+    X(cuOccupancyMaxActiveBlocksPerMultiprocessor) \
     X(cuStreamCreate) \
     X(cuStreamDestroy) \
     X(cuStreamSynchronize) \
@@ -856,6 +857,19 @@ int jt_kernel_attributes(jt_ctx *c, jt_kernel *k, int *regs, int *static_smem, i
     if (static_smem) D.p_cuFuncGetAttribute(static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, k->fn);
     if (local_bytes) D.p_cuFuncGetAttribute(local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, k->fn);
     if (max_threads) D.p_cuFuncGetAttribute(max_threads, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, k->fn);
+    return JT_OK;
+}
+
+int jt_kernel_occupancy(jt_ctx *c, jt_kernel *k, int block_threads, size_t dynamic_smem, int *blocks_per_sm) {
+    if (int e = bind(c)) return e;
+    if (!k || !blocks_per_sm || block_threads < 1) return fail(JT_EINVAL, "bad occupancy arguments");
+    if (dynamic_smem > 48 * 1024 && (unsigned)dynamic_smem != k->smem_attr) {
+        CUresult r = D.p_cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dynamic_smem);
+        if (r != CUDA_SUCCESS) return cu_fail(r, "raise dynamic shared memory limit");
+        k->smem_attr = (unsigned)dynamic_smem;
+    }
+    CU_TRY(D.p_cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k->fn, block_threads, dynamic_smem),
+           "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     return JT_OK;
 }
 

@@ -35,6 +35,16 @@
 //                   A streams past every B column panel), g = groups of g M-tiles
 //                   sweep the N-tiles together, so the resident CTAs' A and B
 //                   panels stay in L2 (fewer DRAM re-reads; same result bits).
+//   SPLIT_TAIL      (B200 addition) 0: one CTA per C tile (2D grid). s > 1: a 1D
+//                   grid in which the tiles that fill whole waves (full_tiles =
+//                   a multiple of SMs x resident CTAs, sized by the host) run
+//                   whole, and the last partial wave's tiles are split along K
+//                   over `split` (<= s) CTAs each. 4096^2 in 128 x 128 tiles is
+//                   1024 tiles = 3.46 waves of 296 CTAs: without the split the
+//                   4th wave runs at 46% occupancy. Partials go to a workspace;
+//                   the last of a tile's CTAs to arrive (per-tile counter, reset
+//                   by that CTA) sums them in part order (so the bits do not
+//                   depend on arrival order) and runs the epilogue.
 //
 // Requirements (the tuning-space restrictions, kernels.py):
 //   MWG % (MDIMC*VWM) == 0, NWG % (NDIMC*VWN) == 0,
@@ -98,6 +108,9 @@
 #endif
 #ifndef GROUP_M  // (B200 addition) CTA rasterisation group along M; 1 = CLBlast's launch order
 #define GROUP_M 1
+#endif
+#ifndef SPLIT_TAIL
+#define SPLIT_TAIL 0
 #endif
 #if FMA2 && (VWN % 2)
 #error "FMA2 needs an even VWN (accumulator pairs inside one B vector)"
@@ -198,17 +211,37 @@ extern "C" __global__ void __launch_bounds__(THREADS, MIN_BLOCKS)
 extern "C" __global__ void __launch_bounds__(THREADS)
 #endif
 sgemm(const int M, const int N, const int K, const float alpha, const float beta,
-      const float *__restrict__ at, const float *__restrict__ b, float *__restrict__ c) {
+      const float *__restrict__ at, const float *__restrict__ b, float *__restrict__ c
+#if SPLIT_TAIL
+      , float *__restrict__ ws, unsigned *__restrict__ counters, const int full_tiles, const int split
+#endif
+) {
     const int tid = threadIdx.x;
     const int tm = tid % MDIMC, tn = tid / MDIMC;
+    const int tiles = K / KWG;  // k-tiles
+#if SPLIT_TAIL
+    // 1D grid: [0, full_tiles) whole tiles, then `split` K-parts of each remaining tile
+    const int tiles_m = M / MWG, tiles_n = N / NWG;
+    int tile = blockIdx.x, part = 0, parts = 1;
+    if (tile >= full_tiles) {
+        const int u = tile - full_tiles;
+        tile = full_tiles + u / split;
+        part = u % split;
+        parts = split;
+    }
+    const int kt0 = part * tiles / parts, kt1 = (part + 1) * tiles / parts;
+    int m_tile = tile % tiles_m, n_tile = tile / tiles_m;
+#else
+    const int kt0 = 0, kt1 = tiles;
+    const int tiles_m = gridDim.x, tiles_n = gridDim.y;
+    int m_tile = blockIdx.x, n_tile = blockIdx.y;
+#endif
     // CTA rasterisation: GROUP_M = 1 is CLBlast's launch order (blockIdx.x walks M with one B
     // column panel); GROUP_M = g walks g M-tiles across all N-tiles before moving on, so the CTAs
     // resident at once share g A panels and a run of B panels in L2 instead of all of A.
-    int m_tile = blockIdx.x, n_tile = blockIdx.y;
 #if GROUP_M > 1
     {
-        const int tiles_m = gridDim.x, tiles_n = gridDim.y;
-        const int pid = blockIdx.x + blockIdx.y * tiles_m;
+        const int pid = m_tile + n_tile * tiles_m;
         const int per_group = GROUP_M * tiles_n;
         const int first = (pid / per_group) * GROUP_M;
         const int rows = min(tiles_m - first, GROUP_M);
@@ -303,8 +336,6 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
             }
         }
     };
-    const int tiles = K / KWG;
-
 #if ASYNC
     // global -> shared copies of k-tile `tile` into stage `buf`, same thread mapping as CLBlast's loads
     auto issue = [&](int tile, int buf) {
@@ -324,16 +355,17 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
     };
 #pragma unroll
     for (int s = 0; s < ASYNC - 1; ++s) {
-        if (s < tiles) issue(s, s);
+        if (kt0 + s < kt1) issue(kt0 + s, s);
         cp_async_commit();  // empty groups keep the wait_group arithmetic uniform
     }
 #pragma unroll 1
-    for (int t = 0; t < tiles; ++t) {
+    for (int t = kt0; t < kt1; ++t) {
+        const int i = t - kt0;
         cp_async_wait<ASYNC - 2>();  // this thread's copies of tile t have landed
         __syncthreads();             // everyone's have; and everyone is done with tile t-1's stage
-        if (t + ASYNC - 1 < tiles) issue(t + ASYNC - 1, (t + ASYNC - 1) % ASYNC);  // refill tile t-1's stage
+        if (t + ASYNC - 1 < kt1) issue(t + ASYNC - 1, (i + ASYNC - 1) % ASYNC);  // refill tile t-1's stage
         cp_async_commit();
-        mac_tile(t % ASYNC, t * KWG);
+        mac_tile(i % ASYNC, t * KWG);
     }
 #else
     auto fetch = [&](int k0) {
@@ -368,20 +400,20 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
     };
 
 #if SA || SB
-    fetch(0);
+    fetch(kt0 * KWG);
     stash(0);
     __syncthreads();
 #endif
 #pragma unroll 1
-    for (int t = 0; t < tiles; ++t) {
-        const int buf = t & 1;
+    for (int t = kt0; t < kt1; ++t) {
+        const int buf = (t - kt0) & 1;
         const int k0 = t * KWG;
 #if SA || SB
-        if (t + 1 < tiles) fetch(k0 + KWG);
+        if (t + 1 < kt1) fetch(k0 + KWG);
 #endif
         mac_tile(buf, k0);
 #if SA || SB
-        if (t + 1 < tiles) stash(buf ^ 1);
+        if (t + 1 < kt1) stash(buf ^ 1);
         __syncthreads();
 #endif
     }
@@ -397,6 +429,39 @@ sgemm(const int M, const int N, const int K, const float alpha, const float beta
             acc[i][j] = __uint_as_float((unsigned)acc2[i][j / 2]);
             acc[i][j + 1] = __uint_as_float((unsigned)(acc2[i][j / 2] >> 32));
         }
+#endif
+#if SPLIT_TAIL
+    if (parts > 1) {
+        // this part's partial tile -> workspace slot (coalesced: element e of every thread together)
+        const int slot0 = (tile - full_tiles) * parts;
+        float *mine = ws + (size_t)(slot0 + part) * (MWG * NWG);
+#pragma unroll
+        for (int i = 0; i < MWI; ++i)
+#pragma unroll
+            for (int j = 0; j < NWI; ++j) __stcg(mine + (i * NWI + j) * THREADS + tid, acc[i][j]);
+        __threadfence();
+        __syncthreads();
+        __shared__ unsigned arrived;
+        if (tid == 0) arrived = atomicAdd(counters + (tile - full_tiles), 1u);
+        __syncthreads();
+        if (arrived != (unsigned)(parts - 1)) return;  // another part finishes this tile
+        if (tid == 0) counters[tile - full_tiles] = 0u;  // every part has arrived: reset for the next launch
+        __threadfence();
+        // every partial (this CTA's too) is re-read from the workspace and summed in part order,
+        // whatever the arrival order, so the bits are reproducible
+        const float *w = ws + (size_t)slot0 * (MWG * NWG) + tid;
+#pragma unroll
+        for (int i = 0; i < MWI; ++i)
+#pragma unroll
+            for (int j = 0; j < NWI; ++j) {
+                const int e = (i * NWI + j) * THREADS;
+                float sum = __ldcg(w + e) + __ldcg(w + MWG * NWG + e);
+#pragma unroll
+                for (int q = 2; q < SPLIT_TAIL; ++q)
+                    if (q < parts) sum += __ldcg(w + q * (MWG * NWG) + e);
+                acc[i][j] = sum;
+            }
+    }
 #endif
     // epilogue: C = alpha * acc + beta * C, VWN-wide row segments
 #pragma unroll

@@ -187,6 +187,13 @@ class Kernel:
             f"set {symbol}",
         )
 
+    def occupancy(self, block_threads: int, dynamic_smem: int = 0) -> int:
+        """Resident CTAs per SM at this block size and dynamic shared memory (``jt_kernel_occupancy``)."""
+        n = ctypes.c_int()
+        check(native.lib().jt_kernel_occupancy(self.gpu.handle, self.handle, int(block_threads), int(dynamic_smem),
+                                               ctypes.byref(n)), f"occupancy {self.name}")
+        return n.value
+
 
 @dataclass
 class BenchRun:

@@ -959,6 +959,7 @@ class SgemmProblem(KernelProblem):
                 "MDIMC": [8, 16, 32], "NDIMC": [8, 16, 32], "MDIMA": [8, 16, 32, 64], "NDIMB": [8, 16, 32, 64],
                 "KWI": [1, 2, 4, 8], "VWM": [1, 2, 4], "VWN": [1, 2, 4], "STRM": [0, 1], "STRN": [0, 1],
                 "SA": [0, 1], "SB": [0, 1], "ASYNC": [0, 2, 3, 4], "FMA2": [0, 1], "GROUP_M": [1, 4, 8, 16],
+                "SPLIT_TAIL": [0, 2, 4],
             }
         return {
             "MWG": [16, 32, 64, 128], "NWG": [16, 32, 64, 128], "KWG": [16, 32],
@@ -995,7 +996,7 @@ class SgemmProblem(KernelProblem):
     def default_config(self):
         return {"MWG": 128, "NWG": 128, "KWG": 16, "MDIMC": 16, "NDIMC": 16, "MDIMA": 32, "NDIMB": 32,
                 "KWI": 2, "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 0, "FMA2": 0,
-                "GROUP_M": 1}
+                "GROUP_M": 1, "SPLIT_TAIL": 0}
 
     def defines(self, config):
         return dict(_as_dict(config))
@@ -1004,14 +1005,59 @@ class SgemmProblem(KernelProblem):
         c = _as_dict(config)
         return {"m": c["MWG"], "n": c["NWG"], "k": c["KWG"]}
 
-    def launch(self, config):
+    @staticmethod
+    def smem_bytes(config) -> int:
         c = _as_dict(config)
         stages = c.get("ASYNC", 0)
         if stages:  # cp.async stages
-            smem = c["KWG"] * (c["MWG"] + c["NWG"]) * 4 * stages
-        else:  # CLBlast's two buffers of the staged operands
-            smem = 2 * 4 * c["KWG"] * (c["SA"] * c["MWG"] + c["SB"] * c["NWG"])
-        return Launch((self.m // c["MWG"], self.n // c["NWG"], 1), (c["MDIMC"] * c["NDIMC"], 1, 1), smem=smem)
+            return c["KWG"] * (c["MWG"] + c["NWG"]) * 4 * stages
+        return 2 * 4 * c["KWG"] * (c["SA"] * c["MWG"] + c["SB"] * c["NWG"])  # CLBlast's two buffers
+
+    def tail_plan(self, config) -> tuple[int, int, int]:
+        """SPLIT_TAIL = s > 0: (full_tiles, split, grid) for the 1D split-tail grid. Whole waves of
+        SMs x resident CTAs (cuOccupancy for this config's registers and shared memory) run one
+        tile per CTA; the remaining tiles are split along K over up to s CTAs each, as many as
+        still fit one wave. Without a GPU (or no tail) every tile is whole."""
+        c = _as_dict(config)
+        tiles = (self.m // c["MWG"]) * (self.n // c["NWG"])
+        s = int(c.get("SPLIT_TAIL", 0))
+        if s < 2 or self.gpu is None:
+            return tiles, 1, tiles
+        key = ("tail", tuple(sorted(c.items())))
+        hit = self._plans.get(key) if hasattr(self, "_plans") else None
+        if hit:
+            return hit
+        per_sm = self.kernel(c).occupancy(c["MDIMC"] * c["NDIMC"], self.smem_bytes(c))
+        slots = max(1, per_sm) * self.gpu.sm_count
+        full = tiles // slots * slots
+        tail = tiles - full
+        split = min(s, slots // tail, self.k // c["KWG"]) if tail else 1
+        if split < 2:
+            full, split = tiles, 1
+        plan = (full, split, full + (tiles - full) * split)
+        if not hasattr(self, "_plans"):
+            self._plans = {}
+        self._plans[key] = plan
+        # workspace: one MWG x NWG partial per split CTA; one arrival counter per split tile (zeroed
+        # once; the last CTA of a tile resets its counter)
+        need_ws = (tiles - full) * split * c["MWG"] * c["NWG"]
+        if need_ws and ("tail_ws" not in self.buffers or self.buffers["tail_ws"].nbytes < 4 * need_ws):
+            if "tail_ws" in self.buffers:
+                self.buffers["tail_ws"].free()
+            self.buffers["tail_ws"] = self.gpu.empty((need_ws,), np.float32)
+        if "tail_counters" not in self.buffers or self.buffers["tail_counters"].nbytes < 4 * tiles:
+            if "tail_counters" in self.buffers:
+                self.buffers["tail_counters"].free()
+            self.buffers["tail_counters"] = self.gpu.empty((tiles,), np.uint32)
+            self.buffers["tail_counters"].fill(0)
+        return plan
+
+    def launch(self, config):
+        c = _as_dict(config)
+        block = (c["MDIMC"] * c["NDIMC"], 1, 1)
+        if c.get("SPLIT_TAIL", 0):
+            return Launch((self.tail_plan(c)[2], 1, 1), block, smem=self.smem_bytes(c))
+        return Launch((self.m // c["MWG"], self.n // c["NWG"], 1), block, smem=self.smem_bytes(c))
 
     def host_inputs(self):
         a = np.random.default_rng(self.seed).uniform(-1.0, 1.0, (self.m, self.k)).astype(np.float32)
@@ -1023,6 +1069,7 @@ class SgemmProblem(KernelProblem):
         self.gpu = gpu
         inputs = inputs or self.host_inputs()
         self.inputs = inputs
+        self._plans = {}  # split-tail plans refer to this buffer set
         self.buffers = {
             "at": gpu.array(np.ascontiguousarray(inputs["a"].T)),  # column-major A == row-major A^T
             "b": gpu.array(inputs["b"]),
@@ -1035,7 +1082,13 @@ class SgemmProblem(KernelProblem):
 
     def args(self, config):
         b = self.buffers
-        return [i32(self.m), i32(self.n), i32(self.k), f32(self.alpha), f32(self.beta), b["at"], b["b"], b["out"]]
+        base = [i32(self.m), i32(self.n), i32(self.k), f32(self.alpha), f32(self.beta), b["at"], b["b"], b["out"]]
+        if _as_dict(config).get("SPLIT_TAIL", 0):
+            full, split, _ = self.tail_plan(config)
+            ws = b.get("tail_ws") or b["out"]  # no split tile: never touched
+            counters = b.get("tail_counters") or b["out"]
+            return [*base, ws, counters, i32(full), i32(split)]
+        return base
 
 
 @dataclass

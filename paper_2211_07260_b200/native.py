@@ -55,7 +55,7 @@ EXPORTS = (
     "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
     "jt_h2d_async", "jt_d2h_async", "jt_tensor_map_2d", "jt_streams_reserve", "jt_stream_select",
     "jt_stream_wait_event", "jt_pnpoly_slabs", "jt_pnpoly_grid", "jt_pnpoly_cells", "jt_h2d_2d_async",
-    "jt_d2h_2d_async", "jt_nvrtc_version",
+    "jt_d2h_2d_async", "jt_nvrtc_version", "jt_kernel_occupancy",
 )
 
 
@@ -211,6 +211,7 @@ def _declare(lib) -> None:
         "jt_kernel_attributes": (
             c.c_int, [P, P, c.POINTER(c.c_int), c.POINTER(c.c_int), c.POINTER(c.c_int), c.POINTER(c.c_int)]
         ),
+        "jt_kernel_occupancy": (c.c_int, [P, P, c.c_int, c.c_size_t, c.POINTER(c.c_int)]),
         "jt_launch": (c.c_int, [P, P, c.POINTER(JTLaunchShape), c.POINTER(JTArg), c.c_int]),
         "jt_time": (
             c.c_int, [P, P, c.POINTER(JTLaunchShape), c.POINTER(JTArg), c.c_int, c.c_int, c.POINTER(c.c_double)]

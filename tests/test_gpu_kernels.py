@@ -290,6 +290,56 @@ def test_sgemm_group_m_rasterisation_bit_identical(gpu):
         np.testing.assert_array_equal(run_once(gpu, p, {**base, "GROUP_M": g}), one)
 
 
+SPLIT_BASE = {"MWG": 128, "NWG": 128, "KWG": 16, "MDIMC": 16, "NDIMC": 8, "MDIMA": 16, "NDIMB": 16, "KWI": 8,
+              "VWM": 4, "VWN": 4, "STRM": 1, "STRN": 1, "SA": 1, "SB": 1, "ASYNC": 4, "FMA2": 1, "GROUP_M": 1}
+
+
+@pytest.mark.parametrize("overrides", [{}, {"GROUP_M": 8}, {"ASYNC": 0}, {"ASYNC": 0, "SA": 0, "SB": 0, "FMA2": 0},
+                                       {"SPLIT_TAIL": 4}], ids=str)
+@pytest.mark.parametrize("mnk", [(2816, 2304, 512), (2560, 2304, 272), (1024, 1024, 400)], ids=str)
+def test_sgemm_split_tail(gpu, overrides, mnk):
+    """SPLIT_TAIL: the last partial wave's tiles split along K over 2-4 CTAs, partials summed through
+    the workspace by the last arriver. Within the FP32 bar, the per-tile counters left at zero, and
+    bit-reproducible over relaunches (the partials are summed in part order, not arrival order)."""
+    from paper_2211_07260_b200.kernels import SgemmProblem
+
+    m, n, k = mnk
+    p = SgemmProblem(m=m, n=n, k=k, beta=0.5, value_set="b200")
+    p.prepare(gpu)
+    cfg = {**SPLIT_BASE, "SPLIT_TAIL": 2, **overrides}
+    full, split, grid = p.tail_plan(cfg)
+    tiles = (m // 128) * (n // 128)
+    assert full % gpu.sm_count == 0 and grid == full + (tiles - full) * split
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    first = run_once(gpu, p, cfg).copy()
+    assert O.sgemm_error(first, ref) <= O.SGEMM_TOL
+    for _ in range(2):
+        np.testing.assert_array_equal(run_once(gpu, p, cfg).view(np.uint32), first.view(np.uint32))
+    if (m, n) == (1024, 1024):  # 64 tiles < half of any wave: all of them split along K
+        assert full == 0 and split >= 2, (full, split, grid)
+    if split > 1:
+        assert not p.buffers["tail_counters"].download().any()
+    whole = run_once(gpu, p, {**cfg, "SPLIT_TAIL": 0})
+    # whole tiles are bit-identical to the plain grid; split tiles differ by one rounding at most
+    assert O.sgemm_error(whole, ref) <= O.SGEMM_TOL
+
+
+def test_sgemm_split_tail_plan_at_4096(gpu):
+    """At 4096^3 the tuned 128 x 128 config leaves a partial 4th wave (1024 tiles over 2 x 148
+    resident CTAs): the plan runs 888 whole tiles and splits the other 136 in two."""
+    from paper_2211_07260_b200.kernels import SgemmProblem
+
+    p = SgemmProblem(value_set="b200")
+    p.prepare(gpu)
+    cfg = {**SPLIT_BASE, "SPLIT_TAIL": 2}
+    per_sm = p.kernel(cfg).occupancy(128, p.smem_bytes(cfg))
+    full, split, grid = p.tail_plan(cfg)
+    slots = per_sm * gpu.sm_count
+    assert full == 1024 // slots * slots and split == min(2, slots // (1024 - full))
+    ref = O.sgemm(p.inputs["a"], p.inputs["b"], p.inputs["c0"], p.alpha, p.beta)
+    assert O.sgemm_error(run_once(gpu, p, cfg), ref) <= O.SGEMM_TOL
+
+
 def test_sgemm_tf32_group_m_walk(gpu):
     """GROUP_M reorders the persistent tile walk only: without split tails the same bits, with them
     (which tiles get K-split changes) still inside the TF32 bar."""
