@@ -96,6 +96,7 @@ class Dist:
 
 E2E_STRIPS = 4  # row bands of the pipelined host-buffer call (suite.CONV2D_STRIPS)
 ENERGY_LOOP_S = 1.5  # the headline's dedicated energy loop (>= 10 energy-counter updates)
+ISSUE_MIX_CYCLES = 5.15  # scheduler cycles per 32 brute-force edge tests (ASM 7 mix, measured)
 ENERGY_SETTLE_S = 0.25  # skipped at its start: power ramp after the timed region
 
 
@@ -308,6 +309,11 @@ def measure_tuned(gpu, name: str, objective: str, seconds: float = 1.0, settle: 
                 peak /= 2.0  # 1 lane-instruction slot per lane per clock, not 2 flop/FFMA
                 out["edge_tests_per_s"] = round(prob.edge_tests / run.per_launch_s, 1)
                 out["j_per_bitmap"] = round(watts * run.per_launch_s, 6) if watts else None
+                # the measured issue bound of the crossing-test instruction mix (DESIGN.md §4,
+                # profiles/r1_issue_probe.jsonl): 5.15 scheduler cycles per 32 edge tests
+                bound_s = prob.edge_tests / 32 * ISSUE_MIX_CYCLES / (4 * gpu.sm_count * summ["sm_mhz"] * 1e6)
+                out["issue_mix_bound_ms"] = round(bound_s * 1e3, 4)
+                out["roofline_frac_issue_mix"] = round(bound_s / run.per_launch_s, 4)
             out["roofline_frac"] = round(rate / peak, 4)
     for b in prob.buffers.values():
         b.free()

@@ -964,7 +964,9 @@ int jt_bench_sets(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, const jt_ar
         float q_ms = 0.f;
         D.p_cuEventElapsedTime(&q_ms, c->ev_a, c->ev_m);
         const double per = std::max(q_ms * 1e-3 / first, 1e-8);
-        long total = std::max<long>((long)std::ceil(min_seconds / per), min_reps);
+        // 3% over: launches after the measured quarter run a little faster (clocks and caches
+        // settle), and the loop must not end short of min_seconds (reference "at least")
+        long total = std::max<long>((long)std::ceil(1.03 * min_seconds / per), min_reps);
         total = std::min<long>(total, max_reps);
         for (; done < total; ++done)
             if (int e = launch_on(c, k, s, params[done % n_sets].data())) return finish(e);
