@@ -415,7 +415,9 @@ int stop_sampler(jt_ctx *c, jt_sample *out, int cap, int *n) {
 }
 
 int launch_on(jt_ctx *c, jt_kernel *k, const jt_launch_shape *s, void **params) {
-    if (s->smem_bytes > 48 * 1024 && s->smem_bytes != k->smem_attr) {
+    // raised whenever it changes: static + dynamic shared memory above 48 KB needs it even when
+    // the dynamic part alone is below (cuLaunchKernel fails with INVALID_VALUE otherwise)
+    if (s->smem_bytes > 0 && s->smem_bytes != k->smem_attr) {
         CUresult r = D.p_cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)s->smem_bytes);
         if (r != CUDA_SUCCESS) return cu_fail(r, "raise dynamic shared memory limit");
         k->smem_attr = s->smem_bytes;
@@ -863,7 +865,7 @@ int jt_kernel_attributes(jt_ctx *c, jt_kernel *k, int *regs, int *static_smem, i
 int jt_kernel_occupancy(jt_ctx *c, jt_kernel *k, int block_threads, size_t dynamic_smem, int *blocks_per_sm) {
     if (int e = bind(c)) return e;
     if (!k || !blocks_per_sm || block_threads < 1) return fail(JT_EINVAL, "bad occupancy arguments");
-    if (dynamic_smem > 48 * 1024 && (unsigned)dynamic_smem != k->smem_attr) {
+    if (dynamic_smem > 0 && (unsigned)dynamic_smem != k->smem_attr) {
         CUresult r = D.p_cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dynamic_smem);
         if (r != CUDA_SUCCESS) return cu_fail(r, "raise dynamic shared memory limit");
         k->smem_attr = (unsigned)dynamic_smem;
