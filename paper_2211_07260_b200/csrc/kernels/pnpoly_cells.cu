@@ -31,6 +31,17 @@
 // dropped: a 2-4 stage shared-memory ring filled by cp.async.bulk from one
 // producer thread (67 us and up: the producer waits for every warp to free a
 // stage, which couples the warps).
+//
+// DEFER (1): no ring. ncu on the ring kernel (profiles/r1_pnpoly_cells_tuned) counts ~56
+// thread instructions per point at 71% issue: the per-point ballot / prefix / push and the
+// drain bookkeeping cost more than the lookup itself, and the 32-register cap makes the
+// compiler re-read constants and thread ids inside the loop. With DEFER every thread keeps
+// up to two undecided points of its own pending in registers: their head loads are issued
+// when the points are classified and consumed one step later (the next step's point loads
+// and lookups cover the L2 latency), so an undecided point costs a divergent head load, a
+// test and a 4-byte store, and a decided one nothing beyond its lookup. A third undecided
+// point in one step (rare) is resolved on the spot. MIN_BLOCKS (1: one block per SM with
+// up to 64 registers) sets the launch bounds.
 #ifndef BLOCK_SIZE_X
 #define BLOCK_SIZE_X 1024
 #endif
@@ -62,6 +73,9 @@
 #endif
 #ifndef HEAD32
 #define HEAD32 0  // 1: 32-byte heads holding up to two undecided edges in place
+#endif
+#ifndef DEFER
+#define DEFER 0
 #endif
 #define HW (1 + HEAD32)  // float4s per head
 // ring slots per warp (a power of two): < 32 left after a drain, + 32 per point push (split
@@ -226,8 +240,12 @@ __device__ __forceinline__ unsigned ballot_nz(unsigned v) {
     return m;
 }
 
-// full occupancy (2048 threads per SM) needs <= 32 registers per thread
-extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X, 2048 / BLOCK_SIZE_X)
+// MIN_BLOCKS resident blocks per SM: the default, full occupancy (2048 threads per SM), caps
+// the kernel at 32 registers per thread; fewer blocks leave room for more registers
+#ifndef MIN_BLOCKS
+#define MIN_BLOCKS (2048 / BLOCK_SIZE_X)
+#endif
+extern "C" __global__ void __launch_bounds__(BLOCK_SIZE_X, MIN_BLOCKS)
 pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n, const unsigned *__restrict__ grid,
              const float4 *__restrict__ heads, const float4 *__restrict__ edges, float gsx, float gox, float gsy,
              float goy, SLAB_PARAMS) {
@@ -251,6 +269,102 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #else
     unsigned *rings = smem;
 #endif
+#if DEFER
+    (void)rings;
+    // Up to two undecided points pending per thread: coordinates, tag = index | base << 31
+    // (~0u: free) and the cell head, loaded when the point was classified and consumed at the
+    // next step, after that step's lookups (its point loads outlast the head's L2 latency).
+    float q0x = 0.f, q0y = 0.f, q1x = 0.f, q1y = 0.f;
+    unsigned q0t = ~0u, q1t = ~0u;
+    float4 h0 = make_float4(0.f, 0.f, 0.f, 0.f), h1 = h0, h0b = h0, h1b = h0;
+    auto settle = [&]() {
+        if (q0t != ~0u)
+            bitmap[q0t & 0x7fffffffu] = resolve(q0x, q0y, (int)(q0t >> 31), h0, h0b, edges, SLAB_ARGS), q0t = ~0u;
+        if (q1t != ~0u)
+            bitmap[q1t & 0x7fffffffu] = resolve(q1x, q1y, (int)(q1t >> 31), h1, h1b, edges, SLAB_ARGS), q1t = ~0u;
+    };
+    auto defer = [&](float px, float py, unsigned tag, unsigned cell) {
+        const float4 *h = heads + HW * cell;
+        if (q0t == ~0u) {
+            q0x = px, q0y = py, q0t = tag, h0 = __ldg(h);
+            if (HEAD32) h0b = __ldg(h + 1);
+        } else if (q1t == ~0u) {
+            q1x = px, q1y = py, q1t = tag, h1 = __ldg(h);
+            if (HEAD32) h1b = __ldg(h + 1);
+        } else {  // a third in one step: on the spot
+            bitmap[tag & 0x7fffffffu] =
+                resolve(px, py, (int)(tag >> 31), __ldg(h), HEAD32 ? __ldg(h + 1) : make_float4(0.f, 0.f, 0.f, 0.f),
+                        edges, SLAB_ARGS);
+        }
+    };
+    const int n_chunks = (nvec + CHUNK - 1) / CHUNK;
+    auto load = [&](int c, pvec *v) {
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) {
+            const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
+            if (c < n_chunks && q < full) v[t] = load_vec(pts + (long long)q * 2 * PPV);
+            else {
+#pragma unroll
+                for (int j = 0; j < 2 * PPV; ++j) v[t].v[j] = 0.f;
+                if (c < n_chunks && q < nvec)  // the partial tail vector: its points one by one
+#pragma unroll
+                    for (int j = 0; j < PPV; ++j)
+                        if (PPV * q + j < n) {
+                            const float2 p = points[PPV * q + j];
+                            v[t].v[2 * j] = p.x, v[t].v[2 * j + 1] = p.y;
+                        }
+            }
+        }
+    };
+    auto chunk = [&](int c, const pvec *cur, const bool FULL) {  // inlined twice with FULL constant
+        unsigned k[TILE][PPV], cl[TILE][PPV];
+#pragma unroll
+        for (int t = 0; t < TILE; ++t)
+#pragma unroll
+            for (int j = 0; j < PPV; ++j) {
+                unsigned cell_;
+                CODE_OF(cur[t].v[2 * j], cur[t].v[2 * j + 1], k[t][j]);
+                cl[t][j] = cell_;
+            }
+        settle();  // the previous step's pending points
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) {
+            const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
+            // decided points get their answer here; undecided ones a placeholder, rewritten
+            // when the point settles (same thread, later store)
+            if (FULL || q < full) store_vec(bitmap + (long long)PPV * q, k[t]);
+            else if (q < nvec)
+#pragma unroll
+                for (int j = 0; j < PPV; ++j)
+                    if (PPV * q + j < n) bitmap[PPV * q + j] = (int)(k[t][j] & 1u);
+#pragma unroll
+            for (int j = 0; j < PPV; ++j)
+                if ((FULL || PPV * q + j < n) && (k[t][j] & 2u))
+                    defer(cur[t].v[2 * j], cur[t].v[2 * j + 1], (unsigned)(PPV * q + j) | (k[t][j] << 31), cl[t][j]);
+        }
+    };
+#if REGPF
+    pvec nxt[TILE];  // the next chunk, loaded while this one is classified
+    load(blockIdx.x, nxt);
+#endif
+    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+#if PREFETCH
+        prefetch_chunk_if(threadIdx.x == 0, pts, c + (PREFETCH + 1) * gridDim.x, full);
+#endif
+        pvec cur[TILE];
+#if REGPF
+#pragma unroll
+        for (int t = 0; t < TILE; ++t) cur[t] = nxt[t];
+        load(c + gridDim.x, nxt);
+#else
+        load(c, cur);
+#endif
+        if ((c + 1) * CHUNK <= full) chunk(c, cur, true);
+        else chunk(c, cur, false);
+    }
+    settle();
+}
+#else
     // per warp: QCAP undecided points {px, py} and their indices (bit 31: base parity)
     float2 *ring_p = reinterpret_cast<float2 *>(rings) + (threadIdx.x >> 5) * QCAP;
     int *ring_i = reinterpret_cast<int *>(rings + 2 * (BLOCK_SIZE_X / 32) * QCAP) + (threadIdx.x >> 5) * QCAP;
@@ -395,3 +509,4 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
         bitmap[i & 0x7fffffff] = cell_search(e.x, e.y, cell_, (int)((unsigned)i >> 31), heads, edges, SLAB_ARGS);
     }
 }
+#endif

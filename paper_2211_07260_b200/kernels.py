@@ -728,7 +728,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         return {"BLOCK_SIZE_X": c["block_size_x"], "TILE": c["tile"], "GRID": c["grid"],
                 "GRID_SMEM": c.get("grid_smem", 1), "STREAM": c.get("stream", 0), "PREFETCH": c.get("prefetch", 0),
                 "REGPF": c.get("regpf", 0), "ADRAIN": c.get("adrain", 0), "HEAD32": c.get("head32", 0),
-                **({"QUAD": 1} if c.get("quad", 0) else {})}
+                **({"QUAD": 1} if c.get("quad", 0) else {}), **({"DEFER": 1} if c.get("defer", 0) else {}),
+                **({"MIN_BLOCKS": c["min_blocks"]} if c.get("min_blocks", 0) else {})}
 
     def cell_table(self, g: int, lmax: int, head_words: int = 4):
         cache = self.__dict__.setdefault("_cell_tables", {})
@@ -741,6 +742,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         c = _as_dict(config)
         words = (c["grid"] * c["grid"] + 15) // 16 if c.get("grid_smem", 1) else 0
         ad, hw = c.get("adrain", 0), 1 + c.get("head32", 0)
+        if c.get("defer", 0):  # no ring: the raster only
+            return (words + 3) // 4 * 16
         return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * (64 if ad else 128) * 12 + 16 * hw * c["block_size_x"] * ad
 
     def launch(self, config, n_points: int | None = None):
@@ -749,7 +752,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         chunks = max(1, math.ceil((self.n_points if n_points is None else n_points) / chunk))
         smem = self.smem_bytes(c)
         sms = self.gpu.sm_count if self.gpu is not None else 148
-        resident = max(1, min(2048 // c["block_size_x"], (228 * 1024) // (smem + 1024)))
+        blocks = c.get("min_blocks", 0) or 2048 // c["block_size_x"]  # the launch bounds' residency
+        resident = max(1, min(blocks, 2048 // c["block_size_x"], (228 * 1024) // (smem + 1024)))
         return Launch((min(chunks, sms * resident), 1, 1), (c["block_size_x"], 1, 1), smem)
 
     def prepare(self, gpu, inputs=None):

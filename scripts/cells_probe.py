@@ -1,0 +1,93 @@
+"""Full-size pnpoly_cells variants on B200: bit-exact check + device-timed loops over 2 rotating sets.
+
+Each variant is the tuned config plus extra -D defines (e.g. MIN_BLOCKS=1: one 1024-thread block
+per SM with up to 64 registers instead of two capped at 32). The grid is SMs x the occupancy
+the driver reports for the compiled kernel. Every variant's bitmap must equal the brute-force
+METHOD 2 oracle's on the 20 M-point BASELINE input.
+
+    python scripts/cells_probe.py                 # the built-in ladder -> gpurun_out/cells_probe.jsonl
+    python scripts/cells_probe.py tile=4 MIN_BLOCKS=1 ...   # one variant
+"""
+from __future__ import annotations
+
+import itertools
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from oracle import kernels_oracle as O  # noqa: E402
+from paper_2211_07260_b200 import native  # noqa: E402
+from paper_2211_07260_b200.gpu import GPU, Launch  # noqa: E402
+from paper_2211_07260_b200.kernels import make_problem  # noqa: E402
+
+CFG_KEYS = {"block_size_x", "tile", "grid", "grid_smem", "lmax", "stream", "prefetch", "regpf", "adrain", "head32",
+            "quad", "defer", "min_blocks"}
+
+
+def variants(base):
+    if len(sys.argv) > 1:
+        kv = dict(a.split("=") for a in sys.argv[1:])
+        return [{k: int(v) for k, v in kv.items()}]
+    out = [{}]
+    for (bs, minb), tile, regpf, quad, pf in itertools.product(((1024, 1), (512, 2), (512, 3), (256, 4), (256, 6)),
+                                                               (1, 2, 4), (0, 1), (0, 1), (0, 1)):
+        out.append({"defer": 1, "block_size_x": bs, "min_blocks": minb, "tile": tile, "regpf": regpf, "quad": quad,
+                    "prefetch": pf})
+    return out
+
+
+def main() -> None:
+    hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6538.6
+    rows = []
+    with GPU(0) as gpu:
+        p = make_problem("pnpoly_cells")
+        p.prepare(gpu)
+        inp = p.inputs
+        want = O.pnpoly(inp["points"], inp["vx"], inp["vy"], 2)
+        base = {"adrain": 0, "block_size_x": 1024, "grid": 448, "grid_smem": 1, "head32": 0, "lmax": 16,
+                "prefetch": 0, "stream": 0, "tile": 2, "regpf": 0, "quad": 0}
+        # a second resident input set (rotation: 2 x 240 MB > L2)
+        pts2 = gpu.array(inp["points"], slack=16)
+        out2 = gpu.empty((p.n_points,), np.int32)
+        for v in variants(base):
+            cfg = {**base, **{k: x for k, x in v.items() if k in CFG_KEYS}}
+            extra = {k: x for k, x in v.items() if k not in CFG_KEYS}
+            defs = {**p.defines(cfg), **extra}
+            try:
+                k = gpu.load(native.compile_cubin(native.kernel_source(p.source), p.name, native._nvrtc_options(defs)),
+                             p.symbol)
+            except Exception as exc:  # noqa: BLE001
+                print("compile failed", v, str(exc)[:300], flush=True)
+                continue
+            lau = p.launch(cfg)
+            occ = k.occupancy(lau.block[0], lau.smem)
+            chunk = (2 + 2 * cfg["quad"]) * cfg["block_size_x"] * cfg["tile"]
+            blocks = min(-(-p.n_points // chunk), gpu.sm_count * max(occ, 1))
+            lau = Launch((blocks, 1, 1), lau.block, lau.smem)
+            args = p.args(cfg)
+            args2 = [out2, pts2, *args[2:]]
+            p.reset_output()
+            gpu.launch(k, lau, args)
+            gpu.synchronize()
+            bad = int((p.fetch_output() != want).sum())
+            run = gpu.bench(k, lau, args, rotate=[args2], min_seconds=0.3, sample=False)
+            t = run.per_launch_s
+            rec = {"variant": v, "regs": k.regs, "local": k.local_bytes, "occ": occ, "blocks": blocks,
+                   "bad": bad, "us": round(t * 1e6, 2), "hbm_frac": round(p.algorithmic_bytes / t / 1e9 / hbm, 4)}
+            print(json.dumps(rec), flush=True)
+            rows.append(rec)
+    ok = [r for r in rows if r["bad"] == 0]
+    if ok:
+        print("best", min(ok, key=lambda r: r["us"]), flush=True)
+    Path("gpurun_out").mkdir(exist_ok=True)
+    with open("gpurun_out/cells_probe.jsonl", "a") as f:
+        for r in rows:
+            f.write(json.dumps(r) + "\n")
+
+
+if __name__ == "__main__":
+    main()
