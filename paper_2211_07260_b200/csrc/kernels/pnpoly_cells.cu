@@ -21,7 +21,8 @@
 //
 // Tunables (-D): BLOCK_SIZE_X, TILE (point vectors per thread per chunk), QUAD, GRID
 // (cells per side), GRID_SMEM (1: raster in shared memory; 0: read through L1),
-// STREAM (1: points loaded / results stored with the evict-first hints), PREFETCH
+// STREAM (1: points loaded / results stored with the evict-first hints; 2: points loaded with
+// L1::no_allocate), PREFETCH
 // (chunks ahead that one thread of the block pulls into L2 with
 // cp.async.bulk.prefetch: the block's points are one contiguous span per chunk,
 // so the next chunk's HBM latency overlaps this chunk's work without holding
@@ -86,7 +87,18 @@
 #define QCAP 128
 #endif
 
-#if STREAM
+#if STREAM == 2  // the point stream bypasses L1 (keeps L1 for the cell heads and edge lists)
+__device__ __forceinline__ float4 ldg_na(const float4 *p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+#define LOAD_PAIR(p) ldg_na(p)
+#define STORE_PAIR(p, v) (*(p) = (v))
+#define LDQ "ld.global.nc.L1::no_allocate"
+#define STQ "st.global"
+#elif STREAM
 #define LOAD_PAIR(p) __ldcs(p)
 #define STORE_PAIR(p, v) __stcs(p, v)
 #define LDQ "ld.global.cs"

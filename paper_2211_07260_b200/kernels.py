@@ -704,14 +704,18 @@ class PnPolyCellsProblem(PnPolyGridProblem):
             "grid": [256, 448, 512, 1024],
             "grid_smem": [0, 1],
             "lmax": [4, 16],
-            "stream": [0, 1],
+            "stream": [0, 1, 2],
             "prefetch": [0, 1, 2],
             "adrain": [0, 1],
             "head32": [0, 1],
             "quad": [0, 1],
+            "min_blocks": [0, 1, 2],
+            "regpf": [0, 1],
         }
-    # REGPF (register double buffering) stays a kernel option (tests/test_gpu_slab.py runs
-    # it); it measured slower everywhere, so it is not tuned
+    # round 2: min_blocks 1 (one block per SM, registers uncapped) makes REGPF (register double
+    # buffering) pay, so both joined the space (profiles/r2_cells_ring_minblocks_probe.jsonl);
+    # DEFER (per-thread pending points, no ring) stays a kernel option: slower everywhere
+    # (profiles/r2_cells_defer_probe.jsonl)
 
     def restrictions(self):
         # ring: 128 x 12-byte slots per warp, or 64 + a 16-byte head slot per thread with
@@ -721,7 +725,7 @@ class PnPolyCellsProblem(PnPolyGridProblem):
 
     def default_config(self):
         return {"block_size_x": 1024, "tile": 2, "grid": 512, "grid_smem": 1, "lmax": 16, "stream": 0, "prefetch": 1, "regpf": 0,
-                "adrain": 1, "head32": 0, "quad": 0}
+                "adrain": 1, "head32": 0, "quad": 0, "min_blocks": 0}
 
     def defines(self, config):
         c = _as_dict(config)

@@ -33,10 +33,11 @@ def variants(base):
         kv = dict(a.split("=") for a in sys.argv[1:])
         return [{k: int(v) for k, v in kv.items()}]
     out = [{}]
-    for (bs, minb), tile, regpf, quad, pf in itertools.product(((1024, 1), (512, 2), (512, 3), (256, 4), (256, 6)),
-                                                               (1, 2, 4), (0, 1), (0, 1), (0, 1)):
-        out.append({"defer": 1, "block_size_x": bs, "min_blocks": minb, "tile": tile, "regpf": regpf, "quad": quad,
-                    "prefetch": pf})
+    # round 2, third ladder: around the best of the second (one 1024-thread block per SM, registers
+    # uncapped, REGPF + L2 prefetch): in-place 2-edge heads, raster size, list limit, L1 policy
+    for quad, h32, g, st, lmax in itertools.product((0, 1), (0, 1), (448, 512), (0, 1, 2), (4, 16)):
+        out.append({"block_size_x": 1024, "min_blocks": 1, "tile": 2, "regpf": 1, "prefetch": 1, "adrain": 0,
+                    "quad": quad, "head32": h32, "grid": g, "stream": st, "lmax": lmax})
     return out
 
 

@@ -263,6 +263,8 @@ def test_grid_other_polygons_and_special_points(gpu, shape, kind):
     cfgs = [c for c in configs if p.is_valid(c)] + [p.default_config()]
     if kind == "cells":
         cfgs.append(dict(p.default_config(), lmax=0))  # every undecided cell -> slab search
+        cfgs += [dict(p.default_config(), defer=1, min_blocks=1), dict(p.default_config(), defer=1, lmax=0, head32=1),
+                 dict(p.default_config(), defer=1, quad=1, tile=2, block_size_x=512, min_blocks=2)]
     for cfg in cfgs:
         np.testing.assert_array_equal(run_once(gpu, p, cfg), want, err_msg=f"{shape} {cfg}")
 
@@ -293,7 +295,18 @@ CELLS_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stre
                  + [dict(block_size_x=b, tile=t, grid=448, grid_smem=1, lmax=16, stream=st, prefetch=pf, regpf=0,
                          adrain=ad, head32=h, quad=1)
                     for b, t, st, pf, ad, h in itertools.product((256, 1024), (1, 2), (0, 1), (0, 1), (0, 1), (0, 1))
-                    if (b + t + st + pf + ad + h) % 2 == 0])
+                    if (b + t + st + pf + ad + h) % 2 == 0]
+                 # one block per SM with uncapped registers, register double buffering, L1-bypassing loads
+                 + [dict(block_size_x=1024, tile=t, grid=g, grid_smem=1, lmax=l, stream=st, prefetch=1, regpf=1,
+                         adrain=ad, head32=(t + st) % 2, quad=q, min_blocks=1)
+                    for t, g, l, st, ad, q in itertools.product((1, 2, 4), (448, 512), (4, 16), (0, 2), (0, 1), (0, 1))
+                    if (t + g // 64 + l + st + ad + q) % 4 == 0]
+                 # DEFER: per-thread pending undecided points instead of the warp ring
+                 + [dict(block_size_x=b, tile=t, grid=(448, 512, 1024)[(t + q) % 3], grid_smem=int((t + q) % 3 < 2),
+                         lmax=(16, 4)[(b // 256 + t) % 2], stream=(t + q) % 2, prefetch=(b // 256 + q) % 2,
+                         regpf=(t + q + b // 512) % 2, adrain=0, head32=(t + b // 256) % 2, quad=q, defer=1,
+                         min_blocks=mb)
+                    for (b, mb), t, q in itertools.product(((1024, 1), (512, 2), (256, 2), (256, 0)), (1, 2, 4), (0, 1))])
 
 
 @pytest.fixture(scope="module")
@@ -325,7 +338,10 @@ def test_cells_tiny_and_ragged_inputs(gpu, n):
                 dict(p.default_config(), adrain=1, tile=1, block_size_x=256),
                 dict(p.default_config(), head32=1, grid=448), dict(p.default_config(), head32=1, adrain=0),
                 dict(p.default_config(), quad=1, tile=1), dict(p.default_config(), quad=1, adrain=0, regpf=1),
-                dict(p.default_config(), quad=1, block_size_x=256, tile=2, stream=1)):
+                dict(p.default_config(), quad=1, block_size_x=256, tile=2, stream=1),
+                dict(p.default_config(), defer=1, min_blocks=1), dict(p.default_config(), defer=1, quad=1, tile=1),
+                dict(p.default_config(), defer=1, block_size_x=256, tile=4, regpf=1, head32=1, min_blocks=2),
+                dict(p.default_config(), defer=1, lmax=0)):
         np.testing.assert_array_equal(run_once(gpu, p, cfg),
                                       O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2), err_msg=str(cfg))
 
