@@ -214,10 +214,10 @@ def run_reference(args, dist: Dist) -> int:
 
 
 def summarize_samples(samples, t0, t1):
-    from paper_2211_07260_b200.b200 import counter_slope
+    from paper_2211_07260_b200.b200 import counter_power
 
     inside = [s for s in samples if t0 <= s[0] <= t1]
-    watts = counter_slope(samples, t0, t1)
+    watts, _ = counter_power(samples, t0, t1)
     clocks = [s[5] for s in inside if s[5]]
     reasons = 0
     for s in inside:
@@ -549,7 +549,7 @@ def run_ours(args, dist: Dist) -> int:
                 "ms_per_launch": round(erun.per_launch_s * 1e3, 5),
                 "sm_mhz": esumm["sm_mhz"],
                 "reasons": esumm["reasons"],
-                "source": (f"NVML total-energy counter slope (libjt sampler) over a dedicated {erun.total_s:.2f} s "
+                "source": (f"NVML total-energy counter, whole 100 ms counter periods (libjt sampler) over a dedicated {erun.total_s:.2f} s "
                            f"loop of {erun.reps} launches of the same kernel/config over the same 4 rotating sets, "
                            f"from {ENERGY_SETTLE_S} s in (past the power ramp); GFLOPS/W = flop / (W x s per launch)"),
             },

@@ -44,7 +44,15 @@ from .gpu import ENERGY, E_STAMP, GPU, MEM_MHZ, P_AVG, P_INST, REASONS, SM_MHZ, 
 from .kernels import KernelProblem, make_problem
 from .spaces import KernelConfig, normalize_value
 
-__all__ = ["B200Device", "counter_slope", "steady_window", "NVML_AVERAGE_WINDOW_S"]
+__all__ = ["B200Device", "counter_power", "counter_slope", "steady_window", "NVML_AVERAGE_WINDOW_S"]
+
+#: The B200 energy counter (nvmlDeviceGetTotalEnergyConsumption) accumulates in fixed periods:
+#: every change adds the energy of one period, while the host-observed change times and the
+#: driver's field timestamps jitter by +-20-40 ms around it (profiles/r2_energy_probe.json:
+#: increments of 74-78 J at ~750 W, 25 J idle, 50 J at ~505 W; 72 changes over 7.20 s).
+COUNTER_PERIOD_S = 0.1
+#: host-side delay allowance between the end of a counter period and the change being seen
+COUNTER_LAG_S = 0.015
 
 #: nvmlDeviceGetPowerUsage on Ampere and newer (incl. B200) reports power averaged over 1 s
 NVML_AVERAGE_WINDOW_S = 1.0
@@ -67,6 +75,45 @@ def counter_updates(samples, t0: float, t1: float) -> int:
         t = s[E_STAMP] if math.isfinite(s[E_STAMP]) else s[T]
         n += t0 <= t <= t1
     return n
+
+
+def _change_points(samples) -> list[tuple[float, float]]:
+    """(host time, energy) of every energy-counter change, in order."""
+    pts, last_e = [], None
+    for s in samples:
+        e = s[ENERGY]
+        if math.isfinite(e) and e != last_e:
+            pts.append((s[T], e))
+            last_e = e
+    return pts
+
+
+def counter_power(samples, t0: float, t1: float) -> tuple[float | None, int]:
+    """Energy-counter power (W) over [t0, t1] and the number of counter periods it used.
+
+    The counter adds one fixed period's energy per change (``COUNTER_PERIOD_S``), but the
+    times at which changes are seen jitter by a large fraction of the period, so a slope
+    dE / dt over two or three changes scatters by tens of percent (a 0.3 s loop: +37% on
+    one config in the r2 probe). Instead: sum the increments whose whole period lies inside
+    the window (the change seen at t covers about [t - period, t]; a change seen k periods
+    after the previous one carries k periods) and divide by their number of periods. The
+    period is the median change interval of the trace when it holds enough changes."""
+    pts = _change_points(samples)
+    if len(pts) < 2:
+        return None, 0
+    gaps = [b[0] - a[0] for a, b in zip(pts, pts[1:])]
+    period = statistics.median(gaps) if len(gaps) >= 8 else COUNTER_PERIOD_S
+    if not 0.5 * COUNTER_PERIOD_S <= period <= 2.0 * COUNTER_PERIOD_S:
+        period = COUNTER_PERIOD_S
+    energy, periods = 0.0, 0
+    for (ta, ea), (tb, eb) in zip(pts, pts[1:]):
+        k = max(1, round((tb - ta) / period))
+        if tb - k * period >= t0 + COUNTER_LAG_S and tb <= t1:
+            energy += eb - ea
+            periods += k
+    if periods == 0:
+        return None, 0
+    return energy / (periods * period), periods
 
 
 def counter_slope(samples, t0: float, t1: float) -> float | None:
@@ -354,16 +401,14 @@ class B200Device:
             trace.append(PowerSample(total, after[0][P_INST]))
         window = steady_window(total, self.settle)
         steady = [s for s in during if window[0] <= s[T] - t0 <= window[1]] or during or run.samples
-        slope = counter_slope(run.samples, t0 + window[0], t0 + window[1])
-        updates = counter_updates(run.samples, t0 + window[0], t0 + window[1])
-        source = 1.0  # energy counter inside the steady window
+        slope, updates = counter_power(run.samples, t0 + window[0], t0 + window[1])
+        source = 1.0  # whole energy-counter periods inside the steady window
         if slope is None:
-            # counter cadence (~100 ms on B200) longer than the window: widen to the loop (the first
-            # reading may then predate the loop, i.e. carry the previous workload's power)
-            slope = counter_slope(run.samples, t0 - 0.05, t0 + total + 0.05)
+            # no whole counter period after the settle: whole periods anywhere in the loop
+            slope, updates = counter_power(run.samples, t0, t0 + total)
             source = 0.5
         if slope is None:
-            # still < 2 counter updates: median instant power over the steady window
+            # a loop shorter than one counter period: median instant power over the steady window
             inst = [s[P_INST] for s in steady if math.isfinite(s[P_INST])]
             slope = float(statistics.median(inst)) if inst else None
             source = 0.0

@@ -109,20 +109,19 @@ class NVMLObserver(BenchmarkObserver):
 
     Results per benchmark (energies are per single kernel execution):
 
-    * ``nvml_energy`` — energy-counter slope over the steady window x runtime
-      (the primary energy source, ``nvmlDeviceGetTotalEnergyConsumption``);
-    * ``nvml_power`` — that counter slope in W;
+    * ``nvml_energy`` — energy-counter power over the steady window x runtime
+      (the primary energy source, ``nvmlDeviceGetTotalEnergyConsumption``): the
+      counter's whole fixed periods inside the window, summed and divided by
+      their duration (``b200.counter_power``);
+    * ``nvml_power`` — that counter power in W;
     * ``nvml_power_instant`` — median instant power over the window;
     * ``nvml_sm_clock`` / ``nvml_temperature`` / ``nvml_mem_clock`` — medians;
     * ``nvml_clock_locked`` — 1.0 if the controller held the requested clock,
       0.0 if NVML refused (the observed clock is then the truth);
-    * ``nvml_energy_source`` — 1.0 energy counter inside the steady window,
-      0.5 energy counter over the whole loop (fewer than two updates inside
-      the steady window: the slope then reaches back to an update taken
-      before the loop), 0.0 instant-power median (loop too short for two
-      counter updates at all);
-    * ``nvml_counter_updates`` — energy-counter updates inside the steady
-      window (>= 2 for a slope free of the previous workload).
+    * ``nvml_energy_source`` — 1.0 counter periods inside the steady window,
+      0.5 counter periods anywhere in the loop (none after the settle), 0.0
+      instant-power median (a loop shorter than one counter period);
+    * ``nvml_counter_updates`` — counter periods the energy used.
 
     Attaching it switches the benchmark energy rule to ``counter`` mode
     (see ``tuner.MeasurementSetup``).

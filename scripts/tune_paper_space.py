@@ -180,7 +180,7 @@ def cmd_sweep(args) -> None:
 
 def cmd_confirm(args) -> None:
     sys.path.insert(0, str(ROOT / "scripts"))
-    from tune_suite import TUNED_PATH, confirm, oracle_check  # noqa: E402
+    from tune_suite import RANKINGS, TUNED_PATH, confirm, oracle_check, screening_leaders  # noqa: E402
 
     problem = SPACES[args.space][0]()
     space = problem.space()
@@ -189,20 +189,8 @@ def cmd_confirm(args) -> None:
     results = [cache.get(c) for c in configs]
     have = [r for r in results if r is not None]
     ok = [r for r in have if not r.failed]
-    # Screening energies come from 0.3 s windows with two energy-counter updates, whose slope
-    # scatters widely against the instant-power median of the same window (the report records
-    # how widely); so the candidates are the leaders of four rankings: counter energy, instant-
-    # power energy, the larger of the two (a config cannot win on one low reading) and time.
-    def inst_energy(r):
-        w = r.observer_results.get("nvml_power_instant")
-        return r.time * w if w else float("inf")
-
-    def robust_energy(r):
-        return max(r.energy, inst_energy(r)) if math.isfinite(inst_energy(r)) else r.energy
-
-    rankings = {"counter_energy": lambda r: r.energy, "instant_energy": inst_energy, "max_energy": robust_energy,
-                "time": lambda r: r.time}
-    leaders = [r for key in rankings.values() for r in sorted(ok, key=key)[: args.top]]
+    rankings = RANKINGS
+    leaders = screening_leaders(ok, args.top)
     with GPU(0) as gpu:
         dev = B200Device(problem, gpu=gpu, min_window=args.window)
         confirmed = confirm(dev, problem, leaders)
@@ -275,9 +263,9 @@ def main() -> None:
     sub.add_parser("verify")
     s = sub.add_parser("sweep")
     s.add_argument("--seconds", type=float, default=1800.0)
-    # >= 0.2 s after the settle: two energy-counter updates (~100 ms cadence) inside the steady window
+    # 0.3 s loops hold two whole 100 ms energy-counter periods after the settle (b200.counter_power)
     s.add_argument("--window", type=float, default=0.3)
-    s.add_argument("--settle", type=float, default=0.08)
+    s.add_argument("--settle", type=float, default=0.02)
     c = sub.add_parser("confirm")
     c.add_argument("--top", type=int, default=8)
     c.add_argument("--window", type=float, default=0.2)

@@ -229,3 +229,38 @@ def test_counter_updates_and_slope_window():
     assert counter_updates(samples, 0.12, 0.19) == 0 and counter_slope(samples, 0.12, 0.19) is None
     samples.append((0.7, 500.0, 500.0, nan, nan, 1965, 3996, 50, 0))  # a missing reading is ignored
     assert counter_updates(samples, 0.0, 1.0) == 6
+
+
+def test_counter_power_whole_periods_ignore_timestamp_jitter():
+    """The counter adds one 100 ms period per change; change times jitter by +-35 ms. A dE/dt slope
+    over two changes scatters with the jitter, whole periods do not (profiles/r2_energy_probe.json)."""
+    import numpy as np
+
+    from paper_2211_07260_b200.b200 import counter_power, counter_slope
+
+    rng = np.random.default_rng(5)
+    nan = float("nan")
+    # 400 W before t = 1.0 (previous config), 750 W in the loop [1.0, 1.31], 250 W after
+    def power(t):
+        return 400.0 if t < 1.0 else (750.0 if t < 1.31 else 250.0)
+
+    changes, e = [], 1000.0
+    for j in range(1, 25):  # period ends every 0.1 s (offset 0.03), seen with jitter
+        end = 0.03 + 0.1 * j
+        e += sum(power(end - 0.1 + 0.001 * i) for i in range(100)) * 0.001
+        changes.append((end + rng.uniform(-0.035, 0.035) + 0.004, e))
+    samples, k = [], 0
+    for i in range(2600):
+        t = 0.001 * i
+        while k < len(changes) and changes[k][0] <= t:
+            k += 1
+        energy = changes[k - 1][1] if k else 1000.0
+        samples.append((t, 500.0, 500.0, energy, nan, 1965, 3996, 50, 0))
+    watts, periods = counter_power(samples, 1.0, 1.31)
+    assert periods >= 2
+    assert watts == pytest.approx(750.0, rel=0.02)
+    # the long trace estimates the period itself
+    assert counter_power(samples, 0.0, 2.5)[1] >= 20
+    # a window shorter than one whole period has none
+    assert counter_power(samples, 1.0, 1.09) == (None, 0)
+    assert counter_slope(samples, 1.0, 1.31) is not None  # the old estimator still exists for comparison
