@@ -28,7 +28,9 @@
 // so the next chunk's HBM latency overlaps this chunk's work without holding
 // registers), REGPF (1: the next chunk's vectors are loaded into registers before
 // this chunk is classified), ADRAIN (1: split drains, the heads fetched by
-// cp.async and tested at the next drain), HEAD32 (32-byte heads). Tried and
+// cp.async and tested at the next drain), HEAD32 (32-byte heads), HPF (a queued point's
+// cell head prefetched into L1, so its drain read hits L1), PUSHV (one warp prefix per point
+// vector for the ring pushes), MIN_BLOCKS. Tried and
 // dropped: a 2-4 stage shared-memory ring filled by cp.async.bulk from one
 // producer thread (67 us and up: the producer waits for every warp to free a
 // stage, which couples the warps).
@@ -78,13 +80,24 @@
 #ifndef DEFER
 #define DEFER 0
 #endif
+#ifndef HPF
+#define HPF 0  // 1: an undecided point's cell head is prefetched into L1 when it is queued
+#endif
 #define HW (1 + HEAD32)  // float4s per head
 // ring slots per warp (a power of two): < 32 left after a drain, + 32 per point push (split
 // drains run after each push) or + 64 per pair step
+#ifndef PUSHV
+#define PUSHV 0  // 1: one warp prefix (2-3 ballots) per point vector instead of one ballot per point
+#endif
 #if ADRAIN
 #define QCAP 64
+#elif PUSHV && QUAD
+#define QCAP 256  // < 32 left after a drain + 128 per 4-point vector step
 #else
 #define QCAP 128
+#endif
+#if PUSHV && ADRAIN
+#error "PUSHV drains once per vector: it needs the whole-drain ring (ADRAIN 0)"
 #endif
 
 #if STREAM == 2  // the point stream bypasses L1 (keeps L1 for the cell heads and edge lists)
@@ -465,9 +478,12 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
         for (int t = 0; t < TILE; ++t) {
             const int q = c * CHUNK + t * BLOCK_SIZE_X + threadIdx.x;
-            unsigned k[PPV], cell_;
+            unsigned k[PPV], cl[PPV], cell_;
 #pragma unroll
-            for (int j = 0; j < PPV; ++j) CODE_OF(cur[t].v[2 * j], cur[t].v[2 * j + 1], k[j]);
+            for (int j = 0; j < PPV; ++j) {
+                CODE_OF(cur[t].v[2 * j], cur[t].v[2 * j + 1], k[j]);
+                cl[j] = cell_;
+            }
             // decided points get their answer here; undecided ones a placeholder, rewritten
             // by a later drain of the same warp
             if (FULL || q < full) store_vec(bitmap + (long long)PPV * q, k);
@@ -475,6 +491,30 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
                 for (int j = 0; j < PPV; ++j)
                     if (PPV * q + j < n) bitmap[PPV * q + j] = (int)(k[j] & 1u);
+#if PUSHV
+            {
+                // the vector's undecided points: one warp prefix over their counts (<= PPV, so
+                // 2-3 ballots of its bits), then each lane writes its own run of slots
+                unsigned um = 0u;
+#pragma unroll
+                for (int j = 0; j < PPV; ++j)
+                    if ((FULL || PPV * q + j < n) && (k[j] & 2u)) um |= 1u << j;
+                const unsigned cnt = __popc(um);
+                const unsigned b0 = ballot_nz(cnt & 1u), b1 = ballot_nz(cnt & 2u), b2 = PPV > 2 ? ballot_nz(cnt & 4u) : 0u;
+                unsigned pos = tail + __popc(b0 & lanes_below) + 2u * __popc(b1 & lanes_below) +
+                               4u * __popc(b2 & lanes_below);
+#pragma unroll
+                for (int j = 0; j < PPV; ++j)
+                    if (um & (1u << j)) {
+                        ring_p[pos % QCAP] = make_float2(cur[t].v[2 * j], cur[t].v[2 * j + 1]);
+                        ring_i[pos % QCAP] = (PPV * q + j) | (int)(k[j] << 31);
+                        if (HPF) asm volatile("prefetch.global.L1 [%0];" ::"l"(heads + HW * cl[j]));
+                        ++pos;
+                    }
+                tail += __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
+                drain();
+            }
+#else
 #pragma unroll
             for (int j = 0; j < PPV; ++j) {
 #if PROBE_FLOOR == 2  // 2 = lookups, nothing queued
@@ -483,10 +523,13 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
                 const unsigned u = (FULL || PPV * q + j < n) ? (k[j] & 2u) : 0u;
 #endif
                 push(cur[t].v[2 * j], cur[t].v[2 * j + 1], PPV * q + j, k[j], u);
+                // the head's L2 -> L1 trip overlaps the point's wait in the ring
+                if (HPF && u) asm volatile("prefetch.global.L1 [%0];" ::"l"(heads + HW * cl[j]));
                 // ring: < 32 left after a drain; split drains after every push (+32), whole
                 // drains after every second push (+64)
                 if (ADRAIN || (j & 1)) drain();
             }
+#endif
         }
     };
 #if REGPF

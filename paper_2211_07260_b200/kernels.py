@@ -733,7 +733,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
                 "GRID_SMEM": c.get("grid_smem", 1), "STREAM": c.get("stream", 0), "PREFETCH": c.get("prefetch", 0),
                 "REGPF": c.get("regpf", 0), "ADRAIN": c.get("adrain", 0), "HEAD32": c.get("head32", 0),
                 **({"QUAD": 1} if c.get("quad", 0) else {}), **({"DEFER": 1} if c.get("defer", 0) else {}),
-                **({"MIN_BLOCKS": c["min_blocks"]} if c.get("min_blocks", 0) else {})}
+                **({"MIN_BLOCKS": c["min_blocks"]} if c.get("min_blocks", 0) else {}),
+                **({"HPF": 1} if c.get("hpf", 0) else {}), **({"PUSHV": 1} if c.get("pushv", 0) else {})}
 
     def cell_table(self, g: int, lmax: int, head_words: int = 4):
         cache = self.__dict__.setdefault("_cell_tables", {})
@@ -748,7 +749,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         ad, hw = c.get("adrain", 0), 1 + c.get("head32", 0)
         if c.get("defer", 0):  # no ring: the raster only
             return (words + 3) // 4 * 16
-        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * (64 if ad else 128) * 12 + 16 * hw * c["block_size_x"] * ad
+        qcap = 64 if ad else (256 if c.get("pushv", 0) and c.get("quad", 0) else 128)  # QCAP in the kernel
+        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * qcap * 12 + 16 * hw * c["block_size_x"] * ad
 
     def launch(self, config, n_points: int | None = None):
         c = _as_dict(config)

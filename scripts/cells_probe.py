@@ -25,7 +25,7 @@ from paper_2211_07260_b200.gpu import GPU, Launch  # noqa: E402
 from paper_2211_07260_b200.kernels import make_problem  # noqa: E402
 
 CFG_KEYS = {"block_size_x", "tile", "grid", "grid_smem", "lmax", "stream", "prefetch", "regpf", "adrain", "head32",
-            "quad", "defer", "min_blocks"}
+            "quad", "defer", "min_blocks", "hpf", "pushv"}
 
 
 def variants(base):
@@ -33,11 +33,12 @@ def variants(base):
         kv = dict(a.split("=") for a in sys.argv[1:])
         return [{k: int(v) for k, v in kv.items()}]
     out = [{}]
-    # round 2, third ladder: around the best of the second (one 1024-thread block per SM, registers
-    # uncapped, REGPF + L2 prefetch): in-place 2-edge heads, raster size, list limit, L1 policy
-    for quad, h32, g, st, lmax in itertools.product((0, 1), (0, 1), (448, 512), (0, 1, 2), (4, 16)):
-        out.append({"block_size_x": 1024, "min_blocks": 1, "tile": 2, "regpf": 1, "prefetch": 1, "adrain": 0,
-                    "quad": quad, "head32": h32, "grid": g, "stream": st, "lmax": lmax})
+    # round 2, fourth ladder: L1 prefetch of queued points' heads (hpf) and one warp prefix per point
+    # vector for the pushes (pushv), on the two occupancies
+    for (bs, mb, rp), hpf, pv, st, tile, quad in itertools.product(((1024, 1, 1), (1024, 0, 0)), (0, 1), (0, 1),
+                                                                   (0, 2), (1, 2), (0, 1)):
+        out.append({"block_size_x": bs, "min_blocks": mb, "tile": tile, "regpf": rp, "prefetch": 1, "adrain": 0,
+                    "quad": quad, "head32": 0, "grid": 448, "stream": st, "lmax": 16, "hpf": hpf, "pushv": pv})
     return out
 
 

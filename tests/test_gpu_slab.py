@@ -263,7 +263,8 @@ def test_grid_other_polygons_and_special_points(gpu, shape, kind):
     cfgs = [c for c in configs if p.is_valid(c)] + [p.default_config()]
     if kind == "cells":
         cfgs.append(dict(p.default_config(), lmax=0))  # every undecided cell -> slab search
-        cfgs += [dict(p.default_config(), defer=1, min_blocks=1), dict(p.default_config(), defer=1, lmax=0, head32=1),
+        cfgs += [dict(p.default_config(), adrain=0, pushv=1, hpf=1, quad=1),
+                 dict(p.default_config(), defer=1, min_blocks=1), dict(p.default_config(), defer=1, lmax=0, head32=1),
                  dict(p.default_config(), defer=1, quad=1, tile=2, block_size_x=512, min_blocks=2)]
     for cfg in cfgs:
         np.testing.assert_array_equal(run_once(gpu, p, cfg), want, err_msg=f"{shape} {cfg}")
@@ -301,6 +302,12 @@ CELLS_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stre
                          adrain=ad, head32=(t + st) % 2, quad=q, min_blocks=1)
                     for t, g, l, st, ad, q in itertools.product((1, 2, 4), (448, 512), (4, 16), (0, 2), (0, 1), (0, 1))
                     if (t + g // 64 + l + st + ad + q) % 4 == 0]
+                 # one warp prefix per point vector for the ring pushes; L1 prefetch of queued heads
+                 + [dict(block_size_x=b, tile=t, grid=448, grid_smem=1, lmax=l, stream=st, prefetch=1, regpf=int(b == 1024),
+                         adrain=0, head32=h, quad=q, min_blocks=int(b == 1024), pushv=1, hpf=hp)
+                    for b, t, l, st, h, q, hp in itertools.product((512, 1024), (1, 2), (4, 16), (0, 2), (0, 1), (0, 1),
+                                                                   (0, 1))
+                    if (b // 512 + t + l + st + h + q + hp) % 4 == 0]
                  # DEFER: per-thread pending undecided points instead of the warp ring
                  + [dict(block_size_x=b, tile=t, grid=(448, 512, 1024)[(t + q) % 3], grid_smem=int((t + q) % 3 < 2),
                          lmax=(16, 4)[(b // 256 + t) % 2], stream=(t + q) % 2, prefetch=(b // 256 + q) % 2,
@@ -341,7 +348,9 @@ def test_cells_tiny_and_ragged_inputs(gpu, n):
                 dict(p.default_config(), quad=1, block_size_x=256, tile=2, stream=1),
                 dict(p.default_config(), defer=1, min_blocks=1), dict(p.default_config(), defer=1, quad=1, tile=1),
                 dict(p.default_config(), defer=1, block_size_x=256, tile=4, regpf=1, head32=1, min_blocks=2),
-                dict(p.default_config(), defer=1, lmax=0)):
+                dict(p.default_config(), defer=1, lmax=0),
+                dict(p.default_config(), adrain=0, pushv=1, hpf=1), dict(p.default_config(), adrain=0, pushv=1, quad=1),
+                dict(p.default_config(), adrain=0, pushv=1, lmax=0, min_blocks=1, regpf=1)):
         np.testing.assert_array_equal(run_once(gpu, p, cfg),
                                       O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2), err_msg=str(cfg))
 
