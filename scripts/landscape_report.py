@@ -147,7 +147,12 @@ def main() -> None:
         })
     lines = ["# Speed vs efficiency over the B200 tuning caches (Fig. 3 view)", "",
              "Generated by `scripts/landscape_report.py` from `results/cache_*.jsonl` (sweep-window values: "
-             "0.2-0.4 s loops, NVML energy-counter slope; confirmed optima are in `tuned_b200.json`). "
+             "0.2-0.4 s loops; confirmed optima are in `tuned_b200.json`). Caches measured before the "
+             "round-2 switch to whole energy-counter periods (every cache except `pnpoly` and the "
+             "`pnpoly_cells_focus` follow-up) hold two-change counter slopes, whose energies scatter by "
+             "tens of percent (DESIGN.md §5, `results/screening_accuracy.json`): their energy-optimal "
+             "screening points and efficiency spreads below are noise-inflated, and only the confirmed "
+             "table at the end is a measurement of record. "
              "Each kernel's directory holds `pareto.csv` / `pareto.json` (the package's `analyze --mode pareto`), "
              "`difficulty.csv` / `difficulty.json` (`analyze --mode difficulty`, energy objective, when the cache "
              "covers its whole space) and `speed_vs_efficiency.svg`.", "",
