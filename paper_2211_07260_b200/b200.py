@@ -88,6 +88,11 @@ def _change_points(samples) -> list[tuple[float, float]]:
     return pts
 
 
+def _changes_within(samples, t0: float, t1: float) -> bool:
+    """Whether the energy counter changed at least once inside [t0, t1]."""
+    return any(t0 <= t <= t1 for t, _ in _change_points(samples)[1:])
+
+
 def counter_power(samples, t0: float, t1: float) -> tuple[float | None, int]:
     """Energy-counter power (W) over [t0, t1] and the number of counter periods it used.
 
@@ -95,9 +100,11 @@ def counter_power(samples, t0: float, t1: float) -> tuple[float | None, int]:
     times at which changes are seen jitter by a large fraction of the period, so a slope
     dE / dt over two or three changes scatters by tens of percent (a 0.3 s loop: +37% on
     one config in the r2 probe). Instead: sum the increments whose whole period lies inside
-    the window (the change seen at t covers about [t - period, t]; a change seen k periods
-    after the previous one carries k periods) and divide by their number of periods. The
-    period is the median change interval of the trace when it holds enough changes."""
+    the window (the change seen at t covers about [t - period, t]) and divide by their
+    number of periods. Every change carries one period, however far from its neighbours it
+    is seen (the probe saw gaps of 45-141 ms, each with one period's energy), unless the gap
+    exceeds 1.75 periods (a change the sampler missed). The period is the median change
+    interval of the trace when it holds enough changes."""
     pts = _change_points(samples)
     if len(pts) < 2:
         return None, 0
@@ -107,7 +114,8 @@ def counter_power(samples, t0: float, t1: float) -> tuple[float | None, int]:
         period = COUNTER_PERIOD_S
     energy, periods = 0.0, 0
     for (ta, ea), (tb, eb) in zip(pts, pts[1:]):
-        k = max(1, round((tb - ta) / period))
+        gap = (tb - ta) / period
+        k = round(gap) if gap > 1.75 else 1
         if tb - k * period >= t0 + COUNTER_LAG_S and tb <= t1:
             energy += eb - ea
             periods += k
@@ -165,6 +173,8 @@ class B200Device:
         self._owns_gpu = gpu is None
         self.min_window = float(min_window)
         self.settle = float(settle)
+        #: re-runs of a loop whose NVML trace held no energy-counter change (see ``execute``)
+        self.max_stale_retries = 2
         self.clock_settle = float(clock_settle)
         self.sample_period_us = int(sample_period_us)
         self.sample_rate_hz = 1e6 / self.sample_period_us
@@ -364,17 +374,29 @@ class B200Device:
         args = self.problem.args(merged)
         if self.answer is not None:
             self.problem.reset_output()
-        run = self.gpu.bench(
-            kernel,
-            launch,
-            args,
-            min_seconds=max(float(duration_hint), self.min_window),
-            sample_period_us=self.sample_period_us,
-        )
-        self.execution_count += 1
+        retries = 0
+        while True:
+            run = self.gpu.bench(
+                kernel,
+                launch,
+                args,
+                min_seconds=max(float(duration_hint), self.min_window),
+                sample_period_us=self.sample_period_us,
+            )
+            self.execution_count += 1
+            # A loop spanning >= 2.5 counter periods in which the sampler saw no counter change
+            # at all (NVML returned stale readings throughout; the instant field then reads idle
+            # too) carries no energy information: run it again, at most twice.
+            stale = run.total_s >= 2.5 * COUNTER_PERIOD_S and not _changes_within(
+                run.samples, run.loop_t0, run.loop_t0 + run.total_s)
+            if not stale or retries == self.max_stale_retries:
+                break
+            retries += 1
         if self.answer is not None:
             self._check_answer(merged)
-        return self._execution(run)
+        ex = self._execution(run)
+        ex.telemetry["stale_retries"] = float(retries)
+        return ex
 
     def _check_answer(self, config) -> None:
         got = self.problem.fetch_output()

@@ -121,7 +121,9 @@ class NVMLObserver(BenchmarkObserver):
     * ``nvml_energy_source`` — 1.0 counter periods inside the steady window,
       0.5 counter periods anywhere in the loop (none after the settle), 0.0
       instant-power median (a loop shorter than one counter period);
-    * ``nvml_counter_updates`` — counter periods the energy used.
+    * ``nvml_counter_updates`` — counter periods the energy used;
+    * ``nvml_stale_retries`` — loops re-run because NVML showed no counter
+      change during them (stale readings).
 
     Attaching it switches the benchmark energy rule to ``counter`` mode
     (see ``tuner.MeasurementSetup``).
@@ -151,7 +153,7 @@ class NVMLObserver(BenchmarkObserver):
         if inside:
             out["nvml_power_instant"] = statistics.median(inside)
         for key in ("sm_clock", "mem_clock", "temperature", "clock_locked", "throttle_reasons", "energy_source",
-                    "counter_updates"):
+                    "counter_updates", "stale_retries"):
             if key in tele:
                 out[f"nvml_{key}"] = float(tele[key])
         self._result = out

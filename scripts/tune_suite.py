@@ -61,8 +61,9 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
         }
         return doc, "exhaustive", None
     if name == "pnpoly_cells_focus":  # round 2: the new knobs (min_blocks, regpf, L1-bypass) around the winners
-        doc = {"parameters": {"block_size_x": [1024], "tile": [1, 2, 4], "grid": [384, 448, 512], "grid_smem": [1],
-                              "lmax": [4, 16], "stream": [0, 2], "prefetch": [0, 1, 2], "adrain": [0, 1],
+        # (pushv and hpf measured neutral / slower in profiles/r2_cells_hpf_pushv_probe.jsonl: not swept)
+        doc = {"parameters": {"block_size_x": [1024], "tile": [1, 2], "grid": [448, 512], "grid_smem": [1],
+                              "lmax": [16], "stream": [0, 2], "prefetch": [0, 1, 2], "adrain": [0, 1],
                               "head32": [0, 1], "quad": [0, 1], "min_blocks": [0, 1], "regpf": [0, 1]},
                "restrictions": problem.restrictions()}
         return doc, "exhaustive", None
