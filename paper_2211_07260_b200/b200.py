@@ -51,7 +51,7 @@ __all__ = ["B200Device", "counter_power", "counter_slope", "steady_window", "NVM
 #: driver's field timestamps jitter by +-20-40 ms around it (profiles/r2_energy_probe.json:
 #: increments of 74-78 J at ~750 W, 25 J idle, 50 J at ~505 W; 72 changes over 7.20 s).
 COUNTER_PERIOD_S = 0.1
-#: host-side delay allowance between the end of a counter period and the change being seen
+#: allowance between the end of a counter period and the change's stamp
 COUNTER_LAG_S = 0.015
 
 #: nvmlDeviceGetPowerUsage on Ampere and newer (incl. B200) reports power averaged over 1 s
@@ -78,19 +78,17 @@ def counter_updates(samples, t0: float, t1: float) -> int:
 
 
 def _change_points(samples) -> list[tuple[float, float]]:
-    """(host time, energy) of every energy-counter change, in order."""
+    """(time, energy) of every energy-counter change, in order. The time is the driver's field
+    timestamp when present: an NVML call can stall for hundreds of ms (profiles/
+    r2_energy_probe2.json: a reading requested at +0.069 s came back stamped +0.617 s), so the
+    host time at which a sample was requested can lie far before the value it returned."""
     pts, last_e = [], None
     for s in samples:
         e = s[ENERGY]
         if math.isfinite(e) and e != last_e:
-            pts.append((s[T], e))
+            pts.append((s[E_STAMP] if math.isfinite(s[E_STAMP]) else s[T], e))
             last_e = e
     return pts
-
-
-def _changes_within(samples, t0: float, t1: float) -> bool:
-    """Whether the energy counter changed at least once inside [t0, t1]."""
-    return any(t0 <= t <= t1 for t, _ in _change_points(samples)[1:])
 
 
 def counter_power(samples, t0: float, t1: float) -> tuple[float | None, int]:
@@ -100,11 +98,12 @@ def counter_power(samples, t0: float, t1: float) -> tuple[float | None, int]:
     times at which changes are seen jitter by a large fraction of the period, so a slope
     dE / dt over two or three changes scatters by tens of percent (a 0.3 s loop: +37% on
     one config in the r2 probe). Instead: sum the increments whose whole period lies inside
-    the window (the change seen at t covers about [t - period, t]) and divide by their
+    the window (the change stamped t covers about [t - period, t]) and divide by their
     number of periods. Every change carries one period, however far from its neighbours it
-    is seen (the probe saw gaps of 45-141 ms, each with one period's energy), unless the gap
-    exceeds 1.75 periods (a change the sampler missed). The period is the median change
-    interval of the trace when it holds enough changes."""
+    is stamped (the probe saw gaps of 45-141 ms, each with one period's energy), unless the
+    gap exceeds 1.75 periods (changes the sampler did not see: a stalled NVML call returns
+    several periods at once). The period is the median change interval of the trace when it
+    holds enough changes."""
     pts = _change_points(samples)
     if len(pts) < 2:
         return None, 0
@@ -384,11 +383,13 @@ class B200Device:
                 sample_period_us=self.sample_period_us,
             )
             self.execution_count += 1
-            # A loop spanning >= 2.5 counter periods in which the sampler saw no counter change
-            # at all (NVML returned stale readings throughout; the instant field then reads idle
-            # too) carries no energy information: run it again, at most twice.
-            stale = run.total_s >= 2.5 * COUNTER_PERIOD_S and not _changes_within(
-                run.samples, run.loop_t0, run.loop_t0 + run.total_s)
+            # A loop spanning >= 2.5 counter periods without one whole counter period inside its
+            # steady window carries no energy information (NVML stalled: a reading requested
+            # early in the loop returned after it, and the instant field then lags too): run it
+            # again, at most twice.
+            w0, w1 = steady_window(run.total_s, self.settle)
+            stale = run.total_s >= 2.5 * COUNTER_PERIOD_S and counter_power(
+                run.samples, run.loop_t0 + w0, run.loop_t0 + w1)[0] is None
             if not stale or retries == self.max_stale_retries:
                 break
             retries += 1

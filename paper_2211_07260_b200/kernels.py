@@ -701,7 +701,7 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         return {
             "block_size_x": [256, 512, 1024],
             "tile": [1, 2, 4],
-            "grid": [256, 448, 512, 1024],
+            "grid": [256, 448, 512, 576, 640, 704, 768, 1024],
             "grid_smem": [0, 1],
             "lmax": [4, 16],
             "stream": [0, 1, 2],

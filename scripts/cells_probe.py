@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import itertools
 import json
+import statistics
 import sys
 from pathlib import Path
 
@@ -21,8 +22,11 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 from oracle import kernels_oracle as O  # noqa: E402
 from paper_2211_07260_b200 import native  # noqa: E402
+from paper_2211_07260_b200.b200 import counter_power  # noqa: E402
 from paper_2211_07260_b200.gpu import GPU, Launch  # noqa: E402
 from paper_2211_07260_b200.kernels import make_problem  # noqa: E402
+
+LOOP_S = 1.0
 
 CFG_KEYS = {"block_size_x", "tile", "grid", "grid_smem", "lmax", "stream", "prefetch", "regpf", "adrain", "head32",
             "quad", "defer", "min_blocks", "hpf", "pushv"}
@@ -33,12 +37,10 @@ def variants(base):
         kv = dict(a.split("=") for a in sys.argv[1:])
         return [{k: int(v) for k, v in kv.items()}]
     out = [{}]
-    # round 2, fourth ladder: L1 prefetch of queued points' heads (hpf) and one warp prefix per point
-    # vector for the pushes (pushv), on the two occupancies
-    for (bs, mb, rp), hpf, pv, st, tile, quad in itertools.product(((1024, 1, 1), (1024, 0, 0)), (0, 1), (0, 1),
-                                                                   (0, 2), (1, 2), (0, 1)):
-        out.append({"block_size_x": bs, "min_blocks": mb, "tile": tile, "regpf": rp, "prefetch": 1, "adrain": 0,
-                    "quad": quad, "head32": 0, "grid": 448, "stream": st, "lmax": 16, "hpf": hpf, "pushv": pv})
+    # round 2, fifth ladder: one block per SM leaves room for finer rasters (fewer undecided points)
+    for g, st, h32, ad in itertools.product((448, 512, 576, 640, 704, 768), (0, 2), (0, 1), (0, 1)):
+        out.append({"block_size_x": 1024, "min_blocks": 1, "tile": 1, "regpf": 1, "prefetch": 1, "adrain": ad,
+                    "quad": 1, "head32": h32, "grid": g, "stream": st, "lmax": 16})
     return out
 
 
@@ -76,10 +78,18 @@ def main() -> None:
             gpu.launch(k, lau, args)
             gpu.synchronize()
             bad = int((p.fetch_output() != want).sum())
-            run = gpu.bench(k, lau, args, rotate=[args2], min_seconds=0.3, sample=False)
+            # 1 s loops: at ~79% of HBM the kernel draws the board's 1 kW cap and the SM clock settles
+            # below 1965 MHz after a few hundred ms, so shorter loops flatter it
+            run = gpu.bench(k, lau, args, rotate=[args2], min_seconds=LOOP_S, sample=True)
             t = run.per_launch_s
+            steady = [smp for smp in run.samples if smp[0] >= run.loop_t0 + 0.5 * run.total_s]
+            watts, _ = counter_power(run.samples, run.loop_t0 + 0.25, run.loop_t0 + run.total_s)
             rec = {"variant": v, "regs": k.regs, "local": k.local_bytes, "occ": occ, "blocks": blocks,
-                   "bad": bad, "us": round(t * 1e6, 2), "hbm_frac": round(p.algorithmic_bytes / t / 1e9 / hbm, 4)}
+                   "bad": bad, "us": round(t * 1e6, 2), "hbm_frac": round(p.algorithmic_bytes / t / 1e9 / hbm, 4),
+                   "loop_s": round(run.total_s, 2),
+                   "sm_mhz": statistics.median([smp[5] for smp in steady]) if steady else None,
+                   "power_w": round(watts, 1) if watts else None,
+                   "j_per_bitmap": round(watts * t, 5) if watts else None}
             print(json.dumps(rec), flush=True)
             rows.append(rec)
     ok = [r for r in rows if r["bad"] == 0]

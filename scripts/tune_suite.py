@@ -67,6 +67,12 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
                               "head32": [0, 1], "quad": [0, 1], "min_blocks": [0, 1], "regpf": [0, 1]},
                "restrictions": problem.restrictions()}
         return doc, "exhaustive", None
+    if name == "pnpoly_cells_focus2":  # round 2: finer rasters fit once one block holds the SM
+        doc = {"parameters": {"block_size_x": [1024], "tile": [1], "grid": [448, 512, 576, 640, 704], "grid_smem": [1],
+                              "lmax": [16], "stream": [0, 2], "prefetch": [1, 2], "adrain": [0, 1],
+                              "head32": [0, 1], "quad": [1], "min_blocks": [1], "regpf": [1]},
+               "restrictions": problem.restrictions()}
+        return doc, "exhaustive", None
     if name in ("conv2d", "sgemm_tf32", "pnpoly_slab", "pnpoly_grid", "pnpoly_cells"):
         return problem.space_document(), "exhaustive", None
     if name == "sgemm":
@@ -197,7 +203,8 @@ def rates(problem, t: float, w: float) -> dict:
 
 
 def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | None) -> dict:
-    problem = make_problem({"sgemm_wide": "sgemm", "pnpoly_cells_focus": "pnpoly_cells"}.get(name, name))
+    problem = make_problem({"sgemm_wide": "sgemm", "pnpoly_cells_focus": "pnpoly_cells",
+                            "pnpoly_cells_focus2": "pnpoly_cells"}.get(name, name))
     doc, strategy, budget = curated_space(name, problem)
     space = SearchSpace.from_dict(doc)
     if clocks:
@@ -312,8 +319,8 @@ def main():
     data = json.loads(TUNED_PATH.read_text()) if TUNED_PATH.exists() else {}
     for name in args.kernels.split(","):
         entry = tune(gpu, name, args.duration, args.seed, clocks)
-        if name in ("sgemm_wide", "pnpoly_cells_focus"):  # follow-up sweeps: keep whichever wins
-            base = {"sgemm_wide": "sgemm", "pnpoly_cells_focus": "pnpoly_cells"}[name]
+        if name in ("sgemm_wide", "pnpoly_cells_focus", "pnpoly_cells_focus2"):  # follow-up sweeps: keep whichever wins
+            base = {"sgemm_wide": "sgemm", "pnpoly_cells_focus": "pnpoly_cells", "pnpoly_cells_focus2": "pnpoly_cells"}[name]
             old = data.get(base)
             if old and old["time_optimal"]["time_s"] <= entry["time_optimal"]["time_s"]:
                 data[name + "_sweep"] = entry

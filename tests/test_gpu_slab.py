@@ -302,6 +302,10 @@ CELLS_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stre
                          adrain=ad, head32=(t + st) % 2, quad=q, min_blocks=1)
                     for t, g, l, st, ad, q in itertools.product((1, 2, 4), (448, 512), (4, 16), (0, 2), (0, 1), (0, 1))
                     if (t + g // 64 + l + st + ad + q) % 4 == 0]
+                 # finer rasters with one block per SM (r2 tuned region)
+                 + [dict(block_size_x=1024, tile=1, grid=g, grid_smem=1, lmax=16, stream=2 * (g // 64 % 2), prefetch=1,
+                         regpf=1, adrain=ad, head32=1 - ad, quad=1, min_blocks=1)
+                    for g in (576, 640, 704, 768) for ad in (0, 1)]
                  # one warp prefix per point vector for the ring pushes; L1 prefetch of queued heads
                  + [dict(block_size_x=b, tile=t, grid=448, grid_smem=1, lmax=l, stream=st, prefetch=1, regpf=int(b == 1024),
                          adrain=0, head32=h, quad=q, min_blocks=int(b == 1024), pushv=1, hpf=hp)
