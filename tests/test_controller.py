@@ -264,3 +264,50 @@ def test_counter_power_whole_periods_ignore_timestamp_jitter():
     # a window shorter than one whole period has none
     assert counter_power(samples, 1.0, 1.09) == (None, 0)
     assert counter_slope(samples, 1.0, 1.31) is not None  # the old estimator still exists for comparison
+
+
+def test_stale_nvml_loop_is_rerun():
+    """A loop whose trace holds no whole energy-counter period (a stalled NVML call returned its
+    reading after the loop) is measured again; the result records the re-run."""
+    from paper_2211_07260_b200.gpu import BenchRun
+
+    nan = float("nan")
+
+    def trace(t0, stale):
+        # counter periods end at t0 + 0.1 k; a stale trace sees the first change stamped after the loop
+        out, e = [], 5000.0
+        for i in range(300):
+            t = t0 + 0.001 * i
+            k = int((t - t0) / 0.1)
+            stamp = t0 + 0.1 * k
+            if stale:
+                k, stamp = 0, t0
+            out.append((t, 700.0, 700.0, e + 70.0 * k, stamp, 1965, 3996, 50, 0))
+        if stale:
+            out.append((t0 + 0.31, 700.0, 700.0, e + 210.0, t0 + 0.6, 1965, 3996, 50, 0))
+        return out
+
+    gpu = FakeGPU()
+    runs = iter([True, True, False])
+    calls = []
+
+    def bench(kernel, launch, args, *, min_seconds, sample_period_us=1000, **kw):
+        stale = next(runs)
+        calls.append(stale)
+        t0 = 10.0 * len(calls)
+        return BenchRun(1e-3, 1e-3, 0.3, 300, t0, t0 + 0.3, trace(t0, stale))
+
+    gpu.bench = bench
+    dev = device(gpu)
+    dev._compiled = lambda config: ({}, None, types.SimpleNamespace(threads=128))
+    dev.problem.bind = lambda kernel, cfg: None
+    dev.problem.args = lambda cfg: []
+    ex = dev.execute(B.KernelConfig(()), duration_hint=0.3)
+    assert calls == [True, True, False]
+    assert ex.telemetry["stale_retries"] == 2.0
+    assert ex.counter_power == pytest.approx(700.0, rel=0.01)
+    # at most two re-runs: a board that stays stale is measured three times and falls back
+    runs = iter([True, True, True])
+    calls.clear()
+    ex = dev.execute(B.KernelConfig(()), duration_hint=0.3)
+    assert calls == [True, True, True] and ex.telemetry["stale_retries"] == 2.0
