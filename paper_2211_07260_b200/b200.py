@@ -172,8 +172,10 @@ class B200Device:
         self._owns_gpu = gpu is None
         self.min_window = float(min_window)
         self.settle = float(settle)
-        #: re-runs of a loop whose NVML trace held no energy-counter change (see ``execute``)
+        #: re-runs of a loop whose NVML trace held no whole counter period, or whose counter and
+        #: instant-power estimates disagree by more than ``disagree`` (see ``execute``)
         self.max_stale_retries = 2
+        self.disagree = 0.15
         self.clock_settle = float(clock_settle)
         self.sample_period_us = int(sample_period_us)
         self.sample_rate_hz = 1e6 / self.sample_period_us
@@ -387,9 +389,16 @@ class B200Device:
             # steady window carries no energy information (NVML stalled: a reading requested
             # early in the loop returned after it, and the instant field then lags too): run it
             # again, at most twice.
+            # The same goes for a loop whose counter power and instant-power median disagree by
+            # more than DISAGREE (one bad counter increment among two, or an instant field still
+            # showing the previous config): the re-run follows a loop of the same config, so a
+            # lagging instant field has caught up and a bad increment is not repeated.
             w0, w1 = steady_window(run.total_s, self.settle)
-            stale = run.total_s >= 2.5 * COUNTER_PERIOD_S and counter_power(
-                run.samples, run.loop_t0 + w0, run.loop_t0 + w1)[0] is None
+            t0, t1 = run.loop_t0 + w0, run.loop_t0 + w1
+            watts = counter_power(run.samples, t0, t1)[0]
+            inst = [smp[P_INST] for smp in run.samples if t0 <= smp[T] <= t1 and math.isfinite(smp[P_INST])]
+            disagree = bool(watts and inst) and abs(watts / statistics.median(inst) - 1.0) > self.disagree
+            stale = run.total_s >= 2.5 * COUNTER_PERIOD_S and (watts is None or disagree)
             if not stale or retries == self.max_stale_retries:
                 break
             retries += 1
@@ -397,6 +406,7 @@ class B200Device:
             self._check_answer(merged)
         ex = self._execution(run)
         ex.telemetry["stale_retries"] = float(retries)
+        ex.telemetry["power_disagree"] = 1.0 if disagree else 0.0
         return ex
 
     def _check_answer(self, config) -> None:

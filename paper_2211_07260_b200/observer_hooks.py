@@ -122,8 +122,10 @@ class NVMLObserver(BenchmarkObserver):
       0.5 counter periods anywhere in the loop (none after the settle), 0.0
       instant-power median (a loop shorter than one counter period);
     * ``nvml_counter_updates`` — counter periods the energy used;
-    * ``nvml_stale_retries`` — loops re-run because NVML showed no counter
-      change during them (stale readings).
+    * ``nvml_stale_retries`` — loops re-run because NVML showed no whole
+      counter period during them (stalled readings) or its counter and
+      instant-power estimates disagreed by more than 15%;
+    * ``nvml_power_disagree`` — 1.0 if they still disagreed after the re-runs.
 
     Attaching it switches the benchmark energy rule to ``counter`` mode
     (see ``tuner.MeasurementSetup``).
@@ -153,7 +155,7 @@ class NVMLObserver(BenchmarkObserver):
         if inside:
             out["nvml_power_instant"] = statistics.median(inside)
         for key in ("sm_clock", "mem_clock", "temperature", "clock_locked", "throttle_reasons", "energy_source",
-                    "counter_updates", "stale_retries"):
+                    "counter_updates", "stale_retries", "power_disagree"):
             if key in tele:
                 out[f"nvml_{key}"] = float(tele[key])
         self._result = out

@@ -311,3 +311,35 @@ def test_stale_nvml_loop_is_rerun():
     calls.clear()
     ex = dev.execute(B.KernelConfig(()), duration_hint=0.3)
     assert calls == [True, True, True] and ex.telemetry["stale_retries"] == 2.0
+
+
+def test_counter_instant_disagreement_is_rerun():
+    """A loop whose counter power is half its instant-power median (one bad increment) is measured
+    again; the agreeing re-run is the one kept."""
+    from paper_2211_07260_b200.gpu import BenchRun
+
+    def trace(t0, per_period_j):
+        out = []
+        for i in range(300):
+            t = t0 + 0.001 * i
+            k = int((t - t0) / 0.1)
+            out.append((t, 700.0, 700.0, 5000.0 + per_period_j * k, t0 + 0.1 * k, 1965, 3996, 50, 0))
+        return out
+
+    gpu = FakeGPU()
+    energies = iter([35.0, 70.0])
+    calls = []
+
+    def bench(kernel, launch, args, *, min_seconds, sample_period_us=1000, **kw):
+        calls.append(1)
+        t0 = 10.0 * len(calls)
+        return BenchRun(1e-3, 1e-3, 0.3, 300, t0, t0 + 0.3, trace(t0, next(energies)))
+
+    gpu.bench = bench
+    dev = device(gpu)
+    dev._compiled = lambda config: ({}, None, types.SimpleNamespace(threads=128))
+    dev.problem.bind = lambda kernel, cfg: None
+    dev.problem.args = lambda cfg: []
+    ex = dev.execute(B.KernelConfig(()), duration_hint=0.3)
+    assert len(calls) == 2 and ex.telemetry["stale_retries"] == 1.0 and ex.telemetry["power_disagree"] == 0.0
+    assert ex.counter_power == pytest.approx(700.0, rel=0.01)
