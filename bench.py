@@ -379,8 +379,10 @@ def tuning_leg(gpu, dist: Dist) -> dict:
                                     "of the shard's configs (8 host threads, cubin cache cold or warm)"},
            "points_per_s_incl_fixed": round(points / dist.max(stats["seconds"] + setup_s + compile_s), 3),
            "timing": "wall clock of each rank's shard loop, max over ranks",
-           "note": "0.25 s windows see 2-3 energy-counter updates: the optima below are screening values "
-                   "(tune_suite.py re-measures leaders in 1 s windows; per_kernel holds the confirmed ones)"}
+           "note": "0.25 s windows hold two whole energy-counter periods (loops that stalled or whose counter "
+                   "and instant power disagree are re-run): the optima below are screening values, each "
+                   "re-measured in a 1 s loop under confirmed_1s (tune_suite.py confirms leaders in 3 x 1 s "
+                   "loops; per_kernel holds those)"}
     if dist.rank == 0:
         merged = partition.merge(space, [workdir / f"shard{r}.jsonl" for r in range(dist.world)],
                                  objective=Objective("energy"))

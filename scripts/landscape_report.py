@@ -72,6 +72,22 @@ def difficulty_space(problem, results) -> dict | None:
     return None
 
 
+def screening_quality(results) -> dict:
+    """Which energy estimator a cache was measured with, read off its observer keys, and how far
+    its counter power strays from the instant-power median of the same window (1st-99th pct)."""
+    keys = set().union(*(r.observer_results.keys() for r in results))
+    if "nvml_power_disagree" in keys:
+        estimator = "counter periods, re-runs"
+    elif "nvml_stale_retries" in keys or "nvml_counter_updates" in keys:
+        estimator = "counter (2-3 changes)"
+    else:
+        estimator = "counter slope (r1)"
+    ratio = sorted(r.observer_results["nvml_power"] / r.observer_results["nvml_power_instant"] for r in results
+                   if r.observer_results.get("nvml_power") and r.observer_results.get("nvml_power_instant"))
+    q = (lambda f: ratio[int(f * (len(ratio) - 1))]) if ratio else None
+    return {"estimator": estimator, "ratio": f"{q(0.01):.2f}-{q(0.99):.2f}" if q else "-"}
+
+
 def svg_scatter(points, front, t_opt, e_opt, units, title, path: Path) -> None:
     """Performance (x) vs efficiency (y): all configs grey, the Pareto front blue, optima marked."""
     w, h, m = 640, 440, 60
@@ -144,31 +160,33 @@ def main() -> None:
             "eff_spread": max(p[1] for p in pts) / min(p[1] for p in pts),
             "minima": None if diff is None else diff["minima"],
             "f_optimal": None if diff is None else diff["f_optimal"],
+            **screening_quality(results),
         })
     lines = ["# Speed vs efficiency over the B200 tuning caches (Fig. 3 view)", "",
              "Generated by `scripts/landscape_report.py` from `results/cache_*.jsonl` (sweep-window values: "
-             "0.2-0.4 s loops; confirmed optima are in `tuned_b200.json`). Caches measured before the "
-             "round-2 switch to whole energy-counter periods (every cache except `pnpoly` and the "
-             "`pnpoly_cells_focus` follow-up) hold two-change counter slopes, whose energies scatter by "
-             "tens of percent (DESIGN.md §5, `results/screening_accuracy.json`): their energy-optimal "
-             "screening points and efficiency spreads below are noise-inflated, and only the confirmed "
-             "table at the end is a measurement of record. "
+             "0.2-0.4 s loops; confirmed optima are in `tuned_b200.json`). The `estimator` column says how "
+             "each cache's energies were taken, and `counter/instant` how far its counter power strays from "
+             "the instant-power median of the same window (1st-99th percentile): caches taken before the "
+             "round-2 measurement fixes (DESIGN.md §5, `results/screening_accuracy.json`) hold a few "
+             "energies off by tens of percent, so their screening energy optima and efficiency spreads "
+             "are noise-inflated; the confirmed table at the end is the measurement of record. "
              "Each kernel's directory holds `pareto.csv` / `pareto.json` (the package's `analyze --mode pareto`), "
              "`difficulty.csv` / `difficulty.json` (`analyze --mode difficulty`, energy objective, when the cache "
              "covers its whole space) and `speed_vs_efficiency.svg`.", "",
-             "| kernel | configs | front | time-optimal (perf, eff) | energy-optimal (perf, eff) | energy saved by the "
-             "energy optimum | its slowdown | eff. spread max/min | local optima (FFG) | f_optimal |",
-             "|---|---|---|---|---|---|---|---|---|---|"]
+             "| kernel | configs | estimator | counter/instant | front | time-optimal (perf, eff) | energy-optimal "
+             "(perf, eff) | energy saved by the energy optimum | its slowdown | eff. spread max/min | local optima "
+             "(FFG) | f_optimal |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         u = r["units"]
         fo = "-" if r["f_optimal"] is None else f"{r['f_optimal']:.3f}"
         minima = "-" if r["minima"] is None else r["minima"]
         lines.append(
-            f"| {r['kernel']} | {r['configs']} | {r['front']} | {r['time_opt'][0]:.4g} {u[0]}, {r['time_opt'][1]:.4g} "
+            f"| {r['kernel']} | {r['configs']} | {r['estimator']} | {r['ratio']} | {r['front']} | "
+            f"{r['time_opt'][0]:.4g} {u[0]}, {r['time_opt'][1]:.4g} "
             f"{u[1]} | {r['energy_opt'][0]:.4g}, {r['energy_opt'][1]:.4g} | {100 * r['energy_saving']:.1f}% | "
             f"{100 * r['slowdown']:.1f}% | {r['eff_spread']:.1f}x | {minima} | {fo} |")
-    # the sweep windows (0.2-0.4 s) read energy 5-25 % low after lighter configs (counter cadence ~100 ms,
-    # power ramp): the optima confirmed in 3 x 1 s interleaved loops are the ones to quote
+    # the optima confirmed in 3 x 1 s interleaved loops are the ones to quote
     tuned = json.loads((ROOT / "paper_2211_07260_b200" / "tuned_b200.json").read_text())
     lines += ["", "Confirmed optima (`tuned_b200.json`: the sweep's energy and time leaders re-measured in 3 "
               "interleaved 1 s loops, energy from 0.25 s in; what bench.py's per_kernel reports):", "",

@@ -133,6 +133,7 @@ def cmd_confirm(args) -> None:
     class Picked:
         def __init__(self, cfg):
             self.config = KernelConfig.from_dict(cfg)
+            self.energy = None  # confirm() records the sweep energy beside the confirmed one
 
     with GPU(0) as gpu:
         for name, entry in doc["kernels"].items():
