@@ -27,10 +27,10 @@
 // cp.async.bulk.prefetch: the block's points are one contiguous span per chunk,
 // so the next chunk's HBM latency overlaps this chunk's work without holding
 // registers), REGPF (1: the next chunk's vectors are loaded into registers before
-// this chunk is classified), ADRAIN (1: split drains, the heads fetched by
+// this chunk is classified; 2: the same with two buffers swapping roles, no copies), ADRAIN (1: split drains, the heads fetched by
 // cp.async and tested at the next drain), HEAD32 (32-byte heads), HPF (a queued point's
 // cell head prefetched into L1, so its drain read hits L1), PUSHV (one warp prefix per point
-// vector for the ring pushes), MIN_BLOCKS. Tried and
+// vector for the ring pushes), RING16 (16-byte ring records), MIN_BLOCKS. Tried and
 // dropped: a 2-4 stage shared-memory ring filled by cp.async.bulk from one
 // producer thread (67 us and up: the producer waits for every warp to free a
 // stage, which couples the warps).
@@ -89,6 +89,10 @@
 #ifndef PUSHV
 #define PUSHV 0  // 1: one warp prefix (2-3 ballots) per point vector instead of one ballot per point
 #endif
+#ifndef RING16
+#define RING16 0  // 1: ring slots are one 16-byte record {px, py, tag, 0} (one address, one STS.128)
+#endif
+#define RSLOT (12 + 4 * RING16)  // bytes per ring slot
 #if ADRAIN
 #define QCAP 64
 #elif PUSHV && QUAD
@@ -368,6 +372,28 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
                     defer(cur[t].v[2 * j], cur[t].v[2 * j + 1], (unsigned)(PPV * q + j) | (k[t][j] << 31), cl[t][j]);
         }
     };
+#if REGPF == 2
+    // register double buffering without the copy: two buffers swap roles every chunk (the loop
+    // body is the pair of chunks c, c + grid)
+    pvec bufa[TILE], bufb[TILE];
+    load(blockIdx.x, bufa);
+    for (int c = blockIdx.x; c < n_chunks; c += 2 * gridDim.x) {
+#if PREFETCH
+        prefetch_chunk_if(threadIdx.x == 0, pts, c + (PREFETCH + 1) * gridDim.x, full);
+#endif
+        load(c + gridDim.x, bufb);
+        if ((c + 1) * CHUNK <= full) chunk(c, bufa, true);
+        else chunk(c, bufa, false);
+        const int c2 = c + gridDim.x;
+        if (c2 >= n_chunks) break;
+#if PREFETCH
+        prefetch_chunk_if(threadIdx.x == 0, pts, c2 + (PREFETCH + 1) * gridDim.x, full);
+#endif
+        load(c2 + gridDim.x, bufa);
+        if ((c2 + 1) * CHUNK <= full) chunk(c2, bufb, true);
+        else chunk(c2, bufb, false);
+    }
+#else
 #if REGPF
     pvec nxt[TILE];  // the next chunk, loaded while this one is classified
     load(blockIdx.x, nxt);
@@ -387,12 +413,29 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
         if ((c + 1) * CHUNK <= full) chunk(c, cur, true);
         else chunk(c, cur, false);
     }
+#endif
     settle();
 }
 #else
     // per warp: QCAP undecided points {px, py} and their indices (bit 31: base parity)
+#if RING16
+    float4 *ring_r = reinterpret_cast<float4 *>(rings) + (threadIdx.x >> 5) * QCAP;
+#define RING_PUT(pos, px, py, tag) (ring_r[pos] = make_float4((px), (py), __int_as_float(tag), 0.f))
+#define RING_GET(pos, px, py, tag)                                                                   \
+    do {                                                                                             \
+        const float4 r_ = ring_r[pos];                                                               \
+        (px) = r_.x, (py) = r_.y, (tag) = __float_as_int(r_.z);                                      \
+    } while (0)
+#else
     float2 *ring_p = reinterpret_cast<float2 *>(rings) + (threadIdx.x >> 5) * QCAP;
     int *ring_i = reinterpret_cast<int *>(rings + 2 * (BLOCK_SIZE_X / 32) * QCAP) + (threadIdx.x >> 5) * QCAP;
+#define RING_PUT(pos, px, py, tag) (ring_p[pos] = make_float2((px), (py)), ring_i[pos] = (tag))
+#define RING_GET(pos, px, py, tag)                                                                   \
+    do {                                                                                             \
+        const float2 e_ = ring_p[pos];                                                               \
+        (px) = e_.x, (py) = e_.y, (tag) = ring_i[pos];                                               \
+    } while (0)
+#endif
     const int lane = threadIdx.x & 31;
     unsigned lanes_below;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_below));
@@ -405,7 +448,7 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
     // batch of 32 takes its points into registers and starts a 16-byte cp.async of each
     // point's cell head into a per-lane slot; the batch is finished (test, store) when the
     // next one starts, or at the end. One batch is pending once any has started (head > 0).
-    float4 *hslot = reinterpret_cast<float4 *>(rings + 3 * (BLOCK_SIZE_X / 32) * QCAP) + HW * threadIdx.x;
+    float4 *hslot = reinterpret_cast<float4 *>(rings + RSLOT / 4 * (BLOCK_SIZE_X / 32) * QCAP) + HW * threadIdx.x;
     float apx = 0.f, apy = 0.f;
     int aidx = 0;
     auto finish = [&]() {
@@ -421,9 +464,7 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #endif
         while (tail - head >= 32u) {
             if (head) finish();
-            const float2 e = ring_p[(head + lane) % QCAP];
-            aidx = ring_i[(head + lane) % QCAP];
-            apx = e.x, apy = e.y;
+            RING_GET((head + lane) % QCAP, apx, apy, aidx);
             head += 32;
             unsigned cell_;
             CELL_OF(apx, apy);
@@ -439,12 +480,13 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
     auto drain = [&]() {
         __syncwarp();
         while (tail - head >= 32u) {
-            const float2 e = ring_p[(head + lane) % QCAP];
-            const int i = ring_i[(head + lane) % QCAP];
+            float ex, ey;
+            int i;
+            RING_GET((head + lane) % QCAP, ex, ey, i);
             head += 32;
             unsigned cell_;
-            CELL_OF(e.x, e.y);
-            bitmap[i & 0x7fffffff] = cell_search(e.x, e.y, cell_, (int)((unsigned)i >> 31), heads, edges, SLAB_ARGS);
+            CELL_OF(ex, ey);
+            bitmap[i & 0x7fffffff] = cell_search(ex, ey, cell_, (int)((unsigned)i >> 31), heads, edges, SLAB_ARGS);
         }
     };
 #endif
@@ -471,7 +513,7 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
     auto push = [&](float px, float py, int idx, unsigned k, unsigned u) {
         const unsigned need = ballot_nz(u);
         const unsigned pos = (tail + __popc(need & lanes_below)) % QCAP;
-        if (u) ring_p[pos] = make_float2(px, py), ring_i[pos] = idx | (int)(k << 31);
+        if (u) RING_PUT(pos, px, py, idx | (int)(k << 31));
         tail += __popc(need);
     };
     auto chunk = [&](int c, const pvec *cur, const bool FULL) {  // inlined twice with FULL constant
@@ -506,8 +548,7 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #pragma unroll
                 for (int j = 0; j < PPV; ++j)
                     if (um & (1u << j)) {
-                        ring_p[pos % QCAP] = make_float2(cur[t].v[2 * j], cur[t].v[2 * j + 1]);
-                        ring_i[pos % QCAP] = (PPV * q + j) | (int)(k[j] << 31);
+                        RING_PUT(pos % QCAP, cur[t].v[2 * j], cur[t].v[2 * j + 1], (PPV * q + j) | (int)(k[j] << 31));
                         if (HPF) asm volatile("prefetch.global.L1 [%0];" ::"l"(heads + HW * cl[j]));
                         ++pos;
                     }
@@ -532,6 +573,28 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
 #endif
         }
     };
+#if REGPF == 2
+    // register double buffering without the copy: two buffers swap roles every chunk (the loop
+    // body is the pair of chunks c, c + grid)
+    pvec bufa[TILE], bufb[TILE];
+    load(blockIdx.x, bufa);
+    for (int c = blockIdx.x; c < n_chunks; c += 2 * gridDim.x) {
+#if PREFETCH
+        prefetch_chunk_if(threadIdx.x == 0, pts, c + (PREFETCH + 1) * gridDim.x, full);
+#endif
+        load(c + gridDim.x, bufb);
+        if ((c + 1) * CHUNK <= full) chunk(c, bufa, true);
+        else chunk(c, bufa, false);
+        const int c2 = c + gridDim.x;
+        if (c2 >= n_chunks) break;
+#if PREFETCH
+        prefetch_chunk_if(threadIdx.x == 0, pts, c2 + (PREFETCH + 1) * gridDim.x, full);
+#endif
+        load(c2 + gridDim.x, bufa);
+        if ((c2 + 1) * CHUNK <= full) chunk(c2, bufb, true);
+        else chunk(c2, bufb, false);
+    }
+#else
 #if REGPF
     pvec nxt[TILE];  // the next chunk, loaded while this one is classified
     load(blockIdx.x, nxt);
@@ -551,17 +614,19 @@ pnpoly_cells(int *__restrict__ bitmap, const float2 *__restrict__ points, int n,
         if ((c + 1) * CHUNK <= full) chunk(c, cur, true);
         else chunk(c, cur, false);
     }
+#endif
 #if ADRAIN
 #if PROBE_FLOOR != 3
     if (head) finish();
 #endif
 #endif
     if (lane < tail - head) {  // the warp's leftovers
-        const float2 e = ring_p[(head + lane) % QCAP];
-        const int i = ring_i[(head + lane) % QCAP];
+        float ex, ey;
+        int i;
+        RING_GET((head + lane) % QCAP, ex, ey, i);
         unsigned cell_;
-        CELL_OF(e.x, e.y);
-        bitmap[i & 0x7fffffff] = cell_search(e.x, e.y, cell_, (int)((unsigned)i >> 31), heads, edges, SLAB_ARGS);
+        CELL_OF(ex, ey);
+        bitmap[i & 0x7fffffff] = cell_search(ex, ey, cell_, (int)((unsigned)i >> 31), heads, edges, SLAB_ARGS);
     }
 }
 #endif

@@ -710,7 +710,7 @@ class PnPolyCellsProblem(PnPolyGridProblem):
             "head32": [0, 1],
             "quad": [0, 1],
             "min_blocks": [0, 1, 2],
-            "regpf": [0, 1],
+            "regpf": [0, 1, 2],
         }
     # round 2: min_blocks 1 (one block per SM, registers uncapped) makes REGPF (register double
     # buffering) pay, so both joined the space (profiles/r2_cells_ring_minblocks_probe.jsonl);
@@ -734,7 +734,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
                 "REGPF": c.get("regpf", 0), "ADRAIN": c.get("adrain", 0), "HEAD32": c.get("head32", 0),
                 **({"QUAD": 1} if c.get("quad", 0) else {}), **({"DEFER": 1} if c.get("defer", 0) else {}),
                 **({"MIN_BLOCKS": c["min_blocks"]} if c.get("min_blocks", 0) else {}),
-                **({"HPF": 1} if c.get("hpf", 0) else {}), **({"PUSHV": 1} if c.get("pushv", 0) else {})}
+                **({"HPF": 1} if c.get("hpf", 0) else {}), **({"PUSHV": 1} if c.get("pushv", 0) else {}),
+                **({"RING16": 1} if c.get("ring16", 0) else {})}
 
     def cell_table(self, g: int, lmax: int, head_words: int = 4):
         cache = self.__dict__.setdefault("_cell_tables", {})
@@ -750,7 +751,8 @@ class PnPolyCellsProblem(PnPolyGridProblem):
         if c.get("defer", 0):  # no ring: the raster only
             return (words + 3) // 4 * 16
         qcap = 64 if ad else (256 if c.get("pushv", 0) and c.get("quad", 0) else 128)  # QCAP in the kernel
-        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * qcap * 12 + 16 * hw * c["block_size_x"] * ad
+        slot = 16 if c.get("ring16", 0) else 12  # RSLOT
+        return (words + 3) // 4 * 16 + c["block_size_x"] // 32 * qcap * slot + 16 * hw * c["block_size_x"] * ad
 
     def launch(self, config, n_points: int | None = None):
         c = _as_dict(config)

@@ -29,7 +29,7 @@ from paper_2211_07260_b200.kernels import make_problem  # noqa: E402
 LOOP_S = 1.0
 
 CFG_KEYS = {"block_size_x", "tile", "grid", "grid_smem", "lmax", "stream", "prefetch", "regpf", "adrain", "head32",
-            "quad", "defer", "min_blocks", "hpf", "pushv"}
+            "quad", "defer", "min_blocks", "hpf", "pushv", "ring16"}
 
 
 def variants(base):
@@ -37,10 +37,13 @@ def variants(base):
         kv = dict(a.split("=") for a in sys.argv[1:])
         return [{k: int(v) for k, v in kv.items()}]
     out = [{}]
-    # round 2, fifth ladder: one block per SM leaves room for finer rasters (fewer undecided points)
-    for g, st, h32, ad in itertools.product((448, 512, 576, 640, 704, 768), (0, 2), (0, 1), (0, 1)):
-        out.append({"block_size_x": 1024, "min_blocks": 1, "tile": 1, "regpf": 1, "prefetch": 1, "adrain": ad,
-                    "quad": 1, "head32": h32, "grid": g, "stream": st, "lmax": 16})
+    # round 2, sixth ladder: fewer instructions in the tuned region (the kernel is issue-bound at the
+    # 1 kW cap): copy-free register double buffering (regpf 2), 16-byte ring records (ring16)
+    for rp, r16, pv, g, h32 in itertools.product((1, 2), (0, 1), (0, 1), (576, 640), (0, 1)):
+        if pv and r16:
+            continue  # QUAD + pushv needs a 256-slot ring: 16-byte slots would not fit beside the raster
+        out.append({"block_size_x": 1024, "min_blocks": 1, "tile": 1, "regpf": rp, "prefetch": 1, "adrain": 0,
+                    "quad": 1, "head32": h32, "grid": g, "stream": 2, "lmax": 16, "ring16": r16, "pushv": pv})
     return out
 
 

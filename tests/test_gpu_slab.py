@@ -306,6 +306,12 @@ CELLS_CONFIGS = ([dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stre
                  + [dict(block_size_x=1024, tile=1, grid=g, grid_smem=1, lmax=16, stream=2 * (g // 64 % 2), prefetch=1,
                          regpf=1, adrain=ad, head32=1 - ad, quad=1, min_blocks=1)
                     for g in (576, 640, 704, 768) for ad in (0, 1)]
+                 # copy-free register double buffering, 16-byte ring records
+                 + [dict(block_size_x=b, tile=t, grid=g, grid_smem=1, lmax=l, stream=2, prefetch=1, regpf=2,
+                         adrain=ad, head32=1, quad=q, min_blocks=int(b == 1024), ring16=r)
+                    for b, t, g, l, ad, q, r in itertools.product((512, 1024), (1, 2), (448, 640), (4, 16), (0, 1),
+                                                                  (0, 1), (0, 1))
+                    if (b // 512 + t + g // 64 + l + ad + q + r) % 4 == 0 and not (b == 512 and g == 640)]
                  # one warp prefix per point vector for the ring pushes; L1 prefetch of queued heads
                  + [dict(block_size_x=b, tile=t, grid=448, grid_smem=1, lmax=l, stream=st, prefetch=1, regpf=int(b == 1024),
                          adrain=0, head32=h, quad=q, min_blocks=int(b == 1024), pushv=1, hpf=hp)
@@ -354,7 +360,9 @@ def test_cells_tiny_and_ragged_inputs(gpu, n):
                 dict(p.default_config(), defer=1, block_size_x=256, tile=4, regpf=1, head32=1, min_blocks=2),
                 dict(p.default_config(), defer=1, lmax=0),
                 dict(p.default_config(), adrain=0, pushv=1, hpf=1), dict(p.default_config(), adrain=0, pushv=1, quad=1),
-                dict(p.default_config(), adrain=0, pushv=1, lmax=0, min_blocks=1, regpf=1)):
+                dict(p.default_config(), adrain=0, pushv=1, lmax=0, min_blocks=1, regpf=1),
+                dict(p.default_config(), regpf=2, ring16=1, min_blocks=1, quad=1, tile=1, grid=640, adrain=0),
+                dict(p.default_config(), regpf=2, ring16=1, adrain=1, tile=2)):
         np.testing.assert_array_equal(run_once(gpu, p, cfg),
                                       O.pnpoly(p.inputs["points"], p.inputs["vx"], p.inputs["vy"], 2), err_msg=str(cfg))
 
