@@ -73,6 +73,12 @@ def curated_space(name: str, problem) -> tuple[dict, str, int | None]:
                               "head32": [0, 1], "quad": [1], "min_blocks": [1], "regpf": [1]},
                "restrictions": problem.restrictions()}
         return doc, "exhaustive", None
+    if name == "pnpoly_cells_focus3":  # round 2: copy-free register buffers, 16-byte ring records
+        doc = {"parameters": {"block_size_x": [1024], "tile": [1], "grid": [576, 640, 704], "grid_smem": [1],
+                              "lmax": [16], "stream": [2], "prefetch": [1], "adrain": [0], "head32": [0, 1],
+                              "quad": [1], "min_blocks": [1], "regpf": [1, 2], "ring16": [0, 1]},
+               "restrictions": problem.restrictions()}
+        return doc, "exhaustive", None
     if name == "sgemm_group":  # round 2: the tuned config's CTA walk, GROUP_M (profiles/r2_group_m.md)
         base = tuned_entry_config("sgemm") or problem.default_config()
         doc = {"parameters": {**{k: [v] for k, v in base.items() if k != "GROUP_M"}, "GROUP_M": [1, 2, 4, 8, 16]},
@@ -209,7 +215,7 @@ def rates(problem, t: float, w: float) -> dict:
 
 def tune(gpu: GPU, name: str, duration: float, seed: int, clocks: list[int] | None) -> dict:
     problem = make_problem({"sgemm_wide": "sgemm", "sgemm_group": "sgemm", "pnpoly_cells_focus": "pnpoly_cells",
-                            "pnpoly_cells_focus2": "pnpoly_cells"}.get(name, name))
+                            "pnpoly_cells_focus2": "pnpoly_cells", "pnpoly_cells_focus3": "pnpoly_cells"}.get(name, name))
     doc, strategy, budget = curated_space(name, problem)
     space = SearchSpace.from_dict(doc)
     if clocks:
@@ -324,9 +330,10 @@ def main():
     data = json.loads(TUNED_PATH.read_text()) if TUNED_PATH.exists() else {}
     for name in args.kernels.split(","):
         entry = tune(gpu, name, args.duration, args.seed, clocks)
-        if name in ("sgemm_wide", "sgemm_group", "pnpoly_cells_focus", "pnpoly_cells_focus2"):  # follow-ups: keep the winner
+        if name in ("sgemm_wide", "sgemm_group", "pnpoly_cells_focus", "pnpoly_cells_focus2",
+                    "pnpoly_cells_focus3"):  # follow-up sweeps: keep whichever wins
             base = {"sgemm_wide": "sgemm", "sgemm_group": "sgemm", "pnpoly_cells_focus": "pnpoly_cells",
-                    "pnpoly_cells_focus2": "pnpoly_cells"}[name]
+                    "pnpoly_cells_focus2": "pnpoly_cells", "pnpoly_cells_focus3": "pnpoly_cells"}[name]
             old = data.get(base)
             if old and old["time_optimal"]["time_s"] <= entry["time_optimal"]["time_s"]:
                 data[name + "_sweep"] = entry
