@@ -434,21 +434,25 @@ def run_ours(args, dist: Dist) -> int:
         img = gpu.array(prob.inputs["image"], slack=64)
         out = gpu.empty((prob.height, prob.width), np.float32)
         sets.append([out, img])
-    for i in range(args.warmup):
-        gpu.launch(kernel, launch, sets[i % 4])
-    gpu.synchronize()
+    # each set's launch packed once: the timed loop below issues back-to-back native launches with no
+    # per-launch Python argument packing (the kernel is ~150 us; the first launch follows the start event)
+    prepared = [gpu.prepare_launch(kernel, launch, s) for s in sets]
+    from paper_2211_07260_b200 import native
 
     gpu.reserve_events(2)
+    # the NVML sampler (its first calls can stall) starts before the warm-up, so the only idle time
+    # between the warm-up and the timed region is the barrier + synchronize the contract requires
+    gpu.sampler_start(1000, 1 << 20)
+    for i in range(args.warmup):
+        gpu.launch_prepared(prepared[i % 4])
+    gpu.synchronize()
     dist.barrier()
     torch_sync()
     gpu.synchronize()
-    from paper_2211_07260_b200 import native
-
-    gpu.sampler_start(1000, 1 << 20)
     t_host0 = native.now()
     gpu.record(0)
     for i in range(args.steps):
-        gpu.launch(kernel, launch, sets[i % 4])
+        gpu.launch_prepared(prepared[i % 4])
     gpu.record(1)
     elapsed = gpu.elapsed(0, 1)
     gpu.synchronize()

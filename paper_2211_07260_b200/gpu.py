@@ -366,6 +366,19 @@ class GPU:
         check(native.lib().jt_launch(self.handle, kernel.handle, ctypes.byref(shape), packed, len(args)),
               f"launch {kernel.name}")
 
+    def prepare_launch(self, kernel: Kernel, launch: Launch, args: Sequence) -> tuple:
+        """Pack one launch's shape and arguments once, for :meth:`launch_prepared` in a timed loop
+        (no per-launch Python argument packing between the kernels)."""
+        shape = launch.shape()
+        packed = _pack(args)
+        return (kernel.handle, ctypes.byref(shape), packed, len(args), shape, kernel.name)
+
+    def launch_prepared(self, prepared: tuple) -> None:
+        handle, shape_ref, packed, n, _shape, name = prepared
+        rc = native.lib().jt_launch(self.handle, handle, shape_ref, packed, n)
+        if rc:
+            check(rc, f"launch {name}")
+
     def time(self, kernel: Kernel, launch: Launch, args: Sequence, reps: int = 1) -> float:
         packed = _pack(args)
         shape = launch.shape()
