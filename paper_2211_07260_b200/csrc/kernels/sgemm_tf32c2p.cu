@@ -30,7 +30,7 @@
 //     no reset.
 //
 // Storage and operand layout as sgemm_tf32c2.cu. Tunables (-D): BN (128,
-// 256), STAGES, SPLIT_TAIL. Requires M % 256 == 0, N % BN == 0, K % 32 == 0. Launch:
+// 256), STAGES, SPLIT_TAIL, BK (32, 64, 128). Requires M % 256 == 0, N % BN == 0, K % BK == 0. Launch:
 // grid (2 * pairs, 1, 1), 192 threads, cluster (2, 1, 1).
 #ifndef BN
 #define BN 256
@@ -39,7 +39,12 @@
 #define STAGES 4
 #endif
 #define BM 128  // rows per CTA (the pair covers 256)
+#ifndef BK  // k-rows per stage (one TMA box per 32 M / N columns; BK / 8 MMAs per stage)
 #define BK 32
+#endif
+#if BK != 32 && BK != 64 && BK != 128
+#error "BK must be 32, 64 or 128"
+#endif
 #define BN_HALF (BN / 2)
 #define A_STAGE_BYTES (BM * BK * 4)
 #define B_STAGE_BYTES (BN_HALF * BK * 4)

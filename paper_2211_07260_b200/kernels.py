@@ -1142,11 +1142,22 @@ class SgemmTF32Problem(SgemmProblem):
             d["SPLIT_TAIL"] = c.get("SPLIT_TAIL", 0)
             if c.get("GROUP_M", 1) > 1:
                 d["GROUP_M"] = c["GROUP_M"]
+        if self._bk(c) != 32:
+            if not (c.get("PAIR", 0) and c.get("PERSIST", 0)):
+                from .errors import ConfigurationError
+
+                raise ConfigurationError("BK != 32 exists only for the persistent CTA-pair kernel (PAIR = PERSIST = 1)")
+            d["BK"] = self._bk(c)
         return d
+
+    @staticmethod
+    def _bk(config) -> int:
+        """k-rows per pipeline stage (optional key, default 32; 64 / 128 only for PAIR + PERSIST)."""
+        return int(_as_dict(config).get("BK", 32))
 
     def tile_multiples(self, config):
         c = _as_dict(config)
-        return {"m": 128 * (1 + c.get("PAIR", 0)), "n": c["BN"], "k": 32}
+        return {"m": 128 * (1 + c.get("PAIR", 0)), "n": c["BN"], "k": self._bk(c)}
 
     def _variant(self, config) -> tuple[str, str]:
         """(source file, kernel symbol): CTA-pair (cta_group::2), persistent warp-specialised, or one
@@ -1171,8 +1182,9 @@ class SgemmTF32Problem(SgemmProblem):
 
     def smem_bytes(self, config) -> int:
         c = _as_dict(config)
-        b_stage = c["BN"] * 32 * 4 // (2 if c.get("PAIR", 0) else 1)
-        return c["STAGES"] * (128 * 32 * 4 + b_stage) + 1024 + 256
+        bk = SgemmTF32Problem._bk(c)
+        b_stage = c["BN"] * bk * 4 // (2 if c.get("PAIR", 0) else 1)
+        return c["STAGES"] * (128 * bk * 4 + b_stage) + 1024 + 256
 
     def tiles(self, config) -> int:
         return (self.m // 128) * (self.n // _as_dict(config)["BN"])
@@ -1195,11 +1207,7 @@ class SgemmTF32Problem(SgemmProblem):
         super().prepare(gpu, inputs)
         # TMA descriptors: A^T is K x M row-major, B is K x N row-major; 32 x 32 fp32 boxes in the
         # 128B-span / 32B-atom swizzle, the only smem layout UMMA accepts for MN-major TF32
-        sw = gpu.SWIZZLE_128B_ATOM_32B
-        self._maps = {
-            "a": gpu.tensor_map_2d(self.buffers["at"], self.k, self.m, 32, 32, sw),
-            "b": gpu.tensor_map_2d(self.buffers["b"], self.k, self.n, 32, 32, sw),
-        }
+        self._maps = {}  # BK -> {"a", "b"}: boxes of BK k-rows x 32 fp32, built on first use
         # split-K tail workspace (two 128 x 256 partials per split tile, < one per SM) and counters
         self.buffers["workspace"] = gpu.empty((2 * gpu.sm_count * 128 * 256,), np.float32)
         counters = gpu.empty((gpu.sm_count,), np.uint32)
@@ -1209,19 +1217,27 @@ class SgemmTF32Problem(SgemmProblem):
     def rotation_sets(self, config, n):
         """As the base class, plus TMA descriptors of each set's own A and B copies."""
         sets = super().rotation_sets(config, n)
-        sw = self.gpu.SWIZZLE_128B_ATOM_32B
+        sw, bk = self.gpu.SWIZZLE_128B_ATOM_32B, self._bk(config)
         for j, args in enumerate(sets, start=1):
-            args[0] = self.gpu.tensor_map_2d(self.buffers[f"at@{j}"], self.k, self.m, 32, 32, sw)
-            args[1] = self.gpu.tensor_map_2d(self.buffers[f"b@{j}"], self.k, self.n, 32, 32, sw)
+            args[0] = self.gpu.tensor_map_2d(self.buffers[f"at@{j}"], self.k, self.m, bk, 32, sw)
+            args[1] = self.gpu.tensor_map_2d(self.buffers[f"b@{j}"], self.k, self.n, bk, 32, sw)
         return sets
+
+    def _maps_for(self, bk: int) -> dict:
+        if bk not in self._maps:
+            sw = self.gpu.SWIZZLE_128B_ATOM_32B
+            self._maps[bk] = {"a": self.gpu.tensor_map_2d(self.buffers["at"], self.k, self.m, bk, 32, sw),
+                              "b": self.gpu.tensor_map_2d(self.buffers["b"], self.k, self.n, bk, 32, sw)}
+        return self._maps[bk]
 
     def args(self, config):
         c = _as_dict(config)
         b = self.buffers
+        maps = self._maps_for(self._bk(c))
         scalars = [i32(self.m), i32(self.n), i32(self.k), f32(self.alpha), f32(self.beta)]
         if c.get("PERSIST", 0):
-            return [self._maps["a"], self._maps["b"], b["out"], b["workspace"], b["counters"], *scalars]
-        return [self._maps["a"], self._maps["b"], b["out"], *scalars]
+            return [maps["a"], maps["b"], b["out"], b["workspace"], b["counters"], *scalars]
+        return [maps["a"], maps["b"], b["out"], *scalars]
 
 
 # -- burner (P(f) sweep load) ---------------------------------------------------------------
