@@ -176,6 +176,15 @@ int jt_bench_sets(jt_ctx *ctx, jt_kernel *kernel, const jt_launch_shape *shape, 
 int jt_events_reserve(jt_ctx *ctx, int n);
 int jt_event_record(jt_ctx *ctx, int index);
 int jt_event_elapsed(jt_ctx *ctx, int start, int stop, double *seconds);
+/* Stream gate for host-independent timed regions: jt_stream_gate makes the
+ * active stream wait (cuStreamWaitValue32 on a mapped host word) so a whole
+ * sequence -- start event, K launches, stop event -- can be enqueued first;
+ * jt_stream_release lets it run back to back, with no host submission (or
+ * driver lock held by the NVML sampler) between the events. Replaces nothing
+ * in the reference (its simulated device has no launch path); used by
+ * bench.py's timed region. */
+int jt_stream_gate(jt_ctx *ctx);
+int jt_stream_release(jt_ctx *ctx);
 /* Streams: index 0 is the context's own; jt_streams_reserve(n) makes 1..n-1.
  * jt_stream_select routes subsequent launches, async copies, memsets, event
  * records and timed loops to that stream (copy/compute overlap for the

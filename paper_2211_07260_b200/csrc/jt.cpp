@@ -86,6 +86,7 @@ double real_now() {
     X(cuMemFree) \
     X(cuMemFreeHost) \
     X(cuMemHostAlloc) \
+    X(cuMemHostGetDevicePointer) \
     X(cuMemcpy2DAsync) \
     X(cuMemcpyDtoHAsync) \
     X(cuMemcpyHtoDAsync) \
@@ -99,6 +100,7 @@ double real_now() {
     X(cuStreamDestroy) \
     X(cuStreamSynchronize) \
     X(cuStreamWaitEvent) \
+    X(cuStreamWaitValue32) \
     X(cuTensorMapEncodeTiled)
 
 struct Driver {
@@ -291,6 +293,10 @@ struct jt_ctx {
     size_t sample_cap = 0;
     int period_us = 1000;
     std::vector<CUevent> events;
+    // stream gate (jt_stream_gate / jt_stream_release): a mapped host word the stream waits on
+    volatile unsigned *gate_host = nullptr;
+    CUdeviceptr gate_dev = 0;
+    unsigned gate_value = 0;
     std::vector<jt_module *> modules;
     std::vector<jt_kernel *> kernels;
 };
@@ -600,6 +606,7 @@ int jt_close(jt_ctx *c) {
         delete m;
     }
     if (c->flush_buf) D.p_cuMemFree(c->flush_buf);
+    if (c->gate_host) D.p_cuMemFreeHost((void *)c->gate_host);
     for (CUevent e : c->events) D.p_cuEventDestroy(e);
     D.p_cuEventDestroy(c->ev_a);
     D.p_cuEventDestroy(c->ev_b);
@@ -1000,6 +1007,37 @@ int jt_event_record(jt_ctx *c, int index) {
     if (int e = bind(c)) return e;
     if (index < 0 || index >= (int)c->events.size()) return fail(JT_EINVAL, "event %d not reserved", index);
     CU_TRY(D.p_cuEventRecord(c->events[index], active(c)), "cuEventRecord");
+    return JT_OK;
+}
+
+int jt_stream_gate(jt_ctx *c) {
+    if (int e = bind(c)) return e;
+    if (!c->gate_host) {
+        void *h = nullptr;
+        CU_TRY(D.p_cuMemHostAlloc(&h, 64, CU_MEMHOSTALLOC_PORTABLE | CU_MEMHOSTALLOC_DEVICEMAP), "cuMemHostAlloc");
+        CUdeviceptr d = 0;
+        CUresult r = D.p_cuMemHostGetDevicePointer(&d, h, 0);
+        if (r != CUDA_SUCCESS) {
+            D.p_cuMemFreeHost(h);
+            return cu_fail(r, "cuMemHostGetDevicePointer");
+        }
+        c->gate_host = static_cast<volatile unsigned *>(h);
+        c->gate_dev = d;
+        __atomic_store_n(const_cast<unsigned *>(c->gate_host), 0u, __ATOMIC_SEQ_CST);
+        c->gate_value = 0;
+    }
+    // the stream holds until the host word reaches the next value; work enqueued behind it (events
+    // included) starts only at jt_stream_release
+    const unsigned want = c->gate_value + 1;
+    CU_TRY(D.p_cuStreamWaitValue32(active(c), c->gate_dev, want, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue32");
+    c->gate_value = want;
+    return JT_OK;
+}
+
+int jt_stream_release(jt_ctx *c) {
+    if (!c) return fail(JT_EINVAL, "null context");
+    if (!c->gate_host) return fail(JT_EINVAL, "no stream gate armed");
+    __atomic_store_n(const_cast<unsigned *>(c->gate_host), c->gate_value, __ATOMIC_SEQ_CST);
     return JT_OK;
 }
 

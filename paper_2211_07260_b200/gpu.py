@@ -276,6 +276,13 @@ class GPU:
     def record(self, index: int) -> None:
         check(native.lib().jt_event_record(self.handle, int(index)), "jt_event_record")
 
+    def gate(self) -> None:
+        """Hold the active stream until :meth:`release` (work enqueued in between starts together)."""
+        check(native.lib().jt_stream_gate(self.handle), "jt_stream_gate")
+
+    def release(self) -> None:
+        check(native.lib().jt_stream_release(self.handle), "jt_stream_release")
+
     def elapsed(self, start: int, stop: int) -> float:
         out = ctypes.c_double()
         check(native.lib().jt_event_elapsed(self.handle, int(start), int(stop), ctypes.byref(out)), "jt_event_elapsed")

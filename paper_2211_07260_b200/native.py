@@ -55,7 +55,7 @@ EXPORTS = (
     "jt_pnpoly_edges", "jt_module_set_global", "jt_events_reserve", "jt_event_record", "jt_event_elapsed",
     "jt_h2d_async", "jt_d2h_async", "jt_tensor_map_2d", "jt_streams_reserve", "jt_stream_select",
     "jt_stream_wait_event", "jt_pnpoly_slabs", "jt_pnpoly_grid", "jt_pnpoly_cells", "jt_h2d_2d_async",
-    "jt_d2h_2d_async", "jt_nvrtc_version", "jt_kernel_occupancy",
+    "jt_d2h_2d_async", "jt_nvrtc_version", "jt_kernel_occupancy", "jt_stream_gate", "jt_stream_release",
 )
 
 
@@ -234,6 +234,8 @@ def _declare(lib) -> None:
         "jt_streams_reserve": (c.c_int, [P, c.c_int]),
         "jt_stream_select": (c.c_int, [P, c.c_int]),
         "jt_stream_wait_event": (c.c_int, [P, c.c_int]),
+        "jt_stream_gate": (c.c_int, [P]),
+        "jt_stream_release": (c.c_int, [P]),
         "jt_tensor_map_2d": (c.c_int, [P, c.c_ulonglong, c.c_ulonglong, c.c_ulonglong, c.c_uint, c.c_uint, c.c_int, P]),
         "jt_d2h_async": (c.c_int, [P, P, c.c_ulonglong, c.c_size_t]),
         "jt_h2d_2d_async": (c.c_int, [P, c.c_ulonglong, c.c_size_t, P, c.c_size_t, c.c_size_t, c.c_size_t]),

@@ -62,6 +62,25 @@ def main():
             res.setdefault("python_loop_20_after_idle", []).append(gpu.elapsed(0, 1) / 20 * 1e3)
             res.setdefault("python_loop_20_after_busy", []).append(gpu.elapsed(1, 2) / 20 * 1e3)
             gpu.synchronize()
+        # with the bench's NVML sampler running: ungated vs gated 20-launch regions
+        gpu.sampler_start(1000, 1 << 20)
+        for trial in range(5):
+            for gated in (False, True):
+                for i in range(5):
+                    gpu.launch_prepared(prepared[i % 4])
+                gpu.synchronize()
+                if gated:
+                    gpu.gate()
+                gpu.record(0)
+                for i in range(20):
+                    gpu.launch_prepared(prepared[i % 4])
+                gpu.record(1)
+                if gated:
+                    gpu.release()
+                key = "sampler_on_20_gated" if gated else "sampler_on_20"
+                res.setdefault(key, []).append(gpu.elapsed(0, 1) / 20 * 1e3)
+                gpu.synchronize()
+        gpu.sampler_stop(1 << 20)
         print(json.dumps({k: [round(v, 5) for v in vs] for k, vs in res.items()}), flush=True)
 
 

@@ -233,3 +233,37 @@ def test_tune_kernel_builtin_problem_and_wrong_answer():
         tune_kernel("vector_add", VECTOR_ADD, 1000, [np.zeros(1000, np.float32), ones, ones, np.int32(1000)],
                     {"block_size_x": [128, 256]}, answer=[np.full(1000, 3.0, np.float32), None, None, None],
                     duration=0.05)
+
+
+def test_stream_gate_holds_then_runs_the_sequence(gpu):
+    """jt_stream_gate / jt_stream_release (bench.py's timed region): nothing enqueued behind the gate
+    runs before the release; after it the start event, the launches and the stop event run back to
+    back, and the output equals the oracle's."""
+    import time
+
+    from paper_2211_07260_b200.kernels import Conv2DProblem
+
+    p = Conv2DProblem(width=512, height=512)
+    p.prepare(gpu)
+    cfg = p.default_config()
+    k = p.kernel(cfg)
+    p.bind(k, cfg)
+    prepared = gpu.prepare_launch(k, p.launch(cfg), p.args(cfg))
+    gpu.reserve_events(2)
+    for _ in range(2):  # the gate re-arms
+        p.reset_output()
+        gpu.synchronize()
+        gpu.gate()
+        gpu.record(0)
+        for _ in range(4):
+            gpu.launch_prepared(prepared)
+        gpu.record(1)
+        time.sleep(0.05)  # held: 50 ms of host time pass before the release
+        gpu.release()
+        ms = gpu.elapsed(0, 1) * 1e3
+        assert 0 < ms < 20, ms  # the held 50 ms are not inside the events
+    gpu.synchronize()
+    ref = O.conv2d(p.inputs["image"], p.inputs["filter"])
+    assert O.conv2d_error(p.fetch_output(), ref, p.inputs["image"], p.inputs["filter"]) <= 1e-5
+    for b in p.buffers.values():
+        b.free()
