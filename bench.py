@@ -439,13 +439,6 @@ def run_ours(args, dist: Dist) -> int:
     prepared = [gpu.prepare_launch(kernel, launch, s) for s in sets]
     from paper_2211_07260_b200 import native
 
-    # energy: a dedicated loop of the same kernel and config over the same 4 rotating sets, independent
-    # of --steps (a 20-step timed region lasts ~3 ms, far below the ~100 ms energy-counter cadence). It
-    # runs before the warm-up, so the timed region starts from the board's steady state under this
-    # kernel rather than from its state right after process start-up
-    erun = gpu.bench(kernel, launch, sets[0], rotate=sets[1:], min_seconds=ENERGY_LOOP_S)
-    esumm = summarize_samples(erun.samples, erun.loop_t0 + ENERGY_SETTLE_S, erun.loop_t1)
-
     gpu.reserve_events(2)
     # the NVML sampler (its first calls can stall) starts before the warm-up, so the only idle time
     # between the warm-up and the timed region is the barrier + synchronize the contract requires
@@ -484,6 +477,11 @@ def run_ours(args, dist: Dist) -> int:
     # the loop occupied the last `elapsed` seconds before t_host1; skip 0.1 s of ramp
     loop_t0 = max(t_host0, t_host1 - elapsed)
     summ = summarize_samples(samples, loop_t0 + min(0.1, 0.5 * elapsed), t_host1)
+
+    # energy: a dedicated loop of the same kernel and config over the same 4 rotating sets, independent
+    # of --steps (a 20-step timed region lasts ~3 ms, far below the ~100 ms energy-counter cadence)
+    erun = gpu.bench(kernel, launch, sets[0], rotate=sets[1:], min_seconds=ENERGY_LOOP_S)
+    esumm = summarize_samples(erun.samples, erun.loop_t0 + ENERGY_SETTLE_S, erun.loop_t1)
 
     per_step = elapsed / args.steps
     value = ranks_flops / elapsed_max / 1e9
