@@ -459,8 +459,10 @@ def run_ours(args, dist: Dist) -> int:
     # Only short regions are gated: launches pile up in the driver's queue behind the gate, and a queue
     # that fills blocks the enqueueing thread (long regions have no start-up gap to hide anyway).
     gated = False
-    if (args.steps <= GATE_MAX_STEPS and not os.environ.get("CUDA_INJECTION64_PATH")
-            and not os.environ.get("BENCH_NO_GATE")):
+    tool = any(k.startswith(("CUDA_INJECTION", "NV_NSIGHT", "NSIGHT", "NV_COMPUTE_PROFILER", "NV_TPS"))
+               for k in os.environ) or any(t in os.environ.get("LD_PRELOAD", "").lower()
+                                           for t in ("nsight", "sanitizer", "injection"))
+    if args.steps <= GATE_MAX_STEPS and not tool and not os.environ.get("BENCH_NO_GATE"):
         try:
             gpu.gate()
             gated = True
